@@ -1,0 +1,544 @@
+#!/usr/bin/env python
+"""Benchmark of the hierarchical ZeRO++ data-parallel hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt1.3b] [--impl hz|reference]
+
+N > 1 is launched by the driver as
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N --steps K --warmup W
+(one rank per GPU; if started without torchrun and --gpus > 1 this script re-launches
+itself that way).
+
+A step = one pass of the whole hot path over every parameter tensor of the model
+(GA = 1, setting T of the paper): per tensor, in forward order, the qwZ all-gather
+(quantize primary -> per-level NCCL all-gather -> dequantize, keeping the hpZ
+secondary), then in backward order the all-gather from the secondary and the qgZ
+reduce-scatter (quantize -> per-level all-to-all -> dequantize+sum(+requantize) ->
+fp32 gradient shard).  Inputs are resident in HBM before the timed region; every
+step touches several GB (> 126 MB L2), so no L2 flush is needed between steps.
+
+value = logical bytes of all ranks / time, logical bytes per tensor per rank =
+2*psi (forward gathered bf16) + 2*psi (backward gathered bf16) + 2*psi (bf16
+gradient in): 6*psi.  Weak scaling: per-rank work is fixed as N grows.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "param all-gather + grad reduce-scatter GB/s per step at 1/2/4/8 B200, % roofline"
+UNIT = "GB/s"
+HIERARCHY = {
+    "gpt1.3b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 4)},
+    "gpt6.7b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
+    "neox20b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
+}
+KERNEL_KINDS = ("quantize", "dequantize", "reduce", "reduce_requant")
+NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["hz", "reference"], default="hz")
+    ap.add_argument("--config", choices=sorted(HIERARCHY), default="gpt1.3b")
+    ap.add_argument("--qwz-bits", type=int, default=8)
+    ap.add_argument("--qgz-bits", type=int, default=4)
+    ap.add_argument("--block", type=int, default=256)
+    ap.add_argument("--layers", type=int, default=0, help="limit the tensor count (debug only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flat", action="store_true")
+    ap.add_argument("--cpu-sample-layers", type=int, default=4)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def relaunch_under_torchrun(args):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", "29533",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+# ------------------------------------------------------------------ measurement
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, devices):
+        self.devices = set(devices)
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8 or not f[0].isdigit() or int(f[0]) not in self.devices:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        loaded = [s for s in sm if s > 0]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (torch copy, read+write, measured)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-element DRAM bytes of each kernel kind from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+# --------------------------------------------------------------------- the step
+class Model:
+    def __init__(self, hz, ctx, torch, config, rank, world, args, device):
+        from paper_2501_04266_b200 import synth
+        self.hz, self.ctx, self.torch = hz, ctx, torch
+        self.args = args
+        tensors = synth.model_tensors(config)
+        if args.layers:
+            tensors = tensors[:args.layers]
+        self.tensors = []
+        L = ctx.levels
+        B = args.block
+        max_np = 0
+        for i, (name, numel) in enumerate(tensors):
+            p = ctx.partition(numel, B, w=1, s=1, gl=L)
+            Np = p.padded_numel
+            off_w, len_w = p.range(1)
+            seed = 2000 + 97 * rank + i
+            full_p = synth.torch_normal(Np, 7000 + i, 0.02, torch.bfloat16, device, outlier_every=0)
+            full_p[numel:] = 0                                       # zero padding (O2)
+            primary = full_p[off_w:off_w + len_w].clone()
+            del full_p
+            grad = synth.torch_normal(Np, seed, 1e-3, torch.bfloat16, device)
+            grad[numel:] = 0
+            _, len_s = p.range(1)
+            _, len_l = p.range(L)
+            t = {
+                "name": name, "numel": numel, "p": p, "primary": primary, "grad": grad,
+                "sec_c": torch.empty(len_s * args.qwz_bits // 8, dtype=torch.uint8, device=device),
+                "sec_s": torch.empty(len_s // B, dtype=torch.float32, device=device),
+                "shard": torch.empty(len_l, dtype=torch.float32, device=device),
+            }
+            self.tensors.append(t)
+            max_np = max(max_np, Np)
+        self.full = [torch.empty(max_np, dtype=torch.bfloat16, device=device) for _ in range(2)]
+        self.bits = [args.qgz_bits] * L
+        self.logical_bytes = sum(6 * t["numel"] for t in self.tensors)
+
+    def step(self, stream):
+        ctx, bits = self.ctx, self.args.qwz_bits
+        for i, t in enumerate(self.tensors):                         # forward: qwZ + hpZ
+            ctx.allgather_params(t["p"], t["primary"], t["sec_c"], t["sec_s"], self.full[i & 1], bits=bits,
+                                 stream=stream)
+        for i, t in reversed(list(enumerate(self.tensors))):        # backward: gather from secondary, qgZ
+            ctx.allgather_params(t["p"], None, t["sec_c"], t["sec_s"], self.full[i & 1], bits=bits,
+                                 backward=True, stream=stream)
+            ctx.reduce_scatter_grads(t["p"], t["grad"], t["shard"], self.bits, stream=stream)
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def summarize_trace(recs, steps):
+    kinds = {}
+    for r in recs:
+        k = kinds.setdefault(r["kind"], {"launches": 0, "ms": 0.0, "bytes": 0, "elems": 0})
+        k["launches"] += 1
+        k["ms"] += r["ms"]
+        k["bytes"] += r["bytes"]
+        k["elems"] += r["elems"]
+    total_ms = sum(v["ms"] for v in kinds.values()) or 1.0
+    out = {}
+    for name, v in kinds.items():
+        out[name] = {
+            "launches_per_step": v["launches"] / steps,
+            "avg_ms": v["ms"] / v["launches"],
+            "avg_bytes": v["bytes"] / v["launches"],
+            "avg_elems": v["elems"] / v["launches"],
+            "GBps": v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else None,
+            "share": v["ms"] / total_ms,
+        }
+    return out
+
+
+def run_hz(args):
+    import torch
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    from paper_2501_04266_b200 import hz
+
+    group = HIERARCHY[args.config].get(world)
+    if group is None:
+        raise SystemExit(f"no hierarchy for {world} GPUs")
+    uid = hz.get_uid() if rank == 0 else None
+    if world > 1:
+        import torch.distributed as dist
+        box = [uid]
+        dist.broadcast_object_list(box, src=0)
+        uid = box[0]
+    ctx = hz.Context(rank, world, uid, group, local)
+    model = Model(hz, ctx, torch, args.config, rank, world, args, device)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(max(args.warmup, 3)):
+        model.step(stream)
+    torch.cuda.synchronize()
+
+    per_step_kernels = 5 * len(model.tensors)
+    hz.trace_begin(capacity=(args.steps + 1) * per_step_kernels * 4 + 64)
+    sampler = ClockSampler([local] if world == 1 else range(world)) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        model.step(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    hz.trace_end()
+    clocks = sampler.stop() if sampler else None
+    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(ms, world)
+    ms_per_step = ms / args.steps
+    recs = hz.trace_read()
+    stages = summarize_trace(recs, args.steps)
+    gpu_launches = sum(1 for r in recs if r["kind"] in KERNEL_KINDS)
+    value = world * model.logical_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # roofline: the kernel kind with the largest share of device time
+    peak, peak_src = measured_peaks()
+    kern = {k: v for k, v in stages.items() if k in KERNEL_KINDS}
+    dom = max(kern, key=lambda k: kern[k]["share"])
+    d = kern[dom]
+    traffic = None
+    tr = ncu_traffic().get(dom)
+    if tr and tr.get("elems"):
+        traffic = tr["dram_bytes"] / tr["elems"] * d["avg_elems"]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
+                "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes_per_launch": d["avg_bytes"],
+                "avg_launch_ms": d["avg_ms"], "peak_source": peak_src}
+    nccl = {k: v for k, v in stages.items() if k.startswith("nccl")}
+    for v in nccl.values():
+        v["frac_of_nvlink_770"] = (v["GBps"] or 0) / NVLINK_PEER_GBS
+
+    # flat ZeRO-3 baseline on the same logical bytes (context, not timed with the step)
+    flat = None
+    if world > 1 and not args.no_flat:
+        flat = flat_baseline(hz, ctx, torch, model, stream, world, args)
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(hz, ctx, torch, model, stream, world, args)
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, group, model)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded torch.Generator on device: params N(0,0.02^2), grads N(0,1e-6) with 1/1024 x64 outliers)",
+        "config": {
+            "workload": f"{args.config}: {len(model.tensors)} flat per-tensor buffers ({model.logical_bytes // 6:,} params), "
+                        f"setting T (w=1, s=1, gl=L), GA=1",
+            "hierarchy": list(group), "block": args.block, "qwz_bits": args.qwz_bits, "qgz_bits": args.qgz_bits,
+            "io": "bf16 params/grads in, bf16 gathered layers out, fp32 scales, fp32 gradient shard",
+            "l2": "inputs larger than L2 (each step streams several GB); no flush",
+            "parallelism": f"dp{world} hierarchical ({'x'.join(map(str, group))})",
+        },
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": gpu_launches,
+        "clocks": clocks,
+        "stages": stages,
+        "flat_zero3_baseline": flat,
+    }
+    ctx.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def flat_baseline(hz, ctx, torch, model, stream, world, args):
+    """Plain NCCL bf16 all-gather (x2) + reduce-scatter on the world communicator over the
+    same tensors: the ZeRO-3 rows of Tables VII/VIII."""
+    bufs = []
+    for t in model.tensors:
+        Np = t["p"].padded_numel
+        bufs.append((torch.empty(Np // world, dtype=torch.bfloat16, device=t["grad"].device), t["grad"],
+                     torch.empty(Np // world, dtype=torch.bfloat16, device=t["grad"].device)))
+
+    def step():
+        for chunk, g, _ in bufs:
+            ctx.flat_allgather(chunk, model.full[0][:g.numel()], stream=stream)
+        for chunk, g, rs in reversed(bufs):
+            ctx.flat_allgather(chunk, model.full[1][:g.numel()], stream=stream)
+            ctx.flat_reduce_scatter(g, rs, stream=stream)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    n = max(1, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(n):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world) / n
+    return {"ms_per_step": ms, "value": world * model.logical_bytes / (ms * 1e-3) / 1e9, "unit": UNIT,
+            "what": "ncclAllGather x2 + ncclReduceScatter, bf16, world communicator"}
+
+
+def run_e2e(hz, ctx, torch, model, stream, world, args):
+    """Same step through the public API with inputs copied from pinned host memory each
+    step (primary + gradient per tensor) and the fp32 gradient shards read back."""
+    maxw = max(t["primary"].numel() for t in model.tensors)
+    maxg = max(t["grad"].numel() for t in model.tensors)
+    maxs = max(t["shard"].numel() for t in model.tensors)
+    hp = torch.empty(maxw, dtype=torch.bfloat16, pin_memory=True)
+    hg = torch.empty(maxg, dtype=torch.bfloat16, pin_memory=True)
+    hs = torch.empty(maxs, dtype=torch.float32, pin_memory=True)
+    # the host copies hold the same data as the device-resident inputs
+    hp[:model.tensors[0]["primary"].numel()].copy_(model.tensors[0]["primary"])
+    hg[:model.tensors[0]["grad"].numel()].copy_(model.tensors[0]["grad"])
+    bits = args.qwz_bits
+    h2d = sum(t["primary"].numel() * 2 + t["grad"].numel() * 2 for t in model.tensors)
+    d2h = sum(t["shard"].numel() * 4 for t in model.tensors)
+
+    def step():
+        for i, t in enumerate(model.tensors):
+            t["primary"].copy_(hp[:t["primary"].numel()], non_blocking=True)
+            model.ctx.allgather_params(t["p"], t["primary"], t["sec_c"], t["sec_s"], model.full[i & 1],
+                                       bits=bits, stream=stream)
+        for i, t in reversed(list(enumerate(model.tensors))):
+            t["grad"].copy_(hg[:t["grad"].numel()], non_blocking=True)
+            model.ctx.allgather_params(t["p"], None, t["sec_c"], t["sec_s"], model.full[i & 1], bits=bits,
+                                       backward=True, stream=stream)
+            model.ctx.reduce_scatter_grads(t["p"], t["grad"], t["shard"], model.bits, stream=stream)
+            hs[:t["shard"].numel()].copy_(t["shard"], non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    barrier(world)
+    n = max(1, min(args.steps, 5))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world) / n
+    return {"value": world * model.logical_bytes / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+
+# ------------------------------------------------------------------ CPU oracle
+def _host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"affinity_cores": len(os.sched_getaffinity(0)), "cpu_count": os.cpu_count(), "cpu_model": model}
+
+
+def _oracle_layer(g, numel, seed, args):
+    """Inputs of one tensor for all W simulated ranks, then the timed oracle step."""
+    import ml_dtypes
+    import numpy as np
+    from oracle import collectives as col
+    from oracle import partition as pm
+    from paper_2501_04266_b200 import synth
+    W = pm.world_of(g)
+    L = len(g)
+    B = args.block
+    Np = pm.padded_numel(numel, g, B)
+    full = np.zeros(Np, np.float32)
+    full[:numel] = synth.params_like(numel, seed, block=B, specials=False)
+    full = full.astype(ml_dtypes.bfloat16)
+    prim = {}
+    for r in range(W):
+        off, ln = pm.range_at(r, g, Np, 1)
+        prim[r] = full[off:off + ln]
+    grads = {}
+    for r in range(W):
+        x = np.zeros(Np, np.float32)
+        x[:numel] = synth.gradient_like(numel, seed + 1 + r, block=B, specials=False)
+        grads[r] = x.astype(ml_dtypes.bfloat16)
+    bpl = {l: args.qgz_bits for l in range(1, L + 1)}
+    t0 = time.perf_counter()
+    _, sec = col.allgather_forward(prim, g, Np, B, 1, 1, bits=args.qwz_bits)
+    col.allgather_backward(sec, g, Np, B, 1, bits=args.qwz_bits)
+    col.reduce_scatter(grads, g, Np, B, 1, L, bpl)
+    return time.perf_counter() - t0, W * 6 * numel
+
+
+def cpu_baseline(args, group, model):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from paper_2501_04266_b200 import synth
+    numel = synth.layer_numel(synth.GPT_CONFIGS[args.config]["hidden"])
+    secs, byts = 0.0, 0
+    n = max(1, args.cpu_sample_layers)
+    for i in range(n):
+        s, b = _oracle_layer(group, numel, 31 + i, args)
+        secs += s
+        byts += b
+    info = _host_info()
+    return {"value": byts / secs / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n} tensors of {numel:,} params ({args.config} layer size), all {math.prod(group)} simulated "
+                      f"rank(s) of hierarchy {list(group)}: fwd+bwd qwZ all-gather + qgZ reduce-scatter, NumPy "
+                      f"single thread; {secs:.1f} s",
+            **info}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, on this arm's config / metric, each step
+    a bounded sample (one tensor split over the N simulated ranks).  Rank 0 only."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2501_04266_b200 import synth
+    n = args.gpus
+    group = HIERARCHY[args.config][n]
+    numel = synth.layer_numel(synth.GPT_CONFIGS[args.config]["hidden"])
+    numel = max(1, numel // n)
+    for i in range(max(args.warmup, 3)):
+        _oracle_layer(group, min(numel, 1 << 20), 100 + i, args)
+    secs, byts = 0.0, 0
+    for i in range(args.steps):
+        s, b = _oracle_layer(group, numel, 200 + i, args)
+        secs += s
+        byts += b
+    value = byts / secs / 1e9
+    info = _host_info()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded numpy)",
+        "config": {"workload": f"{args.config}: per step one tensor of {numel:,} params per simulated rank "
+                               f"(layer size / N), setting T, GA=1",
+                   "hierarchy": list(group), "block": args.block, "qwz_bits": args.qwz_bits,
+                   "qgz_bits": args.qgz_bits},
+        "cpu_baseline": {"value": value, "unit": UNIT, "kind": "oracle", "cores": 1,
+                         "sample": f"{args.steps} steps x {numel:,} params x {n} simulated ranks", **info},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_hz(args)
+
+
+if __name__ == "__main__":
+    main()

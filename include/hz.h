@@ -1,0 +1,235 @@
+/*
+ * hz.h — C ABI of libhz.so: the data-parallel hot path of hierarchical ZeRO++
+ * (arXiv 2501.04266, "Scaling Large Language Model Training on Frontier with
+ * Low-Bandwidth Partitioning") for NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:<n> = line n of the paper's PAPER.md; S:<n> = line n of SPEC.md;
+ * O<k>/R<k> = oracle step / reading, listed in DESIGN.md §3.
+ *
+ * What the library computes (per layer, per rank):
+ *   - qwZ: block-quantize the rank's primary bf16/fp16/fp32 weight shard to
+ *     int8 codes + one fp32 scale per block, all-gather the
+ *     codes level by level inside the hierarchy (Table VII),
+ *     keep the quantized secondary partition (hpZ, Table V) and
+ *     dequantize the full layer.  Backward: gather again from the secondary.
+ *   - qgZ: block-quantize the gradient to int4/int8 and reduce-scatter it as a
+ *     hierarchical all-to-all, dequantizing and summing at each level
+ *     (Table VIII), ending in an fp32 gradient shard.
+ *
+ * Hierarchy: g = (g_1..g_L), innermost level first, prod(g) = world.  Ranks are
+ * numbered node-major: r = sum_l d_l(r) * prod_{k<l} g_k (O1).  Level l's
+ * exchange group = the g_l ranks that differ only in digit d_l.  A level may
+ * have g_l = 1 (no exchange; a one-GPU run uses g = (1)).
+ *
+ * Ownership map (O3, "digit-reversed"): off_0 = 0, len_0 = Np;
+ * len_l = len_{l-1}/g_l, off_l = off_{l-1} + d_l*len_l.  Role levels:
+ * primary weights = range_w, secondary = range_s, gradient = range_gl,
+ * optimizer = range_L.  Nesting range_L c range_gl c range_w is the paper's
+ * dependency rule N >= N_os >= N_g >= N_w.
+ *
+ * Codec (O4-O6, readings R1-R5): blocks of `block` contiguous elements;
+ *   am = max|x|; am < 2^-100 -> scale 0, codes 0; else
+ *   scale = fl32(am/qmax), inv = fl32(qmax/am),
+ *   code = clamp(rne(fl32(x*inv)), -qmax, qmax), qmax = 127 (int8) / 7 (int4);
+ *   x_hat = fl32(code*scale); bf16/fp16 output = RNE(x_hat).
+ *   Reduction (O9): acc = x_hat_0; acc = fl32(acc + x_hat_p) for p = 1..g-1 in
+ *   ascending level digit (no FMA); accumulate: A = fl32(A + acc).
+ * Code layout: one codes array (int8: 1 byte/element, two's complement;
+ * int4: 2 elements/byte, even element in the low nibble) and one fp32 scales
+ * array, block k at index k ("SoA").  Every level chunk is therefore a
+ * contiguous slice of both arrays.
+ *
+ * Conventions for every entry point:
+ *   - Device pointers are CUDA device (or managed) pointers on the current /
+ *     context device; they must be 16-byte aligned.  The caller allocates and
+ *     owns every pointer it passes; the library owns its NCCL communicators and
+ *     internal workspace (grown on first use to the largest layer seen; the
+ *     growth call synchronises the device, so do one warm-up call per size).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     All device work is enqueued on it; calls return once enqueued
+ *     (asynchronous).  Host-side validation is synchronous.
+ *   - Return value: HZ_OK, or an error code with a message naming the offending
+ *     argument available from hz_last_error() (thread-local).  Nothing is
+ *     enqueued when validation fails.
+ *   - Collective calls (hz_init, hz_allgather_params, hz_reduce_scatter_grads,
+ *     hz_finalize) must be issued by every rank in the same order (NCCL rule).
+ *   - Non-finite inputs are a precondition violation; results are
+ *     unspecified for them.
+ */
+#ifndef HZ_H_
+#define HZ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define HZ_API __attribute__((visibility("default")))
+#else
+#define HZ_API
+#endif
+
+#define HZ_MAX_LEVELS 4
+
+typedef struct hz_ctx hz_ctx; /* opaque: device, NCCL comms per level, workspace */
+
+typedef enum {
+  HZ_OK = 0,
+  HZ_ERR_INVALID = 1,     /* bad argument; message names the field */
+  HZ_ERR_CUDA = 2,        /* CUDA runtime / launch error */
+  HZ_ERR_NCCL = 3,        /* NCCL error (incl. asynchronous errors of earlier calls) */
+  HZ_ERR_NONFINITE = 4,   /* reserved for debug builds */
+  HZ_ERR_UNSUPPORTED = 5  /* valid request this build does not implement */
+} hz_status;
+
+typedef enum { HZ_F32 = 0, HZ_BF16 = 1, HZ_F16 = 2 } hz_dtype;
+
+typedef struct { unsigned char bytes[128]; } hz_uid; /* = ncclUniqueId */
+
+/* Per-rank partition of one flat per-layer buffer (O1-O3). */
+typedef struct {
+  int64_t numel;         /* logical element count n */
+  int64_t padded_numel;  /* Np = ceil(n / (world*4*block)) * world*4*block (O2, zero pad) */
+  int32_t block;         /* quantization block B */
+  int32_t levels;        /* L */
+  int32_t world;         /* prod(group) */
+  int32_t rank;
+  int32_t w, s, gl;      /* role levels: primary, secondary, gradient (0..L) */
+  int32_t group[HZ_MAX_LEVELS];  /* g_l, l = 1..L at index l-1 */
+  int32_t digit[HZ_MAX_LEVELS];  /* d_l(rank) at index l-1 */
+  int64_t off[HZ_MAX_LEVELS + 1];/* off_l, l = 0..L (elements) */
+  int64_t len[HZ_MAX_LEVELS + 1];/* len_l, l = 0..L (elements) */
+} hz_partition_t;
+
+/* Library version string, e.g. "hz 0.1 sm_100a". Never NULL. */
+HZ_API const char* hz_version(void);
+
+/* Message of the last non-OK status returned on this thread ("" if none). */
+HZ_API const char* hz_last_error(void);
+
+/* Number of exported entry points and their names (for ABI checks). */
+HZ_API int hz_num_symbols(void);
+HZ_API const char* hz_symbol_name(int i);
+
+/* ---------------------------------------------------------------- host only */
+
+/* O1-O3 (Table IV).  Pure host function; needs no GPU.
+ * rank in [0, prod(group)); levels in [1, HZ_MAX_LEVELS]; group[l] >= 1;
+ * numel >= 0; block a power of two in [32, 2048]; 0 <= w, s, gl <= levels.
+ * Writes *out.  Errors: HZ_ERR_INVALID. */
+HZ_API hz_status hz_partition_ex(int rank, int levels, const int* group, int64_t numel,
+                          int block, int w, int s, int gl, hz_partition_t* out);
+
+/* ------------------------------------------------------- standalone codec ops */
+
+/* O4: quantize x[0..n) (dtype dt) into codes (n*bits/8
+ * bytes) and scales (n/block fp32).  n % block == 0; bits in {4, 8};
+ * block a power of two in [32, 2048].  n == 0 is a no-op. */
+HZ_API hz_status hz_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block,
+                      uint8_t* codes, float* scales, void* stream);
+
+/* O6: y[0..n) = dtype(out_dt)(fl32(code * scale)); same constraints as hz_quantize. */
+HZ_API hz_status hz_dequantize(const uint8_t* codes, const float* scales, int64_t n, int bits,
+                        int block, void* y, hz_dtype out_dt, void* stream);
+
+/* O9 level step (A9): g inputs (host array of g device pointer pairs, input p =
+ * the chunk from the member with level digit p, each n elements coded with
+ * bits_in), summed in ascending p in fp32 without FMA.  Exactly one output:
+ *   bits_out in {4, 8}: requantize the sum into out_codes / out_scales (the
+ *                       next level's send layout = this chunk's SoA arrays);
+ *   bits_out == 0:      write fp32 out_f32[0..n) (accumulate != 0: += ).
+ * 1 <= g <= 16. */
+HZ_API hz_status hz_reduce_chunks(int g, const uint8_t* const* codes, const float* const* scales,
+                           int64_t n, int bits_in, int block, int bits_out,
+                           uint8_t* out_codes, float* out_scales, float* out_f32,
+                           int accumulate, void* stream);
+
+/* ------------------------------------------------------------- collectives */
+
+/* A fresh ncclUniqueId; call on one rank and broadcast the 128 bytes. */
+HZ_API hz_status hz_get_uid(hz_uid* out);
+
+/* Collective over all `world` ranks.  Selects `cuda_device`, creates the world
+ * NCCL communicator and, with ncclCommSplit(color = rank - d_l*stride_l,
+ * key = d_l), one communicator per level with g_l > 1.  levels in
+ * [1, HZ_MAX_LEVELS], prod(group) == world.  workspace_bytes: optional
+ * pre-reservation (0 = grow on first use).  *out owns everything it creates. */
+HZ_API hz_status hz_init(hz_ctx** out, int rank, int world, const hz_uid* uid, int levels,
+                  const int* group, int cuda_device, size_t workspace_bytes);
+
+/* Destroys the communicators and frees the workspace.  NULL is a no-op. */
+HZ_API hz_status hz_finalize(hz_ctx* ctx);
+
+/* hz_partition_ex for the context's rank and hierarchy. */
+HZ_API hz_status hz_partition(const hz_ctx* ctx, int64_t numel, int block, int w, int s, int gl,
+                       hz_partition_t* out);
+
+/* qwZ + hpZ all-gather (O7 forward, O8 backward; Table VII).
+ *   backward == 0: quantize primary (dt[len_w], the rank's range_w; NULL not
+ *     allowed) with `bits`, all-gather levels w..1 (in place, per level
+ *     communicator), write the secondary codes/scales of range_s to
+ *     sec_codes (len_s*bits/8 bytes) / sec_scales (len_s/block fp32), and
+ *     dequantize all of [0, Np) into full_out (out_dt[Np]).
+ *   backward != 0: primary ignored (may be NULL); all-gather from the
+ *     secondary over levels s..1 and dequantize into full_out.  The result is
+ *     bitwise equal to the forward result (O8).
+ * Padding elements [numel, Np) of the primary must be zero (O2). */
+HZ_API hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward,
+                              const void* primary, hz_dtype dt, int bits,
+                              uint8_t* sec_codes, float* sec_scales,
+                              void* full_out, hz_dtype out_dt, void* stream);
+
+/* qgZ hierarchical all-to-all reduce-scatter (O9; Table VIII).
+ * grad: dt[len_{from_level-1}] over the rank's range_{from_level-1}
+ *   (from_level == 1: the full padded gradient dt[Np]).
+ * Levels from_level..to_level (1 <= from <= to <= L) run in order; level l
+ * quantizes with bits_per_level[l-1] in {4, 8}, exchanges chunks with the g_l-1
+ * peers (grouped ncclSend/ncclRecv; the self chunk never enters NCCL), and
+ * dequantizes + sums (+ requantizes for the next level).
+ * shard: fp32[len_to_level] over range_to_level; accumulate != 0: shard += sum.
+ * Setting T (the paper's ZeRO-topo): per micro-batch from=1, to=gl with
+ * accumulate; once per step from=gl+1, to=L on the accumulated shard. */
+HZ_API hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const void* grad,
+                                  hz_dtype dt, int from_level, int to_level,
+                                  const int* bits_per_level, float* shard, int accumulate,
+                                  void* stream);
+
+/* Flat ZeRO-3 baseline (Table VII/VIII row "ZeRO-3"): plain ncclAllGather of
+ * the rank's bf16/fp16/fp32 chunk (numel/world elements, rank order) into
+ * out[numel], and plain ncclReduceScatter(sum) of in[numel] into
+ * out_chunk[numel/world].  numel % world == 0. */
+HZ_API hz_status hz_flat_allgather(hz_ctx* ctx, const void* chunk, void* out, int64_t numel,
+                            hz_dtype dt, void* stream);
+HZ_API hz_status hz_flat_reduce_scatter(hz_ctx* ctx, const void* in, void* out_chunk,
+                                 int64_t numel, hz_dtype dt, void* stream);
+
+/* ------------------------------------------------------------------ tracing */
+
+/* Per-launch device timing of the library's own work (CUDA events around each
+ * kernel / NCCL group on its stream).  hz_trace_begin(cap) starts recording up
+ * to cap records (process-wide); hz_trace_end() stops.  hz_trace_read
+ * synchronises the recorded events and copies up to max records.  kind is a
+ * static string ("quantize", "dequantize", "reduce", "reduce_requant",
+ * "nccl_allgather", "nccl_alltoall", "nccl_flat", "copy"). bytes = algorithmic
+ * HBM bytes (kernels) or bytes sent per rank (NCCL). */
+typedef struct {
+  const char* kind;
+  int32_t level;
+  int32_t bits;
+  int64_t elems;
+  int64_t bytes;
+  float ms;
+} hz_trace_rec;
+
+HZ_API hz_status hz_trace_begin(int capacity);
+HZ_API hz_status hz_trace_end(void);
+HZ_API hz_status hz_trace_read(hz_trace_rec* out, int max, int* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HZ_H_ */

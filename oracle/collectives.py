@@ -134,6 +134,23 @@ def allgather_backward(secondary, g, Np, block, s, bits=8, out="bf16", ledger=No
     return {r: _materialise(held[r], bits, block, out) for r in range(W)}
 
 
+def reduce_coded(coded, block, bits_out=None, accum=None):
+    """A9, one level step for one rank: dequantize the received chunks (list over the
+    sending members in ascending level digit of (codes, scales)) and sum them in that
+    order in fp32, one rounding per add (R10).  Then either requantize the sum for the
+    next level (bits_out 4/8, returns (codes, scales)), or return the fp32 sum,
+    added to ``accum`` when given (A10: A = fl(A + P))."""
+    acc = None
+    for codes, scales in coded:
+        xh = quant.dequantize(codes, scales, block, out="f32")
+        acc = xh.copy() if acc is None else (acc + xh).astype(np.float32)
+    if bits_out:
+        return quant.quantize(acc, bits_out, block)
+    if accum is not None:
+        return (np.asarray(accum, np.float32) + acc).astype(np.float32)
+    return acc
+
+
 def reduce_scatter(inputs, g, Np, block, from_level, to_level, bits_per_level,
                    accum=None, ledger=None, trace=None):
     """O9: hierarchical quantized all-to-all reduce-scatter (qgZ).
@@ -154,17 +171,16 @@ def reduce_scatter(inputs, g, Np, block, from_level, to_level, bits_per_level,
             members = exchange_group(r, g, level)
             d = digits(r, g)[level - 1]
             _, ln = range_at(r, g, Np, level)
-            acc = None
-            scales_used = []
-            for m in members:                                            # ascending d_l (R10)
-                chunk = P[m][d * ln:(d + 1) * ln]                        # member m's chunk for r
-                if bits is None:
-                    xh = chunk
-                else:
-                    c, sc = quant.quantize(chunk, bits, block)           # A7 / requant (R11)
-                    xh = quant.dequantize(c, sc, block, out="f32")       # A9
-                    scales_used.append(sc)
-                acc = xh.copy() if acc is None else (acc + xh).astype(np.float32)
+            chunks = [P[m][d * ln:(d + 1) * ln] for m in members]       # member m's chunk for r
+            if bits is None:
+                acc = None
+                for xh in chunks:                                        # ascending d_l (R10)
+                    acc = xh.copy() if acc is None else (acc + xh).astype(np.float32)
+                scales_used = []
+            else:
+                coded = [quant.quantize(ch, bits, block) for ch in chunks]   # A7 / requant (R11)
+                acc = reduce_coded(coded, block)                          # A9
+                scales_used = [sc for _, sc in coded]
             new[r] = acc
             if trace is not None:
                 trace[(level, r)] = scales_used

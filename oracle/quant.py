@@ -71,7 +71,7 @@ def quantize(x, bits, block):
 
 
 def dequantize(codes, scales, block, out="f32"):
-    """O6.  x_hat = fl32(code * scale); out in {"f32", "bf16"} (bf16 = RNE)."""
+    """O6.  x_hat = fl32(code * scale); out in {"f32", "bf16", "f16"} (RNE narrowing)."""
     c = np.asarray(codes).astype(np.float32).reshape(-1, block)
     s = np.asarray(scales, dtype=np.float32)
     xh = (c * s[:, None]).astype(np.float32).reshape(-1)
@@ -79,6 +79,8 @@ def dequantize(codes, scales, block, out="f32"):
         return xh
     if out == "bf16":
         return xh.astype(ml_dtypes.bfloat16)
+    if out == "f16":
+        return xh.astype(np.float16)                     # IEEE RNE
     raise ValueError(out)
 
 

@@ -1,0 +1,455 @@
+// Level engine: NCCL communicators per hierarchy level and the two collectives of
+// the hot path, stream-ordered on the caller's stream.
+//
+//   hz_allgather_params     qwZ + hpZ (O7/O8): Table VII
+//   hz_reduce_scatter_grads qgZ (O9):          P:122, Table VIII
+//   hz_flat_*               the ZeRO-3 baseline rows of Tables VII/VIII
+//
+// Communicators: one world communicator plus, for every level l with g_l > 1,
+// ncclCommSplit(world, color = rank - d_l*stride_l, key = d_l): the level-l
+// exchange group, whose communicator rank equals the level digit d_l.  On one
+// NVSwitch box every level runs over NVLink at the same per-GPU bandwidth; the
+// hierarchy saves bytes ((g_l-1)/g_l of a shrinking range per level) and peers.
+//
+// All-gather: codes and scales live in two SoA arrays indexed by global element
+// / block, so the level-l gather concatenating the group's range_l pieces into
+// range_{l-1} is an in-place ncclAllGather on both arrays (one NCCL group).
+// Reduce-scatter: the level-l send buffer is the SoA code of range_{l-1}; chunk j
+// (= destination digit j) is a contiguous slice of both arrays, so the
+// all-to-all is grouped ncclSend/ncclRecv of slices; the own chunk is read in
+// place by the reduce kernel and never enters NCCL.
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "hz_internal.h"
+
+struct hz_ctx {
+  int rank = 0, world = 1, levels = 0, device = 0;
+  int group[HZ_MAX_LEVELS] = {0};
+  int digit[HZ_MAX_LEVELS] = {0};
+  ncclComm_t world_comm = nullptr;
+  ncclComm_t lvl[HZ_MAX_LEVELS] = {nullptr};
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  Buf ag_c, ag_s;                      // full-layer codes / scales (all-gather)
+  Buf rs_a_c, rs_a_s, rs_b_c, rs_b_s;  // ping-pong send buffers (reduce-scatter)
+  Buf rs_r_c, rs_r_s;                  // receive slots (reduce-scatter)
+};
+
+namespace hz {
+namespace {
+
+hz_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(HZ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+hz_status nccl_fail(ncclResult_t r, const char* what) {
+  return fail(HZ_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+#define HZ_NCCL(call, what)                     \
+  do {                                          \
+    ncclResult_t r_ = (call);                   \
+    if (r_ != ncclSuccess) return nccl_fail(r_, what); \
+  } while (0)
+
+#define HZ_CUDA(call, what)                     \
+  do {                                          \
+    cudaError_t e_ = (call);                    \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+hz_status grow(hz_ctx::Buf& b, size_t need) {
+  if (need <= b.cap) return HZ_OK;
+  const size_t gran = size_t(2) << 20;
+  const size_t cap = (need + gran - 1) / gran * gran;
+  if (b.p) {
+    HZ_CUDA(cudaDeviceSynchronize(), "workspace growth: cudaDeviceSynchronize");
+    HZ_CUDA(cudaFree(b.p), "workspace growth: cudaFree");
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  HZ_CUDA(cudaMalloc(&b.p, cap), "workspace growth: cudaMalloc");
+  b.cap = cap;
+  return HZ_OK;
+}
+
+void free_buf(hz_ctx::Buf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+hz_status check_async(const hz_ctx* ctx) {
+  ncclResult_t r = ncclSuccess;
+  if (ctx->world_comm && ncclCommGetAsyncError(ctx->world_comm, &r) == ncclSuccess &&
+      r != ncclSuccess && r != ncclInProgress)
+    return nccl_fail(r, "asynchronous NCCL error from an earlier call");
+  return HZ_OK;
+}
+
+hz_status check_partition(const hz_ctx* ctx, const hz_partition_t* p) {
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  if (!p) return fail(HZ_ERR_INVALID, "p: NULL");
+  if (p->rank != ctx->rank || p->world != ctx->world || p->levels != ctx->levels)
+    return fail(HZ_ERR_INVALID, "p: partition was not made for this context (rank/world/levels)");
+  for (int l = 0; l < ctx->levels; ++l)
+    if (p->group[l] != ctx->group[l]) return fail(HZ_ERR_INVALID, "p: group sizes differ from the context");
+  if (!block_ok(p->block)) return fail(HZ_ERR_INVALID, "p.block: must be a power of two in [32, 2048]");
+  if (p->padded_numel % (int64_t(p->world) * 4 * p->block))
+    return fail(HZ_ERR_INVALID, "p.padded_numel: not a multiple of world*4*block");
+  return HZ_OK;
+}
+
+int64_t elem_bytes(hz_dtype dt) { return dt == HZ_F32 ? 4 : 2; }
+
+bool dtype_ok(hz_dtype dt) { return dt == HZ_F32 || dt == HZ_BF16 || dt == HZ_F16; }
+
+ncclDataType_t nccl_dtype(hz_dtype dt) {
+  return dt == HZ_F32 ? ncclFloat32 : (dt == HZ_BF16 ? ncclBfloat16 : ncclFloat16);
+}
+
+// traced kernel launches ----------------------------------------------------
+hz_status run_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block, uint8_t* c,
+                       float* s, cudaStream_t st, int level) {
+  TraceScope t(st, "quantize", level, bits, n, n * elem_bytes(dt) + code_bytes(n, bits) + n / block * 4);
+  cudaError_t e = launch_quantize(x, dt, n, bits, block, c, s, st);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "quantize kernel launch");
+  return HZ_OK;
+}
+
+hz_status run_dequantize(const uint8_t* c, const float* s, int64_t n, int bits, int block, void* y,
+                         hz_dtype odt, cudaStream_t st, int level) {
+  TraceScope t(st, "dequantize", level, bits, n, code_bytes(n, bits) + n / block * 4 + n * elem_bytes(odt));
+  cudaError_t e = launch_dequantize(c, s, n, bits, block, y, odt, st);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "dequantize kernel launch");
+  return HZ_OK;
+}
+
+hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
+                     int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
+                     cudaStream_t st, int level) {
+  const int64_t in_bytes = g * (code_bytes(n, bits_in) + n / block * 4);
+  const int64_t out_bytes =
+      bits_out ? code_bytes(n, bits_out) + n / block * 4 : n * 4 * (acc ? 2 : 1);
+  TraceScope t(st, bits_out ? "reduce_requant" : "reduce", level, bits_in, n, in_bytes + out_bytes);
+  cudaError_t e = launch_reduce(g, c, s, n, bits_in, block, bits_out, oc, os, of, acc, st);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
+  return HZ_OK;
+}
+
+hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0 || dst == src) return HZ_OK;
+  TraceScope t(st, "copy", 0, 0, 0, int64_t(bytes) * 2);
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync");
+  return HZ_OK;
+}
+
+}  // namespace
+}  // namespace hz
+
+extern "C" {
+
+hz_status hz_get_uid(hz_uid* out) {
+  using namespace hz;
+  if (!out) return fail(HZ_ERR_INVALID, "out: NULL");
+  static_assert(sizeof(ncclUniqueId) == sizeof(hz_uid), "hz_uid must be an ncclUniqueId");
+  ncclUniqueId id;
+  HZ_NCCL(ncclGetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out->bytes, &id, sizeof(id));
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_init(hz_ctx** out, int rank, int world, const hz_uid* uid, int levels,
+                  const int* group, int cuda_device, size_t workspace_bytes) {
+  using namespace hz;
+  if (!out) return fail(HZ_ERR_INVALID, "out: NULL");
+  *out = nullptr;
+  if (!uid) return fail(HZ_ERR_INVALID, "uid: NULL");
+  if (!group) return fail(HZ_ERR_INVALID, "group: NULL");
+  if (levels < 1 || levels > HZ_MAX_LEVELS) return fail(HZ_ERR_INVALID, "levels: must be in [1, 4]");
+  int64_t prod = 1;
+  for (int l = 0; l < levels; ++l) {
+    if (group[l] < 1) return fail(HZ_ERR_INVALID, "group[" + std::to_string(l) + "]: must be >= 1");
+    prod *= group[l];
+  }
+  if (world < 1 || prod != world) return fail(HZ_ERR_INVALID, "group: product must equal world");
+  if (rank < 0 || rank >= world) return fail(HZ_ERR_INVALID, "rank: must be in [0, world)");
+  if (cuda_device < 0) return fail(HZ_ERR_INVALID, "cuda_device: negative");
+  HZ_CUDA(cudaSetDevice(cuda_device), "cudaSetDevice");
+
+  hz_ctx* ctx = new hz_ctx();
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->levels = levels;
+  ctx->device = cuda_device;
+  ncclUniqueId id;
+  std::memcpy(&id, uid->bytes, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&ctx->world_comm, world, id, rank);
+  if (r != ncclSuccess) {
+    delete ctx;
+    return nccl_fail(r, "ncclCommInitRank");
+  }
+  int stride = 1;
+  for (int l = 0; l < levels; ++l) {
+    ctx->group[l] = group[l];
+    ctx->digit[l] = (rank / stride) % group[l];
+    if (group[l] > 1) {
+      const int color = rank - ctx->digit[l] * stride;
+      r = ncclCommSplit(ctx->world_comm, color, ctx->digit[l], &ctx->lvl[l], nullptr);
+      if (r != ncclSuccess) {
+        hz_finalize(ctx);
+        return nccl_fail(r, "ncclCommSplit");
+      }
+    }
+    stride *= group[l];
+  }
+  if (workspace_bytes) {
+    hz_status st = grow(ctx->ag_c, workspace_bytes);
+    if (st != HZ_OK) {
+      hz_finalize(ctx);
+      return st;
+    }
+  }
+  *out = ctx;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_finalize(hz_ctx* ctx) {
+  using namespace hz;
+  if (!ctx) return HZ_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (int l = 0; l < HZ_MAX_LEVELS; ++l)
+    if (ctx->lvl[l]) ncclCommDestroy(ctx->lvl[l]);
+  if (ctx->world_comm) ncclCommDestroy(ctx->world_comm);
+  for (auto* b : {&ctx->ag_c, &ctx->ag_s, &ctx->rs_a_c, &ctx->rs_a_s, &ctx->rs_b_c, &ctx->rs_b_s,
+                  &ctx->rs_r_c, &ctx->rs_r_s})
+    free_buf(*b);
+  delete ctx;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_partition(const hz_ctx* ctx, int64_t numel, int block, int w, int s, int gl,
+                       hz_partition_t* out) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  return partition(ctx->rank, ctx->levels, ctx->group, numel, block, w, s, gl, out);
+}
+
+hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward,
+                              const void* primary, hz_dtype dt, int bits, uint8_t* sec_codes,
+                              float* sec_scales, void* full_out, hz_dtype out_dt, void* stream) {
+  using namespace hz;
+  hz_status st0 = check_partition(ctx, p);
+  if (st0 != HZ_OK) return st0;
+  if (!bits_ok(bits)) return fail(HZ_ERR_INVALID, "bits: must be 4 or 8");
+  if (!dtype_ok(out_dt)) return fail(HZ_ERR_INVALID, "out_dt: unknown dtype");
+  if (!backward && !dtype_ok(dt)) return fail(HZ_ERR_INVALID, "dt: unknown dtype");
+  if (!backward && (!primary || !aligned16(primary)))
+    return fail(HZ_ERR_INVALID, "primary: NULL or not 16-byte aligned");
+  if (!sec_codes || !aligned16(sec_codes)) return fail(HZ_ERR_INVALID, "sec_codes: NULL or not 16-byte aligned");
+  if (!sec_scales || !aligned16(sec_scales)) return fail(HZ_ERR_INVALID, "sec_scales: NULL or not 16-byte aligned");
+  if (!full_out || !aligned16(full_out)) return fail(HZ_ERR_INVALID, "full_out: NULL or not 16-byte aligned");
+  st0 = check_async(ctx);
+  if (st0 != HZ_OK) return st0;
+
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t Np = p->padded_numel;
+  const int B = p->block;
+  const int w = p->w, s = p->s;
+  if (Np == 0) {
+    clear_error();
+    return HZ_OK;
+  }
+  hz_status rc;
+  if ((rc = grow(ctx->ag_c, code_bytes(Np, bits))) != HZ_OK) return rc;
+  if ((rc = grow(ctx->ag_s, Np / B * 4)) != HZ_OK) return rc;
+  uint8_t* ws_c = static_cast<uint8_t*>(ctx->ag_c.p);
+  float* ws_s = static_cast<float*>(ctx->ag_s.p);
+
+  const uint8_t* cur_c;
+  const float* cur_s;
+  int top;
+  if (!backward) {
+    // A2: quantize the primary range_w.  With s == w the quantized primary IS the
+    // secondary (setting T, sec-degree = primary degree), so write it there.
+    uint8_t* qc = s == w ? sec_codes : ws_c + code_bytes(p->off[w], bits);
+    float* qs = s == w ? sec_scales : ws_s + p->off[w] / B;
+    if ((rc = run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w)) != HZ_OK) return rc;
+    if (s > w) {   // A4, s > w: the secondary is a sub-slice of the own quantized primary
+      const int64_t rel = p->off[s] - p->off[w];
+      if ((rc = copy_async(sec_codes, qc + code_bytes(rel, bits), code_bytes(p->len[s], bits), st)) != HZ_OK) return rc;
+      if ((rc = copy_async(sec_scales, qs + rel / B, p->len[s] / B * 4, st)) != HZ_OK) return rc;
+    }
+    cur_c = qc;
+    cur_s = qs;
+    top = w;
+  } else {
+    cur_c = sec_codes;   // O8: start from the secondary, no requantization
+    cur_s = sec_scales;
+    top = s;
+  }
+  for (int l = top; l >= 1; --l) {
+    const int g = ctx->group[l - 1];
+    if (g > 1) {   // A3: in-place all-gather of range_l pieces into range_{l-1}
+      uint8_t* dc = ws_c + code_bytes(p->off[l - 1], bits);
+      float* ds = ws_s + p->off[l - 1] / B;
+      const int64_t nb = code_bytes(p->len[l], bits);
+      const int64_t ns = p->len[l] / B;
+      TraceScope t(st, "nccl_allgather", l, bits, p->len[l], (g - 1) * (nb + ns * 4));
+      HZ_NCCL(ncclGroupStart(), "ncclGroupStart");
+      HZ_NCCL(ncclAllGather(cur_c, dc, nb, ncclUint8, ctx->lvl[l - 1], st), "ncclAllGather(codes)");
+      HZ_NCCL(ncclAllGather(cur_s, ds, ns, ncclFloat32, ctx->lvl[l - 1], st), "ncclAllGather(scales)");
+      HZ_NCCL(ncclGroupEnd(), "ncclGroupEnd");
+      t.end();
+      cur_c = dc;
+      cur_s = ds;
+    }
+    if (!backward && s < w && l - 1 == s) {   // A4, s < w: keep the intermediate range_s
+      if ((rc = copy_async(sec_codes, cur_c, code_bytes(p->len[s], bits), st)) != HZ_OK) return rc;
+      if ((rc = copy_async(sec_scales, cur_s, p->len[s] / B * 4, st)) != HZ_OK) return rc;
+    }
+  }
+  // A5 / A6: every rank dequantizes the whole layer from the codes (R9).
+  if ((rc = run_dequantize(cur_c, cur_s, Np, bits, B, full_out, out_dt, st, 0)) != HZ_OK) return rc;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const void* grad,
+                                  hz_dtype dt, int from_level, int to_level,
+                                  const int* bits_per_level, float* shard, int accumulate,
+                                  void* stream) {
+  using namespace hz;
+  hz_status rc = check_partition(ctx, p);
+  if (rc != HZ_OK) return rc;
+  const int L = ctx->levels;
+  if (from_level < 1 || from_level > L) return fail(HZ_ERR_INVALID, "from_level: must be in [1, levels]");
+  if (to_level < from_level || to_level > L) return fail(HZ_ERR_INVALID, "to_level: must be in [from_level, levels]");
+  if (!bits_per_level) return fail(HZ_ERR_INVALID, "bits_per_level: NULL");
+  for (int l = from_level; l <= to_level; ++l)
+    if (!bits_ok(bits_per_level[l - 1]))
+      return fail(HZ_ERR_INVALID, "bits_per_level[" + std::to_string(l - 1) + "]: must be 4 or 8");
+  if (!dtype_ok(dt)) return fail(HZ_ERR_INVALID, "dt: unknown dtype");
+  if (!grad || !aligned16(grad)) return fail(HZ_ERR_INVALID, "grad: NULL or not 16-byte aligned");
+  if (!shard || !aligned16(shard)) return fail(HZ_ERR_INVALID, "shard: NULL or not 16-byte aligned");
+  if ((rc = check_async(ctx)) != HZ_OK) return rc;
+
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int B = p->block;
+  const int64_t base_len = p->len[from_level - 1];
+  if (base_len == 0) {
+    clear_error();
+    return HZ_OK;
+  }
+  if ((rc = grow(ctx->rs_a_c, base_len)) != HZ_OK) return rc;
+  if ((rc = grow(ctx->rs_a_s, base_len / B * 4)) != HZ_OK) return rc;
+  if ((rc = grow(ctx->rs_b_c, base_len)) != HZ_OK) return rc;
+  if ((rc = grow(ctx->rs_b_s, base_len / B * 4)) != HZ_OK) return rc;
+  if ((rc = grow(ctx->rs_r_c, base_len)) != HZ_OK) return rc;
+  if ((rc = grow(ctx->rs_r_s, base_len / B * 4)) != HZ_OK) return rc;
+  uint8_t* a_c = static_cast<uint8_t*>(ctx->rs_a_c.p);
+  float* a_s = static_cast<float*>(ctx->rs_a_s.p);
+  uint8_t* b_c = static_cast<uint8_t*>(ctx->rs_b_c.p);
+  float* b_s = static_cast<float*>(ctx->rs_b_s.p);
+  uint8_t* r_c = static_cast<uint8_t*>(ctx->rs_r_c.p);
+  float* r_s = static_cast<float*>(ctx->rs_r_s.p);
+
+  // A7: quantize the whole input range_{from-1}; chunk j of it goes to digit j.
+  if ((rc = run_quantize(grad, dt, base_len, bits_per_level[from_level - 1], B, a_c, a_s, st,
+                         from_level)) != HZ_OK)
+    return rc;
+  for (int l = from_level; l <= to_level; ++l) {
+    const int g = ctx->group[l - 1];
+    const int d = ctx->digit[l - 1];
+    const int bits = bits_per_level[l - 1];
+    const int64_t cl = p->len[l];
+    const int64_t cb = code_bytes(cl, bits);
+    const int64_t cs = cl / B;
+    const uint8_t* ptr_c[kMaxG];
+    const float* ptr_s[kMaxG];
+    if (g > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "group size > 16 at one level");
+    if (g > 1) {   // A8: all-to-all within the level-l exchange group
+      TraceScope t(st, "nccl_alltoall", l, bits, cl, (g - 1) * (cb + cs * 4));
+      HZ_NCCL(ncclGroupStart(), "ncclGroupStart");
+      for (int j = 0; j < g; ++j) {
+        if (j == d) continue;
+        HZ_NCCL(ncclSend(a_c + j * cb, cb, ncclUint8, j, ctx->lvl[l - 1], st), "ncclSend(codes)");
+        HZ_NCCL(ncclRecv(r_c + j * cb, cb, ncclUint8, j, ctx->lvl[l - 1], st), "ncclRecv(codes)");
+        HZ_NCCL(ncclSend(a_s + j * cs, cs, ncclFloat32, j, ctx->lvl[l - 1], st), "ncclSend(scales)");
+        HZ_NCCL(ncclRecv(r_s + j * cs, cs, ncclFloat32, j, ctx->lvl[l - 1], st), "ncclRecv(scales)");
+      }
+      HZ_NCCL(ncclGroupEnd(), "ncclGroupEnd");
+      t.end();
+    }
+    for (int j = 0; j < g; ++j) {
+      ptr_c[j] = j == d ? a_c + j * cb : r_c + j * cb;
+      ptr_s[j] = j == d ? a_s + j * cs : r_s + j * cs;
+    }
+    if (l < to_level) {   // A9 fused with the next level's requantization
+      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, bits_per_level[l], b_c, b_s, nullptr, 0, st,
+                           l)) != HZ_OK)
+        return rc;
+      std::swap(a_c, b_c);
+      std::swap(a_s, b_s);
+    } else {              // A9/A10: final fp32 shard, optionally accumulated
+      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st,
+                           l)) != HZ_OK)
+        return rc;
+    }
+  }
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_flat_allgather(hz_ctx* ctx, const void* chunk, void* out, int64_t numel, hz_dtype dt,
+                            void* stream) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  if (!dtype_ok(dt)) return fail(HZ_ERR_INVALID, "dt: unknown dtype");
+  if (numel < 0 || numel % ctx->world) return fail(HZ_ERR_INVALID, "numel: must be a non-negative multiple of world");
+  if (!chunk || !out) return fail(HZ_ERR_INVALID, "chunk/out: NULL");
+  hz_status rc = check_async(ctx);
+  if (rc != HZ_OK) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t c = numel / ctx->world;
+  TraceScope t(st, "nccl_flat", 0, 16, numel, (ctx->world - 1) * c * elem_bytes(dt));
+  HZ_NCCL(ncclAllGather(chunk, out, c, nccl_dtype(dt), ctx->world_comm, st), "ncclAllGather");
+  t.end();
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_flat_reduce_scatter(hz_ctx* ctx, const void* in, void* out_chunk, int64_t numel,
+                                 hz_dtype dt, void* stream) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  if (!dtype_ok(dt)) return fail(HZ_ERR_INVALID, "dt: unknown dtype");
+  if (numel < 0 || numel % ctx->world) return fail(HZ_ERR_INVALID, "numel: must be a non-negative multiple of world");
+  if (!in || !out_chunk) return fail(HZ_ERR_INVALID, "in/out_chunk: NULL");
+  hz_status rc = check_async(ctx);
+  if (rc != HZ_OK) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t c = numel / ctx->world;
+  TraceScope t(st, "nccl_flat", 0, 16, numel, (ctx->world - 1) * c * elem_bytes(dt));
+  HZ_NCCL(ncclReduceScatter(in, out_chunk, c, nccl_dtype(dt), ncclSum, ctx->world_comm, st),
+          "ncclReduceScatter");
+  t.end();
+  clear_error();
+  return HZ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+// Internal declarations shared by the libhz.so translation units (not installed).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/hz.h"
+
+namespace hz {
+
+// thread-local error message (abi.cpp)
+hz_status fail(hz_status st, const std::string& msg);
+void clear_error();
+
+// --------------------------------------------------------------- validation
+bool block_ok(int block);          // power of two in [32, 2048]
+bool bits_ok(int bits);            // 4 or 8
+bool aligned16(const void* p);
+int64_t code_bytes(int64_t n, int bits);   // n * bits / 8
+
+// ----------------------------------------------------------------- kernels
+// All launchers validate nothing (the ABI layer does) and return cudaGetLastError().
+cudaError_t launch_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block,
+                            uint8_t* codes, float* scales, cudaStream_t st);
+cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, int64_t n, int bits,
+                              int block, void* y, hz_dtype out_dt, cudaStream_t st);
+constexpr int kMaxG = 16;
+cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
+                          int64_t n, int bits_in, int block, int bits_out, uint8_t* out_codes,
+                          float* out_scales, float* out_f32, int accumulate, cudaStream_t st);
+
+// ------------------------------------------------------------------ tracing
+struct TraceScope {
+  // Records a start event on construction and an end event + record on end().
+  TraceScope(cudaStream_t st, const char* kind, int level, int bits, int64_t elems,
+             int64_t bytes);
+  void end();
+  ~TraceScope();
+  bool active;
+  int slot;
+  cudaStream_t stream;
+};
+
+// ----------------------------------------------------------------- partition
+hz_status partition(int rank, int levels, const int* group, int64_t numel, int block, int w,
+                    int s, int gl, hz_partition_t* out);
+
+}  // namespace hz

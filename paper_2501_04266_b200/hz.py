@@ -1,0 +1,315 @@
+"""Thin ctypes binding of libhz.so (include/hz.h).  Argument marshalling only:
+every step of the hot path runs in the library's CUDA kernels and NCCL calls.
+
+Importing this module loads ``libhz.so`` from the package directory and raises
+``ImportError`` if it is missing: there is no CPU fallback.  Tensor arguments
+are torch CUDA tensors (PyTorch provides device memory, streams and process
+groups only); raw integer device pointers are accepted too.
+"""
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libhz.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2501_04266_b200.build` "
+        "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+MAX_LEVELS = 4
+F32, BF16, F16 = 0, 1, 2
+OK, ERR_INVALID, ERR_CUDA, ERR_NCCL, ERR_NONFINITE, ERR_UNSUPPORTED = range(6)
+_STATUS = {1: "HZ_ERR_INVALID", 2: "HZ_ERR_CUDA", 3: "HZ_ERR_NCCL", 4: "HZ_ERR_NONFINITE",
+           5: "HZ_ERR_UNSUPPORTED"}
+
+
+class HZError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Partition(ctypes.Structure):
+    _fields_ = [
+        ("numel", ctypes.c_int64), ("padded_numel", ctypes.c_int64),
+        ("block", ctypes.c_int32), ("levels", ctypes.c_int32), ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32), ("w", ctypes.c_int32), ("s", ctypes.c_int32),
+        ("gl", ctypes.c_int32),
+        ("group", ctypes.c_int32 * MAX_LEVELS), ("digit", ctypes.c_int32 * MAX_LEVELS),
+        ("off", ctypes.c_int64 * (MAX_LEVELS + 1)), ("len", ctypes.c_int64 * (MAX_LEVELS + 1)),
+    ]
+
+    def range(self, level):
+        return int(self.off[level]), int(self.len[level])
+
+    def as_dict(self):
+        L = self.levels
+        return {
+            "numel": self.numel, "padded_numel": self.padded_numel, "block": self.block,
+            "levels": L, "world": self.world, "rank": self.rank, "w": self.w, "s": self.s,
+            "gl": self.gl, "group": list(self.group[:L]), "digit": list(self.digit[:L]),
+            "off": list(self.off[:L + 1]), "len": list(self.len[:L + 1]),
+        }
+
+
+class Uid(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_ubyte * 128)]
+
+
+class TraceRec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_char_p), ("level", ctypes.c_int32), ("bits", ctypes.c_int32),
+                ("elems", ctypes.c_int64), ("bytes", ctypes.c_int64), ("ms", ctypes.c_float)]
+
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+
+
+def _sig(name, argtypes, restype=ctypes.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = argtypes
+    f.restype = restype
+    return f
+
+
+_sig("hz_version", [], ctypes.c_char_p)
+_sig("hz_last_error", [], ctypes.c_char_p)
+_sig("hz_num_symbols", [], ctypes.c_int)
+_sig("hz_symbol_name", [_int], ctypes.c_char_p)
+_sig("hz_partition_ex", [_int, _int, ctypes.POINTER(ctypes.c_int), _i64, _int, _int, _int, _int,
+                         ctypes.POINTER(Partition)])
+_sig("hz_quantize", [_vp, _int, _i64, _int, _int, _vp, _vp, _vp])
+_sig("hz_dequantize", [_vp, _vp, _i64, _int, _int, _vp, _int, _vp])
+_sig("hz_reduce_chunks", [_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, _int, _int, _int,
+                          _vp, _vp, _vp, _int, _vp])
+_sig("hz_get_uid", [ctypes.POINTER(Uid)])
+_sig("hz_init", [ctypes.POINTER(_vp), _int, _int, ctypes.POINTER(Uid), _int,
+                 ctypes.POINTER(ctypes.c_int), _int, ctypes.c_size_t])
+_sig("hz_finalize", [_vp])
+_sig("hz_partition", [_vp, _i64, _int, _int, _int, _int, ctypes.POINTER(Partition)])
+_sig("hz_allgather_params", [_vp, ctypes.POINTER(Partition), _int, _vp, _int, _int, _vp, _vp, _vp,
+                             _int, _vp])
+_sig("hz_reduce_scatter_grads", [_vp, ctypes.POINTER(Partition), _vp, _int, _int, _int,
+                                 ctypes.POINTER(ctypes.c_int), _vp, _int, _vp])
+_sig("hz_flat_allgather", [_vp, _vp, _vp, _i64, _int, _vp])
+_sig("hz_flat_reduce_scatter", [_vp, _vp, _vp, _i64, _int, _vp])
+_sig("hz_trace_begin", [_int])
+_sig("hz_trace_end", [])
+_sig("hz_trace_read", [ctypes.POINTER(TraceRec), _int, ctypes.POINTER(ctypes.c_int)])
+
+
+def _check(status):
+    if status != OK:
+        raise HZError(status, _lib.hz_last_error().decode())
+
+
+def version():
+    return _lib.hz_version().decode()
+
+
+def exported_symbols():
+    return [_lib.hz_symbol_name(i).decode() for i in range(_lib.hz_num_symbols())]
+
+
+def lib_handle():
+    return _lib
+
+
+# ------------------------------------------------------------------ marshalling
+def _ptr(t):
+    """Device pointer of a torch tensor (or an int / None)."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _dtype_code(t):
+    import torch
+    return {torch.float32: F32, torch.bfloat16: BF16, torch.float16: F16}[t.dtype]
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _groups(group):
+    g = list(group)
+    return (ctypes.c_int * len(g))(*g), len(g)
+
+
+# ---------------------------------------------------------------- host-only API
+def partition_ex(rank, group, numel, block=256, w=1, s=1, gl=None):
+    """hz_partition_ex: the O1-O3 map for one rank (pure host, no GPU)."""
+    arr, L = _groups(group)
+    p = Partition()
+    _check(_lib.hz_partition_ex(rank, L, arr, numel, block, w, s, L if gl is None else gl,
+                                ctypes.byref(p)))
+    return p
+
+
+# ------------------------------------------------------------------- codec ops
+def code_nbytes(n, bits):
+    return n * bits // 8
+
+
+def quantize(x, bits=8, block=256, codes=None, scales=None, stream=None):
+    """hz_quantize on a contiguous CUDA tensor x (fp32/bf16/fp16)."""
+    import torch
+    n = x.numel()
+    if codes is None:
+        codes = torch.empty(code_nbytes(n, bits), dtype=torch.uint8, device=x.device)
+    if scales is None:
+        scales = torch.empty(n // block, dtype=torch.float32, device=x.device)
+    _check(_lib.hz_quantize(_ptr(x), _dtype_code(x), n, bits, block, _ptr(codes), _ptr(scales),
+                            _stream(stream)))
+    return codes, scales
+
+
+def dequantize(codes, scales, n, bits=8, block=256, out_dtype=None, out=None, stream=None):
+    import torch
+    if out is None:
+        out = torch.empty(n, dtype=out_dtype or torch.bfloat16, device=codes.device)
+    _check(_lib.hz_dequantize(_ptr(codes), _ptr(scales), n, bits, block, _ptr(out),
+                              _dtype_code(out), _stream(stream)))
+    return out
+
+
+def reduce_chunks(codes_list, scales_list, n, bits_in=4, block=256, bits_out=0, out_codes=None,
+                  out_scales=None, out_f32=None, accumulate=False, stream=None):
+    """hz_reduce_chunks: sum of g coded chunks (ascending p), requantized (bits_out 4/8)
+    or written / accumulated as fp32 (bits_out 0)."""
+    import torch
+    g = len(codes_list)
+    dev = codes_list[0].device
+    if bits_out:
+        if out_codes is None:
+            out_codes = torch.empty(code_nbytes(n, bits_out), dtype=torch.uint8, device=dev)
+        if out_scales is None:
+            out_scales = torch.empty(n // block, dtype=torch.float32, device=dev)
+    elif out_f32 is None:
+        out_f32 = torch.empty(n, dtype=torch.float32, device=dev)
+    cp = (_vp * g)(*[_ptr(c) for c in codes_list])
+    sp = (_vp * g)(*[_ptr(s) for s in scales_list])
+    _check(_lib.hz_reduce_chunks(g, cp, sp, n, bits_in, block, bits_out, _ptr(out_codes),
+                                 _ptr(out_scales), _ptr(out_f32), int(bool(accumulate)),
+                                 _stream(stream)))
+    return (out_codes, out_scales) if bits_out else out_f32
+
+
+# ---------------------------------------------------------------------- tracing
+def trace_begin(capacity=4096):
+    _check(_lib.hz_trace_begin(capacity))
+
+
+def trace_end():
+    _check(_lib.hz_trace_end())
+
+
+def trace_read(max_records=1 << 16):
+    n = ctypes.c_int(0)
+    _check(_lib.hz_trace_read(None, 0, ctypes.byref(n)))
+    cnt = min(n.value, max_records)
+    recs = (TraceRec * max(cnt, 1))()
+    _check(_lib.hz_trace_read(recs, cnt, ctypes.byref(n)))
+    return [{"kind": r.kind.decode(), "level": r.level, "bits": r.bits, "elems": r.elems,
+             "bytes": r.bytes, "ms": r.ms} for r in recs[:n.value]]
+
+
+# ------------------------------------------------------------------ collectives
+def get_uid():
+    u = Uid()
+    _check(_lib.hz_get_uid(ctypes.byref(u)))
+    return bytes(u.bytes)
+
+
+class Context:
+    """One rank's hz context: NCCL communicators per hierarchy level + workspace.
+
+    group: relative group sizes innermost first, e.g. (2, 2, 2); the cumulative form
+    (2, 4, 8) of the north star is accepted with ``cumulative=True``."""
+
+    def __init__(self, rank, world, uid, group, device, workspace_bytes=0, cumulative=False):
+        g = list(group)
+        if cumulative:
+            rel, prev = [], 1
+            for c in g:
+                if c % prev:
+                    raise ValueError("cumulative group sizes must divide each other")
+                rel.append(c // prev)
+                prev = c
+            g = rel
+        self.group = tuple(g)
+        self.rank, self.world, self.device = rank, world, device
+        u = Uid()
+        ctypes.memmove(ctypes.byref(u), bytes(uid), 128)
+        arr, L = _groups(g)
+        h = _vp()
+        _check(_lib.hz_init(ctypes.byref(h), rank, world, ctypes.byref(u), L, arr, device,
+                            workspace_bytes))
+        self._h = h
+
+    @property
+    def levels(self):
+        return len(self.group)
+
+    def close(self):
+        if self._h:
+            _check(_lib.hz_finalize(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def partition(self, numel, block=256, w=1, s=1, gl=None):
+        p = Partition()
+        _check(_lib.hz_partition(self._h, numel, block, w, s, self.levels if gl is None else gl,
+                                 ctypes.byref(p)))
+        return p
+
+    def allgather_params(self, p, primary, sec_codes, sec_scales, full_out, bits=8,
+                         backward=False, stream=None):
+        """Forward (backward=False): quantize ``primary`` (the rank's range_w), gather,
+        fill the secondary buffers, dequantize into ``full_out`` (Np elements).
+        Backward: gather from the secondary buffers and dequantize."""
+        dt = _dtype_code(primary) if primary is not None else BF16
+        _check(_lib.hz_allgather_params(self._h, ctypes.byref(p), int(bool(backward)),
+                                        _ptr(primary), dt, bits, _ptr(sec_codes),
+                                        _ptr(sec_scales), _ptr(full_out), _dtype_code(full_out),
+                                        _stream(stream)))
+        return full_out
+
+    def reduce_scatter_grads(self, p, grad, shard, bits_per_level=None, from_level=1,
+                             to_level=None, accumulate=False, stream=None):
+        L = self.levels
+        bpl = list(bits_per_level) if bits_per_level is not None else [4] * L
+        bpl = bpl + [4] * (L - len(bpl))
+        arr = (ctypes.c_int * L)(*bpl)
+        _check(_lib.hz_reduce_scatter_grads(self._h, ctypes.byref(p), _ptr(grad), _dtype_code(grad),
+                                            from_level, L if to_level is None else to_level, arr,
+                                            _ptr(shard), int(bool(accumulate)), _stream(stream)))
+        return shard
+
+    def flat_allgather(self, chunk, out, stream=None):
+        _check(_lib.hz_flat_allgather(self._h, _ptr(chunk), _ptr(out), out.numel(),
+                                      _dtype_code(out), _stream(stream)))
+        return out
+
+    def flat_reduce_scatter(self, inp, out_chunk, stream=None):
+        _check(_lib.hz_flat_reduce_scatter(self._h, _ptr(inp), _ptr(out_chunk), inp.numel(),
+                                           _dtype_code(inp), _stream(stream)))
+        return out_chunk

@@ -1,0 +1,164 @@
+"""Multi-rank parity worker for the NCCL path (launched by tests/test_gpu_collectives.py
+under torchrun, one process per GPU; also callable in-process at world 1).
+
+Each rank runs the product path (hz.Context -> libhz.so -> NCCL per-level
+communicators) on seeded inputs, then runs the CPU oracle's all-ranks simulation
+on the same inputs and compares its own rank's results bit for bit: the forward
+and backward gathered layers, the hpZ secondary, and the qgZ fp32 shard (one-call
+GA=1 and the setting-T two-phase GA=2 with accumulation)."""
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import ml_dtypes  # noqa: E402
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import collectives as col  # noqa: E402
+from oracle import partition as pm  # noqa: E402
+from oracle import quant  # noqa: E402
+from paper_2501_04266_b200 import synth  # noqa: E402
+from tests.gpu_util import assert_bitwise, to_dev, to_host  # noqa: E402
+
+HIERARCHIES = {
+    1: [(1,)],
+    2: [(2,), (1, 2)],
+    4: [(2, 2), (4,), (2, 1, 2)],
+    8: [(2, 2, 2), (2, 4), (4, 2), (8,)],
+}
+
+
+def role_cases(L):
+    cases = {(1, 1), (L, max(L - 1, 0)), (1, min(2, L)), (L, L), (0, 0)}
+    return sorted(c for c in cases if 0 <= c[0] <= L and 0 <= c[1] <= L)
+
+
+def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256):
+    errors = []
+    ctx = hz.Context(rank, world, uid, g, device)
+    L = len(g)
+    try:
+        Np = pm.padded_numel(numel, g, B)
+        full = np.zeros(Np, np.float32)
+        full[:numel] = synth.params_like(numel, 7, block=B)
+        full = full.astype(ml_dtypes.bfloat16)
+        for w, s in role_cases(L):
+            p = ctx.partition(numel, B, w, s, L)
+            assert p.padded_numel == Np
+            off, ln = p.range(w)
+            prim = {r: full[pm.range_at(r, g, Np, w)[0]:sum(pm.range_at(r, g, Np, w))] for r in range(world)}
+            want, want_sec = col.allgather_forward(prim, g, Np, B, w, s, bits=8)
+            so, sl = p.range(s)
+            sec_c = torch.empty(sl, dtype=torch.uint8, device="cuda")
+            sec_s = torch.empty(sl // B, dtype=torch.float32, device="cuda")
+            out = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
+            ctx.allgather_params(p, to_dev(full[off:off + ln]), sec_c, sec_s, out, bits=8)
+            torch.cuda.synchronize()
+            try:
+                assert_bitwise(to_host(out), want[rank], f"g={g} w={w} s={s} forward layer")
+                assert_bitwise(to_host(sec_c), quant.wire_codes(want_sec[rank][0], 8), f"g={g} w={w} s={s} secondary codes")
+                assert_bitwise(to_host(sec_s), want_sec[rank][1], f"g={g} w={w} s={s} secondary scales")
+                out2 = torch.empty_like(out)
+                ctx.allgather_params(p, None, sec_c, sec_s, out2, bits=8, backward=True)
+                torch.cuda.synchronize()
+                assert_bitwise(to_host(out2), want[rank], f"g={g} w={w} s={s} backward layer")
+            except AssertionError as e:
+                errors.append(str(e))
+
+        # qgZ: one call over all levels (GA = 1)
+        grads = {r: synth.gradient_like(Np, 900 + r, block=B).astype(ml_dtypes.bfloat16) for r in range(world)}
+        for bits1 in (4, 8):
+            bpl = [bits1] + [4] * (L - 1)
+            p = ctx.partition(numel, B, 1, 1, L)
+            want = col.reduce_scatter(grads, g, Np, B, 1, L, {l: bpl[l - 1] for l in range(1, L + 1)})
+            shard = torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")
+            ctx.reduce_scatter_grads(p, to_dev(grads[rank]), shard, bpl)
+            torch.cuda.synchronize()
+            try:
+                assert_bitwise(to_host(shard), want[rank], f"g={g} qgZ bits={bpl}")
+            except AssertionError as e:
+                errors.append(str(e))
+
+        # setting T, GA = 2: levels 1..gl per micro-batch with accumulate, then gl+1..L once
+        if L >= 2:
+            gl = L - 1
+            p = ctx.partition(numel, B, 1, 1, gl)
+            grads2 = {r: synth.gradient_like(Np, 950 + r, block=B).astype(ml_dtypes.bfloat16) for r in range(world)}
+            bmap = {l: 4 for l in range(1, L + 1)}
+            A = col.reduce_scatter(grads, g, Np, B, 1, gl, bmap)
+            A = col.reduce_scatter(grads2, g, Np, B, 1, gl, bmap, accum=A)
+            want = col.reduce_scatter(A, g, Np, B, gl + 1, L, bmap)
+            acc = torch.empty(p.range(gl)[1], dtype=torch.float32, device="cuda")
+            ctx.reduce_scatter_grads(p, to_dev(grads[rank]), acc, [4] * L, 1, gl, accumulate=False)
+            ctx.reduce_scatter_grads(p, to_dev(grads2[rank]), acc, [4] * L, 1, gl, accumulate=True)
+            shard = torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")
+            ctx.reduce_scatter_grads(p, acc, shard, [4] * L, gl + 1, L)
+            torch.cuda.synchronize()
+            try:
+                assert_bitwise(to_host(acc), A[rank], f"g={g} two-phase accumulated shard")
+                assert_bitwise(to_host(shard), want[rank], f"g={g} two-phase final shard")
+            except AssertionError as e:
+                errors.append(str(e))
+
+        # flat ZeRO-3 baseline collectives (plain NCCL)
+        n = world * 4096
+        x = torch.arange(n, dtype=torch.float32, device="cuda") + rank
+        chunk = x[rank * 4096:(rank + 1) * 4096].contiguous()
+        outf = torch.empty(n, dtype=torch.float32, device="cuda")
+        ctx.flat_allgather(chunk, outf)
+        rs = torch.empty(4096, dtype=torch.float32, device="cuda")
+        ctx.flat_reduce_scatter(x, rs)
+        torch.cuda.synchronize()
+        want_ag = np.concatenate([np.arange(q * 4096, (q + 1) * 4096, dtype=np.float32) + q for q in range(world)])
+        want_rs = (np.arange(rank * 4096, (rank + 1) * 4096, dtype=np.float64) * world + sum(range(world)))
+        try:
+            assert_bitwise(to_host(outf), want_ag, "flat all-gather")
+            assert np.allclose(to_host(rs), want_rs, rtol=1e-6), "flat reduce-scatter"
+        except AssertionError as e:
+            errors.append(str(e))
+    finally:
+        ctx.close()
+    return errors
+
+
+def run(rank, world, local, bcast=None):
+    from paper_2501_04266_b200 import hz
+    torch.cuda.set_device(local)
+    errors = []
+    for g in HIERARCHIES[world]:
+        uid = hz.get_uid() if rank == 0 else None
+        if bcast is not None:
+            uid = bcast(uid)
+        errors += check_hierarchy(hz, rank, world, g, uid, local)
+    return errors
+
+
+def main():
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dist.init_process_group("gloo")
+
+    def bcast(obj):
+        box = [obj]
+        dist.broadcast_object_list(box, src=0)
+        return box[0]
+
+    errors = run(rank, world, local, bcast)
+    for e in errors:
+        print(f"[rank {rank}] {e}", flush=True)
+    n = torch.tensor([len(errors)])
+    dist.all_reduce(n)
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"mp_parity world={world}: {int(n)} failures", flush=True)
+    sys.exit(1 if int(n) else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,34 @@
+"""NCCL path parity (hz_init / hz_allgather_params / hz_reduce_scatter_grads) against
+the oracle.  World 1 (hierarchy (1,)) runs in-process on one GPU; with >= 2 GPUs
+the same worker runs under torchrun on 2, 4 and (if present) 8 GPUs, one process
+per GPU, covering every hierarchy of that size (tests/mp_parity.py)."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_world1_context():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from tests import mp_parity
+    errors = mp_parity.run(0, 1, 0)
+    assert not errors, "\n".join(errors)
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu(n):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n),
+           os.path.join(ROOT, "tests", "mp_parity.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
