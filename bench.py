@@ -79,7 +79,7 @@ def relaunch_under_torchrun(args):
 
 # ------------------------------------------------------------------ measurement
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms from the warm-up through the timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -93,7 +93,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                          "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                                          text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -267,15 +267,22 @@ def run_hz(args):
     model = Model(hz, ctx, torch, args.config, rank, world, args, device)
     stream = torch.cuda.current_stream()
 
-    for _ in range(max(args.warmup, 3)):
-        model.step(stream)
-    torch.cuda.synchronize()
-
-    per_step_kernels = 5 * len(model.tensors)
-    hz.trace_begin(capacity=(args.steps + 1) * per_step_kernels * 4 + 64)
+    # clocks are sampled from the start of the warm-up (under the same load) through
+    # the end of the timed region: the timed region alone is often shorter than the
+    # sampling period
     sampler = ClockSampler([local] if world == 1 else range(world)) if rank == 0 else None
     if sampler:
         sampler.start()
+    for _ in range(max(args.warmup, 3)):
+        model.step(stream)
+    torch.cuda.synchronize()
+    t_end = time.time() + 0.5                      # extra untimed steps: >= 0.5 s under load
+    while max_over_ranks(time.time(), world) < t_end:
+        model.step(stream)
+        torch.cuda.synchronize()
+
+    per_step_kernels = 5 * len(model.tensors)
+    hz.trace_begin(capacity=(args.steps + 1) * per_step_kernels * 4 + 64)
     barrier(world)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)

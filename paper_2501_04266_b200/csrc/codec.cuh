@@ -1,0 +1,265 @@
+// Device helpers shared by the sm_100a codec kernels (k_quantize.cu,
+// k_dequantize.cu, k_reduce.cu).  Internal header.
+//
+// Exactness (oracle readings R1-R5): every operation below
+// rounds exactly like the oracle's fp32 NumPy code.
+//   * bf16/fp16 -> fp32 widening is exact.
+//   * scale = __fdiv_rn(am, qmax), inv = __fdiv_rn(qmax, am) (IEEE division).
+//   * code = rne(fl(x*inv)) is computed as fl(fl(x*inv) + 1.5*2^23): for
+//     |t| <= 2^22 the sum lands in [2^23, 2^24) where the fp32 spacing is 1, so
+//     round-to-nearest-even of the sum IS rint(t), and the low bits of the sum's
+//     bit pattern are rint(t) in two's complement.  This replaces F2I (a
+//     quarter-rate conversion) by one full-rate FADD.  The two roundings are
+//     kept separate (--fmad=false, explicit __fmul_rn/__fadd_rn): a fused FMA
+//     would round x*inv + M once and could differ next to a tie.
+//   * no clamp is needed: |x| <= am and inv <= (qmax/am)(1 + 2^-24), so
+//     |fl(x*inv)| <= qmax*(1 + 2^-23) < qmax + 1/2 and rint stays in
+//     [-qmax, qmax] (the oracle's clamp is provably inactive).
+//   * code -> float uses the same trick backwards: a byte / nibble placed in the
+//     low bits of 0x4B400000 reads as 1.5*2^23 + k; subtracting the exact bias
+//     gives the integer code exactly (replaces I2F).
+//   * x_hat = __fmul_rn(code, scale); sums use __fadd_rn in ascending input order.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "hz_internal.h"
+
+namespace hz {
+namespace dev {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr float kTiny = 0x1p-100f;        // R3: am < 2^-100 -> scale 0, codes 0
+constexpr float kMagic = 12582912.0f;     // 1.5 * 2^23, bit pattern 0x4B400000
+constexpr int kThreads = 256;
+
+template <int B>
+struct Geo {
+  static constexpr int LPB = B >= 256 ? 32 : B / 8;     // lanes per quantization block
+  static constexpr int NSUB = B >= 256 ? B / 256 : 1;   // 8-element sub-chunks per lane per block
+  static constexpr int BPW = 32 / LPB;                  // blocks per warp step
+  static constexpr int SUBSTRIDE = LPB * 8;             // elements between a lane's sub-chunks
+};
+
+template <int BITS>
+struct QMax;
+template <>
+struct QMax<8> { static constexpr int v = 127; };
+template <>
+struct QMax<4> { static constexpr int v = 7; };
+
+// ------------------------------------------------------------ 8-element input
+template <typename T>
+struct In8;
+
+template <>
+struct In8<float> {
+  uint4 r[2];
+  __device__ __forceinline__ void load(const float* p) {
+    r[0] = __ldg(reinterpret_cast<const uint4*>(p));
+    r[1] = __ldg(reinterpret_cast<const uint4*>(p) + 1);
+  }
+  __device__ __forceinline__ void get(float (&v)[8]) const {
+    v[0] = __uint_as_float(r[0].x); v[1] = __uint_as_float(r[0].y);
+    v[2] = __uint_as_float(r[0].z); v[3] = __uint_as_float(r[0].w);
+    v[4] = __uint_as_float(r[1].x); v[5] = __uint_as_float(r[1].y);
+    v[6] = __uint_as_float(r[1].z); v[7] = __uint_as_float(r[1].w);
+  }
+};
+
+template <>
+struct In8<__nv_bfloat16> {
+  uint4 r;
+  __device__ __forceinline__ void load(const __nv_bfloat16* p) {
+    r = __ldg(reinterpret_cast<const uint4*>(p));
+  }
+  __device__ __forceinline__ void get(float (&v)[8]) const {
+    // bf16 -> fp32 is a 16-bit left shift: exact (subnormals included).
+    v[0] = __uint_as_float(r.x << 16); v[1] = __uint_as_float(r.x & 0xffff0000u);
+    v[2] = __uint_as_float(r.y << 16); v[3] = __uint_as_float(r.y & 0xffff0000u);
+    v[4] = __uint_as_float(r.z << 16); v[5] = __uint_as_float(r.z & 0xffff0000u);
+    v[6] = __uint_as_float(r.w << 16); v[7] = __uint_as_float(r.w & 0xffff0000u);
+  }
+};
+
+template <>
+struct In8<__half> {
+  uint4 r;
+  __device__ __forceinline__ void load(const __half* p) {
+    r = __ldg(reinterpret_cast<const uint4*>(p));
+  }
+  __device__ __forceinline__ void get(float (&v)[8]) const {
+    const unsigned w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+      float2 f = __half22float2(h);   // exact
+      v[2 * i] = f.x;
+      v[2 * i + 1] = f.y;
+    }
+  }
+};
+
+// ------------------------------------------------------------------ codes
+// byte i of x (bias 128 already applied) -> 1.5*2^23 + byte
+__device__ __forceinline__ float byte_as_magic(unsigned x, int i) {
+  return __uint_as_float(__byte_perm(x, 0x4B400000u, 0x7650u + i));
+}
+
+// 8 int8 codes (8 bytes)
+template <int BITS>
+struct Codes8;
+
+template <>
+struct Codes8<8> {
+  uint2 r;
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<uint2*>(p) = r; }
+  // exact float value of each code
+  __device__ __forceinline__ void decode(float (&c)[8]) const {
+    const unsigned x = r.x ^ 0x80808080u, y = r.y ^ 0x80808080u;   // two's complement -> +128 bias
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      c[i] = __fsub_rn(byte_as_magic(x, i), kMagic + 128.f);
+      c[4 + i] = __fsub_rn(byte_as_magic(y, i), kMagic + 128.f);
+    }
+  }
+  // b[i] = bit pattern of fl(t_i + 1.5*2^23): its low byte is code i
+  __device__ __forceinline__ void set(const unsigned (&b)[8]) {
+    r.x = __byte_perm(__byte_perm(b[0], b[1], 0x0040u), __byte_perm(b[2], b[3], 0x0040u), 0x5410u);
+    r.y = __byte_perm(__byte_perm(b[4], b[5], 0x0040u), __byte_perm(b[6], b[7], 0x0040u), 0x5410u);
+  }
+};
+
+// 8 int4 codes (4 bytes), even element in the low nibble (R4)
+template <>
+struct Codes8<4> {
+  unsigned r;
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const unsigned*>(p)); }
+  __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<unsigned*>(p) = r; }
+  __device__ __forceinline__ void decode(float (&c)[8]) const {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      // (nibble ^ 8) = code + 8 in [1, 15], placed in the mantissa of 1.5*2^23
+      const unsigned m = ((r >> (4 * i)) & 0xFu) ^ 0x4B400008u;
+      c[i] = __fsub_rn(__uint_as_float(m), kMagic + 8.f);
+    }
+  }
+  __device__ __forceinline__ void set(const unsigned (&b)[8]) {
+    unsigned n[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) n[i] = (b[2 * i] & 0xFu) | ((b[2 * i + 1] << 4) & 0xF0u);
+    r = __byte_perm(__byte_perm(n[0], n[1], 0x0040u), __byte_perm(n[2], n[3], 0x0040u), 0x5410u);
+  }
+};
+
+// 4 codes (elementwise kernels with 4-element units)
+template <int BITS>
+struct Codes4;
+
+template <>
+struct Codes4<8> {
+  unsigned r;
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const unsigned*>(p)); }
+  __device__ __forceinline__ void decode(float (&c)[4]) const {
+    const unsigned x = r ^ 0x80808080u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i] = __fsub_rn(byte_as_magic(x, i), kMagic + 128.f);
+  }
+};
+
+template <>
+struct Codes4<4> {
+  unsigned short r;
+  __device__ __forceinline__ void load(const uint8_t* p) {
+    r = __ldg(reinterpret_cast<const unsigned short*>(p));
+  }
+  __device__ __forceinline__ void decode(float (&c)[4]) const {
+    const unsigned w = r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const unsigned m = ((w >> (4 * i)) & 0xFu) ^ 0x4B400008u;
+      c[i] = __fsub_rn(__uint_as_float(m), kMagic + 8.f);
+    }
+  }
+};
+
+// ------------------------------------------------------------------- codec math
+template <int BITS>
+__device__ __forceinline__ void quant_params(float am, float& scale, float& inv) {
+  constexpr float qmax = static_cast<float>(QMax<BITS>::v);
+  if (am >= kTiny) {
+    scale = __fdiv_rn(am, qmax);
+    inv = __fdiv_rn(qmax, am);
+  } else {
+    scale = 0.f;
+    inv = 0.f;
+  }
+}
+
+// bit pattern of fl(fl(v*inv) + 1.5*2^23); low bits = rne(fl(v*inv)) (see header)
+__device__ __forceinline__ unsigned qbits(float v, float inv) {
+  return __float_as_uint(__fadd_rn(__fmul_rn(v, inv), kMagic));
+}
+
+template <int LPB>
+__device__ __forceinline__ float group_max(float v) {
+#pragma unroll
+  for (int o = LPB / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// ------------------------------------------------------------------ output store
+template <typename TO>
+struct Out8;
+
+template <>
+struct Out8<float> {
+  __device__ __forceinline__ static void store(float* p, const float (&v)[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+
+template <>
+struct Out8<__nv_bfloat16> {
+  __device__ __forceinline__ static void store(__nv_bfloat16* p, const float (&v)[8]) {
+    unsigned w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);   // RNE
+      w[i] = *reinterpret_cast<unsigned*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+template <>
+struct Out8<__half> {
+  __device__ __forceinline__ static void store(__half* p, const float (&v)[8]) {
+    unsigned w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);              // RNE
+      w[i] = *reinterpret_cast<unsigned*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+__device__ __forceinline__ int64_t global_warp() {
+  return (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+}
+__device__ __forceinline__ int64_t num_warps() {
+  return (static_cast<int64_t>(gridDim.x) * kThreads) >> 5;
+}
+
+}  // namespace dev
+
+// host-side grid sizing (codec_util.cu): grid-stride kernels get
+// min(ceil(warp_tasks / warps per CTA), SMs x resident CTAs of that kernel).
+int64_t grid_for(const void* kernel, int64_t warp_tasks);
+
+}  // namespace hz

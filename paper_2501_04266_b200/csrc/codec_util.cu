@@ -1,0 +1,49 @@
+// Grid sizing for the grid-stride codec kernels: SMs x resident CTAs (occupancy
+// API, cached per kernel), never more CTAs than there is work for.
+#include <mutex>
+#include <unordered_map>
+
+#include "codec.cuh"
+
+namespace hz {
+namespace {
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+int resident_ctas(const void* kernel) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(kernel);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, dev::kThreads, 0) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 1;
+  }
+  cache[kernel] = n;
+  return n;
+}
+
+}  // namespace
+
+int64_t grid_for(const void* kernel, int64_t warp_tasks) {
+  const int64_t per_cta = dev::kThreads / 32;
+  const int64_t need = (warp_tasks + per_cta - 1) / per_cta;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(kernel);
+  const int64_t g = need < cap ? need : cap;
+  return g < 1 ? 1 : g;
+}
+
+}  // namespace hz

@@ -1,0 +1,124 @@
+// k_quantize (A2 qwZ / A7 qgZ; oracle O4-O5): x (bf16 | fp16 | fp32) ->
+// int8 | int4 codes + one fp32 scale per block of B elements.
+// Paper: "quantizes blocks of FP16 data into INT8 or INT4 blocks";
+// weights INT8 before the all-gather, gradients INT4.
+//
+// HBM-streaming, no tensor cores.  Mapping: a warp step covers max(B, 256)
+// contiguous elements; lane l owns 8 consecutive elements per 256-element
+// sub-chunk (one 16-byte bf16 load, one 8/4-byte code store per lane: each warp
+// instruction is one contiguous span).  A block's absmax is a shuffle-xor over
+// its LPB = min(32, B/8) lanes.  Each warp loads U steps before quantizing any
+// (memory-level parallelism); grid-stride over SMs x resident CTAs.
+#include "codec.cuh"
+
+namespace hz {
+namespace {
+
+using namespace dev;
+
+template <typename T, int B, int BITS, int U>
+__global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, int64_t nblocks,
+                                                       uint8_t* __restrict__ codes,
+                                                       float* __restrict__ scales) {
+  using G = Geo<B>;
+  const int lane = threadIdx.x & 31;
+  const int lb = lane / G::LPB;
+  const int ll = lane % G::LPB;
+  const int64_t warp = global_warp();
+  const int64_t nwarps = num_warps();
+  const int64_t nsteps = (nblocks + G::BPW - 1) / G::BPW;
+
+  for (int64_t s0 = warp * U; s0 < nsteps; s0 += nwarps * U) {
+    In8<T> raw[U][G::NSUB];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t blk = (s0 + u) * G::BPW + lb;
+      if (s0 + u < nsteps && blk < nblocks) {
+#pragma unroll
+        for (int k = 0; k < G::NSUB; ++k) raw[u][k].load(x + blk * B + k * G::SUBSTRIDE + ll * 8);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t blk = (s0 + u) * G::BPW + lb;
+      const bool valid = (s0 + u < nsteps) && blk < nblocks;
+      float v[G::NSUB][8];
+      float am = 0.f;
+#pragma unroll
+      for (int k = 0; k < G::NSUB; ++k) {
+        if (valid) {
+          raw[u][k].get(v[k]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[k][i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) am = fmaxf(am, fabsf(v[k][i]));
+      }
+      am = group_max<G::LPB>(am);
+      float scale, inv;
+      quant_params<BITS>(am, scale, inv);
+      if (valid) {
+#pragma unroll
+        for (int k = 0; k < G::NSUB; ++k) {
+          unsigned b[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) b[i] = qbits(v[k][i], inv);
+          Codes8<BITS> out;
+          out.set(b);
+          out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
+        }
+        if (ll == 0) scales[blk] = scale;
+      }
+    }
+  }
+}
+
+constexpr int kU = 4;   // warp steps in flight per warp
+constexpr int uq(int B) { return B > 256 ? 1 : kU; }   // B > 256: NSUB loads per step already
+
+template <typename T, int B, int BITS>
+cudaError_t quantize_t(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st) {
+  const int64_t nblocks = n / B;
+  const int64_t nsteps = (nblocks + Geo<B>::BPW - 1) / Geo<B>::BPW;
+  constexpr int U = uq(B);
+  auto kern = k_quantize<T, B, BITS, U>;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nsteps + U - 1) / U);
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(static_cast<const T*>(x), nblocks, codes, scales);
+  return cudaGetLastError();
+}
+
+template <typename T, int B>
+cudaError_t quantize_b(const void* x, int64_t n, int bits, uint8_t* c, float* s, cudaStream_t st) {
+  return bits == 8 ? quantize_t<T, B, 8>(x, n, c, s, st) : quantize_t<T, B, 4>(x, n, c, s, st);
+}
+
+template <typename T>
+cudaError_t quantize_d(const void* x, int64_t n, int bits, int block, uint8_t* c, float* s,
+                       cudaStream_t st) {
+  switch (block) {
+    case 32: return quantize_b<T, 32>(x, n, bits, c, s, st);
+    case 64: return quantize_b<T, 64>(x, n, bits, c, s, st);
+    case 128: return quantize_b<T, 128>(x, n, bits, c, s, st);
+    case 256: return quantize_b<T, 256>(x, n, bits, c, s, st);
+    case 512: return quantize_b<T, 512>(x, n, bits, c, s, st);
+    case 1024: return quantize_b<T, 1024>(x, n, bits, c, s, st);
+    case 2048: return quantize_b<T, 2048>(x, n, bits, c, s, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t launch_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block,
+                            uint8_t* codes, float* scales, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  switch (dt) {
+    case HZ_F32: return quantize_d<float>(x, n, bits, block, codes, scales, st);
+    case HZ_BF16: return quantize_d<__nv_bfloat16>(x, n, bits, block, codes, scales, st);
+    case HZ_F16: return quantize_d<__half>(x, n, bits, block, codes, scales, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hz

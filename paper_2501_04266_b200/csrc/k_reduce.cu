@@ -1,0 +1,315 @@
+// Level reduce of the qgZ reduce-scatter (A9 / A10; oracle O9 `reduce_coded`):
+// g coded chunks (the members of one level exchange group, ascending level
+// digit) -> x_hat_p = fl(code*scale) -> acc = ((x_hat_0 + x_hat_1) + ...) in
+// fp32, one rounding per add (R10), then
+//   k_reduce_requant: requantize acc (int4 | int8) into the next level's send
+//                     layout (same SoA arrays, this chunk's range) — the fused
+//                     dequant+sum+requant that keeps the all-to-all design free
+//                     of repeated error accumulation within a level;
+//   k_reduce_f32:     write the fp32 gradient shard, or add it to the shard
+//                     (A = fl(A + acc), gradient accumulation).
+//
+// k_reduce_requant needs a block-wide absmax, so it uses the block-grouped
+// mapping of k_quantize.  k_reduce_f32 has no cross-element step, so it uses an
+// elementwise mapping with 4-element units: every lane stores one 16-byte
+// float4 and a warp instruction writes one contiguous 512-byte span.
+#include "codec.cuh"
+
+namespace hz {
+namespace {
+
+using namespace dev;
+
+struct RedArgs {
+  const uint8_t* c[kMaxG];
+  const float* s[kMaxG];
+  int g;
+  int accumulate;
+  int64_t n;          // elements
+  uint8_t* oc;
+  float* os;
+  float* of;
+};
+
+// ------------------------------------------------------------ requantizing reduce
+// GT > 0: exactly GT inputs, all loads of a step issued before the sums.
+// GT == 0: runtime a.g inputs, one input at a time.
+template <int B, int BIN, int BOUT, int GT, int U>
+__global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_constant__ RedArgs a) {
+  using G = Geo<B>;
+  const int lane = threadIdx.x & 31;
+  const int lb = lane / G::LPB;
+  const int ll = lane % G::LPB;
+  const int64_t warp = global_warp();
+  const int64_t nwarps = num_warps();
+  const int64_t nblocks = a.n / B;
+  const int64_t nsteps = (nblocks + G::BPW - 1) / G::BPW;
+  constexpr int GP = GT > 0 ? GT : 1;
+
+  for (int64_t s0 = warp * U; s0 < nsteps; s0 += nwarps * U) {
+    float acc[U][G::NSUB][8];
+    if constexpr (GT > 0) {
+      Codes8<BIN> raw[U][GP][G::NSUB];
+      float sc[U][GP];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t blk = (s0 + u) * G::BPW + lb;
+        if (s0 + u < nsteps && blk < nblocks) {
+#pragma unroll
+          for (int p = 0; p < GP; ++p) {
+#pragma unroll
+            for (int k = 0; k < G::NSUB; ++k)
+              raw[u][p][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
+            sc[u][p] = __ldg(a.s[p] + blk);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int k = 0; k < G::NSUB; ++k) {
+          float c[8];
+          raw[u][0][k].decode(c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[u][k][i] = __fmul_rn(c[i], sc[u][0]);
+#pragma unroll
+          for (int p = 1; p < GP; ++p) {
+            raw[u][p][k].decode(c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[u][k][i] = __fadd_rn(acc[u][k][i], __fmul_rn(c[i], sc[u][p]));
+          }
+        }
+      }
+    } else {
+      for (int p = 0; p < a.g; ++p) {
+        Codes8<BIN> raw[U][G::NSUB];
+        float sc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t blk = (s0 + u) * G::BPW + lb;
+          sc[u] = 0.f;
+          if (s0 + u < nsteps && blk < nblocks) {
+#pragma unroll
+            for (int k = 0; k < G::NSUB; ++k)
+              raw[u][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
+            sc[u] = __ldg(a.s[p] + blk);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < G::NSUB; ++k) {
+            float c[8];
+            raw[u][k].decode(c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float xh = __fmul_rn(c[i], sc[u]);
+              acc[u][k][i] = p == 0 ? xh : __fadd_rn(acc[u][k][i], xh);
+            }
+          }
+      }
+    }
+
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t blk = (s0 + u) * G::BPW + lb;
+      const bool valid = (s0 + u < nsteps) && blk < nblocks;
+      float am = 0.f;
+#pragma unroll
+      for (int k = 0; k < G::NSUB; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) am = fmaxf(am, valid ? fabsf(acc[u][k][i]) : 0.f);
+      am = group_max<G::LPB>(am);
+      float scale, inv;
+      quant_params<BOUT>(am, scale, inv);
+      if (valid) {
+#pragma unroll
+        for (int k = 0; k < G::NSUB; ++k) {
+          unsigned b[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) b[i] = qbits(acc[u][k][i], inv);
+          Codes8<BOUT> out;
+          out.set(b);
+          out.store(a.oc + (blk * B + k * G::SUBSTRIDE + ll * 8) * BOUT / 8);
+        }
+        if (ll == 0) a.os[blk] = scale;
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------- fp32-output reduce
+template <int BIN, int GT, int U>
+__global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__ RedArgs a, int log2b) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = global_warp();
+  const int64_t nwarps = num_warps();
+  const int64_t nunits = a.n / 4;
+  constexpr int GP = GT > 0 ? GT : 1;
+  for (int64_t base = warp * 32 * U; base < nunits; base += nwarps * 32 * U) {
+    float acc[U][4];
+    float4 old[U];
+    if constexpr (GT > 0) {
+      Codes4<BIN> raw[U][GP];
+      float sc[U][GP];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t unit = base + u * 32 + lane;
+        if (unit < nunits) {
+#pragma unroll
+          for (int p = 0; p < GP; ++p) {
+            raw[u][p].load(a.c[p] + unit * BIN / 2);
+            sc[u][p] = __ldg(a.s[p] + ((unit * 4) >> log2b));
+          }
+          if (a.accumulate) old[u] = reinterpret_cast<const float4*>(a.of)[unit];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float c[4];
+        raw[u][0].decode(c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[u][i] = __fmul_rn(c[i], sc[u][0]);
+#pragma unroll
+        for (int p = 1; p < GP; ++p) {
+          raw[u][p].decode(c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[u][i] = __fadd_rn(acc[u][i], __fmul_rn(c[i], sc[u][p]));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t unit = base + u * 32 + lane;
+        if (unit < nunits && a.accumulate) old[u] = reinterpret_cast<const float4*>(a.of)[unit];
+      }
+      for (int p = 0; p < a.g; ++p) {
+        Codes4<BIN> raw[U];
+        float sc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t unit = base + u * 32 + lane;
+          sc[u] = 0.f;
+          if (unit < nunits) {
+            raw[u].load(a.c[p] + unit * BIN / 2);
+            sc[u] = __ldg(a.s[p] + ((unit * 4) >> log2b));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          float c[4];
+          raw[u].decode(c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float xh = __fmul_rn(c[i], sc[u]);
+            acc[u][i] = p == 0 ? xh : __fadd_rn(acc[u][i], xh);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t unit = base + u * 32 + lane;
+      if (unit < nunits) {
+        float4 o = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+        if (a.accumulate) {
+          o.x = __fadd_rn(old[u].x, o.x);
+          o.y = __fadd_rn(old[u].y, o.y);
+          o.z = __fadd_rn(old[u].z, o.z);
+          o.w = __fadd_rn(old[u].w, o.w);
+        }
+        reinterpret_cast<float4*>(a.of)[unit] = o;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------- launch
+constexpr int kUR = 2;   // warp steps in flight per warp (requant)
+constexpr int kUF = 4;   // 4-element units in flight per lane (fp32 out)
+constexpr int ur(int B) { return B > 256 ? 1 : kUR; }
+
+template <int B, int BIN, int BOUT, int GT>
+cudaError_t requant_t(const RedArgs& a, cudaStream_t st) {
+  const int64_t nsteps = (a.n / B + Geo<B>::BPW - 1) / Geo<B>::BPW;
+  constexpr int U = ur(B);
+  auto kern = k_reduce_requant<B, BIN, BOUT, GT, U>;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nsteps + U - 1) / U);
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int B, int BIN, int BOUT>
+cudaError_t requant_g(const RedArgs& a, cudaStream_t st) {
+  // Unrolled input prefetch for the common group sizes; large blocks with many
+  // inputs use the one-input-at-a-time loop (register budget).
+  switch (a.g) {
+    case 1: return requant_t<B, BIN, BOUT, 1>(a, st);
+    case 2: return requant_t<B, BIN, BOUT, 2>(a, st);
+    case 4: return B >= 1024 ? requant_t<B, BIN, BOUT, 0>(a, st) : requant_t<B, BIN, BOUT, 4>(a, st);
+    case 8: return B >= 512 ? requant_t<B, BIN, BOUT, 0>(a, st) : requant_t<B, BIN, BOUT, 8>(a, st);
+    default: return requant_t<B, BIN, BOUT, 0>(a, st);
+  }
+}
+
+template <int B>
+cudaError_t requant_b(const RedArgs& a, int bits_in, int bits_out, cudaStream_t st) {
+  if (bits_in == 8) return bits_out == 8 ? requant_g<B, 8, 8>(a, st) : requant_g<B, 8, 4>(a, st);
+  return bits_out == 8 ? requant_g<B, 4, 8>(a, st) : requant_g<B, 4, 4>(a, st);
+}
+
+template <int BIN, int GT>
+cudaError_t f32_t(const RedArgs& a, int log2b, cudaStream_t st) {
+  const int64_t nunits = a.n / 4;
+  auto kern = k_reduce_f32<BIN, GT, kUF>;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * kUF - 1) / (32 * kUF));
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, log2b);
+  return cudaGetLastError();
+}
+
+template <int BIN>
+cudaError_t f32_g(const RedArgs& a, int log2b, cudaStream_t st) {
+  switch (a.g) {
+    case 1: return f32_t<BIN, 1>(a, log2b, st);
+    case 2: return f32_t<BIN, 2>(a, log2b, st);
+    case 4: return f32_t<BIN, 4>(a, log2b, st);
+    case 8: return f32_t<BIN, 8>(a, log2b, st);
+    default: return f32_t<BIN, 0>(a, log2b, st);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
+                          int64_t n, int bits_in, int block, int bits_out, uint8_t* out_codes,
+                          float* out_scales, float* out_f32, int accumulate, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  RedArgs a{};
+  for (int p = 0; p < g; ++p) {
+    a.c[p] = codes[p];
+    a.s[p] = scales[p];
+  }
+  a.g = g;
+  a.accumulate = accumulate;
+  a.n = n;
+  a.oc = out_codes;
+  a.os = out_scales;
+  a.of = out_f32;
+  if (bits_out == 0) {
+    int log2b = 0;
+    while ((1 << log2b) < block) ++log2b;
+    return bits_in == 8 ? f32_g<8>(a, log2b, st) : f32_g<4>(a, log2b, st);
+  }
+  switch (block) {
+    case 32: return requant_b<32>(a, bits_in, bits_out, st);
+    case 64: return requant_b<64>(a, bits_in, bits_out, st);
+    case 128: return requant_b<128>(a, bits_in, bits_out, st);
+    case 256: return requant_b<256>(a, bits_in, bits_out, st);
+    case 512: return requant_b<512>(a, bits_in, bits_out, st);
+    case 1024: return requant_b<1024>(a, bits_in, bits_out, st);
+    case 2048: return requant_b<2048>(a, bits_in, bits_out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hz
