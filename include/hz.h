@@ -123,6 +123,43 @@ HZ_API const char* hz_symbol_name(int i);
 HZ_API hz_status hz_partition_ex(int rank, int levels, const int* group, int64_t numel,
                           int block, int w, int s, int gl, hz_partition_t* out);
 
+/* Communication plan of one rank: the exact NCCL operations hz_allgather_params /
+ * hz_reduce_scatter_grads issue, in order (the engine issues its calls from
+ * these plans).  Pure host functions; used by the CPU (gloo) tests to check
+ * that every send matches a receive on the peer.
+ *   HZ_PLAN_ALLGATHER: level-l all-gather of this rank's piece range_l
+ *     (send_off, elems) into range_{l-1} (recv_off), over the g_l members;
+ *     all-gather top = w (forward) or s (backward) down to 1, levels with
+ *     g_l = 1 omitted (O7/O8, Table VII).
+ *   HZ_PLAN_SENDRECV: level-l exchange with the member of level digit `peer`
+ *     (global rank peer_rank): send chunk `peer` of range_{l-1} (send_off,
+ *     elems) and receive that member's chunk for range_l (recv_off); peers in
+ *     ascending digit, levels from..to (O9, Table VIII).
+ * Offsets are global element offsets of the padded layer; code_bytes /
+ * scale_bytes are the bytes of one piece / chunk.  *n_out = number of steps
+ * (all of them, even when max is smaller; copies min(max, n)). */
+typedef enum { HZ_PLAN_ALLGATHER = 1, HZ_PLAN_SENDRECV = 2 } hz_plan_op;
+
+typedef struct {
+  int32_t op;         /* hz_plan_op */
+  int32_t level;      /* 1..L */
+  int32_t group;      /* g_level */
+  int32_t peer;       /* SENDRECV: peer's level digit (its level-communicator rank); else -1 */
+  int32_t peer_rank;  /* SENDRECV: peer's global rank; else -1 */
+  int32_t bits;       /* code width */
+  int64_t elems;
+  int64_t send_off;
+  int64_t recv_off;
+  int64_t code_bytes;
+  int64_t scale_bytes;
+} hz_comm_step;
+
+HZ_API hz_status hz_plan_allgather(const hz_partition_t* p, int backward, int bits,
+                                   hz_comm_step* out, int max, int* n_out);
+HZ_API hz_status hz_plan_reduce_scatter(const hz_partition_t* p, int from_level, int to_level,
+                                        const int* bits_per_level, hz_comm_step* out, int max,
+                                        int* n_out);
+
 /* ------------------------------------------------------- standalone codec ops */
 
 /* O4: quantize x[0..n) (dtype dt) into codes (n*bits/8

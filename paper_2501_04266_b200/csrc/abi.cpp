@@ -48,7 +48,7 @@ const char* const kSymbols[] = {
     "hz_init",             "hz_finalize",            "hz_partition",
     "hz_allgather_params", "hz_reduce_scatter_grads", "hz_flat_allgather",
     "hz_flat_reduce_scatter", "hz_trace_begin",      "hz_trace_end",
-    "hz_trace_read",
+    "hz_trace_read",       "hz_plan_allgather",      "hz_plan_reduce_scatter",
 };
 }  // namespace
 }  // namespace hz

@@ -302,14 +302,18 @@ hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward
     cur_s = sec_scales;
     top = s;
   }
+  std::vector<hz_comm_step> plan;
+  if ((rc = plan_allgather(p, backward, bits, &plan)) != HZ_OK) return rc;
+  size_t next = 0;
   for (int l = top; l >= 1; --l) {
     const int g = ctx->group[l - 1];
-    if (g > 1) {   // A3: in-place all-gather of range_l pieces into range_{l-1}
-      uint8_t* dc = ws_c + code_bytes(p->off[l - 1], bits);
-      float* ds = ws_s + p->off[l - 1] / B;
-      const int64_t nb = code_bytes(p->len[l], bits);
-      const int64_t ns = p->len[l] / B;
-      TraceScope t(st, "nccl_allgather", l, bits, p->len[l], (g - 1) * (nb + ns * 4));
+    if (next < plan.size() && plan[next].level == l) {   // A3: in-place all-gather of range_l pieces
+      const hz_comm_step& step = plan[next++];             //     into range_{l-1}
+      uint8_t* dc = ws_c + code_bytes(step.recv_off, bits);
+      float* ds = ws_s + step.recv_off / B;
+      const int64_t nb = step.code_bytes;
+      const int64_t ns = step.scale_bytes / 4;
+      TraceScope t(st, "nccl_allgather", l, bits, step.elems, (g - 1) * (nb + ns * 4));
       HZ_NCCL(ncclGroupStart(), "ncclGroupStart");
       HZ_NCCL(ncclAllGather(cur_c, dc, nb, ncclUint8, ctx->lvl[l - 1], st), "ncclAllGather(codes)");
       HZ_NCCL(ncclAllGather(cur_s, ds, ns, ncclFloat32, ctx->lvl[l - 1], st), "ncclAllGather(scales)");
@@ -372,6 +376,9 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
   if ((rc = run_quantize(grad, dt, base_len, bits_per_level[from_level - 1], B, a_c, a_s, st,
                          from_level)) != HZ_OK)
     return rc;
+  std::vector<hz_comm_step> plan;
+  if ((rc = plan_reduce_scatter(p, from_level, to_level, bits_per_level, &plan)) != HZ_OK) return rc;
+  size_t next = 0;
   for (int l = from_level; l <= to_level; ++l) {
     const int g = ctx->group[l - 1];
     const int d = ctx->digit[l - 1];
@@ -382,15 +389,20 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
     const uint8_t* ptr_c[kMaxG];
     const float* ptr_s[kMaxG];
     if (g > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "group size > 16 at one level");
-    if (g > 1) {   // A8: all-to-all within the level-l exchange group
+    if (g > 1) {   // A8: all-to-all within the level-l exchange group, from the plan
       TraceScope t(st, "nccl_alltoall", l, bits, cl, (g - 1) * (cb + cs * 4));
       HZ_NCCL(ncclGroupStart(), "ncclGroupStart");
-      for (int j = 0; j < g; ++j) {
-        if (j == d) continue;
-        HZ_NCCL(ncclSend(a_c + j * cb, cb, ncclUint8, j, ctx->lvl[l - 1], st), "ncclSend(codes)");
-        HZ_NCCL(ncclRecv(r_c + j * cb, cb, ncclUint8, j, ctx->lvl[l - 1], st), "ncclRecv(codes)");
-        HZ_NCCL(ncclSend(a_s + j * cs, cs, ncclFloat32, j, ctx->lvl[l - 1], st), "ncclSend(scales)");
-        HZ_NCCL(ncclRecv(r_s + j * cs, cs, ncclFloat32, j, ctx->lvl[l - 1], st), "ncclRecv(scales)");
+      for (; next < plan.size() && plan[next].level == l; ++next) {
+        const hz_comm_step& s = plan[next];
+        const int j = s.peer;
+        const int64_t rel = s.send_off - p->off[l - 1];   // chunk j of this rank's range_{l-1}
+        HZ_NCCL(ncclSend(a_c + code_bytes(rel, bits), s.code_bytes, ncclUint8, j, ctx->lvl[l - 1], st),
+                "ncclSend(codes)");
+        HZ_NCCL(ncclRecv(r_c + j * cb, s.code_bytes, ncclUint8, j, ctx->lvl[l - 1], st), "ncclRecv(codes)");
+        HZ_NCCL(ncclSend(a_s + rel / B, s.scale_bytes / 4, ncclFloat32, j, ctx->lvl[l - 1], st),
+                "ncclSend(scales)");
+        HZ_NCCL(ncclRecv(r_s + j * cs, s.scale_bytes / 4, ncclFloat32, j, ctx->lvl[l - 1], st),
+                "ncclRecv(scales)");
       }
       HZ_NCCL(ncclGroupEnd(), "ncclGroupEnd");
       t.end();

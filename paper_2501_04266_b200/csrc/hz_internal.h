@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/hz.h"
 
@@ -46,5 +47,10 @@ struct TraceScope {
 // ----------------------------------------------------------------- partition
 hz_status partition(int rank, int levels, const int* group, int64_t numel, int block, int w,
                     int s, int gl, hz_partition_t* out);
+
+// -------------------------------------------------------------------- plans
+hz_status plan_allgather(const hz_partition_t* p, int backward, int bits, std::vector<hz_comm_step>* out);
+hz_status plan_reduce_scatter(const hz_partition_t* p, int from_level, int to_level,
+                              const int* bits_per_level, std::vector<hz_comm_step>* out);
 
 }  // namespace hz

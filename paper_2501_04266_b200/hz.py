@@ -65,6 +65,18 @@ class TraceRec(ctypes.Structure):
                 ("elems", ctypes.c_int64), ("bytes", ctypes.c_int64), ("ms", ctypes.c_float)]
 
 
+class CommStep(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("level", ctypes.c_int32), ("group", ctypes.c_int32),
+                ("peer", ctypes.c_int32), ("peer_rank", ctypes.c_int32), ("bits", ctypes.c_int32),
+                ("elems", ctypes.c_int64), ("send_off", ctypes.c_int64), ("recv_off", ctypes.c_int64),
+                ("code_bytes", ctypes.c_int64), ("scale_bytes", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+PLAN_ALLGATHER, PLAN_SENDRECV = 1, 2
+
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _int = ctypes.c_int
@@ -101,6 +113,10 @@ _sig("hz_flat_reduce_scatter", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_trace_begin", [_int])
 _sig("hz_trace_end", [])
 _sig("hz_trace_read", [ctypes.POINTER(TraceRec), _int, ctypes.POINTER(ctypes.c_int)])
+_sig("hz_plan_allgather", [ctypes.POINTER(Partition), _int, _int, ctypes.POINTER(CommStep), _int,
+                           ctypes.POINTER(ctypes.c_int)])
+_sig("hz_plan_reduce_scatter", [ctypes.POINTER(Partition), _int, _int, ctypes.POINTER(ctypes.c_int),
+                                ctypes.POINTER(CommStep), _int, ctypes.POINTER(ctypes.c_int)])
 
 
 def _check(status):
@@ -157,6 +173,28 @@ def partition_ex(rank, group, numel, block=256, w=1, s=1, gl=None):
     _check(_lib.hz_partition_ex(rank, L, arr, numel, block, w, s, L if gl is None else gl,
                                 ctypes.byref(p)))
     return p
+
+
+def _plan(call, *args):
+    n = ctypes.c_int(0)
+    _check(call(*args, None, 0, ctypes.byref(n)))
+    steps = (CommStep * max(n.value, 1))()
+    _check(call(*args, steps, n.value, ctypes.byref(n)))
+    return [s.as_dict() for s in steps[:n.value]]
+
+
+def plan_allgather(p, backward=False, bits=8):
+    """hz_plan_allgather: the NCCL all-gathers this rank issues (host only)."""
+    return _plan(_lib.hz_plan_allgather, ctypes.byref(p), int(bool(backward)), bits)
+
+
+def plan_reduce_scatter(p, bits_per_level, from_level=1, to_level=None):
+    """hz_plan_reduce_scatter: the NCCL send/recv pairs this rank issues (host only)."""
+    L = p.levels
+    bpl = list(bits_per_level) + [4] * (L - len(bits_per_level))
+    arr = (ctypes.c_int * L)(*bpl)
+    return _plan(_lib.hz_plan_reduce_scatter, ctypes.byref(p), from_level,
+                 L if to_level is None else to_level, arr)
 
 
 # ------------------------------------------------------------------- codec ops
