@@ -117,6 +117,7 @@ struct Codes8<8> {
   uint2 r;
   __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const uint2*>(p)); }
   __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<uint2*>(p) = r; }
+  __device__ __forceinline__ void zero() { r = make_uint2(0u, 0u); }
   // exact float value of each code
   __device__ __forceinline__ void decode(float (&c)[8]) const {
     const unsigned x = r.x ^ 0x80808080u, y = r.y ^ 0x80808080u;   // two's complement -> +128 bias
@@ -139,12 +140,17 @@ struct Codes8<4> {
   unsigned r;
   __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const unsigned*>(p)); }
   __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<unsigned*>(p) = r; }
+  __device__ __forceinline__ void zero() { r = 0u; }
   __device__ __forceinline__ void decode(float (&c)[8]) const {
+    // nibble ^ 8 = code + 8 in [1, 15]; even / odd nibbles spread to bytes, then each
+    // byte is placed in the mantissa of 1.5*2^23 and the bias M + 8 removed.
+    const unsigned x = r ^ 0x88888888u;
+    const unsigned ev = x & 0x0F0F0F0Fu;           // codes 0, 2, 4, 6
+    const unsigned od = (x >> 4) & 0x0F0F0F0Fu;    // codes 1, 3, 5, 7
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      // (nibble ^ 8) = code + 8 in [1, 15], placed in the mantissa of 1.5*2^23
-      const unsigned m = ((r >> (4 * i)) & 0xFu) ^ 0x4B400008u;
-      c[i] = __fsub_rn(__uint_as_float(m), kMagic + 8.f);
+    for (int i = 0; i < 4; ++i) {
+      c[2 * i] = __fsub_rn(byte_as_magic(ev, i), kMagic + 8.f);
+      c[2 * i + 1] = __fsub_rn(byte_as_magic(od, i), kMagic + 8.f);
     }
   }
   __device__ __forceinline__ void set(const unsigned (&b)[8]) {
@@ -177,11 +183,13 @@ struct Codes4<4> {
     r = __ldg(reinterpret_cast<const unsigned short*>(p));
   }
   __device__ __forceinline__ void decode(float (&c)[4]) const {
-    const unsigned w = r;
+    const unsigned x = static_cast<unsigned>(r) ^ 0x8888u;   // nibble ^ 8 = code + 8
+    const unsigned ev = x & 0x0F0Fu;
+    const unsigned od = (x >> 4) & 0x0F0Fu;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const unsigned m = ((w >> (4 * i)) & 0xFu) ^ 0x4B400008u;
-      c[i] = __fsub_rn(__uint_as_float(m), kMagic + 8.f);
+    for (int i = 0; i < 2; ++i) {
+      c[2 * i] = __fsub_rn(byte_as_magic(ev, i), kMagic + 8.f);
+      c[2 * i + 1] = __fsub_rn(byte_as_magic(od, i), kMagic + 8.f);
     }
   }
 };
@@ -209,6 +217,46 @@ __device__ __forceinline__ float group_max(float v) {
 #pragma unroll
   for (int o = LPB / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
   return v;
+}
+
+// Quantize-and-store epilogue shared by k_quantize and k_reduce_requant for one
+// warp iteration of U full warp steps (NB = U * BPW consecutive blocks starting
+// at blk0; no bounds checks).  am[u] must already be the group-reduced absmax of
+// this lane's block in step u.  The scale / inv divisions run once per block:
+// lane k (< NB) divides for block k, then inv is broadcast back by shuffle, and
+// lanes 0..NB-1 store the NB consecutive scales in one coalesced store.
+template <int B, int BITS, int U>
+__device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB][8], const float (&am)[U],
+                                               int64_t blk0, int lane, uint8_t* __restrict__ codes,
+                                               float* __restrict__ scales) {
+  using G = Geo<B>;
+  constexpr int NB = U * G::BPW;
+  static_assert(NB <= 32, "one block per lane at most");
+  const int lb = lane / G::LPB;
+  const int ll = lane % G::LPB;
+  float mine = 0.f;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float t = __shfl_sync(kFull, am[u], (lane % G::BPW) * G::LPB);
+    if (lane / G::BPW == u) mine = t;
+  }
+  float scale, inv;
+  quant_params<BITS>(mine, scale, inv);
+  if (lane < NB) scales[blk0 + lane] = scale;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float iv = __shfl_sync(kFull, inv, u * G::BPW + lb);
+    const int64_t blk = blk0 + u * G::BPW + lb;
+#pragma unroll
+    for (int k = 0; k < G::NSUB; ++k) {
+      unsigned b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) b[i] = qbits(v[u][k][i], iv);
+      Codes8<BITS> out;
+      out.set(b);
+      out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ output store
@@ -262,4 +310,11 @@ __device__ __forceinline__ int64_t num_warps() {
 // min(ceil(warp_tasks / warps per CTA), SMs x resident CTAs of that kernel).
 int64_t grid_for(const void* kernel, int64_t warp_tasks);
 
+}  // namespace hz
+
+namespace hz {
+// Launch-parameter overrides for tuning sweeps (tools/kbench.py --tune): the
+// environment variable HZ_TUNE="name=value,..." is read once per process;
+// unknown names fall back to the compiled defaults.  Product runs leave it unset.
+int tune_param(const char* name, int dflt);
 }  // namespace hz

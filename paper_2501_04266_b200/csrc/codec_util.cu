@@ -47,3 +47,28 @@ int64_t grid_for(const void* kernel, int64_t warp_tasks) {
 }
 
 }  // namespace hz
+
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+namespace hz {
+
+int tune_param(const char* name, int dflt) {
+  static const std::string spec = [] {
+    const char* e = std::getenv("HZ_TUNE");
+    return std::string(e ? e : "");
+  }();
+  if (spec.empty()) return dflt;
+  const std::string key = std::string(name) + "=";
+  size_t pos = 0;
+  while (pos < spec.size()) {
+    size_t end = spec.find(',', pos);
+    if (end == std::string::npos) end = spec.size();
+    if (spec.compare(pos, key.size(), key) == 0) return std::atoi(spec.c_str() + pos + key.size());
+    pos = end + 1;
+  }
+  return dflt;
+}
+
+}  // namespace hz

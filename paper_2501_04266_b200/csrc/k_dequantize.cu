@@ -47,7 +47,16 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const uint8_t* __restri
   }
 }
 
-constexpr int kU = 4;
+constexpr int kU = 4;   // units in flight per lane (HZ_TUNE deq_u: 2, 4, 8, 16)
+
+template <int BITS, typename TO, int U>
+cudaError_t dequantize_u(const uint8_t* codes, const float* scales, int64_t nunits, int log2b, void* y,
+                         cudaStream_t st) {
+  auto kern = k_dequantize<BITS, TO, U>;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(codes, scales, nunits, log2b, static_cast<TO*>(y));
+  return cudaGetLastError();
+}
 
 template <int BITS, typename TO>
 cudaError_t dequantize_t(const uint8_t* codes, const float* scales, int64_t n, int block, void* y,
@@ -55,10 +64,12 @@ cudaError_t dequantize_t(const uint8_t* codes, const float* scales, int64_t n, i
   const int64_t nunits = n / 8;
   int log2b = 0;
   while ((1 << log2b) < block) ++log2b;
-  auto kern = k_dequantize<BITS, TO, kU>;
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * kU - 1) / (32 * kU));
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(codes, scales, nunits, log2b, static_cast<TO*>(y));
-  return cudaGetLastError();
+  switch (tune_param("deq_u", kU)) {
+    case 2: return dequantize_u<BITS, TO, 2>(codes, scales, nunits, log2b, y, st);
+    case 8: return dequantize_u<BITS, TO, 8>(codes, scales, nunits, log2b, y, st);
+    case 16: return dequantize_u<BITS, TO, 16>(codes, scales, nunits, log2b, y, st);
+    default: return dequantize_u<BITS, TO, kU>(codes, scales, nunits, log2b, y, st);
+  }
 }
 
 }  // namespace

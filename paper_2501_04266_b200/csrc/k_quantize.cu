@@ -7,8 +7,11 @@
 // contiguous elements; lane l owns 8 consecutive elements per 256-element
 // sub-chunk (one 16-byte bf16 load, one 8/4-byte code store per lane: each warp
 // instruction is one contiguous span).  A block's absmax is a shuffle-xor over
-// its LPB = min(32, B/8) lanes.  Each warp loads U steps before quantizing any
-// (memory-level parallelism); grid-stride over SMs x resident CTAs.
+// its LPB = min(32, B/8) lanes.  A warp iteration = U full steps (NB = U*BPW
+// blocks): all U*NSUB loads are issued first (memory-level parallelism), the
+// divisions run once per block (quantize_store), and the main loop has no bounds
+// checks so every shuffle is convergent; the last partial iteration (< NB
+// blocks) goes through a checked tail path.  Grid-stride over SMs x resident CTAs.
 #include "codec.cuh"
 
 namespace hz {
@@ -21,43 +24,63 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
                                                        uint8_t* __restrict__ codes,
                                                        float* __restrict__ scales) {
   using G = Geo<B>;
+  constexpr int NB = U * G::BPW;
   const int lane = threadIdx.x & 31;
   const int lb = lane / G::LPB;
   const int ll = lane % G::LPB;
   const int64_t warp = global_warp();
   const int64_t nwarps = num_warps();
-  const int64_t nsteps = (nblocks + G::BPW - 1) / G::BPW;
+  const int64_t nfull = nblocks / NB;
 
-  for (int64_t s0 = warp * U; s0 < nsteps; s0 += nwarps * U) {
+  for (int64_t it = warp; it < nfull; it += nwarps) {
+    const int64_t blk0 = it * NB;
     In8<T> raw[U][G::NSUB];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t blk = (s0 + u) * G::BPW + lb;
-      if (s0 + u < nsteps && blk < nblocks) {
+      const int64_t blk = blk0 + u * G::BPW + lb;
 #pragma unroll
-        for (int k = 0; k < G::NSUB; ++k) raw[u][k].load(x + blk * B + k * G::SUBSTRIDE + ll * 8);
-      }
+      for (int k = 0; k < G::NSUB; ++k) raw[u][k].load(x + blk * B + k * G::SUBSTRIDE + ll * 8);
     }
+    float v[U][G::NSUB][8];
+    float am[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t blk = (s0 + u) * G::BPW + lb;
-      const bool valid = (s0 + u < nsteps) && blk < nblocks;
-      float v[G::NSUB][8];
-      float am = 0.f;
+      float m = 0.f;
 #pragma unroll
       for (int k = 0; k < G::NSUB; ++k) {
+        raw[u][k].get(v[u][k]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(v[u][k][i]));
+      }
+      am[u] = group_max<G::LPB>(m);
+    }
+    quantize_store<B, BITS, U>(v, am, blk0, lane, codes, scales);
+  }
+
+  // tail: the last nblocks % NB blocks, one warp step at a time, bounds-checked
+  const int64_t tail0 = nfull * NB;
+  if (tail0 < nblocks && warp == nwarps - 1) {
+    for (int64_t b0 = tail0; b0 < nblocks; b0 += G::BPW) {
+      const int64_t blk = b0 + lb;
+      const bool valid = blk < nblocks;
+      float v[G::NSUB][8];
+      float m = 0.f;
+#pragma unroll
+      for (int k = 0; k < G::NSUB; ++k) {
+        In8<T> r;
         if (valid) {
-          raw[u][k].get(v[k]);
+          r.load(x + blk * B + k * G::SUBSTRIDE + ll * 8);
+          r.get(v[k]);
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) v[k][i] = 0.f;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) am = fmaxf(am, fabsf(v[k][i]));
+        for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(v[k][i]));
       }
-      am = group_max<G::LPB>(am);
+      m = group_max<G::LPB>(m);
       float scale, inv;
-      quant_params<BITS>(am, scale, inv);
+      quant_params<BITS>(m, scale, inv);
       if (valid) {
 #pragma unroll
         for (int k = 0; k < G::NSUB; ++k) {
@@ -74,18 +97,30 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
   }
 }
 
-constexpr int kU = 4;   // warp steps in flight per warp
-constexpr int uq(int B) { return B > 256 ? 1 : kU; }   // B > 256: NSUB loads per step already
+constexpr int kU = 4;   // warp steps per warp iteration
+// B > 256: NSUB = B/256 loads per step already; B < 256: NB = U*BPW <= 32
+constexpr int uq(int B) { return B > 256 ? 1 : kU; }
+
+template <typename T, int B, int BITS, int U>
+cudaError_t quantize_u(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st) {
+  const int64_t nblocks = n / B;
+  constexpr int NB = U * Geo<B>::BPW;
+  auto kern = k_quantize<T, B, BITS, U>;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), nblocks / NB + 1);
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(static_cast<const T*>(x), nblocks, codes, scales);
+  return cudaGetLastError();
+}
 
 template <typename T, int B, int BITS>
 cudaError_t quantize_t(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st) {
-  const int64_t nblocks = n / B;
-  const int64_t nsteps = (nblocks + Geo<B>::BPW - 1) / Geo<B>::BPW;
-  constexpr int U = uq(B);
-  auto kern = k_quantize<T, B, BITS, U>;
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nsteps + U - 1) / U);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(static_cast<const T*>(x), nblocks, codes, scales);
-  return cudaGetLastError();
+  if constexpr (B == 256) {   // HZ_TUNE q_u: 2, 4, 8 (the default block only)
+    switch (tune_param("q_u", kU)) {
+      case 2: return quantize_u<T, B, BITS, 2>(x, n, codes, scales, st);
+      case 8: return quantize_u<T, B, BITS, 8>(x, n, codes, scales, st);
+      default: break;
+    }
+  }
+  return quantize_u<T, B, BITS, uq(B)>(x, n, codes, scales, st);
 }
 
 template <typename T, int B>

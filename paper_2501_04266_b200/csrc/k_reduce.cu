@@ -32,104 +32,144 @@ struct RedArgs {
 };
 
 // ------------------------------------------------------------ requantizing reduce
-// GT > 0: exactly GT inputs, all loads of a step issued before the sums.
-// GT == 0: runtime a.g inputs, one input at a time.
+// Sum of the inputs for U warp steps starting at block blk0 (this lane's 8-element
+// sub-chunks).  GT > 0: exactly GT inputs, every load of the U steps issued before
+// any sum.  GT == 0: runtime a.g inputs, one input at a time.  `valid` masks
+// steps past the end (tail path only; the main loop passes all-true).
+template <int B, int BIN, int GT, int U>
+__device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int lane, const bool (&valid)[U],
+                                          float (&acc)[U][Geo<B>::NSUB][8]) {
+  using G = Geo<B>;
+  const int lb = lane / G::LPB;
+  const int ll = lane % G::LPB;
+  if constexpr (GT > 0) {
+    Codes8<BIN> raw[U][GT][G::NSUB];
+    float sc[U][GT];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t blk = blk0 + u * G::BPW + lb;
+#pragma unroll
+      for (int p = 0; p < GT; ++p) {
+        sc[u][p] = 0.f;
+        if (valid[u]) {
+#pragma unroll
+          for (int k = 0; k < G::NSUB; ++k)
+            raw[u][p][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
+          sc[u][p] = __ldg(a.s[p] + blk);
+        } else {
+#pragma unroll
+          for (int k = 0; k < G::NSUB; ++k) raw[u][p][k].zero();
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int k = 0; k < G::NSUB; ++k) {
+        float c[8];
+        raw[u][0][k].decode(c);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[u][k][i] = __fmul_rn(c[i], sc[u][0]);
+#pragma unroll
+        for (int p = 1; p < GT; ++p) {
+          raw[u][p][k].decode(c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[u][k][i] = __fadd_rn(acc[u][k][i], __fmul_rn(c[i], sc[u][p]));
+        }
+      }
+    }
+  } else {
+    for (int p = 0; p < a.g; ++p) {
+      Codes8<BIN> raw[U][G::NSUB];
+      float sc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t blk = blk0 + u * G::BPW + lb;
+        sc[u] = 0.f;
+        if (valid[u]) {
+#pragma unroll
+          for (int k = 0; k < G::NSUB; ++k)
+            raw[u][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
+          sc[u] = __ldg(a.s[p] + blk);
+        } else {
+#pragma unroll
+          for (int k = 0; k < G::NSUB; ++k) raw[u][k].zero();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < G::NSUB; ++k) {
+          float c[8];
+          raw[u][k].decode(c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float xh = __fmul_rn(c[i], sc[u]);
+            acc[u][k][i] = p == 0 ? xh : __fadd_rn(acc[u][k][i], xh);
+          }
+        }
+    }
+  }
+}
+
+// Main loop: warp iterations of U full steps (NB = U*BPW blocks), no bounds checks,
+// quantize_store epilogue (one division per block).  Tail (< NB blocks): one
+// checked step at a time by the last warp.
 template <int B, int BIN, int BOUT, int GT, int U>
 __global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_constant__ RedArgs a) {
   using G = Geo<B>;
+  constexpr int NB = U * G::BPW;
   const int lane = threadIdx.x & 31;
   const int lb = lane / G::LPB;
   const int ll = lane % G::LPB;
   const int64_t warp = global_warp();
   const int64_t nwarps = num_warps();
   const int64_t nblocks = a.n / B;
-  const int64_t nsteps = (nblocks + G::BPW - 1) / G::BPW;
-  constexpr int GP = GT > 0 ? GT : 1;
+  const int64_t nfull = nblocks / NB;
 
-  for (int64_t s0 = warp * U; s0 < nsteps; s0 += nwarps * U) {
+  for (int64_t it = warp; it < nfull; it += nwarps) {
+    const int64_t blk0 = it * NB;
+    bool valid[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) valid[u] = true;
     float acc[U][G::NSUB][8];
-    if constexpr (GT > 0) {
-      Codes8<BIN> raw[U][GP][G::NSUB];
-      float sc[U][GP];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t blk = (s0 + u) * G::BPW + lb;
-        if (s0 + u < nsteps && blk < nblocks) {
-#pragma unroll
-          for (int p = 0; p < GP; ++p) {
-#pragma unroll
-            for (int k = 0; k < G::NSUB; ++k)
-              raw[u][p][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
-            sc[u][p] = __ldg(a.s[p] + blk);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-#pragma unroll
-        for (int k = 0; k < G::NSUB; ++k) {
-          float c[8];
-          raw[u][0][k].decode(c);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[u][k][i] = __fmul_rn(c[i], sc[u][0]);
-#pragma unroll
-          for (int p = 1; p < GP; ++p) {
-            raw[u][p][k].decode(c);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[u][k][i] = __fadd_rn(acc[u][k][i], __fmul_rn(c[i], sc[u][p]));
-          }
-        }
-      }
-    } else {
-      for (int p = 0; p < a.g; ++p) {
-        Codes8<BIN> raw[U][G::NSUB];
-        float sc[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t blk = (s0 + u) * G::BPW + lb;
-          sc[u] = 0.f;
-          if (s0 + u < nsteps && blk < nblocks) {
-#pragma unroll
-            for (int k = 0; k < G::NSUB; ++k)
-              raw[u][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
-            sc[u] = __ldg(a.s[p] + blk);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int k = 0; k < G::NSUB; ++k) {
-            float c[8];
-            raw[u][k].decode(c);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float xh = __fmul_rn(c[i], sc[u]);
-              acc[u][k][i] = p == 0 ? xh : __fadd_rn(acc[u][k][i], xh);
-            }
-          }
-      }
-    }
-
+    sum_steps<B, BIN, GT, U>(a, blk0, lane, valid, acc);
+    float am[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t blk = (s0 + u) * G::BPW + lb;
-      const bool valid = (s0 + u < nsteps) && blk < nblocks;
-      float am = 0.f;
+      float m = 0.f;
 #pragma unroll
       for (int k = 0; k < G::NSUB; ++k)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) am = fmaxf(am, valid ? fabsf(acc[u][k][i]) : 0.f);
-      am = group_max<G::LPB>(am);
+        for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(acc[u][k][i]));
+      am[u] = group_max<G::LPB>(m);
+    }
+    quantize_store<B, BOUT, U>(acc, am, blk0, lane, a.oc, a.os);
+  }
+
+  const int64_t tail0 = nfull * NB;
+  if (tail0 < nblocks && warp == nwarps - 1) {
+    for (int64_t b0 = tail0; b0 < nblocks; b0 += G::BPW) {
+      const int64_t blk = b0 + lb;
+      bool valid[1] = {blk < nblocks};
+      float acc[1][G::NSUB][8];
+      sum_steps<B, BIN, GT, 1>(a, b0, lane, valid, acc);
+      float m = 0.f;
+#pragma unroll
+      for (int k = 0; k < G::NSUB; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m = fmaxf(m, valid[0] ? fabsf(acc[0][k][i]) : 0.f);
+      m = group_max<G::LPB>(m);
       float scale, inv;
-      quant_params<BOUT>(am, scale, inv);
-      if (valid) {
+      quant_params<BOUT>(m, scale, inv);
+      if (valid[0]) {
 #pragma unroll
         for (int k = 0; k < G::NSUB; ++k) {
-          unsigned b[8];
+          unsigned bq[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) b[i] = qbits(acc[u][k][i], inv);
+          for (int i = 0; i < 8; ++i) bq[i] = qbits(acc[0][k][i], inv);
           Codes8<BOUT> out;
-          out.set(b);
+          out.set(bq);
           out.store(a.oc + (blk * B + k * G::SUBSTRIDE + ll * 8) * BOUT / 8);
         }
         if (ll == 0) a.os[blk] = scale;
@@ -225,18 +265,29 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
 }
 
 // ---------------------------------------------------------------------- launch
-constexpr int kUR = 2;   // warp steps in flight per warp (requant)
+constexpr int kUR = 4;   // warp steps per warp iteration (requant)
 constexpr int kUF = 4;   // 4-element units in flight per lane (fp32 out)
 constexpr int ur(int B) { return B > 256 ? 1 : kUR; }
 
-template <int B, int BIN, int BOUT, int GT>
-cudaError_t requant_t(const RedArgs& a, cudaStream_t st) {
-  const int64_t nsteps = (a.n / B + Geo<B>::BPW - 1) / Geo<B>::BPW;
-  constexpr int U = ur(B);
+template <int B, int BIN, int BOUT, int GT, int U>
+cudaError_t requant_u(const RedArgs& a, cudaStream_t st) {
+  constexpr int NB = U * Geo<B>::BPW;
   auto kern = k_reduce_requant<B, BIN, BOUT, GT, U>;
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nsteps + U - 1) / U);
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), a.n / B / NB + 1);
   kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a);
   return cudaGetLastError();
+}
+
+template <int B, int BIN, int BOUT, int GT>
+cudaError_t requant_t(const RedArgs& a, cudaStream_t st) {
+  if constexpr (B == 256 && GT > 0 && GT <= 2) {   // HZ_TUNE rq_u: 1, 2, 4
+    switch (tune_param("rq_u", kUR)) {
+      case 1: return requant_u<B, BIN, BOUT, GT, 1>(a, st);
+      case 2: return requant_u<B, BIN, BOUT, GT, 2>(a, st);
+      default: break;
+    }
+  }
+  return requant_u<B, BIN, BOUT, GT, ur(B)>(a, st);
 }
 
 template <int B, int BIN, int BOUT>
@@ -258,13 +309,25 @@ cudaError_t requant_b(const RedArgs& a, int bits_in, int bits_out, cudaStream_t 
   return bits_out == 8 ? requant_g<B, 4, 8>(a, st) : requant_g<B, 4, 4>(a, st);
 }
 
-template <int BIN, int GT>
-cudaError_t f32_t(const RedArgs& a, int log2b, cudaStream_t st) {
+template <int BIN, int GT, int U>
+cudaError_t f32_u(const RedArgs& a, int log2b, cudaStream_t st) {
   const int64_t nunits = a.n / 4;
-  auto kern = k_reduce_f32<BIN, GT, kUF>;
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * kUF - 1) / (32 * kUF));
+  auto kern = k_reduce_f32<BIN, GT, U>;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
   kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, log2b);
   return cudaGetLastError();
+}
+
+template <int BIN, int GT>
+cudaError_t f32_t(const RedArgs& a, int log2b, cudaStream_t st) {
+  if constexpr (GT > 0 && GT <= 2) {   // HZ_TUNE rf_u: 2, 4, 8
+    switch (tune_param("rf_u", kUF)) {
+      case 2: return f32_u<BIN, GT, 2>(a, log2b, st);
+      case 8: return f32_u<BIN, GT, 8>(a, log2b, st);
+      default: break;
+    }
+  }
+  return f32_u<BIN, GT, kUF>(a, log2b, st);
 }
 
 template <int BIN>
