@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flat", action="store_true")
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 collective transport: fused NVLink peer-memory kernels (p2p) or NCCL")
     ap.add_argument("--cpu-sample-layers", type=int, default=4)
     return ap.parse_args()
 
@@ -168,6 +170,7 @@ class Model:
         L = ctx.levels
         B = args.block
         max_np = 0
+        self.p2p = ctx.p2p
         for i, (name, numel) in enumerate(tensors):
             p = ctx.partition(numel, B, w=1, s=1, gl=L)
             Np = p.padded_numel
@@ -183,8 +186,8 @@ class Model:
             _, len_l = p.range(L)
             t = {
                 "name": name, "numel": numel, "p": p, "primary": primary, "grad": grad,
-                "sec_c": torch.empty(len_s * args.qwz_bits // 8, dtype=torch.uint8, device=device),
-                "sec_s": torch.empty(len_s // B, dtype=torch.float32, device=device),
+                "sec_c": self.alloc(len_s * args.qwz_bits // 8, torch.uint8, device),
+                "sec_s": self.alloc(len_s // B, torch.float32, device),
                 "shard": torch.empty(len_l, dtype=torch.float32, device=device),
             }
             self.tensors.append(t)
@@ -192,6 +195,12 @@ class Model:
         self.full = [torch.empty(max_np, dtype=torch.bfloat16, device=device) for _ in range(2)]
         self.bits = [args.qgz_bits] * L
         self.logical_bytes = sum(6 * t["numel"] for t in self.tensors)
+
+    def alloc(self, numel, dtype, device):
+        """hpZ secondaries must be peer-readable (symmetric pool) in P2P mode."""
+        if self.p2p:
+            return self.ctx.sym_alloc(numel, dtype)
+        return self.torch.empty(numel, dtype=dtype, device=device)
 
     def step(self, stream):
         ctx, bits = self.ctx, self.args.qwz_bits
@@ -202,6 +211,23 @@ class Model:
             ctx.allgather_params(t["p"], None, t["sec_c"], t["sec_s"], self.full[i & 1], bits=bits,
                                  backward=True, stream=stream)
             ctx.reduce_scatter_grads(t["p"], t["grad"], t["shard"], self.bits, stream=stream)
+
+
+def p2p_pool_bytes(args, group):
+    """Symmetric pool: every tensor's hpZ secondary + the library's per-level send slots."""
+    from paper_2501_04266_b200 import synth
+    W = math.prod(group)
+    B = args.block
+    unit = W * 4 * B
+    total = 0
+    max_np = 0
+    for _, numel in synth.model_tensors(args.config):
+        Np = -(-numel // unit) * unit
+        len_s = Np // group[0]
+        total += len_s * args.qwz_bits // 8 + len_s // B * 4 + 512
+        max_np = max(max_np, Np)
+    total += 2 * len(group) * (max_np + max_np // B * 4 + 512)   # slots (may grow once)
+    return total + (64 << 20)
 
 
 def max_over_ranks(x, world):
@@ -264,6 +290,9 @@ def run_hz(args):
         dist.broadcast_object_list(box, src=0)
         uid = box[0]
     ctx = hz.Context(rank, world, uid, group, local)
+    transport = args.transport if world > 1 else "local"
+    if transport == "p2p":
+        ctx.enable_p2p(p2p_pool_bytes(args, group))
     model = Model(hz, ctx, torch, args.config, rank, world, args, device)
     stream = torch.cuda.current_stream()
 
@@ -344,6 +373,7 @@ def run_hz(args):
             "io": "bf16 params/grads in, bf16 gathered layers out, fp32 scales, fp32 gradient shard",
             "l2": "inputs larger than L2 (each step streams several GB); no flush",
             "parallelism": f"dp{world} hierarchical ({'x'.join(map(str, group))})",
+            "transport": transport,
         },
         "roofline": roofline,
         "cpu_baseline": cpu,

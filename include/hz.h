@@ -234,6 +234,26 @@ HZ_API hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, c
                                   const int* bits_per_level, float* shard, int accumulate,
                                   void* stream);
 
+/* NVLink peer-memory transport (collective over all ranks of the context; one
+ * node, world <= 8).  Allocates this rank's symmetric pool of pool_bytes,
+ * exchanges CUDA IPC handles over NCCL and maps every peer's pool.  Afterwards
+ * hz_allgather_params / hz_reduce_scatter_grads run with the collective fused
+ * into the codec kernels: the gather+dequantize kernel reads the members' codes
+ * straight from their pools over NVLink and the level reduce reads the peers'
+ * chunks in place (no NCCL on the data path); cross-GPU ordering uses per-phase
+ * flags in the pools.  Results are bitwise identical to the NCCL transport.
+ * Requirements in P2P mode: the hpZ secondary buffers passed to
+ * hz_allgather_params must come from hz_sym_alloc; all calls of the context on
+ * one stream.  HZ_ERR_UNSUPPORTED if a peer cannot be mapped. */
+HZ_API hz_status hz_enable_p2p(hz_ctx* ctx, size_t pool_bytes);
+HZ_API hz_status hz_p2p_enabled(const hz_ctx* ctx, int* out);
+
+/* Symmetric allocation from the P2P pool (256-byte aligned).  Every rank must make
+ * the same sequence of calls with the same sizes, so that a buffer has the same
+ * pool offset on every rank.  Freed with the context.  HZ_ERR_INVALID when the pool
+ * is exhausted or P2P is not enabled. */
+HZ_API hz_status hz_sym_alloc(hz_ctx* ctx, size_t bytes, void** out);
+
 /* Flat ZeRO-3 baseline (Table VII/VIII row "ZeRO-3"): plain ncclAllGather of
  * the rank's bf16/fp16/fp32 chunk (numel/world elements, rank order) into
  * out[numel], and plain ncclReduceScatter(sum) of in[numel] into

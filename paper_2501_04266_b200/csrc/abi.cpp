@@ -49,6 +49,7 @@ const char* const kSymbols[] = {
     "hz_allgather_params", "hz_reduce_scatter_grads", "hz_flat_allgather",
     "hz_flat_reduce_scatter", "hz_trace_begin",      "hz_trace_end",
     "hz_trace_read",       "hz_plan_allgather",      "hz_plan_reduce_scatter",
+    "hz_enable_p2p",       "hz_p2p_enabled",         "hz_sym_alloc",
 };
 }  // namespace
 }  // namespace hz

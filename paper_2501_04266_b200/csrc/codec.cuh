@@ -318,3 +318,62 @@ namespace hz {
 // unknown names fall back to the compiled defaults.  Product runs leave it unset.
 int tune_param(const char* name, int dflt);
 }  // namespace hz
+
+// ======================================================================= P2P sync
+// Cross-GPU phase synchronisation for the NVLink peer-memory transport (engine
+// P2P mode).  Every collective phase has a global number (same on all ranks).
+// Flags live in each rank's IPC-mapped pool header: ready[q] / done[q] = the last
+// phase rank q signalled to this rank.  A kernel may
+//   * wait (prologue, thread 0 of every CTA, ld.acquire.sys spin) until
+//     ready[q] >= wait_ready and done[q] >= wait_done for every rank q;
+//   * signal (epilogue, last CTA to finish, after __threadfence_system) by a
+//     st.release.sys of sig_ready / sig_done into every rank's flag slot for
+//     this rank.
+// A spin longer than ~20 s traps (a dead peer must not hang the GPU).
+namespace hz {
+namespace dev {
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void sync_wait(const SyncArgs& s) {
+  if (!(s.wait_ready | s.wait_done)) return;
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    for (int q = 0; q < s.world; ++q) {
+      while ((s.wait_ready && ld_acquire_sys(s.ready_local + q) < s.wait_ready) ||
+             (s.wait_done && ld_acquire_sys(s.done_local + q) < s.wait_done)) {
+        if (globaltimer() - t0 > 20000000000ull) __trap();
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void sync_signal(const SyncArgs& s) {
+  if (!(s.sig_ready | s.sig_done)) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(s.counter, 1u) == gridDim.x - 1) {
+      *s.counter = 0u;
+      __threadfence_system();
+      for (int q = 0; q < s.world; ++q) {
+        if (s.sig_ready) st_release_sys(s.ready_remote[q], s.sig_ready);
+        if (s.sig_done) st_release_sys(s.done_remote[q], s.sig_done);
+      }
+    }
+  }
+}
+}  // namespace dev
+}  // namespace hz

@@ -1,0 +1,77 @@
+// hz_ctx and the engine helpers shared by engine.cpp (NCCL transport) and
+// p2p.cpp (NVLink peer-memory transport).  Internal header.
+#pragma once
+
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "hz_internal.h"
+
+struct hz_ctx {
+  int rank = 0, world = 1, levels = 0, device = 0;
+  int group[HZ_MAX_LEVELS] = {0};
+  int digit[HZ_MAX_LEVELS] = {0};
+  ncclComm_t world_comm = nullptr;
+  ncclComm_t lvl[HZ_MAX_LEVELS] = {nullptr};
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  // NCCL transport workspace
+  Buf ag_c, ag_s;                      // full-layer codes / scales (all-gather)
+  Buf rs_a_c, rs_a_s, rs_b_c, rs_b_s;  // ping-pong send buffers (reduce-scatter)
+  Buf rs_r_c, rs_r_s;                  // receive slots (reduce-scatter)
+
+  // NVLink P2P transport (hz_enable_p2p): one IPC-mapped symmetric pool per rank.
+  struct P2P {
+    bool on = false;
+    char* pool = nullptr;                       // local base
+    size_t bytes = 0;
+    size_t used = 0;                            // bump allocator (same on every rank)
+    char* peer[hz::kMaxWorld] = {nullptr};      // every rank's pool base, mapped here
+    unsigned long long phase = 0;               // last phase number issued
+    struct Slot {
+      size_t off = 0, cap = 0;
+    };
+    Slot ag_prim_c, ag_prim_s;                  // quantized primary when s != w
+    Slot rs_c[HZ_MAX_LEVELS + 1], rs_s[HZ_MAX_LEVELS + 1];   // level-l send buffers
+  } p2p;
+};
+
+namespace hz {
+
+// header of the symmetric pool: ready[8] u64 | done[8] u64 | counter u32
+constexpr size_t kPoolHeader = 4096;
+constexpr size_t kReadyOff = 0, kDoneOff = 64, kCounterOff = 128;
+
+hz_status cuda_fail(cudaError_t e, const char* what);
+hz_status nccl_fail(ncclResult_t r, const char* what);
+hz_status grow(hz_ctx::Buf& b, size_t need);
+int64_t elem_bytes(hz_dtype dt);
+
+// traced kernel launches (sync may be nullptr)
+hz_status run_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block, uint8_t* c,
+                       float* s, cudaStream_t st, int level, const SyncArgs* sync = nullptr);
+hz_status run_dequantize(const uint8_t* c, const float* s, int64_t n, int bits, int block, void* y,
+                         hz_dtype odt, cudaStream_t st, int level);
+hz_status run_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,
+                                hz_dtype odt, cudaStream_t st, int level, const SyncArgs* sync,
+                                int64_t remote_bytes);
+hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
+                     int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
+                     cudaStream_t st, int level, const SyncArgs* sync = nullptr);
+hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
+
+// P2P transport (p2p.cpp)
+bool in_pool(const hz_ctx* ctx, const void* p, size_t bytes);
+hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, const void* primary,
+                        hz_dtype dt, int bits, uint8_t* sec_codes, float* sec_scales, void* full_out,
+                        hz_dtype out_dt, cudaStream_t st);
+hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
+                             int from_level, int to_level, const int* bits_per_level, float* shard,
+                             int accumulate, cudaStream_t st);
+void p2p_release(hz_ctx* ctx);
+
+}  // namespace hz

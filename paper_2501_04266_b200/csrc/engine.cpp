@@ -18,30 +18,12 @@
 // (= destination digit j) is a contiguous slice of both arrays, so the
 // all-to-all is grouped ncclSend/ncclRecv of slices; the own chunk is read in
 // place by the reduce kernel and never enters NCCL.
-#include <nccl.h>
-
 #include <cstring>
 #include <string>
 
-#include "hz_internal.h"
-
-struct hz_ctx {
-  int rank = 0, world = 1, levels = 0, device = 0;
-  int group[HZ_MAX_LEVELS] = {0};
-  int digit[HZ_MAX_LEVELS] = {0};
-  ncclComm_t world_comm = nullptr;
-  ncclComm_t lvl[HZ_MAX_LEVELS] = {nullptr};
-  struct Buf {
-    void* p = nullptr;
-    size_t cap = 0;
-  };
-  Buf ag_c, ag_s;                      // full-layer codes / scales (all-gather)
-  Buf rs_a_c, rs_a_s, rs_b_c, rs_b_s;  // ping-pong send buffers (reduce-scatter)
-  Buf rs_r_c, rs_r_s;                  // receive slots (reduce-scatter)
-};
+#include "ctx.h"
 
 namespace hz {
-namespace {
 
 hz_status cuda_fail(cudaError_t e, const char* what) {
   return fail(HZ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -78,6 +60,7 @@ hz_status grow(hz_ctx::Buf& b, size_t need) {
   return HZ_OK;
 }
 
+namespace {
 void free_buf(hz_ctx::Buf& b) {
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
@@ -105,19 +88,24 @@ hz_status check_partition(const hz_ctx* ctx, const hz_partition_t* p) {
   return HZ_OK;
 }
 
+}  // namespace
+
 int64_t elem_bytes(hz_dtype dt) { return dt == HZ_F32 ? 4 : 2; }
 
+namespace {
 bool dtype_ok(hz_dtype dt) { return dt == HZ_F32 || dt == HZ_BF16 || dt == HZ_F16; }
 
 ncclDataType_t nccl_dtype(hz_dtype dt) {
   return dt == HZ_F32 ? ncclFloat32 : (dt == HZ_BF16 ? ncclBfloat16 : ncclFloat16);
 }
 
+}  // namespace
+
 // traced kernel launches ----------------------------------------------------
 hz_status run_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block, uint8_t* c,
-                       float* s, cudaStream_t st, int level) {
+                       float* s, cudaStream_t st, int level, const SyncArgs* sync) {
   TraceScope t(st, "quantize", level, bits, n, n * elem_bytes(dt) + code_bytes(n, bits) + n / block * 4);
-  cudaError_t e = launch_quantize(x, dt, n, bits, block, c, s, st);
+  cudaError_t e = launch_quantize(x, dt, n, bits, block, c, s, st, sync);
   t.end();
   if (e != cudaSuccess) return cuda_fail(e, "quantize kernel launch");
   return HZ_OK;
@@ -132,14 +120,25 @@ hz_status run_dequantize(const uint8_t* c, const float* s, int64_t n, int bits, 
   return HZ_OK;
 }
 
+hz_status run_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,
+                                hz_dtype odt, cudaStream_t st, int level, const SyncArgs* sync,
+                                int64_t remote_bytes) {
+  TraceScope t(st, "gather_dequantize", level, bits, n,
+               code_bytes(n, bits) + n / block * 4 + n * elem_bytes(odt) - remote_bytes);
+  cudaError_t e = launch_gather_dequantize(pc, n, bits, block, y, odt, st, sync);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "gather-dequantize kernel launch");
+  return HZ_OK;
+}
+
 hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
                      int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
-                     cudaStream_t st, int level) {
+                     cudaStream_t st, int level, const SyncArgs* sync) {
   const int64_t in_bytes = g * (code_bytes(n, bits_in) + n / block * 4);
   const int64_t out_bytes =
       bits_out ? code_bytes(n, bits_out) + n / block * 4 : n * 4 * (acc ? 2 : 1);
   TraceScope t(st, bits_out ? "reduce_requant" : "reduce", level, bits_in, n, in_bytes + out_bytes);
-  cudaError_t e = launch_reduce(g, c, s, n, bits_in, block, bits_out, oc, os, of, acc, st);
+  cudaError_t e = launch_reduce(g, c, s, n, bits_in, block, bits_out, oc, os, of, acc, st, sync);
   t.end();
   if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
   return HZ_OK;
@@ -154,7 +153,6 @@ hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st) 
   return HZ_OK;
 }
 
-}  // namespace
 }  // namespace hz
 
 extern "C" {
@@ -231,6 +229,7 @@ hz_status hz_finalize(hz_ctx* ctx) {
   if (!ctx) return HZ_OK;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  p2p_release(ctx);
   for (int l = 0; l < HZ_MAX_LEVELS; ++l)
     if (ctx->lvl[l]) ncclCommDestroy(ctx->lvl[l]);
   if (ctx->world_comm) ncclCommDestroy(ctx->world_comm);
@@ -274,6 +273,8 @@ hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward
     clear_error();
     return HZ_OK;
   }
+  if (ctx->p2p.on)   // NVLink peer-memory transport: fused gather + dequantize
+    return p2p_allgather(ctx, p, backward, primary, dt, bits, sec_codes, sec_scales, full_out, out_dt, st);
   hz_status rc;
   if ((rc = grow(ctx->ag_c, code_bytes(Np, bits))) != HZ_OK) return rc;
   if ((rc = grow(ctx->ag_s, Np / B * 4)) != HZ_OK) return rc;
@@ -359,6 +360,8 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
     clear_error();
     return HZ_OK;
   }
+  if (ctx->p2p.on)   // NVLink peer-memory transport: reduce reads the peers' chunks in place
+    return p2p_reduce_scatter(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard, accumulate, st);
   if ((rc = grow(ctx->rs_a_c, base_len)) != HZ_OK) return rc;
   if ((rc = grow(ctx->rs_a_s, base_len / B * 4)) != HZ_OK) return rc;
   if ((rc = grow(ctx->rs_b_c, base_len)) != HZ_OK) return rc;

@@ -21,16 +21,49 @@ bool bits_ok(int bits);            // 4 or 8
 bool aligned16(const void* p);
 int64_t code_bytes(int64_t n, int bits);   // n * bits / 8
 
+// ------------------------------------------------------------- P2P phase sync
+// (see codec.cuh for the protocol).  A zero-initialised SyncArgs means "no sync".
+constexpr int kMaxWorld = 8;
+struct SyncArgs {
+  unsigned long long* ready_local;
+  unsigned long long* done_local;
+  unsigned long long* ready_remote[kMaxWorld];
+  unsigned long long* done_remote[kMaxWorld];
+  unsigned int* counter;
+  int world;
+  unsigned long long wait_ready, wait_done, sig_ready, sig_done;
+};
+
+// Pieces of a gathered layer for the fused gather+dequantize kernel: piece j
+// covers elements [j*len, (j+1)*len) and its codes / scales are read from
+// (possibly peer-mapped) c[j] / s[j].  n == 1 with c[0], s[0] is a plain
+// dequantize.  Optionally the codes of [sec_lo, sec_hi) are also copied into
+// sec_c / sec_s (hpZ secondary kept from a flattened gather).
+struct Pieces {
+  const uint8_t* c[kMaxWorld];
+  const float* s[kMaxWorld];
+  int n;
+  int64_t len;
+  uint8_t* sec_c;
+  float* sec_s;
+  int64_t sec_lo, sec_hi;
+};
+
 // ----------------------------------------------------------------- kernels
 // All launchers validate nothing (the ABI layer does) and return cudaGetLastError().
+// `sync` may be nullptr (no cross-GPU phase synchronisation).
 cudaError_t launch_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block,
-                            uint8_t* codes, float* scales, cudaStream_t st);
+                            uint8_t* codes, float* scales, cudaStream_t st,
+                            const SyncArgs* sync = nullptr);
 cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, int64_t n, int bits,
                               int block, void* y, hz_dtype out_dt, cudaStream_t st);
+cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,
+                                     hz_dtype out_dt, cudaStream_t st, const SyncArgs* sync);
 constexpr int kMaxG = 16;
 cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
                           int64_t n, int bits_in, int block, int bits_out, uint8_t* out_codes,
-                          float* out_scales, float* out_f32, int accumulate, cudaStream_t st);
+                          float* out_scales, float* out_f32, int accumulate, cudaStream_t st,
+                          const SyncArgs* sync = nullptr);
 
 // ------------------------------------------------------------------ tracing
 struct TraceScope {

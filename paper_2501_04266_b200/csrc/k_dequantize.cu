@@ -4,6 +4,15 @@
 // codes (R9), so the layer is bit-identical on all ranks.  Paper: "quantizer and
 // dequantizer operators from ZeRO++".
 //
+// The same kernel is the fused all-gather + dequantize of the NVLink P2P
+// transport: the layer is a list of pieces (one per member of the gathering
+// group, piece j = elements [j*len, (j+1)*len)), each read straight from the
+// owner's IPC-mapped buffer over NVLink (peer loads) or from local HBM, so the
+// gathered codes are never materialised.  With one local piece it is a plain
+// dequantize.  Optionally the codes of [sec_lo, sec_hi) are copied to the hpZ
+// secondary on the way (setting Z, s < w).  In P2P mode the prologue waits for
+// the producers' ready flags and the epilogue signals done (codec.cuh).
+//
 // Elementwise: a unit = 8 consecutive elements (8/4 code bytes in, one 16-byte
 // bf16 store out); the lanes of a warp own 32 consecutive units per instruction
 // (contiguous spans); each lane keeps U units in flight.
@@ -15,13 +24,15 @@ namespace {
 using namespace dev;
 
 template <int BITS, typename TO, int U>
-__global__ void __launch_bounds__(kThreads) k_dequantize(const uint8_t* __restrict__ codes,
-                                                         const float* __restrict__ scales,
+__global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__ Pieces pc,
                                                          int64_t nunits, int log2b,
-                                                         TO* __restrict__ y) {
+                                                         TO* __restrict__ y,
+                                                         const __grid_constant__ SyncArgs sy) {
+  sync_wait(sy);
   const int lane = threadIdx.x & 31;
   const int64_t warp = global_warp();
   const int64_t nwarps = num_warps();
+  const bool copy_sec = pc.sec_c != nullptr;
   for (int64_t base = warp * 32 * U; base < nunits; base += nwarps * 32 * U) {
     Codes8<BITS> raw[U];
     float sc[U];
@@ -29,8 +40,12 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const uint8_t* __restri
     for (int u = 0; u < U; ++u) {
       const int64_t unit = base + u * 32 + lane;
       if (unit < nunits) {
-        raw[u].load(codes + unit * BITS);
-        sc[u] = __ldg(scales + ((unit * 8) >> log2b));
+        const int64_t e = unit * 8;
+        int j = 0;
+        for (int q = 1; q < pc.n; ++q) j += e >= q * pc.len;   // piece of this unit
+        const int64_t r = e - j * pc.len;
+        raw[u].load(pc.c[j] + r * BITS / 8);
+        sc[u] = __ldg(pc.s[j] + (r >> log2b));
       }
     }
 #pragma unroll
@@ -42,55 +57,73 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const uint8_t* __restri
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = __fmul_rn(c[i], sc[u]);
         Out8<TO>::store(y + unit * 8, v);
+        if (copy_sec) {
+          const int64_t e = unit * 8;
+          if (e >= pc.sec_lo && e < pc.sec_hi) {
+            raw[u].store(pc.sec_c + (e - pc.sec_lo) * BITS / 8);
+            if (((e - pc.sec_lo) & ((int64_t(1) << log2b) - 1)) == 0) pc.sec_s[(e - pc.sec_lo) >> log2b] = sc[u];
+          }
+        }
       }
     }
   }
+  sync_signal(sy);
 }
 
 constexpr int kU = 4;   // units in flight per lane (HZ_TUNE deq_u: 2, 4, 8, 16)
 
 template <int BITS, typename TO, int U>
-cudaError_t dequantize_u(const uint8_t* codes, const float* scales, int64_t nunits, int log2b, void* y,
-                         cudaStream_t st) {
+cudaError_t dequantize_u(const Pieces& pc, int64_t nunits, int log2b, void* y, cudaStream_t st,
+                         const SyncArgs& sy) {
   auto kern = k_dequantize<BITS, TO, U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(codes, scales, nunits, log2b, static_cast<TO*>(y));
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(pc, nunits, log2b, static_cast<TO*>(y), sy);
   return cudaGetLastError();
 }
 
 template <int BITS, typename TO>
-cudaError_t dequantize_t(const uint8_t* codes, const float* scales, int64_t n, int block, void* y,
-                         cudaStream_t st) {
+cudaError_t dequantize_t(const Pieces& pc, int64_t n, int block, void* y, cudaStream_t st,
+                         const SyncArgs& sy) {
   const int64_t nunits = n / 8;
   int log2b = 0;
   while ((1 << log2b) < block) ++log2b;
   switch (tune_param("deq_u", kU)) {
-    case 2: return dequantize_u<BITS, TO, 2>(codes, scales, nunits, log2b, y, st);
-    case 8: return dequantize_u<BITS, TO, 8>(codes, scales, nunits, log2b, y, st);
-    case 16: return dequantize_u<BITS, TO, 16>(codes, scales, nunits, log2b, y, st);
-    default: return dequantize_u<BITS, TO, kU>(codes, scales, nunits, log2b, y, st);
+    case 2: return dequantize_u<BITS, TO, 2>(pc, nunits, log2b, y, st, sy);
+    case 8: return dequantize_u<BITS, TO, 8>(pc, nunits, log2b, y, st, sy);
+    case 16: return dequantize_u<BITS, TO, 16>(pc, nunits, log2b, y, st, sy);
+    default: return dequantize_u<BITS, TO, kU>(pc, nunits, log2b, y, st, sy);
   }
+}
+
+template <int BITS>
+cudaError_t dequantize_b(const Pieces& pc, int64_t n, int block, void* y, hz_dtype out_dt,
+                         cudaStream_t st, const SyncArgs& sy) {
+  switch (out_dt) {
+    case HZ_F32: return dequantize_t<BITS, float>(pc, n, block, y, st, sy);
+    case HZ_BF16: return dequantize_t<BITS, __nv_bfloat16>(pc, n, block, y, st, sy);
+    case HZ_F16: return dequantize_t<BITS, __half>(pc, n, block, y, st, sy);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
+cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,
+                                     hz_dtype out_dt, cudaStream_t st, const SyncArgs* sync) {
+  const SyncArgs sy = sync ? *sync : SyncArgs{};
+  if (n == 0 && !sync) return cudaSuccess;
+  return bits == 8 ? dequantize_b<8>(pc, n, block, y, out_dt, st, sy)
+                   : dequantize_b<4>(pc, n, block, y, out_dt, st, sy);
+}
+
 cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, int64_t n, int bits,
                               int block, void* y, hz_dtype out_dt, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  if (bits == 8) {
-    switch (out_dt) {
-      case HZ_F32: return dequantize_t<8, float>(codes, scales, n, block, y, st);
-      case HZ_BF16: return dequantize_t<8, __nv_bfloat16>(codes, scales, n, block, y, st);
-      case HZ_F16: return dequantize_t<8, __half>(codes, scales, n, block, y, st);
-    }
-  } else {
-    switch (out_dt) {
-      case HZ_F32: return dequantize_t<4, float>(codes, scales, n, block, y, st);
-      case HZ_BF16: return dequantize_t<4, __nv_bfloat16>(codes, scales, n, block, y, st);
-      case HZ_F16: return dequantize_t<4, __half>(codes, scales, n, block, y, st);
-    }
-  }
-  return cudaErrorInvalidValue;
+  Pieces pc{};
+  pc.c[0] = codes;
+  pc.s[0] = scales;
+  pc.n = 1;
+  pc.len = n;
+  return launch_gather_dequantize(pc, n, bits, block, y, out_dt, st, nullptr);
 }
 
 }  // namespace hz

@@ -22,8 +22,10 @@ using namespace dev;
 template <typename T, int B, int BITS, int U>
 __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, int64_t nblocks,
                                                        uint8_t* __restrict__ codes,
-                                                       float* __restrict__ scales) {
+                                                       float* __restrict__ scales,
+                                                       const __grid_constant__ SyncArgs sy) {
   using G = Geo<B>;
+  sync_wait(sy);   // P2P mode: every rank is done reading what this call overwrites
   constexpr int NB = U * G::BPW;
   const int lane = threadIdx.x & 31;
   const int lb = lane / G::LPB;
@@ -95,6 +97,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
       }
     }
   }
+  sync_signal(sy);   // P2P mode: codes of this phase are ready for the peers
 }
 
 constexpr int kU = 4;   // warp steps per warp iteration
@@ -102,43 +105,46 @@ constexpr int kU = 4;   // warp steps per warp iteration
 constexpr int uq(int B) { return B > 256 ? 1 : kU; }
 
 template <typename T, int B, int BITS, int U>
-cudaError_t quantize_u(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st) {
+cudaError_t quantize_u(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st,
+                       const SyncArgs& sy) {
   const int64_t nblocks = n / B;
   constexpr int NB = U * Geo<B>::BPW;
   auto kern = k_quantize<T, B, BITS, U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), nblocks / NB + 1);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(static_cast<const T*>(x), nblocks, codes, scales);
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(static_cast<const T*>(x), nblocks, codes, scales, sy);
   return cudaGetLastError();
 }
 
 template <typename T, int B, int BITS>
-cudaError_t quantize_t(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st) {
+cudaError_t quantize_t(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st,
+                       const SyncArgs& sy) {
   if constexpr (B == 256) {   // HZ_TUNE q_u: 2, 4, 8 (the default block only)
     switch (tune_param("q_u", kU)) {
-      case 2: return quantize_u<T, B, BITS, 2>(x, n, codes, scales, st);
-      case 8: return quantize_u<T, B, BITS, 8>(x, n, codes, scales, st);
+      case 2: return quantize_u<T, B, BITS, 2>(x, n, codes, scales, st, sy);
+      case 8: return quantize_u<T, B, BITS, 8>(x, n, codes, scales, st, sy);
       default: break;
     }
   }
-  return quantize_u<T, B, BITS, uq(B)>(x, n, codes, scales, st);
+  return quantize_u<T, B, BITS, uq(B)>(x, n, codes, scales, st, sy);
 }
 
 template <typename T, int B>
-cudaError_t quantize_b(const void* x, int64_t n, int bits, uint8_t* c, float* s, cudaStream_t st) {
-  return bits == 8 ? quantize_t<T, B, 8>(x, n, c, s, st) : quantize_t<T, B, 4>(x, n, c, s, st);
+cudaError_t quantize_b(const void* x, int64_t n, int bits, uint8_t* c, float* s, cudaStream_t st,
+                       const SyncArgs& sy) {
+  return bits == 8 ? quantize_t<T, B, 8>(x, n, c, s, st, sy) : quantize_t<T, B, 4>(x, n, c, s, st, sy);
 }
 
 template <typename T>
 cudaError_t quantize_d(const void* x, int64_t n, int bits, int block, uint8_t* c, float* s,
-                       cudaStream_t st) {
+                       cudaStream_t st, const SyncArgs& sy) {
   switch (block) {
-    case 32: return quantize_b<T, 32>(x, n, bits, c, s, st);
-    case 64: return quantize_b<T, 64>(x, n, bits, c, s, st);
-    case 128: return quantize_b<T, 128>(x, n, bits, c, s, st);
-    case 256: return quantize_b<T, 256>(x, n, bits, c, s, st);
-    case 512: return quantize_b<T, 512>(x, n, bits, c, s, st);
-    case 1024: return quantize_b<T, 1024>(x, n, bits, c, s, st);
-    case 2048: return quantize_b<T, 2048>(x, n, bits, c, s, st);
+    case 32: return quantize_b<T, 32>(x, n, bits, c, s, st, sy);
+    case 64: return quantize_b<T, 64>(x, n, bits, c, s, st, sy);
+    case 128: return quantize_b<T, 128>(x, n, bits, c, s, st, sy);
+    case 256: return quantize_b<T, 256>(x, n, bits, c, s, st, sy);
+    case 512: return quantize_b<T, 512>(x, n, bits, c, s, st, sy);
+    case 1024: return quantize_b<T, 1024>(x, n, bits, c, s, st, sy);
+    case 2048: return quantize_b<T, 2048>(x, n, bits, c, s, st, sy);
   }
   return cudaErrorInvalidValue;
 }
@@ -146,12 +152,13 @@ cudaError_t quantize_d(const void* x, int64_t n, int bits, int block, uint8_t* c
 }  // namespace
 
 cudaError_t launch_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block,
-                            uint8_t* codes, float* scales, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
+                            uint8_t* codes, float* scales, cudaStream_t st, const SyncArgs* sync) {
+  const SyncArgs sy = sync ? *sync : SyncArgs{};
+  if (n == 0 && !sync) return cudaSuccess;
   switch (dt) {
-    case HZ_F32: return quantize_d<float>(x, n, bits, block, codes, scales, st);
-    case HZ_BF16: return quantize_d<__nv_bfloat16>(x, n, bits, block, codes, scales, st);
-    case HZ_F16: return quantize_d<__half>(x, n, bits, block, codes, scales, st);
+    case HZ_F32: return quantize_d<float>(x, n, bits, block, codes, scales, st, sy);
+    case HZ_BF16: return quantize_d<__nv_bfloat16>(x, n, bits, block, codes, scales, st, sy);
+    case HZ_F16: return quantize_d<__half>(x, n, bits, block, codes, scales, st, sy);
   }
   return cudaErrorInvalidValue;
 }

@@ -116,8 +116,10 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
 // quantize_store epilogue (one division per block).  Tail (< NB blocks): one
 // checked step at a time by the last warp.
 template <int B, int BIN, int BOUT, int GT, int U>
-__global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_constant__ RedArgs a) {
+__global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_constant__ RedArgs a,
+                                                             const __grid_constant__ SyncArgs sy) {
   using G = Geo<B>;
+  sync_wait(sy);   // P2P: peers' chunks ready, and nobody still reads our output slot
   constexpr int NB = U * G::BPW;
   const int lane = threadIdx.x & 31;
   const int lb = lane / G::LPB;
@@ -176,11 +178,14 @@ __global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_consta
       }
     }
   }
+  sync_signal(sy);   // P2P: done reading this level, next level's chunks ready
 }
 
 // --------------------------------------------------------------- fp32-output reduce
 template <int BIN, int GT, int U>
-__global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__ RedArgs a, int log2b) {
+__global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__ RedArgs a, int log2b,
+                                                         const __grid_constant__ SyncArgs sy) {
+  sync_wait(sy);
   const int lane = threadIdx.x & 31;
   const int64_t warp = global_warp();
   const int64_t nwarps = num_warps();
@@ -262,6 +267,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
       }
     }
   }
+  sync_signal(sy);
 }
 
 // ---------------------------------------------------------------------- launch
@@ -270,74 +276,74 @@ constexpr int kUF = 4;   // 4-element units in flight per lane (fp32 out)
 constexpr int ur(int B) { return B > 256 ? 1 : kUR; }
 
 template <int B, int BIN, int BOUT, int GT, int U>
-cudaError_t requant_u(const RedArgs& a, cudaStream_t st) {
+cudaError_t requant_u(const RedArgs& a, cudaStream_t st, const SyncArgs& sy) {
   constexpr int NB = U * Geo<B>::BPW;
   auto kern = k_reduce_requant<B, BIN, BOUT, GT, U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), a.n / B / NB + 1);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a);
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, sy);
   return cudaGetLastError();
 }
 
 template <int B, int BIN, int BOUT, int GT>
-cudaError_t requant_t(const RedArgs& a, cudaStream_t st) {
+cudaError_t requant_t(const RedArgs& a, cudaStream_t st, const SyncArgs& sy) {
   if constexpr (B == 256 && GT > 0 && GT <= 2) {   // HZ_TUNE rq_u: 1, 2, 4
     switch (tune_param("rq_u", kUR)) {
-      case 1: return requant_u<B, BIN, BOUT, GT, 1>(a, st);
-      case 2: return requant_u<B, BIN, BOUT, GT, 2>(a, st);
+      case 1: return requant_u<B, BIN, BOUT, GT, 1>(a, st, sy);
+      case 2: return requant_u<B, BIN, BOUT, GT, 2>(a, st, sy);
       default: break;
     }
   }
-  return requant_u<B, BIN, BOUT, GT, ur(B)>(a, st);
+  return requant_u<B, BIN, BOUT, GT, ur(B)>(a, st, sy);
 }
 
 template <int B, int BIN, int BOUT>
-cudaError_t requant_g(const RedArgs& a, cudaStream_t st) {
+cudaError_t requant_g(const RedArgs& a, cudaStream_t st, const SyncArgs& sy) {
   // Unrolled input prefetch for the common group sizes; large blocks with many
   // inputs use the one-input-at-a-time loop (register budget).
   switch (a.g) {
-    case 1: return requant_t<B, BIN, BOUT, 1>(a, st);
-    case 2: return requant_t<B, BIN, BOUT, 2>(a, st);
-    case 4: return B >= 1024 ? requant_t<B, BIN, BOUT, 0>(a, st) : requant_t<B, BIN, BOUT, 4>(a, st);
-    case 8: return B >= 512 ? requant_t<B, BIN, BOUT, 0>(a, st) : requant_t<B, BIN, BOUT, 8>(a, st);
-    default: return requant_t<B, BIN, BOUT, 0>(a, st);
+    case 1: return requant_t<B, BIN, BOUT, 1>(a, st, sy);
+    case 2: return requant_t<B, BIN, BOUT, 2>(a, st, sy);
+    case 4: return B >= 1024 ? requant_t<B, BIN, BOUT, 0>(a, st, sy) : requant_t<B, BIN, BOUT, 4>(a, st, sy);
+    case 8: return B >= 512 ? requant_t<B, BIN, BOUT, 0>(a, st, sy) : requant_t<B, BIN, BOUT, 8>(a, st, sy);
+    default: return requant_t<B, BIN, BOUT, 0>(a, st, sy);
   }
 }
 
 template <int B>
-cudaError_t requant_b(const RedArgs& a, int bits_in, int bits_out, cudaStream_t st) {
-  if (bits_in == 8) return bits_out == 8 ? requant_g<B, 8, 8>(a, st) : requant_g<B, 8, 4>(a, st);
-  return bits_out == 8 ? requant_g<B, 4, 8>(a, st) : requant_g<B, 4, 4>(a, st);
+cudaError_t requant_b(const RedArgs& a, int bits_in, int bits_out, cudaStream_t st, const SyncArgs& sy) {
+  if (bits_in == 8) return bits_out == 8 ? requant_g<B, 8, 8>(a, st, sy) : requant_g<B, 8, 4>(a, st, sy);
+  return bits_out == 8 ? requant_g<B, 4, 8>(a, st, sy) : requant_g<B, 4, 4>(a, st, sy);
 }
 
 template <int BIN, int GT, int U>
-cudaError_t f32_u(const RedArgs& a, int log2b, cudaStream_t st) {
+cudaError_t f32_u(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& sy) {
   const int64_t nunits = a.n / 4;
   auto kern = k_reduce_f32<BIN, GT, U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, log2b);
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, log2b, sy);
   return cudaGetLastError();
 }
 
 template <int BIN, int GT>
-cudaError_t f32_t(const RedArgs& a, int log2b, cudaStream_t st) {
+cudaError_t f32_t(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& sy) {
   if constexpr (GT > 0 && GT <= 2) {   // HZ_TUNE rf_u: 2, 4, 8
     switch (tune_param("rf_u", kUF)) {
-      case 2: return f32_u<BIN, GT, 2>(a, log2b, st);
-      case 8: return f32_u<BIN, GT, 8>(a, log2b, st);
+      case 2: return f32_u<BIN, GT, 2>(a, log2b, st, sy);
+      case 8: return f32_u<BIN, GT, 8>(a, log2b, st, sy);
       default: break;
     }
   }
-  return f32_u<BIN, GT, kUF>(a, log2b, st);
+  return f32_u<BIN, GT, kUF>(a, log2b, st, sy);
 }
 
 template <int BIN>
-cudaError_t f32_g(const RedArgs& a, int log2b, cudaStream_t st) {
+cudaError_t f32_g(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& sy) {
   switch (a.g) {
-    case 1: return f32_t<BIN, 1>(a, log2b, st);
-    case 2: return f32_t<BIN, 2>(a, log2b, st);
-    case 4: return f32_t<BIN, 4>(a, log2b, st);
-    case 8: return f32_t<BIN, 8>(a, log2b, st);
-    default: return f32_t<BIN, 0>(a, log2b, st);
+    case 1: return f32_t<BIN, 1>(a, log2b, st, sy);
+    case 2: return f32_t<BIN, 2>(a, log2b, st, sy);
+    case 4: return f32_t<BIN, 4>(a, log2b, st, sy);
+    case 8: return f32_t<BIN, 8>(a, log2b, st, sy);
+    default: return f32_t<BIN, 0>(a, log2b, st, sy);
   }
 }
 
@@ -345,8 +351,10 @@ cudaError_t f32_g(const RedArgs& a, int log2b, cudaStream_t st) {
 
 cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
                           int64_t n, int bits_in, int block, int bits_out, uint8_t* out_codes,
-                          float* out_scales, float* out_f32, int accumulate, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
+                          float* out_scales, float* out_f32, int accumulate, cudaStream_t st,
+                          const SyncArgs* sync) {
+  const SyncArgs sy = sync ? *sync : SyncArgs{};
+  if (n == 0 && !sync) return cudaSuccess;
   RedArgs a{};
   for (int p = 0; p < g; ++p) {
     a.c[p] = codes[p];
@@ -361,16 +369,16 @@ cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const
   if (bits_out == 0) {
     int log2b = 0;
     while ((1 << log2b) < block) ++log2b;
-    return bits_in == 8 ? f32_g<8>(a, log2b, st) : f32_g<4>(a, log2b, st);
+    return bits_in == 8 ? f32_g<8>(a, log2b, st, sy) : f32_g<4>(a, log2b, st, sy);
   }
   switch (block) {
-    case 32: return requant_b<32>(a, bits_in, bits_out, st);
-    case 64: return requant_b<64>(a, bits_in, bits_out, st);
-    case 128: return requant_b<128>(a, bits_in, bits_out, st);
-    case 256: return requant_b<256>(a, bits_in, bits_out, st);
-    case 512: return requant_b<512>(a, bits_in, bits_out, st);
-    case 1024: return requant_b<1024>(a, bits_in, bits_out, st);
-    case 2048: return requant_b<2048>(a, bits_in, bits_out, st);
+    case 32: return requant_b<32>(a, bits_in, bits_out, st, sy);
+    case 64: return requant_b<64>(a, bits_in, bits_out, st, sy);
+    case 128: return requant_b<128>(a, bits_in, bits_out, st, sy);
+    case 256: return requant_b<256>(a, bits_in, bits_out, st, sy);
+    case 512: return requant_b<512>(a, bits_in, bits_out, st, sy);
+    case 1024: return requant_b<1024>(a, bits_in, bits_out, st, sy);
+    case 2048: return requant_b<2048>(a, bits_in, bits_out, st, sy);
   }
   return cudaErrorInvalidValue;
 }

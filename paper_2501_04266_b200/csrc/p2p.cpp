@@ -1,0 +1,344 @@
+// NVLink peer-memory transport (hz_enable_p2p): the per-level collectives are
+// fused into the codec kernels instead of being staged through NCCL.
+//
+// Every rank owns one symmetric pool (cudaMalloc + cudaIpcGetMemHandle; the
+// handles are exchanged with one ncclAllGather and opened with
+// cudaIpcOpenMemHandle), so a buffer at pool offset X on this rank is at offset
+// X in every peer's pool.  Allocations (hz_sym_alloc and the library's slots)
+// are bump allocations made in the same order on every rank, hence symmetric.
+//
+// qwZ/hpZ all-gather (O7/O8): the owner quantizes its primary into a pool buffer
+// (the caller's pool-allocated secondary when s == w); each rank then runs ONE
+// gather+dequantize kernel whose pieces are the members' codes, read straight
+// over NVLink — the gathered codes never land in HBM.  Backward: the same kernel
+// over the members' secondaries.
+// qgZ reduce-scatter (O9): level l's send buffer (quantize output, or the
+// previous level's requantized sum) lives in the pool; the level-l reduce kernel
+// reads chunk d_l of every group member's send buffer over NVLink and sums in
+// ascending digit order — the all-to-all and the dequant+sum are one kernel.
+//
+// Ordering: every phase has a global number; producers wait until all ranks are
+// done with the previous phase (no one still reads what they overwrite) and
+// signal `ready`, consumers wait for `ready` and signal `done` (codec.cuh).
+// All P2P calls of one context must be issued on one stream, in the same order
+// on every rank (the NCCL discipline).
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ctx.h"
+
+namespace hz {
+namespace {
+
+#define P2P_CUDA(call, what)                              \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what);    \
+  } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+hz_status pool_alloc(hz_ctx* ctx, size_t bytes, size_t* off) {
+  auto& P = ctx->p2p;
+  const size_t o = align_up(P.used, 256);
+  if (o + bytes > P.bytes)
+    return fail(HZ_ERR_INVALID, "P2P pool exhausted: need " + std::to_string(o + bytes) + " of " +
+                                    std::to_string(P.bytes) + " bytes (pass a larger pool_bytes)");
+  *off = o;
+  P.used = o + bytes;
+  return HZ_OK;
+}
+
+hz_status slot(hz_ctx* ctx, hz_ctx::P2P::Slot& sl, size_t bytes) {
+  if (sl.cap >= bytes) return HZ_OK;
+  hz_status rc = pool_alloc(ctx, bytes, &sl.off);
+  if (rc == HZ_OK) sl.cap = bytes;
+  return rc;
+}
+
+template <typename T>
+T* at(hz_ctx* ctx, int q, size_t off) {
+  return reinterpret_cast<T*>(ctx->p2p.peer[q] + off);
+}
+
+size_t off_of(const hz_ctx* ctx, const void* local) {
+  return static_cast<size_t>(static_cast<const char*>(local) - ctx->p2p.pool);
+}
+
+SyncArgs make_sync(hz_ctx* ctx, unsigned long long wait_ready, unsigned long long wait_done,
+                   unsigned long long sig_ready, unsigned long long sig_done) {
+  auto& P = ctx->p2p;
+  SyncArgs s{};
+  s.ready_local = reinterpret_cast<unsigned long long*>(P.pool + kReadyOff);
+  s.done_local = reinterpret_cast<unsigned long long*>(P.pool + kDoneOff);
+  for (int q = 0; q < ctx->world; ++q) {
+    s.ready_remote[q] = reinterpret_cast<unsigned long long*>(P.peer[q] + kReadyOff) + ctx->rank;
+    s.done_remote[q] = reinterpret_cast<unsigned long long*>(P.peer[q] + kDoneOff) + ctx->rank;
+  }
+  s.counter = reinterpret_cast<unsigned int*>(P.pool + kCounterOff);
+  s.world = ctx->world;
+  s.wait_ready = wait_ready;
+  s.wait_done = wait_done;
+  s.sig_ready = sig_ready;
+  s.sig_done = sig_done;
+  return s;
+}
+
+// Members of this rank's cumulative group of `level` (ranks that share every digit
+// above `level`), as (off_level within range_0, rank), sorted by offset: piece k
+// of the gathered layer is owned by the k-th entry.
+std::vector<std::pair<int64_t, int>> cumulative_members(const hz_partition_t* p, int level) {
+  int64_t stride[HZ_MAX_LEVELS];
+  int64_t st = 1;
+  for (int l = 0; l < p->levels; ++l) {
+    stride[l] = st;
+    st *= p->group[l];
+  }
+  int64_t base = p->rank;
+  int64_t D = 1;
+  for (int l = 0; l < level; ++l) {
+    base -= p->digit[l] * stride[l];
+    D *= p->group[l];
+  }
+  std::vector<std::pair<int64_t, int>> out;
+  for (int64_t idx = 0; idx < D; ++idx) {
+    int64_t rem = idx, r = base, off = 0;
+    for (int l = 0; l < level; ++l) {
+      const int d = static_cast<int>(rem % p->group[l]);
+      rem /= p->group[l];
+      r += d * stride[l];
+      off += d * p->len[l + 1];
+    }
+    out.emplace_back(off, static_cast<int>(r));
+  }
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+}  // namespace
+
+bool in_pool(const hz_ctx* ctx, const void* p, size_t bytes) {
+  const char* c = static_cast<const char*>(p);
+  return ctx->p2p.on && c >= ctx->p2p.pool + kPoolHeader && c + bytes <= ctx->p2p.pool + ctx->p2p.bytes;
+}
+
+hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, const void* primary,
+                        hz_dtype dt, int bits, uint8_t* sec_codes, float* sec_scales, void* full_out,
+                        hz_dtype out_dt, cudaStream_t st) {
+  auto& P = ctx->p2p;
+  const int64_t Np = p->padded_numel;
+  const int B = p->block;
+  const int w = p->w, s = p->s;
+  const int top = backward ? s : w;
+  const int64_t len_s = p->len[s];
+  if (!in_pool(ctx, sec_codes, code_bytes(len_s, bits)) || !in_pool(ctx, sec_scales, len_s / B * 4))
+    return fail(HZ_ERR_INVALID, "sec_codes/sec_scales: must be hz_sym_alloc memory when P2P is enabled");
+  hz_status rc;
+  const auto members = cumulative_members(p, top);
+  const int D = static_cast<int>(members.size());
+  if (D > kMaxWorld) return fail(HZ_ERR_UNSUPPORTED, "P2P gather over more than 8 ranks");
+  const unsigned long long phase = D > 1 ? ++P.phase : 0;
+  const int64_t plen = p->len[top];
+
+  const uint8_t* xc;
+  const float* xs;
+  if (!backward) {
+    uint8_t* qc = sec_codes;
+    float* qs = sec_scales;
+    if (s != w) {   // the quantized primary needs its own peer-readable buffer
+      if ((rc = slot(ctx, P.ag_prim_c, code_bytes(p->len[w], 8))) != HZ_OK) return rc;
+      if ((rc = slot(ctx, P.ag_prim_s, p->len[w] / B * 4)) != HZ_OK) return rc;
+      qc = at<uint8_t>(ctx, ctx->rank, P.ag_prim_c.off);
+      qs = at<float>(ctx, ctx->rank, P.ag_prim_s.off);
+    }
+    SyncArgs sq = make_sync(ctx, 0, phase ? phase - 1 : 0, phase, 0);
+    if ((rc = run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w, phase ? &sq : nullptr)) != HZ_OK)
+      return rc;
+    if (s > w) {   // A4, s > w: the secondary is a sub-slice of the own quantized primary
+      const int64_t rel = p->off[s] - p->off[w];
+      if ((rc = copy_async(sec_codes, qc + code_bytes(rel, bits), code_bytes(len_s, bits), st)) != HZ_OK) return rc;
+      if ((rc = copy_async(sec_scales, qs + rel / B, len_s / B * 4, st)) != HZ_OK) return rc;
+    }
+    xc = qc;
+    xs = qs;
+  } else {
+    xc = sec_codes;
+    xs = sec_scales;
+  }
+  Pieces pc{};
+  pc.n = D;
+  pc.len = plen;
+  int64_t remote = 0;
+  for (int k = 0; k < D; ++k) {
+    const int m = members[k].second;
+    pc.c[k] = at<const uint8_t>(ctx, m, off_of(ctx, xc));
+    pc.s[k] = at<const float>(ctx, m, off_of(ctx, xs));
+    if (m != ctx->rank) remote += code_bytes(plen, bits) + plen / B * 4;
+  }
+  if (!backward && s < w) {   // A4, s < w: keep range_s of the gathered codes
+    pc.sec_c = sec_codes;
+    pc.sec_s = sec_scales;
+    pc.sec_lo = p->off[s];
+    pc.sec_hi = p->off[s] + len_s;
+  }
+  SyncArgs sd = backward ? make_sync(ctx, 0, phase - 1, 0, phase) : make_sync(ctx, phase, 0, 0, phase);
+  if ((rc = run_gather_dequantize(pc, Np, bits, B, full_out, out_dt, st, 0, phase ? &sd : nullptr, remote)) != HZ_OK)
+    return rc;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
+                             int from_level, int to_level, const int* bits_per_level, float* shard,
+                             int accumulate, cudaStream_t st) {
+  auto& P = ctx->p2p;
+  const int B = p->block;
+  hz_status rc;
+  for (int l = from_level; l <= to_level; ++l) {   // level-l send buffers (8-bit capacity)
+    if ((rc = slot(ctx, P.rs_c[l], code_bytes(p->len[l - 1], 8))) != HZ_OK) return rc;
+    if ((rc = slot(ctx, P.rs_s[l], p->len[l - 1] / B * 4)) != HZ_OK) return rc;
+  }
+  int64_t stride[HZ_MAX_LEVELS];
+  int64_t sacc = 1;
+  for (int l = 0; l < p->levels; ++l) {
+    stride[l] = sacc;
+    sacc *= p->group[l];
+  }
+  const unsigned long long base = P.phase;
+  P.phase += static_cast<unsigned long long>(to_level - from_level + 1);
+  auto phase_of = [&](int l) { return base + static_cast<unsigned long long>(l - from_level + 1); };
+
+  // A7: quantize the input range_{from-1} into this rank's level-`from` send buffer
+  {
+    const unsigned long long ph = phase_of(from_level);
+    SyncArgs sq = make_sync(ctx, 0, ph - 1, ph, 0);
+    if ((rc = run_quantize(grad, dt, p->len[from_level - 1], bits_per_level[from_level - 1], B,
+                           at<uint8_t>(ctx, ctx->rank, P.rs_c[from_level].off),
+                           at<float>(ctx, ctx->rank, P.rs_s[from_level].off), st, from_level, &sq)) != HZ_OK)
+      return rc;
+  }
+  for (int l = from_level; l <= to_level; ++l) {
+    const int g = p->group[l - 1];
+    const int d = p->digit[l - 1];
+    const int bits = bits_per_level[l - 1];
+    const int64_t cl = p->len[l];
+    if (g > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "group size > 16 at one level");
+    const uint8_t* ptr_c[kMaxG];
+    const float* ptr_s[kMaxG];
+    for (int j = 0; j < g; ++j) {   // A8+A9: chunk d of member j's send buffer, over NVLink
+      const int m = static_cast<int>(p->rank + (static_cast<int64_t>(j) - d) * stride[l - 1]);
+      ptr_c[j] = at<const uint8_t>(ctx, m, P.rs_c[l].off) + code_bytes(d * cl, bits);
+      ptr_s[j] = at<const float>(ctx, m, P.rs_s[l].off) + d * cl / B;
+    }
+    const unsigned long long ph = phase_of(l);
+    if (l < to_level) {
+      SyncArgs sr = make_sync(ctx, ph, ph - 1, ph + 1, ph);
+      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, bits_per_level[l],
+                           at<uint8_t>(ctx, ctx->rank, P.rs_c[l + 1].off),
+                           at<float>(ctx, ctx->rank, P.rs_s[l + 1].off), nullptr, 0, st, l, &sr)) != HZ_OK)
+        return rc;
+    } else {
+      SyncArgs sr = make_sync(ctx, ph, 0, 0, ph);
+      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st, l, &sr)) !=
+          HZ_OK)
+        return rc;
+    }
+  }
+  clear_error();
+  return HZ_OK;
+}
+
+void p2p_release(hz_ctx* ctx) {
+  auto& P = ctx->p2p;
+  if (!P.pool) return;
+  // every rank must be done with every peer's pool before anyone unmaps / frees
+  int* flag = nullptr;
+  if (cudaMalloc(&flag, sizeof(int)) == cudaSuccess) {
+    ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, ctx->world_comm, nullptr);
+    cudaStreamSynchronize(nullptr);
+    cudaFree(flag);
+  }
+  for (int q = 0; q < ctx->world; ++q)
+    if (q != ctx->rank && P.peer[q]) cudaIpcCloseMemHandle(P.peer[q]);
+  cudaFree(P.pool);
+  cudaGetLastError();
+  P = hz_ctx::P2P{};
+}
+
+}  // namespace hz
+
+extern "C" {
+
+hz_status hz_enable_p2p(hz_ctx* ctx, size_t pool_bytes) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  if (ctx->p2p.on) return fail(HZ_ERR_INVALID, "ctx: P2P already enabled");
+  if (ctx->world > kMaxWorld) return fail(HZ_ERR_UNSUPPORTED, "P2P transport supports at most 8 ranks");
+  auto& P = ctx->p2p;
+  const size_t total = align_up(kPoolHeader + pool_bytes, size_t(2) << 20);
+  P2P_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  P2P_CUDA(cudaMalloc(&P.pool, total), "P2P pool cudaMalloc");
+  P.bytes = total;
+  P.used = kPoolHeader;
+  P2P_CUDA(cudaMemset(P.pool, 0, kPoolHeader), "P2P pool header memset");
+  cudaIpcMemHandle_t mine;
+  P2P_CUDA(cudaIpcGetMemHandle(&mine, P.pool), "cudaIpcGetMemHandle");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  char* dev = nullptr;
+  P2P_CUDA(cudaMalloc(&dev, 64 * ctx->world), "handle exchange cudaMalloc");
+  P2P_CUDA(cudaMemcpy(dev + 64 * ctx->rank, &mine, 64, cudaMemcpyHostToDevice), "handle exchange copy");
+  ncclResult_t r = ncclAllGather(dev + 64 * ctx->rank, dev, 64, ncclUint8, ctx->world_comm, nullptr);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather(IPC handles)");
+  std::vector<cudaIpcMemHandle_t> all(ctx->world);
+  P2P_CUDA(cudaMemcpy(all.data(), dev, 64 * ctx->world, cudaMemcpyDeviceToHost), "handle exchange copy back");
+  cudaFree(dev);
+  for (int q = 0; q < ctx->world; ++q) {
+    if (q == ctx->rank) {
+      P.peer[q] = P.pool;
+      continue;
+    }
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      p2p_release(ctx);
+      return fail(HZ_ERR_UNSUPPORTED, std::string("cudaIpcOpenMemHandle (peer not reachable over P2P): ") +
+                                          cudaGetErrorString(e));
+    }
+    P.peer[q] = static_cast<char*>(ptr);
+  }
+  // nobody starts using the pools before every rank has mapped every peer
+  int* flag = nullptr;
+  P2P_CUDA(cudaMalloc(&flag, sizeof(int)), "barrier cudaMalloc");
+  r = ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, ctx->world_comm, nullptr);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(barrier)");
+  P2P_CUDA(cudaStreamSynchronize(nullptr), "barrier sync");
+  cudaFree(flag);
+  P.on = true;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_p2p_enabled(const hz_ctx* ctx, int* out) {
+  using namespace hz;
+  if (!ctx || !out) return fail(HZ_ERR_INVALID, "ctx/out: NULL");
+  *out = ctx->p2p.on ? 1 : 0;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_sym_alloc(hz_ctx* ctx, size_t bytes, void** out) {
+  using namespace hz;
+  if (!ctx || !out) return fail(HZ_ERR_INVALID, "ctx/out: NULL");
+  if (!ctx->p2p.on) return fail(HZ_ERR_INVALID, "ctx: P2P not enabled (call hz_enable_p2p first)");
+  size_t off = 0;
+  hz_status rc = pool_alloc(ctx, bytes, &off);
+  if (rc != HZ_OK) return rc;
+  *out = ctx->p2p.pool + off;
+  clear_error();
+  return HZ_OK;
+}
+
+}  // extern "C"

@@ -113,6 +113,9 @@ _sig("hz_flat_reduce_scatter", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_trace_begin", [_int])
 _sig("hz_trace_end", [])
 _sig("hz_trace_read", [ctypes.POINTER(TraceRec), _int, ctypes.POINTER(ctypes.c_int)])
+_sig("hz_enable_p2p", [_vp, ctypes.c_size_t])
+_sig("hz_p2p_enabled", [_vp, ctypes.POINTER(ctypes.c_int)])
+_sig("hz_sym_alloc", [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)])
 _sig("hz_plan_allgather", [ctypes.POINTER(Partition), _int, _int, ctypes.POINTER(CommStep), _int,
                            ctypes.POINTER(ctypes.c_int)])
 _sig("hz_plan_reduce_scatter", [ctypes.POINTER(Partition), _int, _int, ctypes.POINTER(ctypes.c_int),
@@ -265,6 +268,24 @@ def trace_read(max_records=1 << 16):
              "bytes": r.bytes, "ms": r.ms} for r in recs[:n.value]]
 
 
+_TYPESTR = {"torch.uint8": "|u1", "torch.float32": "<f4", "torch.bfloat16": "<V2", "torch.float16": "<f2"}
+
+
+class _CudaArray:
+    def __init__(self, ptr, numel, typestr):
+        self.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _wrap_device_ptr(ptr, numel, dtype, device):
+    """Zero-copy torch tensor over library-owned device memory."""
+    import torch
+    if dtype == torch.bfloat16:
+        t = torch.as_tensor(_CudaArray(ptr, numel, "<i2"), device=f"cuda:{device}")
+        return t.view(torch.bfloat16)
+    return torch.as_tensor(_CudaArray(ptr, numel, _TYPESTR[str(dtype)]), device=f"cuda:{device}")
+
+
 # ------------------------------------------------------------------ collectives
 def get_uid():
     u = Uid()
@@ -312,6 +333,26 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def enable_p2p(self, pool_bytes):
+        """hz_enable_p2p (collective): NVLink peer-memory transport with a symmetric
+        pool of pool_bytes on every rank."""
+        _check(_lib.hz_enable_p2p(self._h, int(pool_bytes)))
+
+    @property
+    def p2p(self):
+        v = ctypes.c_int(0)
+        _check(_lib.hz_p2p_enabled(self._h, ctypes.byref(v)))
+        return bool(v.value)
+
+    def sym_alloc(self, numel, dtype):
+        """hz_sym_alloc: a torch view of a symmetric pool allocation (same sequence of
+        calls on every rank).  The memory belongs to the context."""
+        import torch
+        itemsize = torch.empty(0, dtype=dtype).element_size()
+        ptr = _vp()
+        _check(_lib.hz_sym_alloc(self._h, numel * itemsize, ctypes.byref(ptr)))
+        return _wrap_device_ptr(ptr.value, numel, dtype, self.device)
 
     def partition(self, numel, block=256, w=1, s=1, gl=None):
         p = Partition()

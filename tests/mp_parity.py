@@ -37,10 +37,19 @@ def role_cases(L):
     return sorted(c for c in cases if 0 <= c[0] <= L and 0 <= c[1] <= L)
 
 
-def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256):
+def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=False):
     errors = []
     ctx = hz.Context(rank, world, uid, g, device)
     L = len(g)
+    tag = "p2p" if p2p else "nccl"
+    if p2p:
+        ctx.enable_p2p(64 << 20)
+
+    def sec_buffers(n_codes, n_scales):
+        if p2p:
+            return (ctx.sym_alloc(n_codes, torch.uint8), ctx.sym_alloc(n_scales, torch.float32))
+        return (torch.empty(n_codes, dtype=torch.uint8, device="cuda"),
+                torch.empty(n_scales, dtype=torch.float32, device="cuda"))
     try:
         Np = pm.padded_numel(numel, g, B)
         full = np.zeros(Np, np.float32)
@@ -53,19 +62,18 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256):
             prim = {r: full[pm.range_at(r, g, Np, w)[0]:sum(pm.range_at(r, g, Np, w))] for r in range(world)}
             want, want_sec = col.allgather_forward(prim, g, Np, B, w, s, bits=8)
             so, sl = p.range(s)
-            sec_c = torch.empty(sl, dtype=torch.uint8, device="cuda")
-            sec_s = torch.empty(sl // B, dtype=torch.float32, device="cuda")
+            sec_c, sec_s = sec_buffers(sl, sl // B)
             out = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
             ctx.allgather_params(p, to_dev(full[off:off + ln]), sec_c, sec_s, out, bits=8)
             torch.cuda.synchronize()
             try:
-                assert_bitwise(to_host(out), want[rank], f"g={g} w={w} s={s} forward layer")
-                assert_bitwise(to_host(sec_c), quant.wire_codes(want_sec[rank][0], 8), f"g={g} w={w} s={s} secondary codes")
-                assert_bitwise(to_host(sec_s), want_sec[rank][1], f"g={g} w={w} s={s} secondary scales")
+                assert_bitwise(to_host(out), want[rank], f"[{tag}] g={g} w={w} s={s} forward layer")
+                assert_bitwise(to_host(sec_c), quant.wire_codes(want_sec[rank][0], 8), f"[{tag}] g={g} w={w} s={s} secondary codes")
+                assert_bitwise(to_host(sec_s), want_sec[rank][1], f"[{tag}] g={g} w={w} s={s} secondary scales")
                 out2 = torch.empty_like(out)
                 ctx.allgather_params(p, None, sec_c, sec_s, out2, bits=8, backward=True)
                 torch.cuda.synchronize()
-                assert_bitwise(to_host(out2), want[rank], f"g={g} w={w} s={s} backward layer")
+                assert_bitwise(to_host(out2), want[rank], f"[{tag}] g={g} w={w} s={s} backward layer")
             except AssertionError as e:
                 errors.append(str(e))
 
@@ -79,7 +87,7 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256):
             ctx.reduce_scatter_grads(p, to_dev(grads[rank]), shard, bpl)
             torch.cuda.synchronize()
             try:
-                assert_bitwise(to_host(shard), want[rank], f"g={g} qgZ bits={bpl}")
+                assert_bitwise(to_host(shard), want[rank], f"[{tag}] g={g} qgZ bits={bpl}")
             except AssertionError as e:
                 errors.append(str(e))
 
@@ -99,8 +107,8 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256):
             ctx.reduce_scatter_grads(p, acc, shard, [4] * L, gl + 1, L)
             torch.cuda.synchronize()
             try:
-                assert_bitwise(to_host(acc), A[rank], f"g={g} two-phase accumulated shard")
-                assert_bitwise(to_host(shard), want[rank], f"g={g} two-phase final shard")
+                assert_bitwise(to_host(acc), A[rank], f"[{tag}] g={g} two-phase accumulated shard")
+                assert_bitwise(to_host(shard), want[rank], f"[{tag}] g={g} two-phase final shard")
             except AssertionError as e:
                 errors.append(str(e))
 
@@ -130,10 +138,11 @@ def run(rank, world, local, bcast=None):
     torch.cuda.set_device(local)
     errors = []
     for g in HIERARCHIES[world]:
-        uid = hz.get_uid() if rank == 0 else None
-        if bcast is not None:
-            uid = bcast(uid)
-        errors += check_hierarchy(hz, rank, world, g, uid, local)
+        for p2p in (False, True):
+            uid = hz.get_uid() if rank == 0 else None
+            if bcast is not None:
+                uid = bcast(uid)
+            errors += check_hierarchy(hz, rank, world, g, uid, local, p2p=p2p)
     return errors
 
 
