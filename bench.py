@@ -249,9 +249,15 @@ def barrier(world):
 def summarize_trace(recs, steps):
     kinds = {}
     for r in recs:
-        k = kinds.setdefault(r["kind"], {"launches": 0, "ms": 0.0, "bytes": 0, "elems": 0})
+        k = kinds.setdefault(r["kind"], {"launches": 0, "ms": 0.0, "bytes": 0, "elems": 0,
+                                         "wait_ms": 0.0, "work_ms": 0.0, "publish_ms": 0.0, "stamped": 0})
         k["launches"] += 1
         k["ms"] += r["ms"]
+        if r.get("wait_ms", -1) >= 0:
+            k["stamped"] += 1
+            k["wait_ms"] += r["wait_ms"]
+            k["work_ms"] += r["work_ms"]
+            k["publish_ms"] += max(r.get("publish_ms", 0.0), 0.0)
         k["bytes"] += r["bytes"]
         k["elems"] += r["elems"]
     total_ms = sum(v["ms"] for v in kinds.values()) or 1.0
@@ -265,6 +271,10 @@ def summarize_trace(recs, steps):
             "GBps": v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else None,
             "share": v["ms"] / total_ms,
         }
+        if v["stamped"]:
+            out[name]["avg_wait_ms"] = v["wait_ms"] / v["stamped"]
+            out[name]["avg_work_ms"] = v["work_ms"] / v["stamped"]
+            out[name]["avg_publish_ms"] = v["publish_ms"] / v["stamped"]
     return out
 
 

@@ -278,7 +278,10 @@ typedef struct {
   int32_t bits;
   int64_t elems;
   int64_t bytes;
-  float ms;
+  float ms;        /* CUDA-event duration of the launch on its stream */
+  float wait_ms;   /* P2P kernels: time CTA 0 spent waiting for peers (device clock); else -1 */
+  float work_ms;   /* P2P kernels: after-wait to last CTA arrival (device clock); else -1 */
+  float publish_ms;/* P2P kernels: last CTA's fence + flag stores (device clock); else -1 */
 } hz_trace_rec;
 
 HZ_API hz_status hz_trace_begin(int capacity);

@@ -340,6 +340,9 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -347,7 +350,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 __device__ __forceinline__ void sync_wait(const SyncArgs& s) {
-  if (!(s.wait_ready | s.wait_done)) return;
+  if (s.stamps && blockIdx.x == 0 && threadIdx.x == 0) s.stamps[0] = globaltimer();
+  if (!(s.wait_ready | s.wait_done)) {
+    if (s.stamps && blockIdx.x == 0 && threadIdx.x == 0) s.stamps[1] = globaltimer();
+    return;
+  }
   if (threadIdx.x == 0) {
     const unsigned long long t0 = globaltimer();
     for (int q = 0; q < s.world; ++q) {
@@ -356,6 +363,7 @@ __device__ __forceinline__ void sync_wait(const SyncArgs& s) {
         if (globaltimer() - t0 > 20000000000ull) __trap();
       }
     }
+    if (s.stamps && blockIdx.x == 0) s.stamps[1] = globaltimer();
   }
   __syncthreads();
 }
@@ -364,14 +372,28 @@ __device__ __forceinline__ void sync_signal(const SyncArgs& s) {
   if (!(s.sig_ready | s.sig_done)) return;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    // gpu-scope release per CTA (peers read this GPU's memory through its L2, the
+    // point of coherence for gpu scope); the last CTA then publishes with a
+    // system-scope release, cumulative over everything it has observed.
+    __threadfence();
     if (atomicAdd(s.counter, 1u) == gridDim.x - 1) {
       *s.counter = 0u;
-      __threadfence_system();
-      for (int q = 0; q < s.world; ++q) {
-        if (s.sig_ready) st_release_sys(s.ready_remote[q], s.sig_ready);
-        if (s.sig_done) st_release_sys(s.done_remote[q], s.sig_done);
+      if (s.stamps) s.stamps[2] = globaltimer();
+      if (s.mode == 0) {
+        __threadfence_system();
+        for (int q = 0; q < s.world; ++q) {
+          if (s.sig_ready) st_release_sys(s.ready_remote[q], s.sig_ready);
+          if (s.sig_done) st_release_sys(s.done_remote[q], s.sig_done);
+        }
+      } else {
+        if (s.mode == 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else if (s.mode == 2) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (int q = 0; q < s.world; ++q) {
+          if (s.sig_ready) st_relaxed_sys(s.ready_remote[q], s.sig_ready);
+          if (s.sig_done) st_relaxed_sys(s.done_remote[q], s.sig_done);
+        }
       }
+      if (s.stamps) s.stamps[3] = globaltimer();
     }
   }
 }

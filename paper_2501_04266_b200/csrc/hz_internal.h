@@ -32,6 +32,8 @@ struct SyncArgs {
   unsigned int* counter;
   int world;
   unsigned long long wait_ready, wait_done, sig_ready, sig_done;
+  unsigned long long* stamps;   // optional [4]: entry, after wait, last-CTA arrival, flags sent (ns)
+  int mode;                     // publication fence variant (HZ_TUNE p2p_sig; 0 = fence.sc.sys)
 };
 
 // Pieces of a gathered layer for the fused gather+dequantize kernel: piece j
@@ -75,6 +77,7 @@ struct TraceScope {
   bool active;
   int slot;
   cudaStream_t stream;
+  unsigned long long* stamps;   // device [3] for this launch when tracing, else nullptr
 };
 
 // ----------------------------------------------------------------- partition

@@ -11,8 +11,9 @@
 //
 // k_reduce_requant needs a block-wide absmax, so it uses the block-grouped
 // mapping of k_quantize.  k_reduce_f32 has no cross-element step, so it uses an
-// elementwise mapping with 4-element units: every lane stores one 16-byte
-// float4 and a warp instruction writes one contiguous 512-byte span.
+// elementwise mapping with one 8-byte code load per lane per input and a
+// shared-memory transpose for coalesced 512-byte fp32 stores.  Inputs may be
+// peer-mapped (NVLink P2P transport): 8-byte loads keep peer reads at full speed.
 #include "codec.cuh"
 
 namespace hz {
@@ -182,70 +183,121 @@ __global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_consta
 }
 
 // --------------------------------------------------------------- fp32-output reduce
-template <int BIN, int GT, int U>
+// Elementwise: a unit is the 8 code bytes of E = 64/BIN consecutive elements (one
+// 8-byte load per input — wide enough for NVLink peer reads, which run at half
+// speed with 2-byte loads); a warp chunk is 32 consecutive units.  The E fp32 sums
+// of a lane are staged through shared memory (XOR-swizzled 16-byte granules:
+// conflict-free both ways) so that every global store / accumulate load of the
+// warp is one contiguous 512-byte span.
+template <int BIN>
+struct Wide;
+template <>
+struct Wide<8> {
+  static constexpr int E = 8;
+  uint2 r;
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void decode(float (&c)[E]) const {
+    Codes8<8> x;
+    x.r = r;
+    x.decode(c);
+  }
+};
+template <>
+struct Wide<4> {
+  static constexpr int E = 16;
+  uint2 r;
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void decode(float (&c)[E]) const {
+    Codes8<4> lo, hi;
+    lo.r = r.x;
+    hi.r = r.y;
+    float a[8], b[8];
+    lo.decode(a);
+    hi.decode(b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      c[i] = a[i];
+      c[8 + i] = b[i];
+    }
+  }
+};
+
+template <int BIN, int GT, int U, bool ACC>
 __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__ RedArgs a, int log2b,
                                                          const __grid_constant__ SyncArgs sy) {
+  constexpr int E = Wide<BIN>::E;
+  constexpr int G = E / 4;                         // float4 granules per lane per unit
+  __shared__ float4 stage[kThreads / 32][32 * G];
   sync_wait(sy);
   const int lane = threadIdx.x & 31;
+  float4* st = stage[threadIdx.x >> 5];
   const int64_t warp = global_warp();
   const int64_t nwarps = num_warps();
-  const int64_t nunits = a.n / 4;
+  const int64_t nunits = a.n / E;
   constexpr int GP = GT > 0 ? GT : 1;
   for (int64_t base = warp * 32 * U; base < nunits; base += nwarps * 32 * U) {
-    float acc[U][4];
-    float4 old[U];
+    float acc[U][E];
+    float4 old[ACC ? U : 1][G];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t chunk = base + u * 32;            // first unit of this warp chunk
+      if (ACC && chunk < nunits) {
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          const int64_t g4 = chunk * G + k * 32 + lane;   // float4 index, contiguous per k
+          if (g4 < nunits * G) old[u][k] = reinterpret_cast<const float4*>(a.of)[g4];
+        }
+      }
+    }
     if constexpr (GT > 0) {
-      Codes4<BIN> raw[U][GP];
+      Wide<BIN> raw[U][GP];
       float sc[U][GP];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t unit = base + u * 32 + lane;
-        if (unit < nunits) {
 #pragma unroll
-          for (int p = 0; p < GP; ++p) {
-            raw[u][p].load(a.c[p] + unit * BIN / 2);
-            sc[u][p] = __ldg(a.s[p] + ((unit * 4) >> log2b));
+        for (int p = 0; p < GP; ++p) {
+          sc[u][p] = 0.f;
+          raw[u][p].r = make_uint2(0u, 0u);
+          if (unit < nunits) {
+            raw[u][p].load(a.c[p] + unit * 8);
+            sc[u][p] = __ldg(a.s[p] + ((unit * E) >> log2b));
           }
-          if (a.accumulate) old[u] = reinterpret_cast<const float4*>(a.of)[unit];
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        float c[4];
+        float c[E];
         raw[u][0].decode(c);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[u][i] = __fmul_rn(c[i], sc[u][0]);
+        for (int i = 0; i < E; ++i) acc[u][i] = __fmul_rn(c[i], sc[u][0]);
 #pragma unroll
         for (int p = 1; p < GP; ++p) {
           raw[u][p].decode(c);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[u][i] = __fadd_rn(acc[u][i], __fmul_rn(c[i], sc[u][p]));
+          for (int i = 0; i < E; ++i) acc[u][i] = __fadd_rn(acc[u][i], __fmul_rn(c[i], sc[u][p]));
         }
       }
     } else {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t unit = base + u * 32 + lane;
-        if (unit < nunits && a.accumulate) old[u] = reinterpret_cast<const float4*>(a.of)[unit];
-      }
       for (int p = 0; p < a.g; ++p) {
-        Codes4<BIN> raw[U];
+        Wide<BIN> raw[U];
         float sc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int64_t unit = base + u * 32 + lane;
           sc[u] = 0.f;
+          raw[u].r = make_uint2(0u, 0u);
           if (unit < nunits) {
-            raw[u].load(a.c[p] + unit * BIN / 2);
-            sc[u] = __ldg(a.s[p] + ((unit * 4) >> log2b));
+            raw[u].load(a.c[p] + unit * 8);
+            sc[u] = __ldg(a.s[p] + ((unit * E) >> log2b));
           }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          float c[4];
+          float c[E];
           raw[u].decode(c);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < E; ++i) {
             const float xh = __fmul_rn(c[i], sc[u]);
             acc[u][i] = p == 0 ? xh : __fadd_rn(acc[u][i], xh);
           }
@@ -254,17 +306,31 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t unit = base + u * 32 + lane;
-      if (unit < nunits) {
-        float4 o = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
-        if (a.accumulate) {
-          o.x = __fadd_rn(old[u].x, o.x);
-          o.y = __fadd_rn(old[u].y, o.y);
-          o.z = __fadd_rn(old[u].z, o.z);
-          o.w = __fadd_rn(old[u].w, o.w);
-        }
-        reinterpret_cast<float4*>(a.of)[unit] = o;
+      const int64_t chunk = base + u * 32;
+      if (chunk >= nunits) break;                      // warp-uniform
+      // lane's E sums -> granules lane*G + j (swizzled), then read back granule k*32 + lane
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int gi = lane * G + j;
+        st[gi ^ ((gi >> 3) & (G - 1))] = make_float4(acc[u][4 * j], acc[u][4 * j + 1], acc[u][4 * j + 2], acc[u][4 * j + 3]);
       }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const int gi = k * 32 + lane;
+        float4 o = st[gi ^ ((gi >> 3) & (G - 1))];
+        const int64_t g4 = chunk * G + gi;
+        if (g4 < nunits * G) {
+          if constexpr (ACC) {
+            o.x = __fadd_rn(old[u][k].x, o.x);
+            o.y = __fadd_rn(old[u][k].y, o.y);
+            o.z = __fadd_rn(old[u][k].z, o.z);
+            o.w = __fadd_rn(old[u][k].w, o.w);
+          }
+          reinterpret_cast<float4*>(a.of)[g4] = o;
+        }
+      }
+      __syncwarp();
     }
   }
   sync_signal(sy);
@@ -272,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
 
 // ---------------------------------------------------------------------- launch
 constexpr int kUR = 4;   // warp steps per warp iteration (requant)
-constexpr int kUF = 4;   // 4-element units in flight per lane (fp32 out)
+constexpr int kUF = 2;   // 8-byte code units in flight per lane per input (fp32 out)
 constexpr int ur(int B) { return B > 256 ? 1 : kUR; }
 
 template <int B, int BIN, int BOUT, int GT, int U>
@@ -317,8 +383,8 @@ cudaError_t requant_b(const RedArgs& a, int bits_in, int bits_out, cudaStream_t 
 
 template <int BIN, int GT, int U>
 cudaError_t f32_u(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& sy) {
-  const int64_t nunits = a.n / 4;
-  auto kern = k_reduce_f32<BIN, GT, U>;
+  const int64_t nunits = a.n / Wide<BIN>::E;
+  auto kern = a.accumulate ? k_reduce_f32<BIN, GT, U, true> : k_reduce_f32<BIN, GT, U, false>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
   kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, log2b, sy);
   return cudaGetLastError();
@@ -326,10 +392,10 @@ cudaError_t f32_u(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& 
 
 template <int BIN, int GT>
 cudaError_t f32_t(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& sy) {
-  if constexpr (GT > 0 && GT <= 2) {   // HZ_TUNE rf_u: 2, 4, 8
+  if constexpr (GT > 0 && GT <= 2) {   // HZ_TUNE rf_u: 1, 2, 4
     switch (tune_param("rf_u", kUF)) {
-      case 2: return f32_u<BIN, GT, 2>(a, log2b, st, sy);
-      case 8: return f32_u<BIN, GT, 8>(a, log2b, st, sy);
+      case 1: return f32_u<BIN, GT, 1>(a, log2b, st, sy);
+      case 4: return f32_u<BIN, GT, 4>(a, log2b, st, sy);
       default: break;
     }
   }

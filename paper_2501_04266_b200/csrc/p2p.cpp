@@ -31,6 +31,10 @@
 #include "ctx.h"
 
 namespace hz {
+int tune_param(const char* name, int dflt);
+}
+
+namespace hz {
 namespace {
 
 #define P2P_CUDA(call, what)                              \
@@ -84,6 +88,7 @@ SyncArgs make_sync(hz_ctx* ctx, unsigned long long wait_ready, unsigned long lon
   s.wait_done = wait_done;
   s.sig_ready = sig_ready;
   s.sig_done = sig_done;
+  s.mode = tune_param("p2p_sig", 1);   // fence.acq_rel.sys + relaxed.sys flag stores
   return s;
 }
 

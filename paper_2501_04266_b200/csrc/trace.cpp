@@ -2,6 +2,9 @@
 // launching stream around every kernel and every NCCL group (hz_trace_*).
 // Events are created up front by hz_trace_begin so that recording inside a timed
 // region costs two cudaEventRecord calls per launch and no allocation.
+// P2P kernels additionally write three %globaltimer stamps into a device array
+// (CTA 0 at entry and after its cross-GPU wait, the last CTA at exit), which
+// splits a launch into the time spent waiting for peers and the work itself.
 #include <mutex>
 #include <vector>
 
@@ -23,19 +26,24 @@ bool g_on = false;
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
 size_t g_used = 0;
+unsigned long long* g_stamps = nullptr;   // device [capacity][4]
+size_t g_cap = 0;
 
 void destroy_pool() {
   for (auto e : g_pool) cudaEventDestroy(e);
   g_pool.clear();
   g_recs.clear();
   g_used = 0;
+  if (g_stamps) cudaFree(g_stamps);
+  g_stamps = nullptr;
+  g_cap = 0;
 }
 
 }  // namespace
 
 TraceScope::TraceScope(cudaStream_t st, const char* kind, int level, int bits, int64_t elems,
                        int64_t bytes)
-    : active(false), slot(-1), stream(st) {
+    : active(false), slot(-1), stream(st), stamps(nullptr) {
   std::lock_guard<std::mutex> lock(g_mu);
   if (!g_on || g_used + 2 > g_pool.size()) return;
   Rec r{kind, level, bits, elems, bytes, g_pool[g_used], g_pool[g_used + 1], st};
@@ -46,6 +54,7 @@ TraceScope::TraceScope(cudaStream_t st, const char* kind, int level, int bits, i
   }
   g_recs.push_back(r);
   slot = static_cast<int>(g_recs.size()) - 1;
+  if (g_stamps && static_cast<size_t>(slot) < g_cap) stamps = g_stamps + 4 * slot;
   active = true;
 }
 
@@ -78,6 +87,13 @@ hz_status hz_trace_begin(int capacity) {
       return fail(HZ_ERR_CUDA, "hz_trace_begin: cudaEventCreate failed");
     }
   }
+  if (cudaMalloc(&g_stamps, sizeof(unsigned long long) * 4 * capacity) != cudaSuccess ||
+      cudaMemset(g_stamps, 0, sizeof(unsigned long long) * 4 * capacity) != cudaSuccess) {
+    cudaGetLastError();
+    g_stamps = nullptr;
+  } else {
+    g_cap = static_cast<size_t>(capacity);
+  }
   g_recs.reserve(capacity);
   g_on = true;
   clear_error();
@@ -96,9 +112,22 @@ hz_status hz_trace_read(hz_trace_rec* out, int max, int* n_out) {
   if (!n_out) return fail(HZ_ERR_INVALID, "n_out: NULL");
   if (max > 0 && !out) return fail(HZ_ERR_INVALID, "out: NULL");
   std::lock_guard<std::mutex> lock(g_mu);
+  std::vector<unsigned long long> st;
+  const size_t nrec = g_recs.size();
+  if (max > 0 && g_stamps && nrec) {
+    const size_t cnt = nrec < g_cap ? nrec : g_cap;
+    st.resize(4 * cnt);
+    if (!g_recs.empty()) cudaEventSynchronize(g_recs.back().b);
+    if (cudaMemcpy(st.data(), g_stamps, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      st.clear();
+    }
+  }
   int n = 0;
-  for (const Rec& r : g_recs) {
+  for (size_t i = 0; i < nrec; ++i) {
     if (n >= max) break;
+    const Rec& r = g_recs[i];
     float ms = 0.f;
     if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) {
       cudaGetLastError();
@@ -110,9 +139,17 @@ hz_status hz_trace_read(hz_trace_rec* out, int max, int* n_out) {
     out[n].elems = r.elems;
     out[n].bytes = r.bytes;
     out[n].ms = ms;
+    out[n].wait_ms = -1.f;
+    out[n].work_ms = -1.f;
+    out[n].publish_ms = -1.f;
+    if (4 * i + 3 < st.size() && st[4 * i] && st[4 * i + 1] && st[4 * i + 2] >= st[4 * i + 1]) {
+      out[n].wait_ms = static_cast<float>(st[4 * i + 1] - st[4 * i]) * 1e-6f;
+      out[n].work_ms = static_cast<float>(st[4 * i + 2] - st[4 * i + 1]) * 1e-6f;
+      out[n].publish_ms = st[4 * i + 3] >= st[4 * i + 2] ? static_cast<float>(st[4 * i + 3] - st[4 * i + 2]) * 1e-6f : -1.f;
+    }
     ++n;
   }
-  *n_out = max > 0 ? n : static_cast<int>(g_recs.size());
+  *n_out = max > 0 ? n : static_cast<int>(nrec);
   clear_error();
   return HZ_OK;
 }

@@ -62,7 +62,8 @@ class Uid(ctypes.Structure):
 
 class TraceRec(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_char_p), ("level", ctypes.c_int32), ("bits", ctypes.c_int32),
-                ("elems", ctypes.c_int64), ("bytes", ctypes.c_int64), ("ms", ctypes.c_float)]
+                ("elems", ctypes.c_int64), ("bytes", ctypes.c_int64), ("ms", ctypes.c_float),
+                ("wait_ms", ctypes.c_float), ("work_ms", ctypes.c_float), ("publish_ms", ctypes.c_float)]
 
 
 class CommStep(ctypes.Structure):
@@ -265,7 +266,9 @@ def trace_read(max_records=1 << 16):
     recs = (TraceRec * max(cnt, 1))()
     _check(_lib.hz_trace_read(recs, cnt, ctypes.byref(n)))
     return [{"kind": r.kind.decode(), "level": r.level, "bits": r.bits, "elems": r.elems,
-             "bytes": r.bytes, "ms": r.ms} for r in recs[:n.value]]
+             "bytes": r.bytes, "ms": r.ms, "wait_ms": r.wait_ms, "work_ms": r.work_ms,
+             "publish_ms": r.publish_ms}
+            for r in recs[:n.value]]
 
 
 _TYPESTR = {"torch.uint8": "|u1", "torch.float32": "<f4", "torch.bfloat16": "<V2", "torch.float16": "<f2"}
