@@ -43,7 +43,7 @@ HIERARCHY = {
     "gpt6.7b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
     "neox20b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
 }
-KERNEL_KINDS = ("quantize", "dequantize", "reduce", "reduce_requant")
+KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "reduce", "reduce_requant")
 NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
 
@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 collective transport: fused NVLink peer-memory kernels (p2p) or NCCL")
     ap.add_argument("--cpu-sample-layers", type=int, default=4)
+    ap.add_argument("--no-trace", action="store_true", help="no per-launch events (overhead check)")
+    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=False,
+                    help="capture one step in a CUDA graph and time graph replays")
     return ap.parse_args()
 
 
@@ -249,7 +252,7 @@ def barrier(world):
 def summarize_trace(recs, steps):
     kinds = {}
     for r in recs:
-        k = kinds.setdefault(r["kind"], {"launches": 0, "ms": 0.0, "bytes": 0, "elems": 0,
+        k = kinds.setdefault(r["kind"], {"launches": 0, "ms": 0.0, "bytes": 0, "elems": 0, "remote": 0,
                                          "wait_ms": 0.0, "work_ms": 0.0, "publish_ms": 0.0, "stamped": 0})
         k["launches"] += 1
         k["ms"] += r["ms"]
@@ -259,6 +262,7 @@ def summarize_trace(recs, steps):
             k["work_ms"] += r["work_ms"]
             k["publish_ms"] += max(r.get("publish_ms", 0.0), 0.0)
         k["bytes"] += r["bytes"]
+        k["remote"] += r.get("remote_bytes", 0)
         k["elems"] += r["elems"]
     total_ms = sum(v["ms"] for v in kinds.values()) or 1.0
     out = {}
@@ -271,6 +275,9 @@ def summarize_trace(recs, steps):
             "GBps": v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else None,
             "share": v["ms"] / total_ms,
         }
+        if v["remote"]:
+            out[name]["avg_remote_bytes"] = v["remote"] / v["launches"]
+            out[name]["nvlink_GBps"] = v["remote"] / (v["ms"] * 1e-3) / 1e9
         if v["stamped"]:
             out[name]["avg_wait_ms"] = v["wait_ms"] / v["stamped"]
             out[name]["avg_work_ms"] = v["work_ms"] / v["stamped"]
@@ -305,6 +312,7 @@ def run_hz(args):
         ctx.enable_p2p(p2p_pool_bytes(args, group))
     model = Model(hz, ctx, torch, args.config, rank, world, args, device)
     stream = torch.cuda.current_stream()
+    use_graph = args.graph
 
     # clocks are sampled from the start of the warm-up (under the same load) through
     # the end of the timed region: the timed region alone is often shorter than the
@@ -321,16 +329,42 @@ def run_hz(args):
         torch.cuda.synchronize()
 
     per_step_kernels = 5 * len(model.tensors)
-    hz.trace_begin(capacity=(args.steps + 1) * per_step_kernels * 4 + 64)
+    if not args.no_trace:
+        hz.trace_begin(capacity=(args.steps + 1) * per_step_kernels * 4 + 64)
+    graph = None
+    if use_graph:
+        # one step captured into a CUDA graph (the library's kernels, NCCL calls and
+        # trace events become graph nodes); each timed step is one replay
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cs):
+            if transport == "p2p":
+                ctx.p2p_capture_begin()
+            model.step(cs)
+            if transport == "p2p":
+                ctx.p2p_capture_end(cs)
+        torch.cuda.synchronize()
+        for _ in range(2):
+            graph.replay()
+        if transport == "p2p":
+            ctx.p2p_replayed(2)
+        torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        model.step(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            model.step(stream)
     e1.record(stream)
     torch.cuda.synchronize()
+    if graph is not None and transport == "p2p":
+        ctx.p2p_replayed(args.steps)
     barrier(world)
     hz.trace_end()
     clocks = sampler.stop() if sampler else None
@@ -338,22 +372,39 @@ def run_hz(args):
     ms = max_over_ranks(ms, world)
     ms_per_step = ms / args.steps
     recs = hz.trace_read()
-    stages = summarize_trace(recs, args.steps)
-    gpu_launches = sum(1 for r in recs if r["kind"] in KERNEL_KINDS)
+    # with a graph the trace holds one step's launches (events re-recorded by every replay)
+    stages = summarize_trace(recs, 1 if graph is not None else args.steps)
+    gpu_launches = sum(1 for r in recs if r["kind"] in KERNEL_KINDS) * (args.steps if graph is not None else 1)
     value = world * model.logical_bytes / (ms_per_step * 1e-3) / 1e9
 
     # roofline: the kernel kind with the largest share of device time
     peak, peak_src = measured_peaks()
     kern = {k: v for k, v in stages.items() if k in KERNEL_KINDS}
-    dom = max(kern, key=lambda k: kern[k]["share"])
-    d = kern[dom]
-    traffic = None
-    tr = ncu_traffic().get(dom)
-    if tr and tr.get("elems"):
-        traffic = tr["dram_bytes"] / tr["elems"] * d["avg_elems"]
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
-                "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes_per_launch": d["avg_bytes"],
-                "avg_launch_ms": d["avg_ms"], "peak_source": peak_src}
+    roofline = None
+    if kern:
+        dom = max(kern, key=lambda k: kern[k]["share"])
+        d = kern[dom]
+        traffic = None
+        tr = ncu_traffic().get(dom)
+        if tr and tr.get("elems"):
+            traffic = tr["dram_bytes"] / tr["elems"] * d["avg_elems"]
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
+                    "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes_per_launch": d["avg_bytes"],
+                    "avg_launch_ms": d["avg_ms"], "peak_source": peak_src}
+        rb = d.get("avg_remote_bytes", 0)
+        if rb:
+            # fused NVLink kernel: the floor is the slower of local HBM bytes / HBM peak and
+            # peer bytes / NVLink peer bandwidth (770 GB/s per direction, measured; 900 nominal)
+            t_hbm = d["avg_bytes"] / (peak * 1e9)
+            t_nvl = rb / (NVLINK_PEER_GBS * 1e9)
+            roofline.update({"hbm_frac": d["GBps"] / peak, "nvlink_achieved": d["nvlink_GBps"],
+                             "nvlink_peak": NVLINK_PEER_GBS, "nvlink_frac": d["nvlink_GBps"] / NVLINK_PEER_GBS,
+                             "remote_bytes_per_launch": rb,
+                             "floor_ms": max(t_hbm, t_nvl) * 1e3, "frac_of_floor": max(t_hbm, t_nvl) * 1e3 / d["avg_ms"]})
+            if t_nvl > t_hbm:
+                roofline.update({"bound": "nvlink", "achieved": d["nvlink_GBps"], "peak": NVLINK_PEER_GBS,
+                                 "frac": d["nvlink_GBps"] / NVLINK_PEER_GBS,
+                                 "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"})
     nccl = {k: v for k, v in stages.items() if k.startswith("nccl")}
     for v in nccl.values():
         v["frac_of_nvlink_770"] = (v["GBps"] or 0) / NVLINK_PEER_GBS
@@ -384,6 +435,7 @@ def run_hz(args):
             "l2": "inputs larger than L2 (each step streams several GB); no flush",
             "parallelism": f"dp{world} hierarchical ({'x'.join(map(str, group))})",
             "transport": transport,
+            "cuda_graph": graph is not None,
         },
         "roofline": roofline,
         "cpu_baseline": cpu,

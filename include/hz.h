@@ -248,6 +248,17 @@ HZ_API hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, c
 HZ_API hz_status hz_enable_p2p(hz_ctx* ctx, size_t pool_bytes);
 HZ_API hz_status hz_p2p_enabled(const hz_ctx* ctx, int* out);
 
+/* CUDA-graph support for the P2P transport.  The cross-GPU phase numbers are
+ * stored in the kernels relative to a device-side epoch, so a captured step can
+ * be replayed: bracket the capture of one step with hz_p2p_capture_begin /
+ * hz_p2p_capture_end (the latter appends a one-thread node that advances the
+ * epoch by the step's phase count, returned in *span_out), and after launching
+ * the graph n times call hz_p2p_replayed(ctx, n) so that later eager calls
+ * continue the numbering.  Every rank must capture and replay identically. */
+HZ_API hz_status hz_p2p_capture_begin(hz_ctx* ctx);
+HZ_API hz_status hz_p2p_capture_end(hz_ctx* ctx, void* stream, unsigned long long* span_out);
+HZ_API hz_status hz_p2p_replayed(hz_ctx* ctx, unsigned long long n);
+
 /* Symmetric allocation from the P2P pool (256-byte aligned).  Every rank must make
  * the same sequence of calls with the same sizes, so that a buffer has the same
  * pool offset on every rank.  Freed with the context.  HZ_ERR_INVALID when the pool
@@ -277,7 +288,8 @@ typedef struct {
   int32_t level;
   int32_t bits;
   int64_t elems;
-  int64_t bytes;
+  int64_t bytes;        /* algorithmic bytes of this GPU's HBM (kernels) / bytes sent (NCCL) */
+  int64_t remote_bytes; /* P2P kernels: bytes read from peers over NVLink; else 0 */
   float ms;        /* CUDA-event duration of the launch on its stream */
   float wait_ms;   /* P2P kernels: time CTA 0 spent waiting for peers (device clock); else -1 */
   float work_ms;   /* P2P kernels: after-wait to last CTA arrival (device clock); else -1 */

@@ -351,15 +351,18 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __device__ __forceinline__ void sync_wait(const SyncArgs& s) {
   if (s.stamps && blockIdx.x == 0 && threadIdx.x == 0) s.stamps[0] = globaltimer();
-  if (!(s.wait_ready | s.wait_done)) {
+  if (!(s.en & (kWaitReady | kWaitDone))) {
     if (s.stamps && blockIdx.x == 0 && threadIdx.x == 0) s.stamps[1] = globaltimer();
     return;
   }
   if (threadIdx.x == 0) {
     const unsigned long long t0 = globaltimer();
+    const unsigned long long e = s.epoch ? *s.epoch : 0ull;
+    const unsigned long long wr = (s.en & kWaitReady) ? s.wait_ready + e : 0ull;
+    const unsigned long long wd = (s.en & kWaitDone) ? s.wait_done + e : 0ull;
     for (int q = 0; q < s.world; ++q) {
-      while ((s.wait_ready && ld_acquire_sys(s.ready_local + q) < s.wait_ready) ||
-             (s.wait_done && ld_acquire_sys(s.done_local + q) < s.wait_done)) {
+      while ((wr && ld_acquire_sys(s.ready_local + q) < wr) ||
+             (wd && ld_acquire_sys(s.done_local + q) < wd)) {
         if (globaltimer() - t0 > 20000000000ull) __trap();
       }
     }
@@ -369,7 +372,7 @@ __device__ __forceinline__ void sync_wait(const SyncArgs& s) {
 }
 
 __device__ __forceinline__ void sync_signal(const SyncArgs& s) {
-  if (!(s.sig_ready | s.sig_done)) return;
+  if (!(s.en & (kSigReady | kSigDone))) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     // gpu-scope release per CTA (peers read this GPU's memory through its L2, the
@@ -379,18 +382,21 @@ __device__ __forceinline__ void sync_signal(const SyncArgs& s) {
     if (atomicAdd(s.counter, 1u) == gridDim.x - 1) {
       *s.counter = 0u;
       if (s.stamps) s.stamps[2] = globaltimer();
+      const unsigned long long e = s.epoch ? *s.epoch : 0ull;
+      const unsigned long long sr = (s.en & kSigReady) ? s.sig_ready + e : 0ull;
+      const unsigned long long sd = (s.en & kSigDone) ? s.sig_done + e : 0ull;
       if (s.mode == 0) {
         __threadfence_system();
         for (int q = 0; q < s.world; ++q) {
-          if (s.sig_ready) st_release_sys(s.ready_remote[q], s.sig_ready);
-          if (s.sig_done) st_release_sys(s.done_remote[q], s.sig_done);
+          if (sr) st_release_sys(s.ready_remote[q], sr);
+          if (sd) st_release_sys(s.done_remote[q], sd);
         }
       } else {
         if (s.mode == 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
         else if (s.mode == 2) asm volatile("fence.acq_rel.gpu;" ::: "memory");
         for (int q = 0; q < s.world; ++q) {
-          if (s.sig_ready) st_relaxed_sys(s.ready_remote[q], s.sig_ready);
-          if (s.sig_done) st_relaxed_sys(s.done_remote[q], s.sig_done);
+          if (sr) st_relaxed_sys(s.ready_remote[q], sr);
+          if (sd) st_relaxed_sys(s.done_remote[q], sd);
         }
       }
       if (s.stamps) s.stamps[3] = globaltimer();

@@ -72,3 +72,16 @@ int tune_param(const char* name, int dflt) {
 }
 
 }  // namespace hz
+
+namespace hz {
+namespace {
+__global__ void k_epoch_advance(unsigned long long* epoch, unsigned long long span) { *epoch += span; }
+}  // namespace
+
+// P2P + CUDA graphs: the last node of a captured step advances the device phase
+// epoch, so every replay signals / waits on fresh phase numbers.
+cudaError_t launch_epoch_advance(unsigned long long* epoch, unsigned long long span, cudaStream_t st) {
+  k_epoch_advance<<<1, 1, 0, st>>>(epoch, span);
+  return cudaGetLastError();
+}
+}  // namespace hz

@@ -31,7 +31,11 @@ struct hz_ctx {
     size_t bytes = 0;
     size_t used = 0;                            // bump allocator (same on every rank)
     char* peer[hz::kMaxWorld] = {nullptr};      // every rank's pool base, mapped here
-    unsigned long long phase = 0;               // last phase number issued
+    unsigned long long phase = 0;               // last phase number issued (absolute)
+    unsigned long long epoch_host = 0;          // value *epoch will hold once enqueued work ran
+    unsigned long long capture_start = 0;       // phase at hz_p2p_capture_begin
+    unsigned long long span = 0;                // phases of the last captured graph
+    bool capturing = false;
     struct Slot {
       size_t off = 0, cap = 0;
     };
@@ -44,7 +48,7 @@ namespace hz {
 
 // header of the symmetric pool: ready[8] u64 | done[8] u64 | counter u32
 constexpr size_t kPoolHeader = 4096;
-constexpr size_t kReadyOff = 0, kDoneOff = 64, kCounterOff = 128;
+constexpr size_t kReadyOff = 0, kDoneOff = 64, kCounterOff = 128, kEpochOff = 192;
 
 hz_status cuda_fail(cudaError_t e, const char* what);
 hz_status nccl_fail(ncclResult_t r, const char* what);
@@ -61,7 +65,8 @@ hz_status run_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block
                                 int64_t remote_bytes);
 hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
                      int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
-                     cudaStream_t st, int level, const SyncArgs* sync = nullptr);
+                     cudaStream_t st, int level, const SyncArgs* sync = nullptr,
+                     int64_t remote_bytes = 0);
 hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
 
 // P2P transport (p2p.cpp)

@@ -129,7 +129,7 @@ hz_status run_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block
                                 hz_dtype odt, cudaStream_t st, int level, const SyncArgs* sync,
                                 int64_t remote_bytes) {
   TraceScope t(st, "gather_dequantize", level, bits, n,
-               code_bytes(n, bits) + n / block * 4 + n * elem_bytes(odt) - remote_bytes);
+               code_bytes(n, bits) + n / block * 4 + n * elem_bytes(odt) - remote_bytes, remote_bytes);
   SyncArgs sy{};
   if (sync) {
     sy = *sync;
@@ -143,11 +143,12 @@ hz_status run_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block
 
 hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
                      int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
-                     cudaStream_t st, int level, const SyncArgs* sync) {
+                     cudaStream_t st, int level, const SyncArgs* sync, int64_t remote_bytes) {
   const int64_t in_bytes = g * (code_bytes(n, bits_in) + n / block * 4);
   const int64_t out_bytes =
       bits_out ? code_bytes(n, bits_out) + n / block * 4 : n * 4 * (acc ? 2 : 1);
-  TraceScope t(st, bits_out ? "reduce_requant" : "reduce", level, bits_in, n, in_bytes + out_bytes);
+  TraceScope t(st, bits_out ? "reduce_requant" : "reduce", level, bits_in, n,
+               in_bytes + out_bytes - remote_bytes, remote_bytes);
   SyncArgs sy{};
   if (sync) {
     sy = *sync;

@@ -24,6 +24,7 @@ int64_t code_bytes(int64_t n, int bits);   // n * bits / 8
 // ------------------------------------------------------------- P2P phase sync
 // (see codec.cuh for the protocol).  A zero-initialised SyncArgs means "no sync".
 constexpr int kMaxWorld = 8;
+constexpr unsigned kWaitReady = 1u, kWaitDone = 2u, kSigReady = 4u, kSigDone = 8u;
 struct SyncArgs {
   unsigned long long* ready_local;
   unsigned long long* done_local;
@@ -31,7 +32,11 @@ struct SyncArgs {
   unsigned long long* done_remote[kMaxWorld];
   unsigned int* counter;
   int world;
+  // phase thresholds relative to *epoch (the device-side phase offset advanced by
+  // every replay of a captured CUDA graph); `en` says which of them are active
   unsigned long long wait_ready, wait_done, sig_ready, sig_done;
+  const unsigned long long* epoch;
+  unsigned en;   // kWaitReady | kWaitDone | kSigReady | kSigDone
   unsigned long long* stamps;   // optional [4]: entry, after wait, last-CTA arrival, flags sent (ns)
   int mode;                     // publication fence variant (HZ_TUNE p2p_sig; 0 = fence.sc.sys)
 };
@@ -62,6 +67,7 @@ cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, int64_t
 cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,
                                      hz_dtype out_dt, cudaStream_t st, const SyncArgs* sync);
 constexpr int kMaxG = 16;
+cudaError_t launch_epoch_advance(unsigned long long* epoch, unsigned long long span, cudaStream_t st);
 cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
                           int64_t n, int bits_in, int block, int bits_out, uint8_t* out_codes,
                           float* out_scales, float* out_f32, int accumulate, cudaStream_t st,
@@ -70,8 +76,9 @@ cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const
 // ------------------------------------------------------------------ tracing
 struct TraceScope {
   // Records a start event on construction and an end event + record on end().
+  // bytes = algorithmic bytes of this GPU's HBM; remote = bytes read from peers over NVLink
   TraceScope(cudaStream_t st, const char* kind, int level, int bits, int64_t elems,
-             int64_t bytes);
+             int64_t bytes, int64_t remote = 0);
   void end();
   ~TraceScope();
   bool active;

@@ -336,6 +336,103 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
   sync_signal(sy);
 }
 
+// Direct-store variant: E (4 or 8) consecutive elements per lane, E/4 float4 stores
+// per lane at lane-contiguous addresses (no shared-memory staging).  Narrower code
+// loads (E*BIN/8 bytes per lane); kept for the HZ_TUNE rf_e sweep.
+template <int BIN, int E>
+struct Narrow {
+  static constexpr int NB = E * BIN / 8;   // code bytes per lane
+  unsigned r;
+  __device__ __forceinline__ void load(const uint8_t* p) {
+    if constexpr (NB == 2) r = __ldg(reinterpret_cast<const unsigned short*>(p));
+    else r = __ldg(reinterpret_cast<const unsigned*>(p));
+  }
+  __device__ __forceinline__ void decode(float (&c)[E]) const {
+    if constexpr (BIN == 8) {
+      const unsigned x = r ^ 0x80808080u;
+#pragma unroll
+      for (int i = 0; i < E; ++i) c[i] = __fsub_rn(byte_as_magic(x, i), kMagic + 128.f);
+    } else {
+      const unsigned x = r ^ 0x88888888u;
+      const unsigned ev = x & 0x0F0F0F0Fu;
+      const unsigned od = (x >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+      for (int i = 0; i < E / 2; ++i) {
+        c[2 * i] = __fsub_rn(byte_as_magic(ev, i), kMagic + 8.f);
+        c[2 * i + 1] = __fsub_rn(byte_as_magic(od, i), kMagic + 8.f);
+      }
+    }
+  }
+};
+
+template <int BIN, int E, int GT, int U, bool ACC>
+__global__ void __launch_bounds__(kThreads) k_reduce_f32_direct(const __grid_constant__ RedArgs a, int log2b,
+                                                                const __grid_constant__ SyncArgs sy) {
+  static_assert(BIN == 8 ? E == 4 : (E == 4 || E == 8), "unit width");
+  sync_wait(sy);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = global_warp();
+  const int64_t nwarps = num_warps();
+  const int64_t nunits = a.n / E;
+  constexpr int GP = GT > 0 ? GT : 1;
+  for (int64_t base = warp * 32 * U; base < nunits; base += nwarps * 32 * U) {
+    float acc[U][E];
+    float4 old[ACC ? U : 1][E / 4];
+    Narrow<BIN, E> raw[U][GP];
+    float sc[U][GP];
+    const int np = GT > 0 ? GT : a.g;
+    for (int p0 = 0; p0 < np; p0 += GP) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t unit = base + u * 32 + lane;
+#pragma unroll
+        for (int q = 0; q < GP; ++q) {
+          sc[u][q] = 0.f;
+          raw[u][q].r = 0u;
+          if (unit < nunits) {
+            raw[u][q].load(a.c[p0 + q] + unit * Narrow<BIN, E>::NB);
+            sc[u][q] = __ldg(a.s[p0 + q] + ((unit * E) >> log2b));
+          }
+        }
+        if (ACC && p0 == 0 && unit < nunits) {
+#pragma unroll
+          for (int k = 0; k < E / 4; ++k) old[u][k] = reinterpret_cast<const float4*>(a.of)[unit * (E / 4) + k];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < GP; ++q) {
+          float c[E];
+          raw[u][q].decode(c);
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            const float xh = __fmul_rn(c[i], sc[u][q]);
+            acc[u][i] = (p0 + q) == 0 ? xh : __fadd_rn(acc[u][i], xh);
+          }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t unit = base + u * 32 + lane;
+      if (unit < nunits) {
+#pragma unroll
+        for (int k = 0; k < E / 4; ++k) {
+          float4 o = make_float4(acc[u][4 * k], acc[u][4 * k + 1], acc[u][4 * k + 2], acc[u][4 * k + 3]);
+          if constexpr (ACC) {
+            o.x = __fadd_rn(old[u][k].x, o.x);
+            o.y = __fadd_rn(old[u][k].y, o.y);
+            o.z = __fadd_rn(old[u][k].z, o.z);
+            o.w = __fadd_rn(old[u][k].w, o.w);
+          }
+          reinterpret_cast<float4*>(a.of)[unit * (E / 4) + k] = o;
+        }
+      }
+    }
+  }
+  sync_signal(sy);
+}
+
 // ---------------------------------------------------------------------- launch
 constexpr int kUR = 4;   // warp steps per warp iteration (requant)
 constexpr int kUF = 2;   // 8-byte code units in flight per lane per input (fp32 out)
@@ -390,8 +487,24 @@ cudaError_t f32_u(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& 
   return cudaGetLastError();
 }
 
+template <int BIN, int E, int GT>
+cudaError_t f32_direct(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& sy) {
+  constexpr int U = 4;
+  const int64_t nunits = a.n / E;
+  auto kern = a.accumulate ? k_reduce_f32_direct<BIN, E, GT, U, true> : k_reduce_f32_direct<BIN, E, GT, U, false>;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, log2b, sy);
+  return cudaGetLastError();
+}
+
 template <int BIN, int GT>
 cudaError_t f32_t(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& sy) {
+  if constexpr (GT > 0 && GT <= 2) {   // HZ_TUNE rf_e: 4, 8 = direct-store variants
+    const int e = tune_param("rf_e", 0);
+    if (e == 4) return f32_direct<BIN, 4, GT>(a, log2b, st, sy);
+    if constexpr (BIN == 4)
+      if (e == 8) return f32_direct<BIN, 8, GT>(a, log2b, st, sy);
+  }
   if constexpr (GT > 0 && GT <= 2) {   // HZ_TUNE rf_u: 1, 2, 4
     switch (tune_param("rf_u", kUF)) {
       case 1: return f32_u<BIN, GT, 1>(a, log2b, st, sy);

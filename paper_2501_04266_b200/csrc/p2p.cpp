@@ -84,10 +84,16 @@ SyncArgs make_sync(hz_ctx* ctx, unsigned long long wait_ready, unsigned long lon
   }
   s.counter = reinterpret_cast<unsigned int*>(P.pool + kCounterOff);
   s.world = ctx->world;
-  s.wait_ready = wait_ready;
-  s.wait_done = wait_done;
-  s.sig_ready = sig_ready;
-  s.sig_done = sig_done;
+  // thresholds are stored relative to the device epoch the kernel will see
+  // (arguments: absolute phase numbers, 0 = none; phase numbers are > epoch_host)
+  const unsigned long long e = P.epoch_host;
+  s.en = (wait_ready ? kWaitReady : 0u) | (wait_done ? kWaitDone : 0u) | (sig_ready ? kSigReady : 0u) |
+         (sig_done ? kSigDone : 0u);
+  s.wait_ready = wait_ready - e;
+  s.wait_done = wait_done - e;
+  s.sig_ready = sig_ready - e;
+  s.sig_done = sig_done - e;
+  s.epoch = reinterpret_cast<const unsigned long long*>(P.pool + kEpochOff);
   s.mode = tune_param("p2p_sig", 1);   // fence.acq_rel.sys + relaxed.sys flag stores
   return s;
 }
@@ -239,15 +245,16 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
       ptr_s[j] = at<const float>(ctx, m, P.rs_s[l].off) + d * cl / B;
     }
     const unsigned long long ph = phase_of(l);
+    const int64_t remote = (g - 1) * (code_bytes(cl, bits) + cl / B * 4);
     if (l < to_level) {
       SyncArgs sr = make_sync(ctx, ph, ph - 1, ph + 1, ph);
       if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, bits_per_level[l],
                            at<uint8_t>(ctx, ctx->rank, P.rs_c[l + 1].off),
-                           at<float>(ctx, ctx->rank, P.rs_s[l + 1].off), nullptr, 0, st, l, &sr)) != HZ_OK)
+                           at<float>(ctx, ctx->rank, P.rs_s[l + 1].off), nullptr, 0, st, l, &sr, remote)) != HZ_OK)
         return rc;
     } else {
       SyncArgs sr = make_sync(ctx, ph, 0, 0, ph);
-      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st, l, &sr)) !=
+      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st, l, &sr, remote)) !=
           HZ_OK)
         return rc;
     }
@@ -330,6 +337,42 @@ hz_status hz_p2p_enabled(const hz_ctx* ctx, int* out) {
   using namespace hz;
   if (!ctx || !out) return fail(HZ_ERR_INVALID, "ctx/out: NULL");
   *out = ctx->p2p.on ? 1 : 0;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_p2p_capture_begin(hz_ctx* ctx) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  if (!ctx->p2p.on) return fail(HZ_ERR_INVALID, "ctx: P2P not enabled");
+  if (ctx->p2p.capturing) return fail(HZ_ERR_INVALID, "ctx: capture already begun");
+  ctx->p2p.capturing = true;
+  ctx->p2p.capture_start = ctx->p2p.phase;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_p2p_capture_end(hz_ctx* ctx, void* stream, unsigned long long* span_out) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  auto& P = ctx->p2p;
+  if (!P.capturing) return fail(HZ_ERR_INVALID, "ctx: no capture in progress");
+  P.capturing = false;
+  P.span = P.phase - P.capture_start;
+  P.phase = P.capture_start;   // nothing captured has run yet
+  cudaError_t e = launch_epoch_advance(reinterpret_cast<unsigned long long*>(P.pool + kEpochOff), P.span,
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "epoch-advance kernel launch");
+  if (span_out) *span_out = P.span;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_p2p_replayed(hz_ctx* ctx, unsigned long long n) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  ctx->p2p.phase += n * ctx->p2p.span;
+  ctx->p2p.epoch_host += n * ctx->p2p.span;
   clear_error();
   return HZ_OK;
 }

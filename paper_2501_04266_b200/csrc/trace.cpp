@@ -16,7 +16,7 @@ namespace {
 struct Rec {
   const char* kind;
   int level, bits;
-  int64_t elems, bytes;
+  int64_t elems, bytes, remote;
   cudaEvent_t a, b;
   cudaStream_t st;
 };
@@ -42,11 +42,11 @@ void destroy_pool() {
 }  // namespace
 
 TraceScope::TraceScope(cudaStream_t st, const char* kind, int level, int bits, int64_t elems,
-                       int64_t bytes)
+                       int64_t bytes, int64_t remote)
     : active(false), slot(-1), stream(st), stamps(nullptr) {
   std::lock_guard<std::mutex> lock(g_mu);
   if (!g_on || g_used + 2 > g_pool.size()) return;
-  Rec r{kind, level, bits, elems, bytes, g_pool[g_used], g_pool[g_used + 1], st};
+  Rec r{kind, level, bits, elems, bytes, remote, g_pool[g_used], g_pool[g_used + 1], st};
   g_used += 2;
   if (cudaEventRecord(r.a, st) != cudaSuccess) {
     cudaGetLastError();
@@ -138,6 +138,7 @@ hz_status hz_trace_read(hz_trace_rec* out, int max, int* n_out) {
     out[n].bits = r.bits;
     out[n].elems = r.elems;
     out[n].bytes = r.bytes;
+    out[n].remote_bytes = r.remote;
     out[n].ms = ms;
     out[n].wait_ms = -1.f;
     out[n].work_ms = -1.f;

@@ -62,7 +62,8 @@ class Uid(ctypes.Structure):
 
 class TraceRec(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_char_p), ("level", ctypes.c_int32), ("bits", ctypes.c_int32),
-                ("elems", ctypes.c_int64), ("bytes", ctypes.c_int64), ("ms", ctypes.c_float),
+                ("elems", ctypes.c_int64), ("bytes", ctypes.c_int64), ("remote_bytes", ctypes.c_int64),
+                ("ms", ctypes.c_float),
                 ("wait_ms", ctypes.c_float), ("work_ms", ctypes.c_float), ("publish_ms", ctypes.c_float)]
 
 
@@ -117,6 +118,9 @@ _sig("hz_trace_read", [ctypes.POINTER(TraceRec), _int, ctypes.POINTER(ctypes.c_i
 _sig("hz_enable_p2p", [_vp, ctypes.c_size_t])
 _sig("hz_p2p_enabled", [_vp, ctypes.POINTER(ctypes.c_int)])
 _sig("hz_sym_alloc", [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)])
+_sig("hz_p2p_capture_begin", [_vp])
+_sig("hz_p2p_capture_end", [_vp, _vp, ctypes.POINTER(ctypes.c_ulonglong)])
+_sig("hz_p2p_replayed", [_vp, ctypes.c_ulonglong])
 _sig("hz_plan_allgather", [ctypes.POINTER(Partition), _int, _int, ctypes.POINTER(CommStep), _int,
                            ctypes.POINTER(ctypes.c_int)])
 _sig("hz_plan_reduce_scatter", [ctypes.POINTER(Partition), _int, _int, ctypes.POINTER(ctypes.c_int),
@@ -266,7 +270,7 @@ def trace_read(max_records=1 << 16):
     recs = (TraceRec * max(cnt, 1))()
     _check(_lib.hz_trace_read(recs, cnt, ctypes.byref(n)))
     return [{"kind": r.kind.decode(), "level": r.level, "bits": r.bits, "elems": r.elems,
-             "bytes": r.bytes, "ms": r.ms, "wait_ms": r.wait_ms, "work_ms": r.work_ms,
+             "bytes": r.bytes, "remote_bytes": r.remote_bytes, "ms": r.ms, "wait_ms": r.wait_ms, "work_ms": r.work_ms,
              "publish_ms": r.publish_ms}
             for r in recs[:n.value]]
 
@@ -347,6 +351,17 @@ class Context:
         v = ctypes.c_int(0)
         _check(_lib.hz_p2p_enabled(self._h, ctypes.byref(v)))
         return bool(v.value)
+
+    def p2p_capture_begin(self):
+        _check(_lib.hz_p2p_capture_begin(self._h))
+
+    def p2p_capture_end(self, stream=None):
+        span = ctypes.c_ulonglong(0)
+        _check(_lib.hz_p2p_capture_end(self._h, _stream(stream), ctypes.byref(span)))
+        return span.value
+
+    def p2p_replayed(self, n):
+        _check(_lib.hz_p2p_replayed(self._h, int(n)))
 
     def sym_alloc(self, numel, dtype):
         """hz_sym_alloc: a torch view of a symmetric pool allocation (same sequence of

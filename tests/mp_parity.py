@@ -112,6 +112,66 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             except AssertionError as e:
                 errors.append(str(e))
 
+        # CUDA graph: one captured step (forward gather, backward gather, qgZ) replayed
+        # three times with fresh inputs copied into the captured buffers
+        p = ctx.partition(numel, B, 1, 1, L)
+        off, ln = p.range(1)
+        _, sl = p.range(1)
+        sec_c, sec_s = sec_buffers(sl, sl // B)
+        prim_d = torch.empty(ln, dtype=torch.bfloat16, device="cuda")
+        grad_d = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
+        fwd = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
+        bwd = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
+        shard = torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")
+
+        def one_step(st):
+            ctx.allgather_params(p, prim_d, sec_c, sec_s, fwd, bits=8, stream=st)
+            ctx.allgather_params(p, None, sec_c, sec_s, bwd, bits=8, backward=True, stream=st)
+            ctx.reduce_scatter_grads(p, grad_d, shard, [4] * L, stream=st)
+
+        prim_d.copy_(to_dev(full[off:off + ln]))
+        grad_d.copy_(to_dev(grads[rank]))
+        one_step(torch.cuda.current_stream())          # eager warm-up (workspaces)
+        torch.cuda.synchronize()
+        cs = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cs):
+            if p2p:
+                ctx.p2p_capture_begin()
+            one_step(cs)
+            if p2p:
+                ctx.p2p_capture_end(cs)
+        for it in range(3):
+            fr = np.zeros(Np, np.float32)
+            fr[:numel] = synth.params_like(numel, 70 + it, block=B)
+            fr = fr.astype(ml_dtypes.bfloat16)
+            gr = {r: synth.gradient_like(Np, 700 + 10 * it + r, block=B).astype(ml_dtypes.bfloat16) for r in range(world)}
+            prim_d.copy_(to_dev(fr[off:off + ln]))
+            grad_d.copy_(to_dev(gr[rank]))
+            torch.cuda.synchronize()
+            graph.replay()
+            torch.cuda.synchronize()
+            if p2p:
+                ctx.p2p_replayed(1)
+            prim = {r: fr[pm.range_at(r, g, Np, 1)[0]:sum(pm.range_at(r, g, Np, 1))] for r in range(world)}
+            want_f, _ = col.allgather_forward(prim, g, Np, B, 1, 1, bits=8)
+            want_r = col.reduce_scatter(gr, g, Np, B, 1, L, {l: 4 for l in range(1, L + 1)})
+            try:
+                assert_bitwise(to_host(fwd), want_f[rank], f"[{tag}] g={g} graph replay {it} forward")
+                assert_bitwise(to_host(bwd), want_f[rank], f"[{tag}] g={g} graph replay {it} backward")
+                assert_bitwise(to_host(shard), want_r[rank], f"[{tag}] g={g} graph replay {it} qgZ")
+            except AssertionError as e:
+                errors.append(str(e))
+        # an eager call after the replays continues the phase numbering
+        one_step(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        try:
+            assert_bitwise(to_host(shard), col.reduce_scatter(gr, g, Np, B, 1, L, {l: 4 for l in range(1, L + 1)})[rank],
+                           f"[{tag}] g={g} eager after graph")
+        except AssertionError as e:
+            errors.append(str(e))
+        del graph
+
         # flat ZeRO-3 baseline collectives (plain NCCL)
         n = world * 4096
         x = torch.arange(n, dtype=torch.float32, device="cuda") + rank
