@@ -252,6 +252,11 @@ def barrier(world):
 def summarize_trace(recs, steps):
     kinds = {}
     for r in recs:
+        r = dict(r)
+        if r["ms"] < 0:                      # stamps-only trace: device-clock duration
+            r["ms"] = r.get("stamp_ms", -1.0)
+        if r["ms"] < 0:
+            continue
         k = kinds.setdefault(r["kind"], {"launches": 0, "ms": 0.0, "bytes": 0, "elems": 0, "remote": 0,
                                          "wait_ms": 0.0, "work_ms": 0.0, "publish_ms": 0.0, "stamped": 0})
         k["launches"] += 1
@@ -330,7 +335,8 @@ def run_hz(args):
 
     per_step_kernels = 5 * len(model.tensors)
     if not args.no_trace:
-        hz.trace_begin(capacity=(args.steps + 1) * per_step_kernels * 4 + 64)
+        # in-kernel device-clock stamps only: no stream operations inside the timed region
+        hz.trace_begin(capacity=(args.steps + 1) * per_step_kernels * 4 + 64, events=False, stamps=True)
     graph = None
     if use_graph:
         # one step captured into a CUDA graph (the library's kernels, NCCL calls and
@@ -408,6 +414,22 @@ def run_hz(args):
     nccl = {k: v for k, v in stages.items() if k.startswith("nccl")}
     for v in nccl.values():
         v["frac_of_nvlink_770"] = (v["GBps"] or 0) / NVLINK_PEER_GBS
+
+    # cross-check of the per-kernel durations with CUDA events on the launching stream
+    # (a separate eager pass: the events add stream operations between launches)
+    if roofline is not None and not args.no_trace:
+        hz.trace_begin(capacity=(args.steps + 1) * per_step_kernels * 4 + 64, events=True, stamps=False)
+        barrier(world)
+        for _ in range(args.steps):
+            model.step(stream)
+        torch.cuda.synchronize()
+        hz.trace_end()
+        ev = summarize_trace(hz.trace_read(), args.steps).get(roofline["kernel"])
+        if ev:
+            roofline["events_avg_launch_ms"] = ev["avg_ms"]
+            roofline["events_achieved_hbm_GBps"] = ev["GBps"]
+            roofline["timer"] = ("in-kernel %globaltimer stamps (CTA 0 entry -> last CTA exit) over the timed "
+                                 "region; CUDA events on the launching stream in a second eager pass: events_*")
 
     # flat ZeRO-3 baseline on the same logical bytes (context, not timed with the step)
     flat = None

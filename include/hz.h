@@ -276,9 +276,10 @@ HZ_API hz_status hz_flat_reduce_scatter(hz_ctx* ctx, const void* in, void* out_c
 
 /* ------------------------------------------------------------------ tracing */
 
-/* Per-launch device timing of the library's own work (CUDA events around each
- * kernel / NCCL group on its stream).  hz_trace_begin(cap) starts recording up
- * to cap records (process-wide); hz_trace_end() stops.  hz_trace_read
+/* Per-launch device timing of the library's own work: CUDA events around each
+ * kernel / NCCL group on its stream and/or in-kernel device-clock stamps.
+ * hz_trace_begin(cap, flags) starts recording up to cap records (process-wide);
+ * hz_trace_end() stops.  hz_trace_read
  * synchronises the recorded events and copies up to max records.  kind is a
  * static string ("quantize", "dequantize", "reduce", "reduce_requant",
  * "nccl_allgather", "nccl_alltoall", "nccl_flat", "copy"). bytes = algorithmic
@@ -294,9 +295,12 @@ typedef struct {
   float wait_ms;   /* P2P kernels: time CTA 0 spent waiting for peers (device clock); else -1 */
   float work_ms;   /* P2P kernels: after-wait to last CTA arrival (device clock); else -1 */
   float publish_ms;/* P2P kernels: last CTA's fence + flag stores (device clock); else -1 */
+  float stamp_ms;  /* kernels, HZ_TRACE_STAMPS: CTA 0 entry to last CTA exit (device clock); else -1 */
 } hz_trace_rec;
 
-HZ_API hz_status hz_trace_begin(int capacity);
+#define HZ_TRACE_EVENTS 1  /* CUDA event pair around every launch (adds stream operations) */
+#define HZ_TRACE_STAMPS 2  /* in-kernel %globaltimer stamps (no stream operations; kernels only) */
+HZ_API hz_status hz_trace_begin(int capacity, int flags);
 HZ_API hz_status hz_trace_end(void);
 HZ_API hz_status hz_trace_read(hz_trace_rec* out, int max, int* n_out);
 

@@ -88,7 +88,9 @@ hz_status hz_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block
   if (!scales || !aligned16(scales)) return fail(HZ_ERR_INVALID, "scales: NULL or not 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   TraceScope t(st, "quantize", 0, bits, n, n * (dt == HZ_F32 ? 4 : 2) + code_bytes(n, bits) + n / block * 4);
-  cudaError_t e = launch_quantize(x, dt, n, bits, block, codes, scales, st);
+  SyncArgs sy{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_quantize(x, dt, n, bits, block, codes, scales, st, t.stamps ? &sy : nullptr);
   t.end();
   return launch_status(e, "quantize kernel launch");
 }
@@ -109,7 +111,14 @@ hz_status hz_dequantize(const uint8_t* codes, const float* scales, int64_t n, in
   if (!y || !aligned16(y)) return fail(HZ_ERR_INVALID, "y: NULL or not 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   TraceScope t(st, "dequantize", 0, bits, n, code_bytes(n, bits) + n / block * 4 + n * (out_dt == HZ_F32 ? 4 : 2));
-  cudaError_t e = launch_dequantize(codes, scales, n, bits, block, y, out_dt, st);
+  Pieces pc{};
+  pc.c[0] = codes;
+  pc.s[0] = scales;
+  pc.n = 1;
+  pc.len = n;
+  SyncArgs sy{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_gather_dequantize(pc, n, bits, block, y, out_dt, st, t.stamps ? &sy : nullptr);
   t.end();
   return launch_status(e, "dequantize kernel launch");
 }
@@ -143,8 +152,10 @@ hz_status hz_reduce_chunks(int g, const uint8_t* const* codes, const float* cons
   const int64_t in_bytes = g * (code_bytes(n, bits_in) + n / block * 4);
   const int64_t out_bytes = bits_out ? code_bytes(n, bits_out) + n / block * 4 : n * 4 * (accumulate ? 2 : 1);
   TraceScope t(st, bits_out ? "reduce_requant" : "reduce", 0, bits_in, n, in_bytes + out_bytes);
+  SyncArgs sy{};
+  sy.stamps = t.stamps;
   cudaError_t e = launch_reduce(g, codes, scales, n, bits_in, block, bits_out, out_codes, out_scales,
-                                out_f32, accumulate, st);
+                                out_f32, accumulate, st, t.stamps ? &sy : nullptr);
   t.end();
   return launch_status(e, "reduce kernel launch");
 }

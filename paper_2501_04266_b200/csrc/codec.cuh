@@ -371,17 +371,23 @@ __device__ __forceinline__ void sync_wait(const SyncArgs& s) {
   __syncthreads();
 }
 
+// Kernel epilogue: trace stamp of the last CTA to finish (stamps[2], with its own
+// arrival counter in stamps[4]) and, in P2P mode, the phase publication.
 __device__ __forceinline__ void sync_signal(const SyncArgs& s) {
-  if (!(s.en & (kSigReady | kSigDone))) return;
+  const bool sig = (s.en & (kSigReady | kSigDone)) != 0;
+  if (!sig && !s.stamps) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     // gpu-scope release per CTA (peers read this GPU's memory through its L2, the
     // point of coherence for gpu scope); the last CTA then publishes with a
     // system-scope release, cumulative over everything it has observed.
     __threadfence();
-    if (atomicAdd(s.counter, 1u) == gridDim.x - 1) {
+    if (s.stamps && atomicAdd(s.stamps + 4, 1ull) == gridDim.x - 1ull) {
+      s.stamps[2] = globaltimer();
+      s.stamps[4] = 0ull;   // graph replays reuse the slot
+    }
+    if (sig && atomicAdd(s.counter, 1u) == gridDim.x - 1) {
       *s.counter = 0u;
-      if (s.stamps) s.stamps[2] = globaltimer();
       const unsigned long long e = s.epoch ? *s.epoch : 0ull;
       const unsigned long long sr = (s.en & kSigReady) ? s.sig_ready + e : 0ull;
       const unsigned long long sd = (s.en & kSigDone) ? s.sig_done + e : 0ull;

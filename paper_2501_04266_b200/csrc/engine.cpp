@@ -105,12 +105,9 @@ ncclDataType_t nccl_dtype(hz_dtype dt) {
 hz_status run_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block, uint8_t* c,
                        float* s, cudaStream_t st, int level, const SyncArgs* sync) {
   TraceScope t(st, "quantize", level, bits, n, n * elem_bytes(dt) + code_bytes(n, bits) + n / block * 4);
-  SyncArgs sy{};
-  if (sync) {
-    sy = *sync;
-    sy.stamps = t.stamps;
-  }
-  cudaError_t e = launch_quantize(x, dt, n, bits, block, c, s, st, sync ? &sy : nullptr);
+  SyncArgs sy = sync ? *sync : SyncArgs{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_quantize(x, dt, n, bits, block, c, s, st, (sync || t.stamps) ? &sy : nullptr);
   t.end();
   if (e != cudaSuccess) return cuda_fail(e, "quantize kernel launch");
   return HZ_OK;
@@ -119,7 +116,14 @@ hz_status run_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int bloc
 hz_status run_dequantize(const uint8_t* c, const float* s, int64_t n, int bits, int block, void* y,
                          hz_dtype odt, cudaStream_t st, int level) {
   TraceScope t(st, "dequantize", level, bits, n, code_bytes(n, bits) + n / block * 4 + n * elem_bytes(odt));
-  cudaError_t e = launch_dequantize(c, s, n, bits, block, y, odt, st);
+  Pieces pc{};
+  pc.c[0] = c;
+  pc.s[0] = s;
+  pc.n = 1;
+  pc.len = n;
+  SyncArgs sy{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_gather_dequantize(pc, n, bits, block, y, odt, st, t.stamps ? &sy : nullptr);
   t.end();
   if (e != cudaSuccess) return cuda_fail(e, "dequantize kernel launch");
   return HZ_OK;
@@ -130,12 +134,9 @@ hz_status run_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block
                                 int64_t remote_bytes) {
   TraceScope t(st, "gather_dequantize", level, bits, n,
                code_bytes(n, bits) + n / block * 4 + n * elem_bytes(odt) - remote_bytes, remote_bytes);
-  SyncArgs sy{};
-  if (sync) {
-    sy = *sync;
-    sy.stamps = t.stamps;
-  }
-  cudaError_t e = launch_gather_dequantize(pc, n, bits, block, y, odt, st, sync ? &sy : nullptr);
+  SyncArgs sy = sync ? *sync : SyncArgs{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_gather_dequantize(pc, n, bits, block, y, odt, st, (sync || t.stamps) ? &sy : nullptr);
   t.end();
   if (e != cudaSuccess) return cuda_fail(e, "gather-dequantize kernel launch");
   return HZ_OK;
@@ -149,12 +150,10 @@ hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int6
       bits_out ? code_bytes(n, bits_out) + n / block * 4 : n * 4 * (acc ? 2 : 1);
   TraceScope t(st, bits_out ? "reduce_requant" : "reduce", level, bits_in, n,
                in_bytes + out_bytes - remote_bytes, remote_bytes);
-  SyncArgs sy{};
-  if (sync) {
-    sy = *sync;
-    sy.stamps = t.stamps;
-  }
-  cudaError_t e = launch_reduce(g, c, s, n, bits_in, block, bits_out, oc, os, of, acc, st, sync ? &sy : nullptr);
+  SyncArgs sy = sync ? *sync : SyncArgs{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_reduce(g, c, s, n, bits_in, block, bits_out, oc, os, of, acc, st,
+                                (sync || t.stamps) ? &sy : nullptr);
   t.end();
   if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
   return HZ_OK;

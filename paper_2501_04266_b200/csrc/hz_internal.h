@@ -37,7 +37,7 @@ struct SyncArgs {
   unsigned long long wait_ready, wait_done, sig_ready, sig_done;
   const unsigned long long* epoch;
   unsigned en;   // kWaitReady | kWaitDone | kSigReady | kSigDone
-  unsigned long long* stamps;   // optional [4]: entry, after wait, last-CTA arrival, flags sent (ns)
+  unsigned long long* stamps;   // optional [8]: entry, after wait, last-CTA arrival, flags sent (ns), counter
   int mode;                     // publication fence variant (HZ_TUNE p2p_sig; 0 = fence.sc.sys)
 };
 

@@ -2,9 +2,11 @@
 // launching stream around every kernel and every NCCL group (hz_trace_*).
 // Events are created up front by hz_trace_begin so that recording inside a timed
 // region costs two cudaEventRecord calls per launch and no allocation.
-// P2P kernels additionally write three %globaltimer stamps into a device array
-// (CTA 0 at entry and after its cross-GPU wait, the last CTA at exit), which
-// splits a launch into the time spent waiting for peers and the work itself.
+// With HZ_TRACE_STAMPS every libhz kernel also writes %globaltimer stamps into a
+// device array (CTA 0 at entry and after its cross-GPU wait, the last CTA to
+// finish, and in P2P mode after the flag publication): a per-launch duration
+// measured on the device without any extra stream operation (CUDA events
+// between dependent launches cost several microseconds each).
 #include <mutex>
 #include <vector>
 
@@ -26,7 +28,8 @@ bool g_on = false;
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
 size_t g_used = 0;
-unsigned long long* g_stamps = nullptr;   // device [capacity][4]
+unsigned long long* g_stamps = nullptr;   // device [capacity][8]
+bool g_events = true;
 size_t g_cap = 0;
 
 void destroy_pool() {
@@ -48,20 +51,20 @@ TraceScope::TraceScope(cudaStream_t st, const char* kind, int level, int bits, i
   if (!g_on || g_used + 2 > g_pool.size()) return;
   Rec r{kind, level, bits, elems, bytes, remote, g_pool[g_used], g_pool[g_used + 1], st};
   g_used += 2;
-  if (cudaEventRecord(r.a, st) != cudaSuccess) {
+  if (g_events && cudaEventRecord(r.a, st) != cudaSuccess) {
     cudaGetLastError();
     return;
   }
   g_recs.push_back(r);
   slot = static_cast<int>(g_recs.size()) - 1;
-  if (g_stamps && static_cast<size_t>(slot) < g_cap) stamps = g_stamps + 4 * slot;
+  if (g_stamps && static_cast<size_t>(slot) < g_cap) stamps = g_stamps + 8 * slot;
   active = true;
 }
 
 void TraceScope::end() {
   if (!active) return;
   std::lock_guard<std::mutex> lock(g_mu);
-  if (slot >= 0 && slot < static_cast<int>(g_recs.size())) {
+  if (g_events && slot >= 0 && slot < static_cast<int>(g_recs.size())) {
     if (cudaEventRecord(g_recs[slot].b, stream) != cudaSuccess) cudaGetLastError();
   }
   active = false;
@@ -73,11 +76,13 @@ TraceScope::~TraceScope() { end(); }
 
 extern "C" {
 
-hz_status hz_trace_begin(int capacity) {
+hz_status hz_trace_begin(int capacity, int flags) {
   using namespace hz;
   if (capacity < 1 || capacity > (1 << 20)) return fail(HZ_ERR_INVALID, "capacity: must be in [1, 2^20]");
+  if (!(flags & (HZ_TRACE_EVENTS | HZ_TRACE_STAMPS))) return fail(HZ_ERR_INVALID, "flags: no timer selected");
   std::lock_guard<std::mutex> lock(g_mu);
   destroy_pool();
+  g_events = (flags & HZ_TRACE_EVENTS) != 0;
   g_pool.resize(static_cast<size_t>(capacity) * 2);
   for (auto& e : g_pool) {
     if (cudaEventCreate(&e) != cudaSuccess) {
@@ -87,8 +92,10 @@ hz_status hz_trace_begin(int capacity) {
       return fail(HZ_ERR_CUDA, "hz_trace_begin: cudaEventCreate failed");
     }
   }
-  if (cudaMalloc(&g_stamps, sizeof(unsigned long long) * 4 * capacity) != cudaSuccess ||
-      cudaMemset(g_stamps, 0, sizeof(unsigned long long) * 4 * capacity) != cudaSuccess) {
+  if (!(flags & HZ_TRACE_STAMPS)) {
+    g_stamps = nullptr;
+  } else if (cudaMalloc(&g_stamps, sizeof(unsigned long long) * 8 * capacity) != cudaSuccess ||
+      cudaMemset(g_stamps, 0, sizeof(unsigned long long) * 8 * capacity) != cudaSuccess) {
     cudaGetLastError();
     g_stamps = nullptr;
   } else {
@@ -116,8 +123,8 @@ hz_status hz_trace_read(hz_trace_rec* out, int max, int* n_out) {
   const size_t nrec = g_recs.size();
   if (max > 0 && g_stamps && nrec) {
     const size_t cnt = nrec < g_cap ? nrec : g_cap;
-    st.resize(4 * cnt);
-    if (!g_recs.empty()) cudaEventSynchronize(g_recs.back().b);
+    st.resize(8 * cnt);
+    cudaDeviceSynchronize();
     if (cudaMemcpy(st.data(), g_stamps, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) !=
         cudaSuccess) {
       cudaGetLastError();
@@ -128,8 +135,9 @@ hz_status hz_trace_read(hz_trace_rec* out, int max, int* n_out) {
   for (size_t i = 0; i < nrec; ++i) {
     if (n >= max) break;
     const Rec& r = g_recs[i];
-    float ms = 0.f;
-    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) {
+    float ms = -1.f;
+    if (g_events &&
+        (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess)) {
       cudaGetLastError();
       ms = -1.f;
     }
@@ -143,10 +151,13 @@ hz_status hz_trace_read(hz_trace_rec* out, int max, int* n_out) {
     out[n].wait_ms = -1.f;
     out[n].work_ms = -1.f;
     out[n].publish_ms = -1.f;
-    if (4 * i + 3 < st.size() && st[4 * i] && st[4 * i + 1] && st[4 * i + 2] >= st[4 * i + 1]) {
-      out[n].wait_ms = static_cast<float>(st[4 * i + 1] - st[4 * i]) * 1e-6f;
-      out[n].work_ms = static_cast<float>(st[4 * i + 2] - st[4 * i + 1]) * 1e-6f;
-      out[n].publish_ms = st[4 * i + 3] >= st[4 * i + 2] ? static_cast<float>(st[4 * i + 3] - st[4 * i + 2]) * 1e-6f : -1.f;
+    out[n].stamp_ms = -1.f;
+    const unsigned long long* t = st.size() >= 8 * (i + 1) ? &st[8 * i] : nullptr;
+    if (t && t[0] && t[1] && t[2] >= t[1]) {
+      out[n].wait_ms = static_cast<float>(t[1] - t[0]) * 1e-6f;
+      out[n].work_ms = static_cast<float>(t[2] - t[1]) * 1e-6f;
+      out[n].stamp_ms = static_cast<float>(t[2] - t[0]) * 1e-6f;
+      out[n].publish_ms = t[3] >= t[2] ? static_cast<float>(t[3] - t[2]) * 1e-6f : -1.f;
     }
     ++n;
   }

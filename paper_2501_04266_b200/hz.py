@@ -64,7 +64,8 @@ class TraceRec(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_char_p), ("level", ctypes.c_int32), ("bits", ctypes.c_int32),
                 ("elems", ctypes.c_int64), ("bytes", ctypes.c_int64), ("remote_bytes", ctypes.c_int64),
                 ("ms", ctypes.c_float),
-                ("wait_ms", ctypes.c_float), ("work_ms", ctypes.c_float), ("publish_ms", ctypes.c_float)]
+                ("wait_ms", ctypes.c_float), ("work_ms", ctypes.c_float), ("publish_ms", ctypes.c_float),
+                ("stamp_ms", ctypes.c_float)]
 
 
 class CommStep(ctypes.Structure):
@@ -112,7 +113,7 @@ _sig("hz_reduce_scatter_grads", [_vp, ctypes.POINTER(Partition), _vp, _int, _int
                                  ctypes.POINTER(ctypes.c_int), _vp, _int, _vp])
 _sig("hz_flat_allgather", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_flat_reduce_scatter", [_vp, _vp, _vp, _i64, _int, _vp])
-_sig("hz_trace_begin", [_int])
+_sig("hz_trace_begin", [_int, _int])
 _sig("hz_trace_end", [])
 _sig("hz_trace_read", [ctypes.POINTER(TraceRec), _int, ctypes.POINTER(ctypes.c_int)])
 _sig("hz_enable_p2p", [_vp, ctypes.c_size_t])
@@ -255,8 +256,11 @@ def reduce_chunks(codes_list, scales_list, n, bits_in=4, block=256, bits_out=0, 
 
 
 # ---------------------------------------------------------------------- tracing
-def trace_begin(capacity=4096):
-    _check(_lib.hz_trace_begin(capacity))
+TRACE_EVENTS, TRACE_STAMPS = 1, 2
+
+
+def trace_begin(capacity=4096, events=True, stamps=True):
+    _check(_lib.hz_trace_begin(capacity, (TRACE_EVENTS if events else 0) | (TRACE_STAMPS if stamps else 0)))
 
 
 def trace_end():
@@ -271,7 +275,7 @@ def trace_read(max_records=1 << 16):
     _check(_lib.hz_trace_read(recs, cnt, ctypes.byref(n)))
     return [{"kind": r.kind.decode(), "level": r.level, "bits": r.bits, "elems": r.elems,
              "bytes": r.bytes, "remote_bytes": r.remote_bytes, "ms": r.ms, "wait_ms": r.wait_ms, "work_ms": r.work_ms,
-             "publish_ms": r.publish_ms}
+             "publish_ms": r.publish_ms, "stamp_ms": r.stamp_ms}
             for r in recs[:n.value]]
 
 

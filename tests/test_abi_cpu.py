@@ -104,4 +104,5 @@ def test_codec_validation_without_gpu(hz):
     assert b"bits_out" in lib.hz_last_error()
     assert lib.hz_init(None, 0, 1, None, 1, None, 0, 0) == hz.ERR_INVALID
     assert lib.hz_finalize(None) == hz.OK
-    assert lib.hz_trace_begin(0) == hz.ERR_INVALID
+    assert lib.hz_trace_begin(0, 3) == hz.ERR_INVALID
+    assert lib.hz_trace_begin(16, 0) == hz.ERR_INVALID
