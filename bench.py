@@ -65,8 +65,8 @@ def parse():
                     help="N>1 collective transport: fused NVLink peer-memory kernels (p2p) or NCCL")
     ap.add_argument("--cpu-sample-layers", type=int, default=4)
     ap.add_argument("--no-trace", action="store_true", help="no per-launch events (overhead check)")
-    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=False,
-                    help="capture one step in a CUDA graph and time graph replays")
+    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
+                    help="capture one step in a CUDA graph and time graph replays (--no-graph: eager)")
     return ap.parse_args()
 
 

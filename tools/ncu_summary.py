@@ -69,14 +69,21 @@ def rep_metrics(rep):
         if r["Metric Name"] in want:
             d[r["Metric Name"]] = f'{r["Metric Value"]} {r["Metric Unit"]}'.strip()
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rr = read_csv_text(raw, header_skip=True)
-    for r in rr:
+    lines = [l for l in raw.splitlines() if l and not l.startswith("==")]
+    hdr = next(csv.reader([lines[0]]))
+    units = dict(zip(hdr, next(csv.reader([lines[1]]))))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for row in csv.reader(lines[2:]):
+        r = dict(zip(hdr, row))
         d = per.get(r.get("ID"))
         if d is None:
             continue
         try:
-            d["dram_bytes"] = float(r["dram__bytes_read.sum"].replace(",", "")) + float(r["dram__bytes_write.sum"].replace(",", ""))
-            d["dram_unit"] = "byte"
+            rd = float(r["dram__bytes_read.sum"].replace(",", "")) * scale[units["dram__bytes_read.sum"]]
+            wr = float(r["dram__bytes_write.sum"].replace(",", "")) * scale[units["dram__bytes_write.sum"]]
+            d["dram_read_bytes"] = rd
+            d["dram_write_bytes"] = wr
+            d["dram_bytes"] = rd + wr
         except (KeyError, ValueError):
             pass
     return per
@@ -125,7 +132,9 @@ def main():
                     if k not in ("name",):
                         f.write(f"- {k}: {v}\n")
                 if i < len(elems) and "dram_bytes" in d:
-                    f.write(f"- elements: {elems[i]}; DRAM bytes / element: {d['dram_bytes']/elems[i]:.4f}\n")
+                    f.write(f"- elements: {elems[i]}; DRAM bytes / element: {d['dram_bytes']/elems[i]:.4f} "
+                            f"(read {d['dram_read_bytes']/elems[i]:.4f}, write {d['dram_write_bytes']/elems[i]:.4f}; "
+                            "writes still dirty in L2 at kernel end are not counted)\n")
                     k = kind_of(d["name"])
                     if k and k not in traffic:
                         traffic[k] = {"dram_bytes": d["dram_bytes"], "elems": elems[i], "source": os.path.basename(a.rep),
