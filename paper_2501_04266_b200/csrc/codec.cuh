@@ -219,46 +219,6 @@ __device__ __forceinline__ float group_max(float v) {
   return v;
 }
 
-// Quantize-and-store epilogue shared by k_quantize and k_reduce_requant for one
-// warp iteration of U full warp steps (NB = U * BPW consecutive blocks starting
-// at blk0; no bounds checks).  am[u] must already be the group-reduced absmax of
-// this lane's block in step u.  The scale / inv divisions run once per block:
-// lane k (< NB) divides for block k, then inv is broadcast back by shuffle, and
-// lanes 0..NB-1 store the NB consecutive scales in one coalesced store.
-template <int B, int BITS, int U>
-__device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB][8], const float (&am)[U],
-                                               int64_t blk0, int lane, uint8_t* __restrict__ codes,
-                                               float* __restrict__ scales) {
-  using G = Geo<B>;
-  constexpr int NB = U * G::BPW;
-  static_assert(NB <= 32, "one block per lane at most");
-  const int lb = lane / G::LPB;
-  const int ll = lane % G::LPB;
-  float mine = 0.f;
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const float t = __shfl_sync(kFull, am[u], (lane % G::BPW) * G::LPB);
-    if (lane / G::BPW == u) mine = t;
-  }
-  float scale, inv;
-  quant_params<BITS>(mine, scale, inv);
-  if (lane < NB) scales[blk0 + lane] = scale;
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const float iv = __shfl_sync(kFull, inv, u * G::BPW + lb);
-    const int64_t blk = blk0 + u * G::BPW + lb;
-#pragma unroll
-    for (int k = 0; k < G::NSUB; ++k) {
-      unsigned b[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) b[i] = qbits(v[u][k][i], iv);
-      Codes8<BITS> out;
-      out.set(b);
-      out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
-    }
-  }
-}
-
 // ------------------------------------------------------------------ output store
 template <typename TO>
 struct Out8;
@@ -294,6 +254,106 @@ struct Out8<__half> {
       w[i] = *reinterpret_cast<unsigned*>(&h);
     }
     *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+// Quantize-and-store epilogue shared by k_quantize and k_reduce_requant for one
+// warp iteration of U full warp steps (NB = U * BPW consecutive blocks starting
+// at blk0; no bounds checks).  am[u] must already be the group-reduced absmax of
+// this lane's block in step u.  The scale / inv divisions run once per block:
+// lane k (< NB) divides for block k, then inv is broadcast back by shuffle, and
+// lanes 0..NB-1 store the NB consecutive scales in one coalesced store.
+//
+// Emit (optional) receives the dequantized value x_hat = fl(code * scale) of the
+// lane's 8 elements starting at global element e0, warp-uniformly: the fused
+// quantize -> dequantize of a level without exchange (group size 1).
+struct NoEmit {
+  static constexpr bool on = false;
+  __device__ __forceinline__ void operator()(int64_t, int, const float (&)[8]) const {}
+};
+
+template <int B, int BITS, int U, class Emit = NoEmit>
+__device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB][8], const float (&am)[U],
+                                               int64_t blk0, int lane, uint8_t* __restrict__ codes,
+                                               float* __restrict__ scales, const Emit& emit = Emit{}) {
+  using G = Geo<B>;
+  constexpr int NB = U * G::BPW;
+  static_assert(NB <= 32, "one block per lane at most");
+  const int lb = lane / G::LPB;
+  const int ll = lane % G::LPB;
+  float mine = 0.f;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float t = __shfl_sync(kFull, am[u], (lane % G::BPW) * G::LPB);
+    if (lane / G::BPW == u) mine = t;
+  }
+  float scale, inv;
+  quant_params<BITS>(mine, scale, inv);
+  if (lane < NB) scales[blk0 + lane] = scale;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float iv = __shfl_sync(kFull, inv, u * G::BPW + lb);
+    const float sc = Emit::on ? __shfl_sync(kFull, scale, u * G::BPW + lb) : 0.f;
+    const int64_t blk = blk0 + u * G::BPW + lb;
+#pragma unroll
+    for (int k = 0; k < G::NSUB; ++k) {
+      unsigned b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) b[i] = qbits(v[u][k][i], iv);
+      Codes8<BITS> out;
+      out.set(b);
+      out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
+      if constexpr (Emit::on) {
+        float xh[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xh[i] = __fmul_rn(__fsub_rn(__uint_as_float(b[i]), kMagic), sc);
+        emit(blk * B + k * G::SUBSTRIDE + ll * 8, lane, xh);
+      }
+    }
+  }
+}
+
+// Emitters for the fused round trip.  16-bit outputs: one 16-byte store per lane
+// (the lanes of a warp step own 256 consecutive elements).  fp32: staged through
+// 1 KB of shared memory per warp (swizzled granules) so that each store, and the
+// accumulate load, is one contiguous 512-byte span; A = fl(A + x_hat) when acc.
+template <typename TO>
+struct EmitOut {
+  static constexpr bool on = true;
+  TO* y;
+  __device__ __forceinline__ void operator()(int64_t e0, int, const float (&xh)[8]) const {
+    Out8<TO>::store(y + e0, xh);
+  }
+};
+
+struct EmitF32 {
+  static constexpr bool on = true;
+  float* y;
+  float4* stage;   // this warp's 64 granules
+  int acc;
+  __device__ __forceinline__ void operator()(int64_t e0, int lane, const float (&xh)[8]) const {
+    const int64_t base = e0 - 8 * lane;   // first element of the warp step's 256
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int gi = lane * 2 + j;
+      stage[gi ^ ((gi >> 3) & 1)] = make_float4(xh[4 * j], xh[4 * j + 1], xh[4 * j + 2], xh[4 * j + 3]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int gi = k * 32 + lane;
+      float4 o = stage[gi ^ ((gi >> 3) & 1)];
+      float4* dst = reinterpret_cast<float4*>(y + base) + gi;
+      if (acc) {
+        const float4 a = *dst;
+        o.x = __fadd_rn(a.x, o.x);
+        o.y = __fadd_rn(a.y, o.y);
+        o.z = __fadd_rn(a.z, o.z);
+        o.w = __fadd_rn(a.w, o.w);
+      }
+      *dst = o;
+    }
+    __syncwarp();
   }
 };
 

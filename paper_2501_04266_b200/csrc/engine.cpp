@@ -159,6 +159,19 @@ hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int6
   return HZ_OK;
 }
 
+hz_status run_roundtrip(const void* x, hz_dtype dt, int64_t n, int bits, int block, uint8_t* c, float* s,
+                        void* y, hz_dtype odt, int acc, cudaStream_t st, int level) {
+  const int64_t out = n * elem_bytes(odt) * (acc ? 2 : 1);
+  TraceScope t(st, "quantize_dequantize", level, bits, n,
+               n * elem_bytes(dt) + code_bytes(n, bits) + n / block * 4 + out);
+  SyncArgs sy{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_quantize_roundtrip(x, dt, n, bits, block, c, s, y, odt, acc, st, t.stamps ? &sy : nullptr);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "quantize-dequantize kernel launch");
+  return HZ_OK;
+}
+
 hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (bytes == 0 || dst == src) return HZ_OK;
   TraceScope t(st, "copy", 0, 0, 0, int64_t(bytes) * 2);
@@ -299,6 +312,22 @@ hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward
   const uint8_t* cur_c;
   const float* cur_s;
   int top;
+  if (!backward && p->len[w] == Np && roundtrip_supported(B)) {
+    // A2 + A5 fused: no level up to w exchanges anything (all its groups have one
+    // member), so the gathered layer is the own quantized primary: one kernel writes
+    // the codes (the secondary when it covers the same range) and the dequantized layer.
+    const bool direct = p->len[s] == Np;
+    uint8_t* qc = direct ? sec_codes : ws_c;
+    float* qs = direct ? sec_scales : ws_s;
+    if ((rc = run_roundtrip(primary, dt, Np, bits, B, qc, qs, full_out, out_dt, 0, st, w)) != HZ_OK) return rc;
+    if (!direct) {   // A4, s > w: sub-slice of the quantized primary
+      if ((rc = copy_async(sec_codes, qc + code_bytes(p->off[s], bits), code_bytes(p->len[s], bits), st)) != HZ_OK)
+        return rc;
+      if ((rc = copy_async(sec_scales, qs + p->off[s] / B, p->len[s] / B * 4, st)) != HZ_OK) return rc;
+    }
+    clear_error();
+    return HZ_OK;
+  }
   if (!backward) {
     // A2: quantize the primary range_w.  With s == w the quantized primary IS the
     // secondary (setting T, sec-degree = primary degree), so write it there.
@@ -390,6 +419,15 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
   uint8_t* r_c = static_cast<uint8_t*>(ctx->rs_r_c.p);
   float* r_s = static_cast<float*>(ctx->rs_r_s.p);
 
+  if (from_level == to_level && ctx->group[from_level - 1] == 1 && roundtrip_supported(B)) {
+    // A7 + A9 fused: a single level whose group has one member exchanges nothing, so
+    // the shard is the round trip of the own gradient: one kernel, codes never reread.
+    if ((rc = run_roundtrip(grad, dt, base_len, bits_per_level[from_level - 1], B, a_c, a_s, shard, HZ_F32,
+                            accumulate, st, from_level)) != HZ_OK)
+      return rc;
+    clear_error();
+    return HZ_OK;
+  }
   // A7: quantize the whole input range_{from-1}; chunk j of it goes to digit j.
   if ((rc = run_quantize(grad, dt, base_len, bits_per_level[from_level - 1], B, a_c, a_s, st,
                          from_level)) != HZ_OK)

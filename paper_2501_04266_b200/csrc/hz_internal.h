@@ -62,6 +62,13 @@ struct Pieces {
 cudaError_t launch_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block,
                             uint8_t* codes, float* scales, cudaStream_t st,
                             const SyncArgs* sync = nullptr);
+// Fused quantize + dequantize (a level whose exchange group has one member): codes
+// and scales as launch_quantize, plus y = out_dt(fl(code*scale)) (fp32: += when acc).
+// block must be 256 (roundtrip_supported).
+bool roundtrip_supported(int block);
+cudaError_t launch_quantize_roundtrip(const void* x, hz_dtype dt, int64_t n, int bits, int block,
+                                      uint8_t* codes, float* scales, void* y, hz_dtype out_dt, int acc,
+                                      cudaStream_t st, const SyncArgs* sync);
 cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, int64_t n, int bits,
                               int block, void* y, hz_dtype out_dt, cudaStream_t st);
 cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,

@@ -19,12 +19,37 @@ namespace {
 
 using namespace dev;
 
-template <typename T, int B, int BITS, int U>
+// OUT: 0 = codes only; 1 / 2 / 3 = also emit the dequantized round trip x_hat as
+// bf16 / fp16 / fp32 (+= when acc) — the fused quantize -> dequantize of a level
+// whose exchange group has one member (nothing to exchange).
+template <int OUT>
+struct OutOf;
+template <>
+struct OutOf<0> { using E = NoEmit; };
+template <>
+struct OutOf<1> { using E = EmitOut<__nv_bfloat16>; };
+template <>
+struct OutOf<2> { using E = EmitOut<__half>; };
+template <>
+struct OutOf<3> { using E = EmitF32; };
+
+template <typename T, int B, int BITS, int U, int OUT>
 __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, int64_t nblocks,
                                                        uint8_t* __restrict__ codes,
                                                        float* __restrict__ scales,
-                                                       const __grid_constant__ SyncArgs sy) {
+                                                       const __grid_constant__ SyncArgs sy,
+                                                       void* __restrict__ y, int acc) {
   using G = Geo<B>;
+  using Emit = typename OutOf<OUT>::E;
+  __shared__ float4 stage[OUT == 3 ? kThreads / 32 : 1][OUT == 3 ? 64 : 1];
+  Emit emit;
+  if constexpr (OUT == 1 || OUT == 2) {
+    emit.y = static_cast<decltype(emit.y)>(y);
+  } else if constexpr (OUT == 3) {
+    emit.y = static_cast<float*>(y);
+    emit.stage = stage[threadIdx.x >> 5];
+    emit.acc = acc;
+  }
   sync_wait(sy);   // P2P mode: every rank is done reading what this call overwrites
   constexpr int NB = U * G::BPW;
   const int lane = threadIdx.x & 31;
@@ -56,7 +81,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
       }
       am[u] = group_max<G::LPB>(m);
     }
-    quantize_store<B, BITS, U>(v, am, blk0, lane, codes, scales);
+    quantize_store<B, BITS, U, Emit>(v, am, blk0, lane, codes, scales, emit);
   }
 
   // tail: the last nblocks % NB blocks, one warp step at a time, bounds-checked
@@ -83,18 +108,36 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
       m = group_max<G::LPB>(m);
       float scale, inv;
       quant_params<BITS>(m, scale, inv);
-      if (valid) {
 #pragma unroll
-        for (int k = 0; k < G::NSUB; ++k) {
-          unsigned b[8];
+      for (int k = 0; k < G::NSUB; ++k) {
+        unsigned b[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) b[i] = qbits(v[k][i], inv);
+        for (int i = 0; i < 8; ++i) b[i] = qbits(v[k][i], inv);
+        if (valid) {
           Codes8<BITS> out;
           out.set(b);
           out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
         }
-        if (ll == 0) scales[blk] = scale;
+        if constexpr (OUT == 1 || OUT == 2) {
+          if (valid) {
+            float xh[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xh[i] = __fmul_rn(__fsub_rn(__uint_as_float(b[i]), kMagic), scale);
+            emit(blk * B + k * G::SUBSTRIDE + ll * 8, lane, xh);
+          }
+        } else if constexpr (OUT == 3) {
+          // tail (< U blocks): plain per-lane stores, no staging
+          float xh[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xh[i] = __fmul_rn(__fsub_rn(__uint_as_float(b[i]), kMagic), scale);
+          if (valid) {
+            float* yy = static_cast<float*>(y) + blk * B + k * G::SUBSTRIDE + ll * 8;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) yy[i] = acc ? __fadd_rn(yy[i], xh[i]) : xh[i];
+          }
+        }
       }
+      if (valid && ll == 0) scales[blk] = scale;
     }
   }
   sync_signal(sy);   // P2P mode: codes of this phase are ready for the peers
@@ -104,15 +147,27 @@ constexpr int kU = 4;   // warp steps per warp iteration
 // B > 256: NSUB = B/256 loads per step already; B < 256: NB = U*BPW <= 32
 constexpr int uq(int B) { return B > 256 ? 1 : kU; }
 
-template <typename T, int B, int BITS, int U>
+template <typename T, int B, int BITS, int U, int OUT = 0>
 cudaError_t quantize_u(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st,
-                       const SyncArgs& sy) {
+                       const SyncArgs& sy, void* y = nullptr, int acc = 0) {
   const int64_t nblocks = n / B;
   constexpr int NB = U * Geo<B>::BPW;
-  auto kern = k_quantize<T, B, BITS, U>;
+  auto kern = k_quantize<T, B, BITS, U, OUT>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), nblocks / NB + 1);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(static_cast<const T*>(x), nblocks, codes, scales, sy);
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(static_cast<const T*>(x), nblocks, codes, scales, sy,
+                                                         y, acc);
   return cudaGetLastError();
+}
+
+template <typename T, int BITS>
+cudaError_t roundtrip_t(const void* x, int64_t n, uint8_t* codes, float* scales, void* y, hz_dtype out_dt,
+                        int acc, cudaStream_t st, const SyncArgs& sy) {
+  switch (out_dt) {
+    case HZ_BF16: return quantize_u<T, 256, BITS, kU, 1>(x, n, codes, scales, st, sy, y, 0);
+    case HZ_F16: return quantize_u<T, 256, BITS, kU, 2>(x, n, codes, scales, st, sy, y, 0);
+    case HZ_F32: return quantize_u<T, 256, BITS, kU, 3>(x, n, codes, scales, st, sy, y, acc);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <typename T, int B, int BITS>
@@ -150,6 +205,28 @@ cudaError_t quantize_d(const void* x, int64_t n, int bits, int block, uint8_t* c
 }
 
 }  // namespace
+
+bool roundtrip_supported(int block) { return block == 256; }
+
+cudaError_t launch_quantize_roundtrip(const void* x, hz_dtype dt, int64_t n, int bits, int block,
+                                      uint8_t* codes, float* scales, void* y, hz_dtype out_dt, int acc,
+                                      cudaStream_t st, const SyncArgs* sync) {
+  const SyncArgs sy = sync ? *sync : SyncArgs{};
+  if (block != 256) return cudaErrorInvalidValue;
+  if (n == 0 && !sync) return cudaSuccess;
+  switch (dt) {
+    case HZ_F32:
+      return bits == 8 ? roundtrip_t<float, 8>(x, n, codes, scales, y, out_dt, acc, st, sy)
+                       : roundtrip_t<float, 4>(x, n, codes, scales, y, out_dt, acc, st, sy);
+    case HZ_BF16:
+      return bits == 8 ? roundtrip_t<__nv_bfloat16, 8>(x, n, codes, scales, y, out_dt, acc, st, sy)
+                       : roundtrip_t<__nv_bfloat16, 4>(x, n, codes, scales, y, out_dt, acc, st, sy);
+    case HZ_F16:
+      return bits == 8 ? roundtrip_t<__half, 8>(x, n, codes, scales, y, out_dt, acc, st, sy)
+                       : roundtrip_t<__half, 4>(x, n, codes, scales, y, out_dt, acc, st, sy);
+  }
+  return cudaErrorInvalidValue;
+}
 
 cudaError_t launch_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block,
                             uint8_t* codes, float* scales, cudaStream_t st, const SyncArgs* sync) {

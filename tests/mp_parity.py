@@ -90,6 +90,14 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
                 assert_bitwise(to_host(shard), want[rank], f"[{tag}] g={g} qgZ bits={bpl}")
             except AssertionError as e:
                 errors.append(str(e))
+            # accumulate into the shard (A = fl(A + P)): second micro-batch
+            ctx.reduce_scatter_grads(p, to_dev(grads[rank]), shard, bpl, accumulate=True)
+            torch.cuda.synchronize()
+            try:
+                assert_bitwise(to_host(shard), (want[rank] + want[rank]).astype(np.float32),
+                               f"[{tag}] g={g} qgZ accumulate bits={bpl}")
+            except AssertionError as e:
+                errors.append(str(e))
 
         # setting T, GA = 2: levels 1..gl per micro-batch with accumulate, then gl+1..L once
         if L >= 2:
