@@ -289,7 +289,8 @@ __device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB]
   }
   float scale, inv;
   quant_params<BITS>(mine, scale, inv);
-  if (lane < NB) scales[blk0 + lane] = scale;
+  // codes == nullptr (round trip only, nobody reads the codes): skip code/scale stores
+  if (codes && lane < NB) scales[blk0 + lane] = scale;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const float iv = __shfl_sync(kFull, inv, u * G::BPW + lb);
@@ -300,9 +301,11 @@ __device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB]
       unsigned b[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) b[i] = qbits(v[u][k][i], iv);
-      Codes8<BITS> out;
-      out.set(b);
-      out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
+      if (!Emit::on || codes) {
+        Codes8<BITS> out;
+        out.set(b);
+        out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
+      }
       if constexpr (Emit::on) {
         float xh[8];
 #pragma unroll

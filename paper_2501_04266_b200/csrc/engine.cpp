@@ -163,7 +163,7 @@ hz_status run_roundtrip(const void* x, hz_dtype dt, int64_t n, int bits, int blo
                         void* y, hz_dtype odt, int acc, cudaStream_t st, int level) {
   const int64_t out = n * elem_bytes(odt) * (acc ? 2 : 1);
   TraceScope t(st, "quantize_dequantize", level, bits, n,
-               n * elem_bytes(dt) + code_bytes(n, bits) + n / block * 4 + out);
+               n * elem_bytes(dt) + (c ? code_bytes(n, bits) + n / block * 4 : 0) + out);
   SyncArgs sy{};
   sy.stamps = t.stamps;
   cudaError_t e = launch_quantize_roundtrip(x, dt, n, bits, block, c, s, y, odt, acc, st, t.stamps ? &sy : nullptr);
@@ -422,7 +422,8 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
   if (from_level == to_level && ctx->group[from_level - 1] == 1 && roundtrip_supported(B)) {
     // A7 + A9 fused: a single level whose group has one member exchanges nothing, so
     // the shard is the round trip of the own gradient: one kernel, codes never reread.
-    if ((rc = run_roundtrip(grad, dt, base_len, bits_per_level[from_level - 1], B, a_c, a_s, shard, HZ_F32,
+    // (the gradient's codes are never read by anyone here, so they are not stored)
+    if ((rc = run_roundtrip(grad, dt, base_len, bits_per_level[from_level - 1], B, nullptr, nullptr, shard, HZ_F32,
                             accumulate, st, from_level)) != HZ_OK)
       return rc;
     clear_error();

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
         unsigned b[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) b[i] = qbits(v[k][i], inv);
-        if (valid) {
+        if (valid && codes) {
           Codes8<BITS> out;
           out.set(b);
           out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
           }
         }
       }
-      if (valid && ll == 0) scales[blk] = scale;
+      if (valid && codes && ll == 0) scales[blk] = scale;
     }
   }
   sync_signal(sy);   // P2P mode: codes of this phase are ready for the peers

@@ -151,7 +151,10 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   const auto members = cumulative_members(p, top);
   const int D = static_cast<int>(members.size());
   if (D > kMaxWorld) return fail(HZ_ERR_UNSUPPORTED, "P2P gather over more than 8 ranks");
-  const unsigned long long phase = D > 1 ? ++P.phase : 0;
+  // every call is a phase, even without peers to read from: it may write a
+  // secondary that peers read in a later backward phase (s > w), and the final
+  // kernel's done(phase) is what tells them the write (incl. its copies) is complete
+  const unsigned long long phase = ++P.phase;
   const int64_t plen = p->len[top];
 
   const uint8_t* xc;
@@ -165,9 +168,8 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
       qc = at<uint8_t>(ctx, ctx->rank, P.ag_prim_c.off);
       qs = at<float>(ctx, ctx->rank, P.ag_prim_s.off);
     }
-    SyncArgs sq = make_sync(ctx, 0, phase ? phase - 1 : 0, phase, 0);
-    if ((rc = run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w, phase ? &sq : nullptr)) != HZ_OK)
-      return rc;
+    SyncArgs sq = make_sync(ctx, 0, phase - 1, phase, 0);
+    if ((rc = run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w, &sq)) != HZ_OK) return rc;
     if (s > w) {   // A4, s > w: the secondary is a sub-slice of the own quantized primary
       const int64_t rel = p->off[s] - p->off[w];
       if ((rc = copy_async(sec_codes, qc + code_bytes(rel, bits), code_bytes(len_s, bits), st)) != HZ_OK) return rc;
@@ -196,7 +198,7 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
     pc.sec_hi = p->off[s] + len_s;
   }
   SyncArgs sd = backward ? make_sync(ctx, 0, phase - 1, 0, phase) : make_sync(ctx, phase, 0, 0, phase);
-  if ((rc = run_gather_dequantize(pc, Np, bits, B, full_out, out_dt, st, 0, phase ? &sd : nullptr, remote)) != HZ_OK)
+  if ((rc = run_gather_dequantize(pc, Np, bits, B, full_out, out_dt, st, 0, &sd, remote)) != HZ_OK)
     return rc;
   clear_error();
   return HZ_OK;
