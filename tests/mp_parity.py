@@ -201,6 +201,84 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
     return errors
 
 
+def check_full_size(hz, rank, world, g, uid, device, numel, p2p, B=256):
+    """The bench configuration (GPT layer size, setting T w=s=1, gl=L, int8 qwZ, int4
+    qgZ) checked on sampled blocks: every output block depends only on the same global
+    block of the inputs, and the qgZ reduction tree does not depend on the block's
+    position, so the oracle runs on a small layer made of the sampled blocks only."""
+    errors = []
+    tag = "p2p" if p2p else "nccl"
+    ctx = hz.Context(rank, world, uid, g, device)
+    L = len(g)
+    try:
+        p = ctx.partition(numel, B, 1, 1, L)
+        Np = p.padded_numel
+        if p2p:
+            ctx.enable_p2p(2 * Np + (64 << 20))
+        off, ln = p.range(1)
+        full = synth.torch_normal(Np, 7000, 0.02, torch.bfloat16, "cuda", outlier_every=0)
+        full[numel:] = 0
+        grads = []
+        for q in range(world):                       # every rank can regenerate every gradient
+            gq = synth.torch_normal(Np, 900 + q, 1e-3, torch.bfloat16, "cuda")
+            gq[numel:] = 0
+            grads.append(gq)
+        if p2p:
+            sec_c, sec_s = ctx.sym_alloc(ln, torch.uint8), ctx.sym_alloc(ln // B, torch.float32)
+        else:
+            sec_c = torch.empty(ln, dtype=torch.uint8, device="cuda")
+            sec_s = torch.empty(ln // B, dtype=torch.float32, device="cuda")
+        fwd = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
+        bwd = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
+        shard = torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")
+        ctx.allgather_params(p, full[off:off + ln].contiguous(), sec_c, sec_s, fwd, bits=8)
+        ctx.allgather_params(p, None, sec_c, sec_s, bwd, bits=8, backward=True)
+        ctx.reduce_scatter_grads(p, grads[rank], shard, [4] * L)
+        torch.cuda.synchronize()
+
+        nb = Np // B
+        bounds = sorted({pm.range_at(r, g, Np, l)[0] // B for r in range(world) for l in range(L + 1)})
+        idx = synth.sample_blocks(nb, bounds, every=499)
+        it = torch.from_numpy(idx).cuda()
+        pick = lambda t: to_host(t.view(nb, B)[it].contiguous().view(-1))   # noqa: E731
+        xs = pick(full)
+        want = quant.dequantize(*quant.quantize(xs, 8, B), B, out="bf16")
+        for name, t in (("forward", fwd), ("backward", bwd)):
+            try:
+                assert_bitwise(pick(t), want, f"[{tag}] g={g} full-size {name} layer ({len(idx)} sampled blocks)")
+            except AssertionError as e:
+                errors.append(str(e))
+        # qgZ: a small layer made of the sampled blocks, same hierarchy and bits
+        ns = len(idx)
+        tnp = pm.padded_numel(ns * B, g, B)
+        tiny = {}
+        for q in range(world):
+            a = np.zeros(tnp, np.float32).astype(ml_dtypes.bfloat16)
+            a[:ns * B] = pick(grads[q])
+            tiny[q] = a
+        tout = col.reduce_scatter(tiny, g, tnp, B, 1, L, {l: 4 for l in range(1, L + 1)})
+        tflat = np.zeros(tnp, np.float32)
+        for q in range(world):
+            o, n_ = pm.range_at(q, g, tnp, L)
+            tflat[o:o + n_] = tout[q]
+        my_off, my_len = p.range(L)
+        sh = to_host(shard)
+        checked = 0
+        for i, b in enumerate(idx):
+            e0 = int(b) * B
+            if my_off <= e0 < my_off + my_len:
+                got = sh[e0 - my_off:e0 - my_off + B]
+                ref = tflat[i * B:(i + 1) * B]
+                if not np.array_equal(got.view(np.uint32), ref.view(np.uint32)):
+                    errors.append(f"[{tag}] g={g} full-size qgZ block {b}: mismatch")
+                    break
+                checked += 1
+        assert checked > 0 or world > 8
+    finally:
+        ctx.close()
+    return errors
+
+
 def run(rank, world, local, bcast=None):
     from paper_2501_04266_b200 import hz
     torch.cuda.set_device(local)
@@ -211,6 +289,13 @@ def run(rank, world, local, bcast=None):
             if bcast is not None:
                 uid = bcast(uid)
             errors += check_hierarchy(hz, rank, world, g, uid, local, p2p=p2p)
+    # bench configuration at GPT-1.3B layer size, first hierarchy of this world size
+    numel = synth.layer_numel(synth.GPT_CONFIGS["gpt1.3b"]["hidden"])
+    for p2p in (False, True):
+        uid = hz.get_uid() if rank == 0 else None
+        if bcast is not None:
+            uid = bcast(uid)
+        errors += check_full_size(hz, rank, world, HIERARCHIES[world][0], uid, local, numel, p2p)
     return errors
 
 

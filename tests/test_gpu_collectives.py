@@ -32,3 +32,16 @@ def test_multi_gpu(n):
            os.path.join(ROOT, "tests", "mp_parity.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+
+
+def test_world1_full_size_neox20b():
+    """NeoX-20B layer (453 M parameters) through hz_allgather_params / hz_reduce_scatter_grads
+    in the bench configuration, checked on sampled blocks."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2501_04266_b200 import hz, synth
+    from tests import mp_parity
+    numel = synth.layer_numel(synth.GPT_CONFIGS["neox20b"]["hidden"])
+    errors = mp_parity.check_full_size(hz, 0, 1, (1,), hz.get_uid(), 0, numel, p2p=False)
+    assert not errors, "\n".join(errors)
+    torch.cuda.empty_cache()
