@@ -46,9 +46,14 @@ struct hz_ctx {
 
 namespace hz {
 
-// header of the symmetric pool: ready[8] u64 | done[8] u64 | counter u32
-constexpr size_t kPoolHeader = 4096;
+// header of the symmetric pool: ready[8] u64 | done[8] u64 | counter u32 | epoch u64 |
+// fused-kernel work counters | per-chunk flags of the fused all-gather [8][kMaxChunks]
+// and of the fused reduce-scatter [16][kMaxChunks]
 constexpr size_t kReadyOff = 0, kDoneOff = 64, kCounterOff = 128, kEpochOff = 192;
+constexpr size_t kWorkAGOff = 256, kWorkRSOff = 320;
+constexpr size_t kChunkAGOff = 4096;
+constexpr size_t kChunkRSOff = kChunkAGOff + size_t(kMaxWorld) * kMaxChunks * 8;
+constexpr size_t kPoolHeader = kChunkRSOff + size_t(kMaxG) * kMaxChunks * 8;
 
 hz_status cuda_fail(cudaError_t e, const char* what);
 hz_status nccl_fail(ncclResult_t r, const char* what);

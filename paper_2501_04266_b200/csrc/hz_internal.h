@@ -80,6 +80,51 @@ cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const
                           float* out_scales, float* out_f32, int accumulate, cudaStream_t st,
                           const SyncArgs* sync = nullptr);
 
+// Fused codec + NVLink collective kernels (k_fused.cu, B = 256 only).
+constexpr int kMaxChunks = 4096;   // per-chunk flags per member in the P2P pool header
+struct FusedAGArgs {
+  const void* x;
+  hz_dtype dt;
+  int bits;
+  uint8_t* qc;
+  float* qs;
+  const uint8_t* pc[kMaxWorld];
+  const float* ps[kMaxWorld];
+  int D, me;
+  int64_t plen, C;
+  int nch;
+  unsigned long long* flags;
+  unsigned long long* flags_remote[kMaxWorld];
+  unsigned long long* work;
+  void* y;
+  hz_dtype out_dt;
+  unsigned long long phase;
+  const unsigned long long* epoch;
+};
+struct FusedRSArgs {
+  const void* x;
+  hz_dtype dt;
+  int bits_in, bits_out, acc;
+  uint8_t* qc;
+  float* qs;
+  const uint8_t* mc[kMaxG];
+  const float* ms[kMaxG];
+  int g, d;
+  int64_t cl, C;
+  int ncl;
+  unsigned long long* flags;
+  unsigned long long* flags_remote[kMaxG];
+  unsigned long long* work;
+  float* of;
+  uint8_t* oc;
+  float* os;
+  unsigned long long phase;
+  const unsigned long long* epoch;
+};
+bool fused_rs_supported(int g);
+cudaError_t launch_ag_fused(const FusedAGArgs& a, cudaStream_t st, const SyncArgs& sy);
+cudaError_t launch_rs_fused(const FusedRSArgs& a, cudaStream_t st, const SyncArgs& sy);
+
 // ------------------------------------------------------------------ tracing
 struct TraceScope {
   // Records a start event on construction and an end event + record on end().

@@ -63,6 +63,14 @@ hz_status slot(hz_ctx* ctx, hz_ctx::P2P::Slot& sl, size_t bytes) {
   return rc;
 }
 
+// fused-kernel chunk: >= 32768 elements, a multiple of 1024 (4 blocks of 256), and
+// few enough chunks for the per-member flag arrays
+int64_t chunk_elems(int64_t len) {
+  int64_t c = (len + kMaxChunks - 1) / kMaxChunks;
+  c = (c + 1023) / 1024 * 1024;
+  return c < 32768 ? 32768 : c;
+}
+
 template <typename T>
 T* at(hz_ctx* ctx, int q, size_t off) {
   return reinterpret_cast<T*>(ctx->p2p.peer[q] + off);
@@ -157,6 +165,47 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   const unsigned long long phase = ++P.phase;
   const int64_t plen = p->len[top];
 
+  if (!backward && s == w && D > 1 && B == 256 && tune_param("fused", 1)) {
+    // A2 + A3 + A5 in ONE kernel: quantize the own primary chunk by chunk into the
+    // (peer-readable) secondary, publish each chunk, and dequantize every member's
+    // chunks as they become ready — NVLink transfers overlap the quantization.
+    FusedAGArgs h{};
+    h.x = primary;
+    h.dt = dt;
+    h.bits = bits;
+    h.qc = sec_codes;
+    h.qs = sec_scales;
+    h.D = D;
+    h.plen = plen;
+    h.C = chunk_elems(plen);
+    h.nch = static_cast<int>((plen + h.C - 1) / h.C);
+    int64_t remote = 0;
+    for (int k = 0; k < D; ++k) {
+      const int m = members[k].second;
+      if (m == ctx->rank) h.me = k;
+      h.pc[k] = at<const uint8_t>(ctx, m, off_of(ctx, sec_codes));
+      h.ps[k] = at<const float>(ctx, m, off_of(ctx, sec_scales));
+      if (m != ctx->rank) remote += code_bytes(plen, bits) + plen / B * 4;
+    }
+    for (int k = 0; k < D; ++k)
+      h.flags_remote[k] = at<unsigned long long>(ctx, members[k].second, kChunkAGOff) + h.me * kMaxChunks;
+    h.flags = at<unsigned long long>(ctx, ctx->rank, kChunkAGOff);
+    h.work = at<unsigned long long>(ctx, ctx->rank, kWorkAGOff);
+    h.y = full_out;
+    h.out_dt = out_dt;
+    h.phase = phase - P.epoch_host;
+    h.epoch = at<const unsigned long long>(ctx, ctx->rank, kEpochOff);
+    SyncArgs sy = make_sync(ctx, 0, phase - 1, 0, phase);
+    const int64_t local = p->len[w] * elem_bytes(dt) + code_bytes(plen, bits) + plen / B * 4 +
+                          code_bytes(Np, bits) + Np / B * 4 - remote + Np * elem_bytes(out_dt);
+    TraceScope t(st, "ag_fused", w, bits, Np, local, remote);
+    sy.stamps = t.stamps;
+    cudaError_t e = launch_ag_fused(h, st, sy);
+    t.end();
+    if (e != cudaSuccess) return cuda_fail(e, "fused all-gather kernel launch");
+    clear_error();
+    return HZ_OK;
+  }
   const uint8_t* xc;
   const float* xs;
   if (!backward) {
@@ -224,8 +273,59 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
   P.phase += static_cast<unsigned long long>(to_level - from_level + 1);
   auto phase_of = [&](int l) { return base + static_cast<unsigned long long>(l - from_level + 1); };
 
-  // A7: quantize the input range_{from-1} into this rank's level-`from` send buffer
-  {
+  int first = from_level;   // first level handled by the per-level kernels below
+  if (B == 256 && fused_rs_supported(p->group[from_level - 1]) && tune_param("fused", 1)) {
+    // A7 + A8 + A9 of the first level in ONE kernel: quantize the own input chunk by
+    // chunk (destinations interleaved), publish each chunk to its destination, and
+    // reduce the members' chunks destined here as they become ready.
+    const int l = from_level;
+    const int g = p->group[l - 1];
+    const int d = p->digit[l - 1];
+    const int bits = bits_per_level[l - 1];
+    const int64_t cl = p->len[l];
+    const unsigned long long ph = phase_of(l);
+    FusedRSArgs h{};
+    h.x = grad;
+    h.dt = dt;
+    h.bits_in = bits;
+    h.bits_out = l < to_level ? bits_per_level[l] : 0;
+    h.acc = l < to_level ? 0 : accumulate;
+    h.qc = at<uint8_t>(ctx, ctx->rank, P.rs_c[l].off);
+    h.qs = at<float>(ctx, ctx->rank, P.rs_s[l].off);
+    h.g = g;
+    h.d = d;
+    h.cl = cl;
+    h.C = chunk_elems(cl);
+    h.ncl = static_cast<int>((cl + h.C - 1) / h.C);
+    for (int j = 0; j < g; ++j) {
+      const int m = static_cast<int>(p->rank + (static_cast<int64_t>(j) - d) * stride[l - 1]);
+      h.mc[j] = at<const uint8_t>(ctx, m, P.rs_c[l].off) + code_bytes(d * cl, bits);
+      h.ms[j] = at<const float>(ctx, m, P.rs_s[l].off) + d * cl / B;
+      h.flags_remote[j] = at<unsigned long long>(ctx, m, kChunkRSOff) + d * kMaxChunks;
+    }
+    h.flags = at<unsigned long long>(ctx, ctx->rank, kChunkRSOff);
+    h.work = at<unsigned long long>(ctx, ctx->rank, kWorkRSOff);
+    h.of = shard;
+    if (l < to_level) {
+      h.oc = at<uint8_t>(ctx, ctx->rank, P.rs_c[l + 1].off);
+      h.os = at<float>(ctx, ctx->rank, P.rs_s[l + 1].off);
+    }
+    h.phase = ph - P.epoch_host;
+    h.epoch = at<const unsigned long long>(ctx, ctx->rank, kEpochOff);
+    SyncArgs sy = l < to_level ? make_sync(ctx, 0, ph - 1, ph + 1, ph) : make_sync(ctx, 0, ph - 1, 0, ph);
+    const int64_t n_in = p->len[l - 1];
+    const int64_t remote = (g - 1) * (code_bytes(cl, bits) + cl / B * 4);
+    const int64_t out = h.bits_out ? code_bytes(cl, h.bits_out) + cl / B * 4 : cl * 4 * (h.acc ? 2 : 1);
+    const int64_t local = n_in * elem_bytes(dt) + code_bytes(n_in, bits) + n_in / B * 4 +
+                          g * (code_bytes(cl, bits) + cl / B * 4) - remote + out;
+    TraceScope t(st, "rs_fused", l, bits, n_in, local, remote);
+    sy.stamps = t.stamps;
+    cudaError_t e = launch_rs_fused(h, st, sy);
+    t.end();
+    if (e != cudaSuccess) return cuda_fail(e, "fused reduce-scatter kernel launch");
+    first = l + 1;
+  } else {
+    // A7: quantize the input range_{from-1} into this rank's level-`from` send buffer
     const unsigned long long ph = phase_of(from_level);
     SyncArgs sq = make_sync(ctx, 0, ph - 1, ph, 0);
     if ((rc = run_quantize(grad, dt, p->len[from_level - 1], bits_per_level[from_level - 1], B,
@@ -233,7 +333,7 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
                            at<float>(ctx, ctx->rank, P.rs_s[from_level].off), st, from_level, &sq)) != HZ_OK)
       return rc;
   }
-  for (int l = from_level; l <= to_level; ++l) {
+  for (int l = first; l <= to_level; ++l) {
     const int g = p->group[l - 1];
     const int d = p->digit[l - 1];
     const int bits = bits_per_level[l - 1];
