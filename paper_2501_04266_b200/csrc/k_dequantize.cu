@@ -33,16 +33,32 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
   const int64_t warp = global_warp();
   const int64_t nwarps = num_warps();
   const bool copy_sec = pc.sec_c != nullptr;
+  // Pieces interleaved by warp tile (32*U units): consecutive tiles alternate between
+  // pieces, so local (HBM) and peer (NVLink) tiles are in flight at the same time
+  // instead of one half of the layer after the other.
+  const bool inter = pc.n > 1 && (pc.len % (256 * U)) == 0;
+  const int64_t tiles_per_piece = pc.len / (256 * U);
   for (int64_t base = warp * 32 * U; base < nunits; base += nwarps * 32 * U) {
+    int64_t ub = base;            // first unit of this warp tile in the layer
+    int jt = -1;                  // its piece, when interleaved
+    if (inter) {
+      const int64_t tile = base / (32 * U);
+      jt = static_cast<int>(tile % pc.n);
+      ub = jt * (pc.len / 8) + (tile / pc.n) * (32 * U);
+      (void)tiles_per_piece;
+    }
     Codes8<BITS> raw[U];
     float sc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t unit = base + u * 32 + lane;
+      const int64_t unit = ub + u * 32 + lane;
       if (unit < nunits) {
         const int64_t e = unit * 8;
-        int j = 0;
-        for (int q = 1; q < pc.n; ++q) j += e >= q * pc.len;   // piece of this unit
+        int j = jt;
+        if (j < 0) {
+          j = 0;
+          for (int q = 1; q < pc.n; ++q) j += e >= q * pc.len;   // piece of this unit
+        }
         const int64_t r = e - j * pc.len;
         raw[u].load(pc.c[j] + r * BITS / 8);
         sc[u] = __ldg(pc.s[j] + (r >> log2b));
@@ -50,7 +66,7 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t unit = base + u * 32 + lane;
+      const int64_t unit = ub + u * 32 + lane;
       if (unit < nunits) {
         float c[8], v[8];
         raw[u].decode(c);

@@ -12,6 +12,13 @@
 //                the members' chunks destined to this rank (ascending digit, fp32,
 //                no FMA) into the fp32 shard or the next level's requantized buffer.
 //
+// STATUS: experimental, off by default (HZ_TUNE fused=1).  Measured on 2 B200s at
+// GPT-1.3B layer size these are slower than the two-kernel P2P path (74 vs 59 µs
+// for the forward gather, 83 vs 49 µs for the qgZ level): a work item is one
+// 32K-element chunk processed by one CTA, and that serialisation costs more than
+// the overlap gains.  Kept (and parity-tested with fused=1) for a finer-grained
+// interleaved design.
+//
 // Work distribution: persistent CTAs take work items from a global counter —
 // first every production item, then the consumption items (remote pieces before
 // the own one).  A consumption item waits (thread 0, ld.acquire.sys) for the
@@ -210,20 +217,28 @@ template <int BIN, int GT>
 __device__ __forceinline__ void cta_reduce_f32(const FusedRS& a, int64_t off, int64_t n, float4* stage) {
   constexpr int E = 64 / BIN;
   constexpr int G = E / 4;
+  constexpr int U = 2;                                  // warp chunks in flight per warp
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const int64_t nunits = n / E;
+  const int64_t nunits = n / E;                         // a multiple of 32 * U * kWarps
   float4* st = stage + w * 32 * G;
-  for (int64_t base = w * 32; base < nunits; base += kThreads) {   // one warp chunk = 32 units
-    const int64_t unit = base + lane;
-    float acc[E];
-    uint2 raw[GT];
-    float sc[GT];
+  for (int64_t base0 = w * 32 * U; base0 < nunits; base0 += kThreads * U) {
+  uint2 rawu[U][GT];
+  float scu[U][GT];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
 #pragma unroll
     for (int p = 0; p < GT; ++p) {
-      raw[p] = __ldg(reinterpret_cast<const uint2*>(a.mc[p] + (off / E + unit) * 8));
-      sc[p] = __ldg(a.ms[p] + (off + unit * E) / kB);
+      const int64_t unit = base0 + u * 32 + lane;
+      rawu[u][p] = __ldg(reinterpret_cast<const uint2*>(a.mc[p] + (off / E + unit) * 8));
+      scu[u][p] = __ldg(a.ms[p] + (off + unit * E) / kB);
     }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t base = base0 + u * 32;
+    float acc[E];
+    const uint2 (&raw)[GT] = rawu[u];
+    const float (&sc)[GT] = scu[u];
 #pragma unroll
     for (int p = 0; p < GT; ++p) {
       float c[E];
@@ -271,6 +286,7 @@ __device__ __forceinline__ void cta_reduce_f32(const FusedRS& a, int64_t off, in
       *dst = o;
     }
     __syncwarp();
+  }
   }
 }
 

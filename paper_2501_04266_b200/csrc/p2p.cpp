@@ -68,7 +68,8 @@ hz_status slot(hz_ctx* ctx, hz_ctx::P2P::Slot& sl, size_t bytes) {
 int64_t chunk_elems(int64_t len) {
   int64_t c = (len + kMaxChunks - 1) / kMaxChunks;
   c = (c + 1023) / 1024 * 1024;
-  return c < 32768 ? 32768 : c;
+  const int64_t lo = int64_t(tune_param("fchunk", 32)) * 1024;   // HZ_TUNE fchunk (KiElements)
+  return c < lo ? lo : c;
 }
 
 template <typename T>
@@ -165,7 +166,7 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   const unsigned long long phase = ++P.phase;
   const int64_t plen = p->len[top];
 
-  if (!backward && s == w && D > 1 && B == 256 && tune_param("fused", 1)) {
+  if (!backward && s == w && D > 1 && B == 256 && tune_param("fused", 0)) {
     // A2 + A3 + A5 in ONE kernel: quantize the own primary chunk by chunk into the
     // (peer-readable) secondary, publish each chunk, and dequantize every member's
     // chunks as they become ready — NVLink transfers overlap the quantization.
@@ -274,7 +275,7 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
   auto phase_of = [&](int l) { return base + static_cast<unsigned long long>(l - from_level + 1); };
 
   int first = from_level;   // first level handled by the per-level kernels below
-  if (B == 256 && fused_rs_supported(p->group[from_level - 1]) && tune_param("fused", 1)) {
+  if (B == 256 && fused_rs_supported(p->group[from_level - 1]) && tune_param("fused", 0)) {
     // A7 + A8 + A9 of the first level in ONE kernel: quantize the own input chunk by
     // chunk (destinations interleaved), publish each chunk to its destination, and
     // reduce the members' chunks destined here as they become ready.
