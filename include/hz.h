@@ -265,6 +265,25 @@ HZ_API hz_status hz_p2p_replayed(hz_ctx* ctx, unsigned long long n);
  * is exhausted or P2P is not enabled. */
 HZ_API hz_status hz_sym_alloc(hz_ctx* ctx, size_t bytes, void** out);
 
+/* Step tail: AdamW on the rank's optimizer shard followed by
+ * the post-update all-gather of the updated weights.
+ * grad_shard, master, m, v: fp32[len_L] over range_L (master / m / v updated in
+ * place).  primary: dt[len_w] over range_w, overwritten with the updated weights
+ * of range_w (its range_L part from this rank's update, the rest gathered from
+ * the ranks that share digits 1..w, over levels L..w+1; no quantization — the
+ * narrow form of P:399's exchange allowed by the nested ownership map).
+ * Arithmetic (reading R19, PyTorch AdamW, fp32, one rounding per operation):
+ *   m' = b1*m + omb1*g;  v' = b2*v + (omb2*g)*g;  th1 = th - lr_wd*th;
+ *   th' = th1 - step * (m' / (sqrt(v')/sqrt_bc2 + eps));  primary = dt(th')
+ * with the host scalars of hz_adamw_t (omb = 1 - b, lr_wd = lr*wd,
+ * sqrt_bc2 = sqrt(1 - b2^t), step = lr / (1 - b1^t)). */
+typedef struct {
+  float b1, omb1, b2, omb2, lr_wd, sqrt_bc2, eps, step;
+} hz_adamw_t;
+HZ_API hz_status hz_adamw_step(hz_ctx* ctx, const hz_partition_t* p, const float* grad_shard,
+                               float* master, float* m, float* v, const hz_adamw_t* hp,
+                               void* primary, hz_dtype dt, void* stream);
+
 /* Flat ZeRO-3 baseline (Table VII/VIII row "ZeRO-3"): plain ncclAllGather of
  * the rank's bf16/fp16/fp32 chunk (numel/world elements, rank order) into
  * out[numel], and plain ncclReduceScatter(sum) of in[numel] into

@@ -41,6 +41,7 @@ struct hz_ctx {
     };
     Slot ag_prim_c, ag_prim_s;                  // quantized primary when s != w
     Slot rs_c[HZ_MAX_LEVELS + 1], rs_s[HZ_MAX_LEVELS + 1];   // level-l send buffers
+    Slot upd;                                   // updated weights of range_L (step tail)
   } p2p;
 };
 
@@ -83,5 +84,9 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
                              int from_level, int to_level, const int* bits_per_level, float* shard,
                              int accumulate, cudaStream_t st);
 void p2p_release(hz_ctx* ctx);
+hz_status p2p_adamw_gather(hz_ctx* ctx, const hz_partition_t* p, const float* g, float* th, float* m, float* v,
+                           const AdamW& hp, void* primary, hz_dtype dt, cudaStream_t st);
+hz_status run_adamw(const float* g, float* th, float* m, float* v, void* out, hz_dtype dt, int64_t n,
+                    const AdamW& hp, cudaStream_t st, const SyncArgs* sync);
 
 }  // namespace hz

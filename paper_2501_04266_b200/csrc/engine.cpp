@@ -172,6 +172,17 @@ hz_status run_roundtrip(const void* x, hz_dtype dt, int64_t n, int bits, int blo
   return HZ_OK;
 }
 
+hz_status run_adamw(const float* g, float* th, float* m, float* v, void* out, hz_dtype dt, int64_t n,
+                    const AdamW& hp, cudaStream_t st, const SyncArgs* sync) {
+  TraceScope t(st, "adamw", 0, 32, n, n * (16 + 12 + elem_bytes(dt)));
+  SyncArgs sy = sync ? *sync : SyncArgs{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_adamw(g, th, m, v, out, dt, n, hp, st, (sync || t.stamps) ? &sy : nullptr);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "adamw kernel launch");
+  return HZ_OK;
+}
+
 hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (bytes == 0 || dst == src) return HZ_OK;
   TraceScope t(st, "copy", 0, 0, 0, int64_t(bytes) * 2);
@@ -479,6 +490,45 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
                            l)) != HZ_OK)
         return rc;
     }
+  }
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_adamw_step(hz_ctx* ctx, const hz_partition_t* p, const float* grad_shard, float* master,
+                        float* m, float* v, const hz_adamw_t* hp, void* primary, hz_dtype dt, void* stream) {
+  using namespace hz;
+  hz_status rc = check_partition(ctx, p);
+  if (rc != HZ_OK) return rc;
+  if (!hp) return fail(HZ_ERR_INVALID, "hp: NULL");
+  if (!dtype_ok(dt)) return fail(HZ_ERR_INVALID, "dt: unknown dtype");
+  for (const void* q : {static_cast<const void*>(grad_shard), static_cast<const void*>(master),
+                        static_cast<const void*>(m), static_cast<const void*>(v), static_cast<const void*>(primary)})
+    if (!q || !aligned16(q)) return fail(HZ_ERR_INVALID, "grad_shard/master/m/v/primary: NULL or not 16-byte aligned");
+  if ((rc = check_async(ctx)) != HZ_OK) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int L = p->levels, w = p->w;
+  const int64_t lenL = p->len[L];
+  if (lenL == 0) {
+    clear_error();
+    return HZ_OK;
+  }
+  AdamW a{hp->b1, hp->omb1, hp->b2, hp->omb2, hp->lr_wd, hp->sqrt_bc2, hp->eps, hp->step};
+  if (ctx->p2p.on) return p2p_adamw_gather(ctx, p, grad_shard, master, m, v, a, primary, dt, st);
+  // the update lands in its place inside the primary; levels L..w+1 then gather in place
+  char* prim = static_cast<char*>(primary);
+  const int64_t eb = elem_bytes(dt);
+  if ((rc = run_adamw(grad_shard, master, m, v, prim + (p->off[L] - p->off[w]) * eb, dt, lenL, a, st, nullptr)) !=
+      HZ_OK)
+    return rc;
+  for (int l = L; l > w; --l) {
+    const int g = ctx->group[l - 1];
+    if (g <= 1) continue;
+    TraceScope t(st, "nccl_allgather", l, 16, p->len[l], (g - 1) * p->len[l] * eb);
+    HZ_NCCL(ncclAllGather(prim + (p->off[l] - p->off[w]) * eb, prim + (p->off[l - 1] - p->off[w]) * eb,
+                          p->len[l], nccl_dtype(dt), ctx->lvl[l - 1], st),
+            "ncclAllGather(updated weights)");
+    t.end();
   }
   clear_error();
   return HZ_OK;

@@ -80,6 +80,15 @@ cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const
                           float* out_scales, float* out_f32, int accumulate, cudaStream_t st,
                           const SyncArgs* sync = nullptr);
 
+// Step tail (k_optim.cu): AdamW on the optimizer shard and the bf16/fp16/fp32
+// gather copy of the post-update all-gather.  Same layout as hz_adamw_t.
+struct AdamW {
+  float b1, omb1, b2, omb2, lr_wd, sqrt_bc2, eps, step;
+};
+cudaError_t launch_adamw(const float* g, float* th, float* m, float* v, void* out, hz_dtype out_dt, int64_t n,
+                         const AdamW& hp, cudaStream_t st, const SyncArgs* sync);
+cudaError_t launch_gather_copy(const Pieces& pc, void* out, cudaStream_t st, const SyncArgs* sync);
+
 // Fused codec + NVLink collective kernels (k_fused.cu, B = 256 only).
 constexpr int kMaxChunks = 4096;   // per-chunk flags per member in the P2P pool header
 struct FusedAGArgs {

@@ -366,6 +366,64 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
   return HZ_OK;
 }
 
+// Step tail over NVLink: AdamW writes the updated weights of range_L into a pool
+// slot (producer), then one copy kernel gathers the members' slots — the ranks that
+// share digits 1..w — into the primary range_w (consumer).
+hz_status p2p_adamw_gather(hz_ctx* ctx, const hz_partition_t* p, const float* g, float* th, float* m, float* v,
+                           const AdamW& hp, void* primary, hz_dtype dt, cudaStream_t st) {
+  auto& P = ctx->p2p;
+  const int L = p->levels, w = p->w;
+  const int64_t lenL = p->len[L];
+  const int64_t eb = elem_bytes(dt);
+  hz_status rc;
+  if ((rc = slot(ctx, P.upd, lenL * 4)) != HZ_OK) return rc;   // fp32 capacity
+  const unsigned long long phase = ++P.phase;
+  char* mine = at<char>(ctx, ctx->rank, P.upd.off);
+  SyncArgs sq = make_sync(ctx, 0, phase - 1, phase, 0);
+  if ((rc = run_adamw(g, th, m, v, mine, dt, lenL, hp, st, &sq)) != HZ_OK) return rc;
+  // members: vary digits w+1..L, keep digits 1..w
+  int64_t stride[HZ_MAX_LEVELS];
+  int64_t sacc = 1;
+  for (int l = 0; l < L; ++l) {
+    stride[l] = sacc;
+    sacc *= p->group[l];
+  }
+  int64_t base = p->rank, D = 1;
+  for (int l = w; l < L; ++l) {
+    base -= p->digit[l] * stride[l];
+    D *= p->group[l];
+  }
+  if (D > kMaxWorld) return fail(HZ_ERR_UNSUPPORTED, "P2P gather over more than 8 ranks");
+  std::vector<std::pair<int64_t, int>> mem;
+  for (int64_t idx = 0; idx < D; ++idx) {
+    int64_t rem = idx, r = base, off = 0;
+    for (int l = w; l < L; ++l) {
+      const int d = static_cast<int>(rem % p->group[l]);
+      rem /= p->group[l];
+      r += d * stride[l];
+      off += d * p->len[l + 1];
+    }
+    mem.emplace_back(off, static_cast<int>(r));
+  }
+  std::sort(mem.begin(), mem.end());
+  Pieces pc{};
+  pc.n = static_cast<int>(D);
+  pc.len = lenL * eb;   // bytes
+  int64_t remote = 0;
+  for (int k = 0; k < pc.n; ++k) {
+    pc.c[k] = at<const uint8_t>(ctx, mem[k].second, P.upd.off);
+    if (mem[k].second != ctx->rank) remote += pc.len;
+  }
+  SyncArgs sd = make_sync(ctx, phase, 0, 0, phase);
+  TraceScope t(st, "gather_copy", w, 16, lenL * D, D * pc.len * 2 - remote, remote);
+  sd.stamps = t.stamps;
+  cudaError_t e = launch_gather_copy(pc, primary, st, &sd);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "post-update gather kernel launch");
+  clear_error();
+  return HZ_OK;
+}
+
 void p2p_release(hz_ctx* ctx) {
   auto& P = ctx->p2p;
   if (!P.pool) return;

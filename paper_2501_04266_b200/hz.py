@@ -111,6 +111,18 @@ _sig("hz_allgather_params", [_vp, ctypes.POINTER(Partition), _int, _vp, _int, _i
                              _int, _vp])
 _sig("hz_reduce_scatter_grads", [_vp, ctypes.POINTER(Partition), _vp, _int, _int, _int,
                                  ctypes.POINTER(ctypes.c_int), _vp, _int, _vp])
+class AdamWParams(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_float) for n in ("b1", "omb1", "b2", "omb2", "lr_wd", "sqrt_bc2", "eps", "step")]
+
+
+def adamw_params(lr, b1, b2, eps, wd, t):
+    """hz_adamw_t of step t (t >= 1): host scalars rounded once to fp32 (reading R19)."""
+    import math
+    return AdamWParams(b1, 1.0 - b1, b2, 1.0 - b2, lr * wd, math.sqrt(1.0 - b2 ** t), eps, lr / (1.0 - b1 ** t))
+
+
+_sig("hz_adamw_step", [_vp, ctypes.POINTER(Partition), _vp, _vp, _vp, _vp, ctypes.POINTER(AdamWParams), _vp, _int,
+                       _vp])
 _sig("hz_flat_allgather", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_flat_reduce_scatter", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_trace_begin", [_int, _int])
@@ -404,6 +416,12 @@ class Context:
                                             from_level, L if to_level is None else to_level, arr,
                                             _ptr(shard), int(bool(accumulate)), _stream(stream)))
         return shard
+
+    def adamw_step(self, p, grad_shard, master, m, v, hp, primary, stream=None):
+        """hz_adamw_step: AdamW on range_L, then the post-update all-gather into primary."""
+        _check(_lib.hz_adamw_step(self._h, ctypes.byref(p), _ptr(grad_shard), _ptr(master), _ptr(m), _ptr(v),
+                                  ctypes.byref(hp), _ptr(primary), _dtype_code(primary), _stream(stream)))
+        return primary
 
     def flat_allgather(self, chunk, out, stream=None):
         _check(_lib.hz_flat_allgather(self._h, _ptr(chunk), _ptr(out), out.numel(),

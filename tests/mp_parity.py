@@ -120,6 +120,39 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             except AssertionError as e:
                 errors.append(str(e))
 
+        # step tail (N2): AdamW on range_L, post-update all-gather into range_w
+        from oracle import optim
+        for w in sorted({1, L, 0} & set(range(L + 1))):
+            p = ctx.partition(numel, B, w, w, L)
+            oL, nL = p.range(L)
+            ow, nw = p.range(w)
+            rs = np.random.default_rng(77 + rank)
+            th0 = {}
+            upd = {}
+            for q in range(world):
+                rq = np.random.default_rng(500 + q)
+                o, n_ = pm.range_at(q, g, Np, L)
+                th_q = (rq.standard_normal(n_) * 0.02).astype(np.float32)
+                m_q = (rq.standard_normal(n_) * 1e-3).astype(np.float32)
+                v_q = (rq.random(n_) * 1e-6).astype(np.float32)
+                g_q = (rq.standard_normal(n_) * 1e-3).astype(np.float32)
+                th0[q] = (th_q, m_q, v_q, g_q)
+                s = optim.adamw_scalars(1e-3, 0.9, 0.95, 1e-8, 0.1, 3)
+                upd[q] = optim.adamw(th_q, m_q, v_q, g_q, s)
+            want_prim = optim.post_update_allgather({q: upd[q][0].astype(ml_dtypes.bfloat16) for q in range(world)},
+                                                    g, Np, w)
+            th_d, m_d, v_d, g_d = (to_dev(a.copy()) for a in th0[rank])
+            prim = torch.zeros(nw, dtype=torch.bfloat16, device="cuda")
+            ctx.adamw_step(p, g_d, th_d, m_d, v_d, hz.adamw_params(1e-3, 0.9, 0.95, 1e-8, 0.1, 3), prim)
+            torch.cuda.synchronize()
+            try:
+                assert_bitwise(to_host(th_d), upd[rank][0], f"[{tag}] g={g} w={w} adamw master")
+                assert_bitwise(to_host(m_d), upd[rank][1], f"[{tag}] g={g} w={w} adamw m")
+                assert_bitwise(to_host(v_d), upd[rank][2], f"[{tag}] g={g} w={w} adamw v")
+                assert_bitwise(to_host(prim), want_prim[rank], f"[{tag}] g={g} w={w} post-update all-gather")
+            except AssertionError as e:
+                errors.append(str(e))
+
         # CUDA graph: one captured step (forward gather, backward gather, qgZ) replayed
         # three times with fresh inputs copied into the captured buffers
         p = ctx.partition(numel, B, 1, 1, L)
