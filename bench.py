@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flat", action="store_true")
+    ap.add_argument("--no-tail", action="store_true", help="skip the step-tail (AdamW + post-update gather) timing")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 collective transport: fused NVLink peer-memory kernels (p2p) or NCCL")
     ap.add_argument("--cpu-sample-layers", type=int, default=4)
@@ -431,6 +432,12 @@ def run_hz(args):
             roofline["timer"] = ("in-kernel %globaltimer stamps (CTA 0 entry -> last CTA exit) over the timed "
                                  "region; CUDA events on the launching stream in a second eager pass: events_*")
 
+    # step tail, timed separately: AdamW on every optimizer shard and
+    # the post-update all-gather of the updated weights into the primaries
+    tail = None
+    if not args.no_tail:
+        tail = step_tail(hz, ctx, torch, model, stream, world, args)
+
     # flat ZeRO-3 baseline on the same logical bytes (context, not timed with the step)
     flat = None
     if world > 1 and not args.no_flat:
@@ -466,6 +473,7 @@ def run_hz(args):
         "clocks": clocks,
         "stages": stages,
         "flat_zero3_baseline": flat,
+        "step_tail": tail,
     }
     ctx.close()
     if rank == 0:
@@ -506,6 +514,41 @@ def flat_baseline(hz, ctx, torch, model, stream, world, args):
     ms = max_over_ranks(e0.elapsed_time(e1), world) / n
     return {"ms_per_step": ms, "value": world * model.logical_bytes / (ms * 1e-3) / 1e9, "unit": UNIT,
             "what": "ncclAllGather x2 + ncclReduceScatter, bf16, world communicator"}
+
+
+def step_tail(hz, ctx, torch, model, stream, world, args):
+    """AdamW (fp32 master, m, v over range_L; the qgZ shard is the gradient) + post-update
+    all-gather of every tensor, eager, CUDA events around K steps, max over ranks."""
+    states = []
+    for t in model.tensors:
+        n = t["shard"].numel()
+        states.append((torch.randn(n, device=t["shard"].device).mul_(0.02),
+                       torch.zeros(n, device=t["shard"].device), torch.zeros(n, device=t["shard"].device)))
+    hp = hz.adamw_params(1e-4, 0.9, 0.95, 1e-8, 0.1, 1)
+
+    def one():
+        for t, (th, m, v) in zip(model.tensors, states):
+            ctx.adamw_step(t["p"], t["shard"], th, m, v, hp, t["primary"], stream=stream)
+
+    one()
+    torch.cuda.synchronize()
+    barrier(world)
+    n = max(1, min(args.steps, 5))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world) / n
+    opt_elems = sum(t["shard"].numel() for t in model.tensors)
+    del states
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "optimizer_elems_per_rank": opt_elems,
+            "adamw_hbm_bytes_per_step": opt_elems * 30,
+            "what": "AdamW on the fp32 optimizer shards + post-update all-gather of the bf16 weights into the "
+                    "primaries (eager; not part of the headline metric)"}
 
 
 def run_e2e(hz, ctx, torch, model, stream, world, args):
