@@ -231,6 +231,7 @@ def p2p_pool_bytes(args, group):
         total += len_s * args.qwz_bits // 8 + len_s // B * 4 + 512
         max_np = max(max_np, Np)
     total += 2 * len(group) * (max_np + max_np // B * 4 + 512)   # slots (may grow once)
+    total += 2 * (max_np // W) * 4 + 1024                       # step-tail update slot
     return total + (64 << 20)
 
 
@@ -436,16 +437,16 @@ def run_hz(args):
     # the post-update all-gather of the updated weights into the primaries
     tail = None
     if not args.no_tail:
-        tail = step_tail(hz, ctx, torch, model, stream, world, args)
+        tail = extra(step_tail, hz, ctx, torch, model, stream, world, args)
 
     # flat ZeRO-3 baseline on the same logical bytes (context, not timed with the step)
     flat = None
     if world > 1 and not args.no_flat:
-        flat = flat_baseline(hz, ctx, torch, model, stream, world, args)
+        flat = extra(flat_baseline, hz, ctx, torch, model, stream, world, args)
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(hz, ctx, torch, model, stream, world, args)
+        e2e = extra(run_e2e, hz, ctx, torch, model, stream, world, args)
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -481,6 +482,14 @@ def run_hz(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def extra(fn, *a):
+    """Secondary measurements never take the headline line down with them."""
+    try:
+        return fn(*a)
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def flat_baseline(hz, ctx, torch, model, stream, world, args):
