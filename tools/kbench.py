@@ -24,7 +24,11 @@ def main():
     ap.add_argument("--block", type=int, default=256)
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--step1", action="store_true",
+                    help="one world-1 step of one tensor through the collective API (fused round trips)")
     args = ap.parse_args()
+    if args.step1:
+        return step1(args)
 
     import torch
     from paper_2501_04266_b200 import hz
@@ -86,6 +90,56 @@ def main():
         gbs = byts / (ms * 1e-3) / 1e9
         print(json.dumps({"kernel": name, "numel": n, "us": round(ms * 1e3, 2), "bytes": byts,
                           "GBps": round(gbs, 1), "frac_of_copy_peak": round(gbs / peak, 3)}), flush=True)
+
+
+def step1(args):
+    """World-1 context, one GPT-1.3B layer: forward gather (fused quantize+dequantize,
+    bf16), backward gather (dequantize), qgZ (fused quantize+dequantize, fp32 shard).
+    --once: each kernel once (ncu); else timed with CUDA events per call."""
+    import torch
+    from paper_2501_04266_b200 import hz, synth
+    sys.path.insert(0, ROOT)
+    import bench
+    peak, _ = bench.measured_peaks()
+    ctx = hz.Context(0, 1, hz.get_uid(), (1,), 0)
+    numel = synth.layer_numel(2048)
+    p = ctx.partition(numel, 256, 1, 1, 1)
+    Np = p.padded_numel
+    nsets = 4
+    prim = [synth.torch_normal(Np, 1 + i, 0.02, torch.bfloat16, "cuda", outlier_every=0) for i in range(nsets)]
+    grad = [synth.torch_normal(Np, 11 + i, 1e-3, torch.bfloat16, "cuda") for i in range(nsets)]
+    sec_c = [torch.empty(Np, dtype=torch.uint8, device="cuda") for _ in range(nsets)]
+    sec_s = [torch.empty(Np // 256, dtype=torch.float32, device="cuda") for _ in range(nsets)]
+    out = [torch.empty(Np, dtype=torch.bfloat16, device="cuda") for _ in range(nsets)]
+    shard = [torch.empty(Np, dtype=torch.float32, device="cuda") for _ in range(nsets)]
+    cases = {
+        "fwd_quantize_dequantize_bf16": (lambda i: ctx.allgather_params(p, prim[i], sec_c[i], sec_s[i], out[i]),
+                                         Np * (2 + 1 + 2) + Np // 64),
+        "bwd_dequantize": (lambda i: ctx.allgather_params(p, None, sec_c[i], sec_s[i], out[i], backward=True),
+                           Np * (1 + 2) + Np // 64),
+        "qgz_quantize_dequantize_f32": (lambda i: ctx.reduce_scatter_grads(p, grad[i], shard[i], [4]), Np * (2 + 4)),
+    }
+    for i in range(nsets):
+        for name, (fn, _) in cases.items():
+            fn(i)
+    torch.cuda.synchronize()
+    for name, (fn, byts) in cases.items():
+        if args.once:
+            fn(0)
+            torch.cuda.synchronize()
+            continue
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.iters):
+            fn(i % nsets)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.iters
+        gbs = byts / (ms * 1e-3) / 1e9
+        print(json.dumps({"kernel": name, "numel": Np, "us": round(ms * 1e3, 2), "bytes": byts,
+                          "GBps": round(gbs, 1), "frac_of_copy_peak": round(gbs / peak, 3)}), flush=True)
+    ctx.close()
 
 
 if __name__ == "__main__":
