@@ -162,6 +162,14 @@ cudaError_t quantize_u(const void* x, int64_t n, uint8_t* codes, float* scales, 
 template <typename T, int BITS>
 cudaError_t roundtrip_t(const void* x, int64_t n, uint8_t* codes, float* scales, void* y, hz_dtype out_dt,
                         int acc, cudaStream_t st, const SyncArgs& sy) {
+  if (tune_param("rt_u", 4) == 2) {   // HZ_TUNE rt_u: 2 (fewer registers, more warps) or 4
+    switch (out_dt) {
+      case HZ_BF16: return quantize_u<T, 256, BITS, 2, 1>(x, n, codes, scales, st, sy, y, 0);
+      case HZ_F16: return quantize_u<T, 256, BITS, 2, 2>(x, n, codes, scales, st, sy, y, 0);
+      case HZ_F32: return quantize_u<T, 256, BITS, 2, 3>(x, n, codes, scales, st, sy, y, acc);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (out_dt) {
     case HZ_BF16: return quantize_u<T, 256, BITS, kU, 1>(x, n, codes, scales, st, sy, y, 0);
     case HZ_F16: return quantize_u<T, 256, BITS, kU, 2>(x, n, codes, scales, st, sy, y, 0);

@@ -119,6 +119,11 @@ def step1(args):
                            Np * (1 + 2) + Np // 64),
         "qgz_quantize_dequantize_f32": (lambda i: ctx.reduce_scatter_grads(p, grad[i], shard[i], [4]), Np * (2 + 4)),
     }
+    # calibration: torch copies with the same read:write mixes (bf16 -> bf16 is the
+    # 1:1 copy of MEASURED_PEAKS; bf16 -> fp32 is the 1:2 mix of the fp32 shard)
+    xf = [torch.empty(Np, dtype=torch.float32, device="cuda") for _ in range(nsets)]
+    cases["torch_copy_bf16_bf16"] = (lambda i: out[i].copy_(prim[i]), Np * 4)
+    cases["torch_copy_bf16_f32"] = (lambda i: xf[i].copy_(grad[i]), Np * 6)
     for i in range(nsets):
         for name, (fn, _) in cases.items():
             fn(i)
