@@ -19,6 +19,7 @@ import re
 import subprocess
 
 KIND = [  # (regex on the demangled kernel name, kind used by the library trace)
+    (r"k_quantize<[^>]*, [1-3]>", "quantize_dequantize"),
     (r"k_quantize", "quantize"),
     (r"k_dequantize", "dequantize"),
     (r"k_reduce_requant", "reduce_requant"),
@@ -136,9 +137,16 @@ def main():
                             f"(read {d['dram_read_bytes']/elems[i]:.4f}, write {d['dram_write_bytes']/elems[i]:.4f}; "
                             "writes still dirty in L2 at kernel end are not counted)\n")
                     k = kind_of(d["name"])
-                    if k and k not in traffic:
-                        traffic[k] = {"dram_bytes": d["dram_bytes"], "elems": elems[i], "source": os.path.basename(a.rep),
-                                      "kernel": d["name"][:160]}
+                    if k:
+                        # several variants of one kind in one capture: average bytes per element
+                        prev = traffic.get(k) if traffic.get(k, {}).get("source") == os.path.basename(a.rep) else None
+                        if prev:
+                            prev["dram_bytes"] = (prev["dram_bytes"] / prev["elems"] + d["dram_bytes"] / elems[i]) / 2 * elems[i]
+                            prev["elems"] = elems[i]
+                            prev["kernel"] += " | " + d["name"][:120]
+                        elif k not in traffic or traffic[k].get("source") != os.path.basename(a.rep):
+                            traffic[k] = {"dram_bytes": d["dram_bytes"], "elems": elems[i],
+                                          "source": os.path.basename(a.rep), "kernel": d["name"][:160]}
                 f.write("\n")
         json.dump(traffic, open(traffic_path, "w"), indent=1)
         print(open(a.out + "_kernels.md").read()[:6000])
