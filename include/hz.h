@@ -293,6 +293,12 @@ HZ_API hz_status hz_flat_allgather(hz_ctx* ctx, const void* chunk, void* out, in
 HZ_API hz_status hz_flat_reduce_scatter(hz_ctx* ctx, const void* in, void* out_chunk,
                                  int64_t numel, hz_dtype dt, void* stream);
 
+/* Upper bound on the CTAs of every libhz kernel launch (process-wide; 0 = no bound,
+ * the default: SMs x resident CTAs).  All kernels are grid-stride loops, so any
+ * bound is correct; a small bound (e.g. 32-64) leaves SMs to compute kernels that
+ * run concurrently on other streams (communication / computation overlap). */
+HZ_API hz_status hz_set_grid_limit(int max_ctas);
+
 /* ------------------------------------------------------------------ tracing */
 
 /* Per-launch device timing of the library's own work: CUDA events around each

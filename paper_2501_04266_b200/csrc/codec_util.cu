@@ -1,5 +1,6 @@
 // Grid sizing for the grid-stride codec kernels: SMs x resident CTAs (occupancy
 // API, cached per kernel), never more CTAs than there is work for.
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 
@@ -38,10 +39,14 @@ int resident_ctas(const void* kernel) {
 
 }  // namespace
 
+std::atomic<int> g_grid_limit{0};
+
 int64_t grid_for(const void* kernel, int64_t warp_tasks) {
   const int64_t per_cta = dev::kThreads / 32;
   const int64_t need = (warp_tasks + per_cta - 1) / per_cta;
-  const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(kernel);
+  int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(kernel);
+  const int lim = g_grid_limit.load(std::memory_order_relaxed);
+  if (lim > 0 && cap > lim) cap = lim;
   const int64_t g = need < cap ? need : cap;
   return g < 1 ? 1 : g;
 }
@@ -85,3 +90,10 @@ cudaError_t launch_epoch_advance(unsigned long long* epoch, unsigned long long s
   return cudaGetLastError();
 }
 }  // namespace hz
+
+extern "C" hz_status hz_set_grid_limit(int max_ctas) {
+  if (max_ctas < 0) return hz::fail(HZ_ERR_INVALID, "max_ctas: negative");
+  hz::g_grid_limit.store(max_ctas, std::memory_order_relaxed);
+  hz::clear_error();
+  return HZ_OK;
+}

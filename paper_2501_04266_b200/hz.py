@@ -123,6 +123,7 @@ def adamw_params(lr, b1, b2, eps, wd, t):
 
 _sig("hz_adamw_step", [_vp, ctypes.POINTER(Partition), _vp, _vp, _vp, _vp, ctypes.POINTER(AdamWParams), _vp, _int,
                        _vp])
+_sig("hz_set_grid_limit", [_int])
 _sig("hz_flat_allgather", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_flat_reduce_scatter", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_trace_begin", [_int, _int])
@@ -310,6 +311,11 @@ def _wrap_device_ptr(ptr, numel, dtype, device):
 
 
 # ------------------------------------------------------------------ collectives
+def set_grid_limit(max_ctas):
+    """hz_set_grid_limit: cap the CTAs of every libhz launch (0 = SMs x occupancy)."""
+    _check(_lib.hz_set_grid_limit(int(max_ctas)))
+
+
 def get_uid():
     u = Uid()
     _check(_lib.hz_get_uid(ctypes.byref(u)))

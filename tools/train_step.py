@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--modes", default="compute,hz,flat")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
+    ap.add_argument("--grid-limit", type=int, default=0,
+                    help="cap on the CTAs of every libhz kernel (leaves SMs to the GEMMs)")
     args = ap.parse_args()
 
     import torch
@@ -72,6 +74,7 @@ def main():
         dist.broadcast_object_list(box, src=0)
         uid = box[0]
     ctx = hz.Context(rank, world, uid, group, local)
+    hz.set_grid_limit(args.grid_limit)
     L = len(group)
     numel = synth.layer_numel(h)
     p = ctx.partition(numel, B, 1, 1, L)
@@ -224,7 +227,8 @@ def main():
         results["hz_over_flat"] = results["flat"]["ms_per_step"] / results["hz"]["ms_per_step"]
     line = {"what": "synthetic ZeRO-topo training step (layer GEMMs + sharded collectives, overlapped)",
             "config": args.config, "layers": nl, "tokens_per_gpu": T, "n_gpus": world, "hierarchy": list(group),
-            "transport": "p2p" if use_p2p else ("nccl" if world > 1 else "local"), "results": results}
+            "transport": "p2p" if use_p2p else ("nccl" if world > 1 else "local"),
+            "grid_limit": args.grid_limit, "results": results}
     ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
