@@ -22,7 +22,7 @@ from oracle import collectives as col  # noqa: E402
 from oracle import partition as pm  # noqa: E402
 from oracle import quant  # noqa: E402
 from paper_2501_04266_b200 import synth  # noqa: E402
-from tests.gpu_util import assert_bitwise, to_dev, to_host  # noqa: E402
+from tests.gpu_util import Guarded, assert_bitwise, assert_unchanged, to_dev, to_host  # noqa: E402
 
 HIERARCHIES = {
     1: [(1,)],
@@ -50,6 +50,10 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             return (ctx.sym_alloc(n_codes, torch.uint8), ctx.sym_alloc(n_scales, torch.float32))
         return (torch.empty(n_codes, dtype=torch.uint8, device="cuda"),
                 torch.empty(n_scales, dtype=torch.float32, device="cuda"))
+
+    def guarded_sec(n_codes, n_scales):
+        alloc = ctx.sym_alloc if p2p else None
+        return Guarded(n_codes, torch.uint8, alloc), Guarded(n_scales, torch.float32, alloc)
     try:
         Np = pm.padded_numel(numel, g, B)
         full = np.zeros(Np, np.float32)
@@ -62,18 +66,29 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             prim = {r: full[pm.range_at(r, g, Np, w)[0]:sum(pm.range_at(r, g, Np, w))] for r in range(world)}
             want, want_sec = col.allgather_forward(prim, g, Np, B, w, s, bits=8)
             so, sl = p.range(s)
-            sec_c, sec_s = sec_buffers(sl, sl // B)
-            out = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
-            ctx.allgather_params(p, to_dev(full[off:off + ln]), sec_c, sec_s, out, bits=8)
+            gc, gs = guarded_sec(sl, sl // B)
+            sec_c, sec_s = gc.t, gs.t
+            go = Guarded(Np, torch.bfloat16)
+            out = go.t
+            prim_in = to_dev(full[off:off + ln])
+            ctx.allgather_params(p, prim_in, sec_c, sec_s, out, bits=8)
             torch.cuda.synchronize()
             try:
+                what = f"[{tag}] g={g} w={w} s={s} forward"
+                go.check(what + " layer")
+                gc.check(what + " secondary codes")
+                gs.check(what + " secondary scales")
+                assert_unchanged(prim_in, full[off:off + ln], what + " primary")
                 assert_bitwise(to_host(out), want[rank], f"[{tag}] g={g} w={w} s={s} forward layer")
                 assert_bitwise(to_host(sec_c), quant.wire_codes(want_sec[rank][0], 8), f"[{tag}] g={g} w={w} s={s} secondary codes")
                 assert_bitwise(to_host(sec_s), want_sec[rank][1], f"[{tag}] g={g} w={w} s={s} secondary scales")
-                out2 = torch.empty_like(out)
+                go2 = Guarded(Np, torch.bfloat16)
+                out2 = go2.t
                 ctx.allgather_params(p, None, sec_c, sec_s, out2, bits=8, backward=True)
                 torch.cuda.synchronize()
                 assert_bitwise(to_host(out2), want[rank], f"[{tag}] g={g} w={w} s={s} backward layer")
+                go2.check(f"[{tag}] g={g} w={w} s={s} backward layer")
+                gc.check(f"[{tag}] g={g} w={w} s={s} backward: secondary codes")
             except AssertionError as e:
                 errors.append(str(e))
 
@@ -83,11 +98,15 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             bpl = [bits1] + [4] * (L - 1)
             p = ctx.partition(numel, B, 1, 1, L)
             want = col.reduce_scatter(grads, g, Np, B, 1, L, {l: bpl[l - 1] for l in range(1, L + 1)})
-            shard = torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")
-            ctx.reduce_scatter_grads(p, to_dev(grads[rank]), shard, bpl)
+            gsh = Guarded(p.range(L)[1], torch.float32)
+            shard = gsh.t
+            grad_in = to_dev(grads[rank])
+            ctx.reduce_scatter_grads(p, grad_in, shard, bpl)
             torch.cuda.synchronize()
             try:
                 assert_bitwise(to_host(shard), want[rank], f"[{tag}] g={g} qgZ bits={bpl}")
+                gsh.check(f"[{tag}] g={g} qgZ bits={bpl} shard")
+                assert_unchanged(grad_in, grads[rank], f"[{tag}] g={g} qgZ bits={bpl} gradient")
             except AssertionError as e:
                 errors.append(str(e))
             # accumulate into the shard (A = fl(A + P)): second micro-batch
@@ -142,10 +161,13 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             want_prim = optim.post_update_allgather({q: upd[q][0].astype(ml_dtypes.bfloat16) for q in range(world)},
                                                     g, Np, w)
             th_d, m_d, v_d, g_d = (to_dev(a.copy()) for a in th0[rank])
-            prim = torch.zeros(nw, dtype=torch.bfloat16, device="cuda")
+            gpr = Guarded(nw, torch.bfloat16)
+            prim = gpr.t
             ctx.adamw_step(p, g_d, th_d, m_d, v_d, hz.adamw_params(1e-3, 0.9, 0.95, 1e-8, 0.1, 3), prim)
             torch.cuda.synchronize()
             try:
+                gpr.check(f"[{tag}] g={g} w={w} post-update primary")
+                assert_unchanged(g_d, th0[rank][3], f"[{tag}] g={g} w={w} adamw gradient")
                 assert_bitwise(to_host(th_d), upd[rank][0], f"[{tag}] g={g} w={w} adamw master")
                 assert_bitwise(to_host(m_d), upd[rank][1], f"[{tag}] g={g} w={w} adamw m")
                 assert_bitwise(to_host(v_d), upd[rank][2], f"[{tag}] g={g} w={w} adamw v")
