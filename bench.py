@@ -43,7 +43,8 @@ HIERARCHY = {
     "gpt6.7b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
     "neox20b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
 }
-KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "quantize_dequantize", "reduce", "reduce_requant")
+KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "quantize_dequantize", "reduce", "reduce_requant",
+                "quantize_push", "reduce_push", "ag_fused", "rs_fused")
 NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
 

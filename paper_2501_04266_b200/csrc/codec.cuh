@@ -272,10 +272,46 @@ struct NoEmit {
   __device__ __forceinline__ void operator()(int64_t, int, const float (&)[8]) const {}
 };
 
-template <int B, int BITS, int U, class Emit = NoEmit>
+// Push targets (PushDst, hz_internal.h): NoPush compiles to nothing.
+struct NoPush {
+  static constexpr bool on = false;
+  template <int BITS>
+  __device__ __forceinline__ void put(int64_t, const Codes8<BITS>&) const {}
+  template <int B>
+  __device__ __forceinline__ void put_scale(int64_t, float) const {}
+};
+
+struct Push {
+  static constexpr bool on = true;
+  PushDst d;
+  template <int BITS>
+  __device__ __forceinline__ void put(int64_t e, const Codes8<BITS>& v) const {
+    if (d.scatter) {
+      const int j = static_cast<int>(e / d.seg);
+      const int64_t r = e - j * d.seg;
+      if (d.lim <= 0 || r < d.lim) v.store(d.c[j] + r * BITS / 8);
+    } else if (d.lim <= 0 || e < d.lim) {
+      for (int j = 0; j < d.n; ++j) v.store(d.c[j] + e * BITS / 8);
+    }
+  }
+  template <int B>
+  __device__ __forceinline__ void put_scale(int64_t blk, float s) const {
+    if (d.scatter) {
+      const int64_t sb = d.seg / B;
+      const int j = static_cast<int>(blk / sb);
+      const int64_t r = blk - j * sb;
+      if (d.lim <= 0 || r * B < d.lim) d.s[j][r] = s;
+    } else if (d.lim <= 0 || blk * B < d.lim) {
+      for (int j = 0; j < d.n; ++j) d.s[j][blk] = s;
+    }
+  }
+};
+
+template <int B, int BITS, int U, class Emit = NoEmit, class P = NoPush>
 __device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB][8], const float (&am)[U],
                                                int64_t blk0, int lane, uint8_t* __restrict__ codes,
-                                               float* __restrict__ scales, const Emit& emit = Emit{}) {
+                                               float* __restrict__ scales, const Emit& emit = Emit{},
+                                               const P& push = P{}) {
   using G = Geo<B>;
   constexpr int NB = U * G::BPW;
   static_assert(NB <= 32, "one block per lane at most");
@@ -289,8 +325,11 @@ __device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB]
   }
   float scale, inv;
   quant_params<BITS>(mine, scale, inv);
-  // codes == nullptr (round trip only, nobody reads the codes): skip code/scale stores
+  // codes == nullptr (round trip / push only): no local code / scale stores
   if (codes && lane < NB) scales[blk0 + lane] = scale;
+  if constexpr (P::on) {
+    if (lane < NB) push.template put_scale<B>(blk0 + lane, scale);
+  }
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const float iv = __shfl_sync(kFull, inv, u * G::BPW + lb);
@@ -301,10 +340,11 @@ __device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB]
       unsigned b[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) b[i] = qbits(v[u][k][i], iv);
-      if (!Emit::on || codes) {
+      if (codes || P::on) {
         Codes8<BITS> out;
         out.set(b);
-        out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
+        if (codes) out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
+        if constexpr (P::on) push.template put<BITS>(blk * B + k * G::SUBSTRIDE + ll * 8, out);
       }
       if constexpr (Emit::on) {
         float xh[8];
@@ -443,8 +483,10 @@ __device__ __forceinline__ void sync_signal(const SyncArgs& s) {
   if (threadIdx.x == 0) {
     // gpu-scope release per CTA (peers read this GPU's memory through its L2, the
     // point of coherence for gpu scope); the last CTA then publishes with a
-    // system-scope release, cumulative over everything it has observed.
-    __threadfence();
+    // system-scope release, cumulative over everything it has observed.  Kernels
+    // that stored into peer memory fence at system scope.
+    if (s.sysfence) __threadfence_system();
+    else __threadfence();
     if (s.stamps && atomicAdd(s.stamps + 4, 1ull) == gridDim.x - 1ull) {
       s.stamps[2] = globaltimer();
       s.stamps[4] = 0ull;   // graph replays reuse the slot

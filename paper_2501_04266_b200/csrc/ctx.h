@@ -42,19 +42,26 @@ struct hz_ctx {
     Slot ag_prim_c, ag_prim_s;                  // quantized primary when s != w
     Slot rs_c[HZ_MAX_LEVELS + 1], rs_s[HZ_MAX_LEVELS + 1];   // level-l send buffers
     Slot upd;                                   // updated weights of range_L (step tail)
+    // push mode: receive buffers the producers store into over NVLink
+    Slot ag_recv_c, ag_recv_s;                  // forward gather: D pieces of the primary codes
+    Slot rs_recv_c[HZ_MAX_LEVELS + 1], rs_recv_s[HZ_MAX_LEVELS + 1];   // level-l: g chunks destined here
   } p2p;
 };
 
 namespace hz {
 
 // header of the symmetric pool: ready[8] u64 | done[8] u64 | counter u32 | epoch u64 |
-// fused-kernel work counters | per-chunk flags of the fused all-gather [8][kMaxChunks]
-// and of the fused reduce-scatter [16][kMaxChunks]
+// pipelined-kernel ticket counters | per-chunk flags of the pipelined all-gather
+// [8][kMaxChunks] and reduce-scatter [16][kMaxChunks] | per-chunk producer arrival
+// counters (u32 [kMaxChunks] each)
 constexpr size_t kReadyOff = 0, kDoneOff = 64, kCounterOff = 128, kEpochOff = 192;
 constexpr size_t kWorkAGOff = 256, kWorkRSOff = 320;
 constexpr size_t kChunkAGOff = 4096;
 constexpr size_t kChunkRSOff = kChunkAGOff + size_t(kMaxWorld) * kMaxChunks * 8;
-constexpr size_t kPoolHeader = kChunkRSOff + size_t(kMaxG) * kMaxChunks * 8;
+constexpr size_t kCntAGOff = kChunkRSOff + size_t(kMaxG) * kMaxChunks * 8;
+constexpr size_t kCntRSOff = kCntAGOff + size_t(kMaxChunks) * 4;
+constexpr size_t kDbgOff = kCntRSOff + size_t(kMaxChunks) * 4;   // HZ_TUNE pdbg timelines [kMaxChunks][4]
+constexpr size_t kPoolHeader = kDbgOff + size_t(kMaxChunks) * 32;
 
 hz_status cuda_fail(cudaError_t e, const char* what);
 hz_status nccl_fail(ncclResult_t r, const char* what);
@@ -73,6 +80,13 @@ hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int6
                      int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
                      cudaStream_t st, int level, const SyncArgs* sync = nullptr,
                      int64_t remote_bytes = 0);
+// push kernels (P2P): `remote` = bytes stored into peer memory per launch
+hz_status run_quantize_push(const void* x, hz_dtype dt, int64_t n, int bits, uint8_t* c, float* s, void* y,
+                            hz_dtype odt, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
+                            int64_t remote);
+hz_status run_reduce_push(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
+                          int bits_out, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
+                          int64_t remote);
 hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
 
 // P2P transport (p2p.cpp)

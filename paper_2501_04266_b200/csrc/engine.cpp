@@ -159,6 +159,31 @@ hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int6
   return HZ_OK;
 }
 
+hz_status run_quantize_push(const void* x, hz_dtype dt, int64_t n, int bits, uint8_t* c, float* s, void* y,
+                            hz_dtype odt, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
+                            int64_t remote) {
+  const int64_t local = n * elem_bytes(dt) + (c ? code_bytes(n, bits) + n / 256 * 4 : 0) + (y ? n * elem_bytes(odt) : 0);
+  TraceScope t(st, "quantize_push", level, bits, n, local, remote);
+  SyncArgs sy = sync ? *sync : SyncArgs{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_quantize_push(x, dt, n, bits, c, s, y, odt, dst, st, &sy);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "quantize-push kernel launch");
+  return HZ_OK;
+}
+
+hz_status run_reduce_push(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
+                          int bits_out, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
+                          int64_t remote) {
+  TraceScope t(st, "reduce_push", level, bits_in, n, g * (code_bytes(n, bits_in) + n / 256 * 4), remote);
+  SyncArgs sy = sync ? *sync : SyncArgs{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_reduce_push(g, c, s, n, bits_in, bits_out, dst, st, &sy);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "reduce-push kernel launch");
+  return HZ_OK;
+}
+
 hz_status run_roundtrip(const void* x, hz_dtype dt, int64_t n, int bits, int block, uint8_t* c, float* s,
                         void* y, hz_dtype odt, int acc, cudaStream_t st, int level) {
   const int64_t out = n * elem_bytes(odt) * (acc ? 2 : 1);

@@ -39,6 +39,7 @@ struct SyncArgs {
   unsigned en;   // kWaitReady | kWaitDone | kSigReady | kSigDone
   unsigned long long* stamps;   // optional [8]: entry, after wait, last-CTA arrival, flags sent (ns), counter
   int mode;                     // publication fence variant (HZ_TUNE p2p_sig; 0 = fence.sc.sys)
+  int sysfence;                 // per-CTA fence at system scope (kernels that store into peer memory)
 };
 
 // Pieces of a gathered layer for the fused gather+dequantize kernel: piece j
@@ -54,6 +55,11 @@ struct Pieces {
   uint8_t* sec_c;
   float* sec_s;
   int64_t sec_lo, sec_hi;
+  // hybrid push/pull: elements [0, split) of piece j come from cr[j] / sr[j] (local
+  // receive buffer) when cr[j] is set
+  const uint8_t* cr[kMaxWorld];
+  const float* sr[kMaxWorld];
+  int64_t split;
 };
 
 // ----------------------------------------------------------------- kernels
@@ -74,6 +80,30 @@ cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, int64_t
 cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,
                                      hz_dtype out_dt, cudaStream_t st, const SyncArgs* sync);
 constexpr int kMaxG = 16;
+
+// Push destinations of the P2P push kernels (quantize / requantize that store their
+// codes straight into the consumers' receive buffers over NVLink).  The codes and
+// scales of element e go, besides the local buffers (if any), to every c[j] + e
+// (mirror), or only to segment j = e / seg at c[j] + (e - j*seg) (scatter).
+struct PushDst {
+  uint8_t* c[kMaxG];
+  float* s[kMaxG];
+  int64_t seg;      // scatter segment in elements (a multiple of the block)
+  int n;
+  int scatter;
+  int64_t lim;      // > 0: only elements whose offset (within the segment) is < lim
+};
+// Push variants (P2P transport, block 256): codes / scales also (or only, when
+// codes == nullptr) stored to `dst` (peer receive buffers); y (optional) = the own
+// round trip x_hat.  The per-CTA release fences at system scope.
+cudaError_t launch_quantize_push(const void* x, hz_dtype dt, int64_t n, int bits, uint8_t* codes, float* scales,
+                                 void* y, hz_dtype out_dt, const PushDst& dst, cudaStream_t st,
+                                 const SyncArgs* sync);
+bool push_reduce_supported(int g, int block);
+cudaError_t launch_reduce_push(int g, const uint8_t* const* codes, const float* const* scales, int64_t n,
+                               int bits_in, int bits_out, const PushDst& dst, cudaStream_t st,
+                               const SyncArgs* sync);
+
 cudaError_t launch_epoch_advance(unsigned long long* epoch, unsigned long long span, cudaStream_t st);
 cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
                           int64_t n, int bits_in, int block, int bits_out, uint8_t* out_codes,
@@ -105,6 +135,8 @@ struct FusedAGArgs {
   unsigned long long* flags;
   unsigned long long* flags_remote[kMaxWorld];
   unsigned long long* work;
+  unsigned int* cnt;      // per-chunk producer arrival counters (local, zero between launches)
+  unsigned long long* dbg;   // optional per-chunk timeline (HZ_TUNE pdbg)
   void* y;
   hz_dtype out_dt;
   unsigned long long phase;
@@ -124,6 +156,7 @@ struct FusedRSArgs {
   unsigned long long* flags;
   unsigned long long* flags_remote[kMaxG];
   unsigned long long* work;
+  unsigned int* cnt;
   float* of;
   uint8_t* oc;
   float* os;

@@ -60,8 +60,9 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
           for (int q = 1; q < pc.n; ++q) j += e >= q * pc.len;   // piece of this unit
         }
         const int64_t r = e - j * pc.len;
-        raw[u].load(pc.c[j] + r * BITS / 8);
-        sc[u] = __ldg(pc.s[j] + (r >> log2b));
+        const bool head = r < pc.split && pc.cr[j] != nullptr;   // pushed head: local receive buffer
+        raw[u].load((head ? pc.cr[j] : pc.c[j]) + r * BITS / 8);
+        sc[u] = __ldg((head ? pc.sr[j] : pc.s[j]) + (r >> log2b));
       }
     }
 #pragma unroll

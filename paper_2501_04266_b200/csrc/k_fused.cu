@@ -1,41 +1,49 @@
-// Fused codec + NVLink collective kernels (P2P transport, B = 256): one launch per
-// collective call in which production (quantize) and consumption (peer loads +
-// dequantize / reduce) overlap chunk by chunk.
+// Pipelined codec + NVLink collective kernels (P2P transport, B = 256): ONE launch
+// per collective call in which production (quantize, HBM-bound) and consumption
+// (peer loads + dequantize / reduce, NVLink-bound) run at the same time on
+// different CTAs, chunk by chunk.
 //
-//   k_ag_fused   qwZ forward all-gather (A2 + A3 + A5): quantize the
-//                own primary into the peer-readable buffer, publish per-chunk
-//                ready flags to every member, and dequantize every member's
-//                chunks (read straight from its pool over NVLink) into the layer.
-//   k_rs_fused   first qgZ level (A7 + A8 + A9): quantize the own
-//                gradient chunk by chunk (chunks for all destinations interleaved),
-//                publish each chunk's flag to its destination member, and reduce
-//                the members' chunks destined to this rank (ascending digit, fp32,
-//                no FMA) into the fp32 shard or the next level's requantized buffer.
+//   k_ag_pipe   qwZ forward all-gather (A2 + A3 + A5): producers
+//               quantize the own primary into the peer-readable buffer chunk by
+//               chunk and publish each chunk to every member; consumers dequantize
+//               every member's chunk c (read straight from its pool over NVLink)
+//               into the layer as soon as chunk c is published everywhere.
+//   k_rs_pipe   first qgZ level (A7 + A8 + A9): producers quantize
+//               the own gradient chunk c for every destination (int4/int8) and
+//               publish it to its destination; consumers reduce the members' chunk
+//               c destined here (ascending digit, fp32, no FMA) into the fp32 shard
+//               or the next level's requantized send buffer.
 //
-// STATUS: experimental, off by default (HZ_TUNE fused=1).  Measured on 2 B200s at
-// GPT-1.3B layer size these are slower than the two-kernel P2P path (74 vs 59 µs
-// for the forward gather, 83 vs 49 µs for the qgZ level): a work item is one
-// 32K-element chunk processed by one CTA, and that serialisation costs more than
-// the overlap gains.  Kept (and parity-tested with fused=1) for a finer-grained
-// interleaved design.
+// Roles: every CTA takes a ticket (atomicAdd on a local counter) at entry; the
+// first Gp tickets are producers, the rest consumers.  A consumer only ever waits
+// for chunks whose producers hold a ticket already (here and on every peer, since
+// producers never wait), so the waits make progress however many CTAs are
+// resident.  Within a role, CTAs stride over the chunk as one grid (virtual warp
+// index = ticket * warps + warp), with the warp-level access pattern of the
+// two-kernel path (k_quantize / k_dequantize / k_reduce).
 //
-// Work distribution: persistent CTAs take work items from a global counter —
-// first every production item, then the consumption items (remote pieces before
-// the own one).  A consumption item waits (thread 0, ld.acquire.sys) for the
-// chunk flags it needs; every item a CTA waits for has already been taken by a
-// running CTA (here or on the producing peer), so the waits always make progress
-// and no co-residency of the whole grid is required.  The whole call is one phase
-// of the P2P protocol (codec.cuh): prologue waits until every rank is done with the
-// previous phase; the last CTA publishes done (and, with requantization, ready for
-// the next level).  Chunk flags hold the phase number (relative to the graph epoch).
+// Chunk publication: a producer CTA finishing its part of chunk c fences (gpu
+// scope) and increments the chunk's local arrival counter; the CTA completing the
+// count issues fence.acq_rel.sys and stores the phase number into every member's
+// flag for (this rank, c) — the cumulative last-CTA publication of the phase
+// protocol in codec.cuh.  Flags hold the phase number relative to the graph epoch,
+// so they never need resetting; the arrival counters and the ticket counter are
+// reset by the last CTA of the launch.  The whole call is one phase: the prologue
+// waits until every rank is done with the previous phase, the last CTA signals
+// done(phase).
+//
+// Results are bit-identical to the two-kernel path (same per-block arithmetic,
+// same summation order).  Selected with HZ_TUNE fused=1 (pf = producer share of
+// the grid in %, pk = target chunks per call).
 #include "codec.cuh"
 
 namespace hz {
 namespace {
 
 using namespace dev;
-constexpr int kB = 256;                 // block size of the fused kernels
+constexpr int kB = 256;                 // block size of the pipelined kernels
 constexpr int kWarps = kThreads / 32;
+constexpr int kU = 4;                   // blocks (quantize) / 32-unit steps (consume) per warp item
 
 struct FusedAG {
   const void* x;                        // own primary, plen elements
@@ -46,9 +54,12 @@ struct FusedAG {
   int D, me;
   int64_t plen, C;
   int nch;
+  int gp;                               // producer CTAs
   unsigned long long* flags;            // local [kMaxWorld][kMaxChunks]: flag[j][c] set by member j
   unsigned long long* flags_remote[kMaxWorld];   // &flag[me][0] in member j's pool
-  unsigned long long* work;             // [0] work counter, [1] arrival counter (local)
+  unsigned long long* work;             // [0] ticket counter, [1] exit counter (local)
+  unsigned int* cnt;                    // [nch] producer arrivals per chunk (local)
+  unsigned long long* dbg;              // optional timeline [c][4]: publish, first consumer start, last consumer end
   void* y;                              // the layer, D * plen elements
   unsigned long long phase;             // relative to *epoch
   const unsigned long long* epoch;
@@ -58,14 +69,16 @@ struct FusedRS {
   const void* x;                        // own input over range_{l-1}: g * cl elements
   uint8_t* qc;                          // own send buffer (peer-readable)
   float* qs;
-  const uint8_t* mc[kMaxG];             // member j's send buffer at the chunk destined to me
+  const uint8_t* mc[kMaxG];             // member j's send buffer at the slice destined to me
   const float* ms[kMaxG];
   int g, d, bits_out, acc;
   int64_t cl, C;
-  int ncl;                              // chunks per destination
+  int ncl;
+  int gp;
   unsigned long long* flags;            // local [kMaxG][kMaxChunks]: flag[j][c] set by member j
   unsigned long long* flags_remote[kMaxG];       // &flag[d][0] in member j's pool
   unsigned long long* work;
+  unsigned int* cnt;
   float* of;                            // fp32 output (bits_out == 0)
   uint8_t* oc;                          // requantized output (bits_out 4 / 8)
   float* os;
@@ -73,302 +86,245 @@ struct FusedRS {
   const unsigned long long* epoch;
 };
 
-__device__ __forceinline__ long long grab(unsigned long long* work) {
-  __shared__ long long s_item;
-  if (threadIdx.x == 0) s_item = static_cast<long long>(atomicAdd(work, 1ull));
+__device__ __forceinline__ int take_ticket(unsigned long long* work) {
+  __shared__ int s_t;
+  if (threadIdx.x == 0) s_t = static_cast<int>(atomicAdd(work, 1ull));
   __syncthreads();
-  const long long it = s_item;
-  __syncthreads();
-  return it;
+  return s_t;
 }
 
-__device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long target) {
+// flags f[j * kMaxChunks] >= target for j < n (thread 0 spins, the CTA waits)
+__device__ __forceinline__ void wait_flags(const unsigned long long* f, int n, unsigned long long target) {
   if (threadIdx.x == 0) {
     const unsigned long long t0 = globaltimer();
-    while (ld_acquire_sys(f) < target)
-      if (globaltimer() - t0 > 20000000000ull) __trap();
+    for (int j = 0; j < n; ++j)
+      while (ld_acquire_sys(f + static_cast<int64_t>(j) * kMaxChunks) < target)
+        if (globaltimer() - t0 > 20000000000ull) __trap();
   }
   __syncthreads();
 }
 
-__device__ __forceinline__ void publish(unsigned long long* const* dst, int n, int64_t idx,
-                                        unsigned long long v) {
+// producer CTA done with chunk c: the last of the gp producers publishes it
+__device__ __forceinline__ void arrive(unsigned int* cnt, int c, int gp, unsigned long long* const* dst, int n,
+                                       unsigned long long v, unsigned long long* dbg = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
-    for (int j = 0; j < n; ++j) st_relaxed_sys(dst[j] + idx, v);
+    if (atomicAdd(cnt + c, 1u) == static_cast<unsigned>(gp) - 1u) {
+      if (dbg) dbg[c * 4 + 3] = globaltimer();
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int j = 0; j < n; ++j) st_relaxed_sys(dst[j] + c, v);
+      if (dbg) dbg[c * 4 + 0] = globaltimer();
+    }
   }
 }
 
-__device__ __forceinline__ void finish(unsigned long long* work) {
-  // the last CTA resets the work counter for the next launch
+// the last CTA of the launch resets the ticket / exit / chunk counters
+__device__ __forceinline__ void finish(unsigned long long* work, unsigned int* cnt, int nch) {
+  __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(work + 1, 1ull) == gridDim.x - 1ull) {
+    s_last = atomicAdd(work + 1, 1ull) == gridDim.x - 1ull;
+  }
+  __syncthreads();
+  if (s_last) {
+    for (int c = threadIdx.x; c < nch; c += kThreads) cnt[c] = 0u;
+    if (threadIdx.x == 0) {
       work[0] = 0ull;
       work[1] = 0ull;
-      __threadfence();
     }
+    __threadfence();
   }
 }
 
-// Quantize elements [e0, e0 + n) of x (n a multiple of 1024) into codes / scales at
-// the same offsets: warp iterations of 4 blocks, one division per block.
-template <typename T, int BITS>
-__device__ __forceinline__ void cta_quantize(const T* __restrict__ x, int64_t e0, int64_t n,
-                                             uint8_t* __restrict__ codes, float* __restrict__ scales) {
-  constexpr int U = 4;
+// one warp item: quantize the U blocks starting at block blk0 (codes / scales at
+// the same block offsets)
+template <typename T, int BITS, int U = kU>
+__device__ __forceinline__ void quantize_item(const T* __restrict__ x, int64_t blk0, uint8_t* __restrict__ codes,
+                                              float* __restrict__ scales) {
   const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  for (int64_t it = w; it < n / (kB * U); it += kWarps) {
-    const int64_t blk0 = (e0 / kB) + it * U;
-    In8<T> raw[U][1];
+  In8<T> raw[U][1];
 #pragma unroll
-    for (int u = 0; u < U; ++u) raw[u][0].load(x + (blk0 + u) * kB + lane * 8);
-    float v[U][1][8];
-    float am[U];
+  for (int u = 0; u < U; ++u) raw[u][0].load(x + (blk0 + u) * kB + lane * 8);
+  float v[U][1][8];
+  float am[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      raw[u][0].get(v[u][0]);
-      float m = 0.f;
+  for (int u = 0; u < U; ++u) {
+    raw[u][0].get(v[u][0]);
+    float m = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(v[u][0][i]));
-      am[u] = group_max<32>(m);
-    }
-    quantize_store<kB, BITS, U>(v, am, blk0, lane, codes, scales);
+    for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(v[u][0][i]));
+    am[u] = group_max<32>(m);
   }
+  quantize_store<kB, BITS, U>(v, am, blk0, lane, codes, scales);
 }
 
-// Dequantize n elements (multiple of 8) from codes / scales (maybe peer memory) to y.
-template <int BITS, typename TO>
-__device__ __forceinline__ void cta_dequantize(const uint8_t* __restrict__ codes, const float* __restrict__ scales,
-                                               int64_t n, TO* __restrict__ y) {
-  constexpr int U = 4;
-  const int64_t nunits = n / 8;
-  for (int64_t base = threadIdx.x; base < nunits; base += kThreads * U) {
-    Codes8<BITS> raw[U];
-    float sc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t unit = base + u * kThreads;
-      if (unit < nunits) {
-        raw[u].load(codes + unit * BITS);
-        sc[u] = __ldg(scales + (unit * 8) / kB);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t unit = base + u * kThreads;
-      if (unit < nunits) {
-        float c[8], v[8];
-        raw[u].decode(c);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = __fmul_rn(c[i], sc[u]);
-        Out8<TO>::store(y + unit * 8, v);
-      }
-    }
-  }
-}
-
+// ------------------------------------------------------------------------ AG
 template <typename T, int BITS, typename TO>
-__global__ void __launch_bounds__(kThreads) k_ag_fused(const __grid_constant__ FusedAG a,
-                                                       const __grid_constant__ SyncArgs sy) {
-  sync_wait(sy);   // every rank is done with the previous phase: our buffer is free
+__global__ void __launch_bounds__(kThreads) k_ag_pipe(const __grid_constant__ FusedAG a,
+                                                      const __grid_constant__ SyncArgs sy) {
+  sync_wait(sy);   // every rank is done with the previous phase: our buffers are free
   const unsigned long long target = a.phase + (a.epoch ? *a.epoch : 0ull);
-  const long long nprod = a.nch;
-  const long long nremote = static_cast<long long>(a.D - 1) * a.nch;
-  const long long ntotal = nprod + nremote + a.nch;
-  for (;;) {
-    const long long item = grab(a.work);
-    if (item >= ntotal) break;
-    if (item < nprod) {                                   // produce own chunk
-      const int64_t e0 = item * a.C;
-      const int64_t n = min(a.C, a.plen - e0);
-      cta_quantize<T, BITS>(static_cast<const T*>(a.x), e0, n, a.qc, a.qs);
-      publish(a.flags_remote, a.D, item, target);
-    } else {                                              // consume a member's chunk
-      long long k = item - nprod;
-      int piece;
-      int64_t c;
-      if (k < nremote) {
-        const int jj = static_cast<int>(k / a.nch);
-        piece = jj < a.me ? jj : jj + 1;
-        c = k % a.nch;
-      } else {
-        piece = a.me;
-        c = k - nremote;
-      }
-      wait_flag(a.flags + static_cast<int64_t>(piece) * kMaxChunks + c, target);
+  const int ticket = take_ticket(a.work);
+  const int w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (a.dbg && ticket == 0 && threadIdx.x == 0) a.dbg[(kMaxChunks - 1) * 4] = globaltimer();
+  if (ticket < a.gp) {                                    // producer
+    const int64_t stride = static_cast<int64_t>(a.gp) * kWarps;
+    const int64_t vw = static_cast<int64_t>(ticket) * kWarps + w;
+    for (int c = 0; c < a.nch; ++c) {
       const int64_t e0 = c * a.C;
-      const int64_t n = min(a.C, a.plen - e0);
-      cta_dequantize<BITS, TO>(a.pc[piece] + e0 * BITS / 8, a.ps[piece] + e0 / kB, n,
-                               static_cast<TO*>(a.y) + piece * a.plen + e0);
+      const int64_t nit = min(a.C, a.plen - e0) / (kB * kU);
+      for (int64_t it = vw; it < nit; it += stride)
+        quantize_item<T, BITS>(static_cast<const T*>(a.x), e0 / kB + it * kU, a.qc, a.qs);
+      arrive(a.cnt, c, a.gp, a.flags_remote, a.D, target, a.dbg);
+    }
+  } else {                                                // consumer
+    const int64_t gc = static_cast<int64_t>(gridDim.x) - a.gp;
+    const int64_t vw = static_cast<int64_t>(ticket - a.gp) * kWarps + w;
+    const int64_t stride = gc * kWarps;
+    TO* y = static_cast<TO*>(a.y);
+    for (int c = 0; c < a.nch; ++c) {
+      wait_flags(a.flags + c, a.D, target);               // chunk c published by every member
+      if (a.dbg && threadIdx.x == 0) atomicMin(a.dbg + c * 4 + 1, globaltimer());
+      const int64_t e0 = c * a.C;
+      const int64_t nt = min(a.C, a.plen - e0) / (256 * kU);   // warp tiles per piece
+      // tiles interleave the pieces: local (HBM) and peer (NVLink) tiles in flight together
+      for (int64_t t = vw; t < nt * a.D; t += stride) {
+        const int j = static_cast<int>((t + a.me + 1) % a.D);
+        const int64_t eb = e0 + (t / a.D) * (256 * kU);
+        Codes8<BITS> raw[kU];
+        float sc[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int64_t e = eb + (u * 32 + lane) * 8;
+          raw[u].load(a.pc[j] + e * BITS / 8);
+          sc[u] = __ldg(a.ps[j] + e / kB);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int64_t e = eb + (u * 32 + lane) * 8;
+          float cd[8], v[8];
+          raw[u].decode(cd);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = __fmul_rn(cd[i], sc[u]);
+          Out8<TO>::store(y + j * a.plen + e, v);
+        }
+      }
+      if (a.dbg) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(a.dbg + c * 4 + 2, globaltimer());
+      }
     }
   }
-  finish(a.work);
+  finish(a.work, a.cnt, a.nch);
   sync_signal(sy);   // done(phase)
 }
 
 // ------------------------------------------------------------------------ RS
-// Reduce n elements (multiple of 256) of GT inputs into fp32 (staged, coalesced).
-template <int BIN, int GT>
-__device__ __forceinline__ void cta_reduce_f32(const FusedRS& a, int64_t off, int64_t n, float4* stage) {
-  constexpr int E = 64 / BIN;
-  constexpr int G = E / 4;
-  constexpr int U = 2;                                  // warp chunks in flight per warp
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const int64_t nunits = n / E;                         // a multiple of 32 * U * kWarps
-  float4* st = stage + w * 32 * G;
-  for (int64_t base0 = w * 32 * U; base0 < nunits; base0 += kThreads * U) {
-  uint2 rawu[U][GT];
-  float scu[U][GT];
-#pragma unroll
-  for (int u = 0; u < U; ++u)
-#pragma unroll
-    for (int p = 0; p < GT; ++p) {
-      const int64_t unit = base0 + u * 32 + lane;
-      rawu[u][p] = __ldg(reinterpret_cast<const uint2*>(a.mc[p] + (off / E + unit) * 8));
-      scu[u][p] = __ldg(a.ms[p] + (off + unit * E) / kB);
-    }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t base = base0 + u * 32;
-    float acc[E];
-    const uint2 (&raw)[GT] = rawu[u];
-    const float (&sc)[GT] = scu[u];
-#pragma unroll
-    for (int p = 0; p < GT; ++p) {
-      float c[E];
-      if constexpr (BIN == 8) {
-        Codes8<8> cc;
-        cc.r = raw[p];
-        cc.decode(c);
-      } else {
-        Codes8<4> lo, hi;
-        lo.r = raw[p].x;
-        hi.r = raw[p].y;
-        float t0[8], t1[8];
-        lo.decode(t0);
-        hi.decode(t1);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          c[i] = t0[i];
-          c[8 + i] = t1[i];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const float xh = __fmul_rn(c[i], sc[p]);
-        acc[i] = p == 0 ? xh : __fadd_rn(acc[i], xh);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const int gi = lane * G + j;
-      st[gi ^ ((gi >> 3) & (G - 1))] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-      const int gi = k * 32 + lane;
-      float4 o = st[gi ^ ((gi >> 3) & (G - 1))];
-      float4* dst = reinterpret_cast<float4*>(a.of + off) + base * G + gi;
-      if (a.acc) {
-        const float4 old = *dst;
-        o.x = __fadd_rn(old.x, o.x);
-        o.y = __fadd_rn(old.y, o.y);
-        o.z = __fadd_rn(old.z, o.z);
-        o.w = __fadd_rn(old.w, o.w);
-      }
-      *dst = o;
-    }
-    __syncwarp();
-  }
-  }
-}
-
-// Reduce + requantize n elements (multiple of 1024) of GT inputs into oc / os at off.
-template <int BIN, int BOUT, int GT>
-__device__ __forceinline__ void cta_reduce_requant(const FusedRS& a, int64_t off, int64_t n) {
-  constexpr int U = 4;
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  for (int64_t it = w; it < n / (kB * U); it += kWarps) {
-    const int64_t blk0 = off / kB + it * U;
-    float v[U][1][8];
-    float am[U];
-    Codes8<BIN> raw[U][GT];
-    float sc[U][GT];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int p = 0; p < GT; ++p) {
-        raw[u][p].load(a.mc[p] + ((blk0 + u) * kB + lane * 8) * BIN / 8);
-        sc[u][p] = __ldg(a.ms[p] + blk0 + u);
-      }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      float c[8];
-#pragma unroll
-      for (int p = 0; p < GT; ++p) {
-        raw[u][p].decode(c);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float xh = __fmul_rn(c[i], sc[u][p]);
-          v[u][0][i] = p == 0 ? xh : __fadd_rn(v[u][0][i], xh);
-        }
-      }
-      float m = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(v[u][0][i]));
-      am[u] = group_max<32>(m);
-    }
-    quantize_store<kB, BOUT, U>(v, am, blk0, lane, a.oc, a.os);
-  }
-}
-
 template <typename T, int BIN, int BOUT, int GT>
-__global__ void __launch_bounds__(kThreads) k_rs_fused(const __grid_constant__ FusedRS a,
-                                                       const __grid_constant__ SyncArgs sy) {
-  __shared__ float4 stage[BOUT == 0 ? kThreads / 32 * 32 * (16 / BIN) : 1];
+__global__ void __launch_bounds__(kThreads) k_rs_pipe(const __grid_constant__ FusedRS a,
+                                                      const __grid_constant__ SyncArgs sy) {
   sync_wait(sy);
   const unsigned long long target = a.phase + (a.epoch ? *a.epoch : 0ull);
-  const long long nprod = static_cast<long long>(a.g) * a.ncl;
-  const long long ntotal = nprod + a.ncl;
-  for (;;) {
-    const long long item = grab(a.work);
-    if (item >= ntotal) break;
-    if (item < nprod) {   // produce: destinations interleaved so every member's chunks come early
-      const int dest = static_cast<int>(item % a.g);
-      const int64_t c = item / a.g;
-      const int64_t e0 = dest * a.cl + c * a.C;
-      const int64_t n = min(a.C, a.cl - c * a.C);
-      cta_quantize<T, BIN>(static_cast<const T*>(a.x), e0, n, a.qc, a.qs);
-      publish(a.flags_remote + dest, 1, c, target);
-    } else {
-      const int64_t c = item - nprod;
-      for (int j = 0; j < GT; ++j) wait_flag(a.flags + static_cast<int64_t>(j) * kMaxChunks + c, target);
+  const int ticket = take_ticket(a.work);
+  const int w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (ticket < a.gp) {                                    // producer: chunk c for every destination
+    const int64_t stride = static_cast<int64_t>(a.gp) * kWarps;
+    const int64_t vw = static_cast<int64_t>(ticket) * kWarps + w;
+    for (int c = 0; c < a.ncl; ++c) {
       const int64_t off = c * a.C;
-      const int64_t n = min(a.C, a.cl - off);
-      if constexpr (BOUT == 0) cta_reduce_f32<BIN, GT>(a, off, n, stage);
-      else cta_reduce_requant<BIN, BOUT, GT>(a, off, n);
+      const int64_t nit = min(a.C, a.cl - off) / (kB * kU);   // warp items per destination
+      for (int64_t t = vw; t < nit * GT; t += stride) {
+        const int dest = static_cast<int>(t % GT);
+        quantize_item<T, BIN>(static_cast<const T*>(a.x), (dest * a.cl + off) / kB + (t / GT) * kU, a.qc, a.qs);
+      }
+      arrive(a.cnt, c, a.gp, a.flags_remote, GT, target);   // flag row d in member j's pool
+    }
+  } else {                                                // consumer: reduce chunk c destined here
+    const int64_t gc = static_cast<int64_t>(gridDim.x) - a.gp;
+    const int64_t vw = static_cast<int64_t>(ticket - a.gp) * kWarps + w;
+    const int64_t stride = gc * kWarps;
+    for (int c = 0; c < a.ncl; ++c) {
+      wait_flags(a.flags + c, GT, target);
+      const int64_t off = c * a.C;
+      const int64_t nit = min(a.C, a.cl - off) / (kB * kU);
+      for (int64_t it = vw; it < nit; it += stride) {
+        const int64_t blk0 = off / kB + it * kU;
+        Codes8<BIN> raw[kU][GT];
+        float sc[kU][GT];
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+          for (int p = 0; p < GT; ++p) {
+            raw[u][p].load(a.mc[p] + ((blk0 + u) * kB + lane * 8) * BIN / 8);
+            sc[u][p] = __ldg(a.ms[p] + blk0 + u);
+          }
+        float v[kU][1][8];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          float cd[8];
+#pragma unroll
+          for (int p = 0; p < GT; ++p) {
+            raw[u][p].decode(cd);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float xh = __fmul_rn(cd[i], sc[u][p]);
+              v[u][0][i] = p == 0 ? xh : __fadd_rn(v[u][0][i], xh);   // ascending member digit
+            }
+          }
+        }
+        if constexpr (BOUT == 0) {
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            float* dst = a.of + (blk0 + u) * kB + lane * 8;
+            if (a.acc) {
+              const float4 o0 = reinterpret_cast<const float4*>(dst)[0];
+              const float4 o1 = reinterpret_cast<const float4*>(dst)[1];
+              const float old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[u][0][i] = __fadd_rn(old[i], v[u][0][i]);   // A = fl(A + P)
+            }
+            Out8<float>::store(dst, v[u][0]);
+          }
+        } else {
+          float am[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            float m = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(v[u][0][i]));
+            am[u] = group_max<32>(m);
+          }
+          quantize_store<kB, BOUT, kU>(v, am, blk0, lane, a.oc, a.os);
+        }
+      }
     }
   }
-  finish(a.work);
+  finish(a.work, a.cnt, a.ncl);
   sync_signal(sy);
 }
 
-int64_t fused_grid(const void* kernel, int64_t items) {
-  return grid_for(kernel, items * kWarps);   // at most one CTA per work item
+// grid: SMs x resident CTAs; producers = pf % of it (HZ_TUNE pf, default 30)
+int producers(int64_t grid) {
+  int64_t gp = grid * tune_param("pf", 30) / 100;
+  if (gp < 1) gp = 1;
+  if (gp > grid - 1) gp = grid - 1;
+  return static_cast<int>(gp);
+}
+
+int64_t pipe_grid(const void* kernel) {
+  const int64_t g = grid_for(kernel, int64_t(1) << 40);   // capacity
+  return g < 2 ? 2 : g;
 }
 
 template <typename T, int BITS, typename TO>
-cudaError_t ag_t(const FusedAG& a, cudaStream_t st, const SyncArgs& sy) {
-  auto kern = k_ag_fused<T, BITS, TO>;
-  const int64_t grid = fused_grid(reinterpret_cast<const void*>(kern), static_cast<int64_t>(a.D + 1) * a.nch);
+cudaError_t ag_t(FusedAG a, cudaStream_t st, const SyncArgs& sy) {
+  auto kern = k_ag_pipe<T, BITS, TO>;
+  const int64_t grid = pipe_grid(reinterpret_cast<const void*>(kern));
+  a.gp = producers(grid);
   kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, sy);
   return cudaGetLastError();
 }
@@ -384,9 +340,10 @@ cudaError_t ag_o(const FusedAG& a, hz_dtype out_dt, cudaStream_t st, const SyncA
 }
 
 template <typename T, int BIN, int BOUT, int GT>
-cudaError_t rs_t(const FusedRS& a, cudaStream_t st, const SyncArgs& sy) {
-  auto kern = k_rs_fused<T, BIN, BOUT, GT>;
-  const int64_t grid = fused_grid(reinterpret_cast<const void*>(kern), static_cast<int64_t>(a.g + 1) * a.ncl);
+cudaError_t rs_t(FusedRS a, cudaStream_t st, const SyncArgs& sy) {
+  auto kern = k_rs_pipe<T, BIN, BOUT, GT>;
+  const int64_t grid = pipe_grid(reinterpret_cast<const void*>(kern));
+  a.gp = producers(grid);
   kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, sy);
   return cudaGetLastError();
 }
@@ -437,6 +394,8 @@ cudaError_t launch_ag_fused(const FusedAGArgs& h, cudaStream_t st, const SyncArg
   a.nch = h.nch;
   a.flags = h.flags;
   a.work = h.work;
+  a.cnt = h.cnt;
+  a.dbg = h.dbg;
   a.y = h.y;
   a.phase = h.phase;
   a.epoch = h.epoch;
@@ -475,6 +434,7 @@ cudaError_t launch_rs_fused(const FusedRSArgs& h, cudaStream_t st, const SyncArg
   a.ncl = h.ncl;
   a.flags = h.flags;
   a.work = h.work;
+  a.cnt = h.cnt;
   a.of = h.of;
   a.oc = h.oc;
   a.os = h.os;

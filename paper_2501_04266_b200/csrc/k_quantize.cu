@@ -33,12 +33,13 @@ struct OutOf<2> { using E = EmitOut<__half>; };
 template <>
 struct OutOf<3> { using E = EmitF32; };
 
-template <typename T, int B, int BITS, int U, int OUT>
+template <typename T, int B, int BITS, int U, int OUT, class P = NoPush>
 __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, int64_t nblocks,
                                                        uint8_t* __restrict__ codes,
                                                        float* __restrict__ scales,
                                                        const __grid_constant__ SyncArgs sy,
-                                                       void* __restrict__ y, int acc) {
+                                                       void* __restrict__ y, int acc,
+                                                       const __grid_constant__ P push) {
   using G = Geo<B>;
   using Emit = typename OutOf<OUT>::E;
   __shared__ float4 stage[OUT == 3 ? kThreads / 32 : 1][OUT == 3 ? 64 : 1];
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
       }
       am[u] = group_max<G::LPB>(m);
     }
-    quantize_store<B, BITS, U, Emit>(v, am, blk0, lane, codes, scales, emit);
+    quantize_store<B, BITS, U, Emit, P>(v, am, blk0, lane, codes, scales, emit, push);
   }
 
   // tail: the last nblocks % NB blocks, one warp step at a time, bounds-checked
@@ -113,10 +114,11 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
         unsigned b[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) b[i] = qbits(v[k][i], inv);
-        if (valid && codes) {
+        if (valid && (codes || P::on)) {
           Codes8<BITS> out;
           out.set(b);
-          out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
+          if (codes) out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
+          if constexpr (P::on) push.template put<BITS>(blk * B + k * G::SUBSTRIDE + ll * 8, out);
         }
         if constexpr (OUT == 1 || OUT == 2) {
           if (valid) {
@@ -138,6 +140,9 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
         }
       }
       if (valid && codes && ll == 0) scales[blk] = scale;
+      if constexpr (P::on) {
+        if (valid && ll == 0) push.template put_scale<B>(blk, scale);
+      }
     }
   }
   sync_signal(sy);   // P2P mode: codes of this phase are ready for the peers
@@ -147,16 +152,30 @@ constexpr int kU = 4;   // warp steps per warp iteration
 // B > 256: NSUB = B/256 loads per step already; B < 256: NB = U*BPW <= 32
 constexpr int uq(int B) { return B > 256 ? 1 : kU; }
 
-template <typename T, int B, int BITS, int U, int OUT = 0>
+template <typename T, int B, int BITS, int U, int OUT = 0, class P = NoPush>
 cudaError_t quantize_u(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st,
-                       const SyncArgs& sy, void* y = nullptr, int acc = 0) {
+                       const SyncArgs& sy, void* y = nullptr, int acc = 0, const P& push = P{}) {
   const int64_t nblocks = n / B;
   constexpr int NB = U * Geo<B>::BPW;
-  auto kern = k_quantize<T, B, BITS, U, OUT>;
+  auto kern = k_quantize<T, B, BITS, U, OUT, P>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), nblocks / NB + 1);
   kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(static_cast<const T*>(x), nblocks, codes, scales, sy,
-                                                         y, acc);
+                                                         y, acc, push);
   return cudaGetLastError();
+}
+
+// push variants (B = 256): codes / scales also stored into the consumers' receive
+// buffers; y (optional) receives the own data's round trip x_hat
+template <typename T, int BITS>
+cudaError_t push_t(const void* x, int64_t n, uint8_t* codes, float* scales, void* y, hz_dtype out_dt,
+                   const Push& push, cudaStream_t st, const SyncArgs& sy) {
+  if (!y) return quantize_u<T, 256, BITS, kU, 0, Push>(x, n, codes, scales, st, sy, nullptr, 0, push);
+  switch (out_dt) {
+    case HZ_BF16: return quantize_u<T, 256, BITS, kU, 1, Push>(x, n, codes, scales, st, sy, y, 0, push);
+    case HZ_F16: return quantize_u<T, 256, BITS, kU, 2, Push>(x, n, codes, scales, st, sy, y, 0, push);
+    case HZ_F32: return quantize_u<T, 256, BITS, kU, 3, Push>(x, n, codes, scales, st, sy, y, 0, push);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <typename T, int BITS>
@@ -232,6 +251,27 @@ cudaError_t launch_quantize_roundtrip(const void* x, hz_dtype dt, int64_t n, int
     case HZ_F16:
       return bits == 8 ? roundtrip_t<__half, 8>(x, n, codes, scales, y, out_dt, acc, st, sy)
                        : roundtrip_t<__half, 4>(x, n, codes, scales, y, out_dt, acc, st, sy);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_quantize_push(const void* x, hz_dtype dt, int64_t n, int bits, uint8_t* codes, float* scales,
+                                 void* y, hz_dtype out_dt, const PushDst& dst, cudaStream_t st,
+                                 const SyncArgs* sync) {
+  SyncArgs sy = sync ? *sync : SyncArgs{};
+  sy.sysfence = 1;
+  Push push{};
+  push.d = dst;
+  switch (dt) {
+    case HZ_F32:
+      return bits == 8 ? push_t<float, 8>(x, n, codes, scales, y, out_dt, push, st, sy)
+                       : push_t<float, 4>(x, n, codes, scales, y, out_dt, push, st, sy);
+    case HZ_BF16:
+      return bits == 8 ? push_t<__nv_bfloat16, 8>(x, n, codes, scales, y, out_dt, push, st, sy)
+                       : push_t<__nv_bfloat16, 4>(x, n, codes, scales, y, out_dt, push, st, sy);
+    case HZ_F16:
+      return bits == 8 ? push_t<__half, 8>(x, n, codes, scales, y, out_dt, push, st, sy)
+                       : push_t<__half, 4>(x, n, codes, scales, y, out_dt, push, st, sy);
   }
   return cudaErrorInvalidValue;
 }

@@ -116,9 +116,10 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
 // Main loop: warp iterations of U full steps (NB = U*BPW blocks), no bounds checks,
 // quantize_store epilogue (one division per block).  Tail (< NB blocks): one
 // checked step at a time by the last warp.
-template <int B, int BIN, int BOUT, int GT, int U>
+template <int B, int BIN, int BOUT, int GT, int U, class P = NoPush>
 __global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_constant__ RedArgs a,
-                                                             const __grid_constant__ SyncArgs sy) {
+                                                             const __grid_constant__ SyncArgs sy,
+                                                             const __grid_constant__ P push) {
   using G = Geo<B>;
   sync_wait(sy);   // P2P: peers' chunks ready, and nobody still reads our output slot
   constexpr int NB = U * G::BPW;
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_consta
         for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(acc[u][k][i]));
       am[u] = group_max<G::LPB>(m);
     }
-    quantize_store<B, BOUT, U>(acc, am, blk0, lane, a.oc, a.os);
+    quantize_store<B, BOUT, U, NoEmit, P>(acc, am, blk0, lane, a.oc, a.os, NoEmit{}, push);
   }
 
   const int64_t tail0 = nfull * NB;
@@ -173,9 +174,13 @@ __global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_consta
           for (int i = 0; i < 8; ++i) bq[i] = qbits(acc[0][k][i], inv);
           Codes8<BOUT> out;
           out.set(bq);
-          out.store(a.oc + (blk * B + k * G::SUBSTRIDE + ll * 8) * BOUT / 8);
+          if (a.oc) out.store(a.oc + (blk * B + k * G::SUBSTRIDE + ll * 8) * BOUT / 8);
+          if constexpr (P::on) push.template put<BOUT>(blk * B + k * G::SUBSTRIDE + ll * 8, out);
         }
-        if (ll == 0) a.os[blk] = scale;
+        if (ll == 0 && a.oc) a.os[blk] = scale;
+        if constexpr (P::on) {
+          if (ll == 0) push.template put_scale<B>(blk, scale);
+        }
       }
     }
   }
@@ -438,13 +443,26 @@ constexpr int kUR = 4;   // warp steps per warp iteration (requant)
 constexpr int kUF = 2;   // 8-byte code units in flight per lane per input (fp32 out)
 constexpr int ur(int B) { return B > 256 ? 1 : kUR; }
 
-template <int B, int BIN, int BOUT, int GT, int U>
-cudaError_t requant_u(const RedArgs& a, cudaStream_t st, const SyncArgs& sy) {
+template <int B, int BIN, int BOUT, int GT, int U, class P = NoPush>
+cudaError_t requant_u(const RedArgs& a, cudaStream_t st, const SyncArgs& sy, const P& push = P{}) {
   constexpr int NB = U * Geo<B>::BPW;
-  auto kern = k_reduce_requant<B, BIN, BOUT, GT, U>;
+  auto kern = k_reduce_requant<B, BIN, BOUT, GT, U, P>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), a.n / B / NB + 1);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, sy);
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, sy, push);
   return cudaGetLastError();
+}
+
+// push variant (B = 256): the requantized sum goes straight into the next level's
+// receive buffers (scatter by destination)
+template <int BIN, int BOUT>
+cudaError_t requant_push(const RedArgs& a, const Push& push, cudaStream_t st, const SyncArgs& sy) {
+  switch (a.g) {
+    case 1: return requant_u<256, BIN, BOUT, 1, kUR, Push>(a, st, sy, push);
+    case 2: return requant_u<256, BIN, BOUT, 2, kUR, Push>(a, st, sy, push);
+    case 4: return requant_u<256, BIN, BOUT, 4, kUR, Push>(a, st, sy, push);
+    case 8: return requant_u<256, BIN, BOUT, 8, kUR, Push>(a, st, sy, push);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <int B, int BIN, int BOUT, int GT>
@@ -527,6 +545,26 @@ cudaError_t f32_g(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& 
 }
 
 }  // namespace
+
+bool push_reduce_supported(int g, int block) { return block == 256 && (g == 1 || g == 2 || g == 4 || g == 8); }
+
+cudaError_t launch_reduce_push(int g, const uint8_t* const* codes, const float* const* scales, int64_t n,
+                               int bits_in, int bits_out, const PushDst& dst, cudaStream_t st,
+                               const SyncArgs* sync) {
+  SyncArgs sy = sync ? *sync : SyncArgs{};
+  sy.sysfence = 1;
+  RedArgs a{};
+  for (int p = 0; p < g; ++p) {
+    a.c[p] = codes[p];
+    a.s[p] = scales[p];
+  }
+  a.g = g;
+  a.n = n;
+  Push push{};
+  push.d = dst;
+  if (bits_in == 8) return bits_out == 8 ? requant_push<8, 8>(a, push, st, sy) : requant_push<8, 4>(a, push, st, sy);
+  return bits_out == 8 ? requant_push<4, 8>(a, push, st, sy) : requant_push<4, 4>(a, push, st, sy);
+}
 
 cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
                           int64_t n, int bits_in, int block, int bits_out, uint8_t* out_codes,

@@ -63,13 +63,16 @@ hz_status slot(hz_ctx* ctx, hz_ctx::P2P::Slot& sl, size_t bytes) {
   return rc;
 }
 
-// fused-kernel chunk: >= 32768 elements, a multiple of 1024 (4 blocks of 256), and
-// few enough chunks for the per-member flag arrays
+// pipelined-kernel chunk: about len / pk (HZ_TUNE pk, default 16) elements, a
+// multiple of 1024 (4 blocks of 256), >= fchunk KiElements (default 64), and few
+// enough chunks for the per-member flag arrays
 int64_t chunk_elems(int64_t len) {
-  int64_t c = (len + kMaxChunks - 1) / kMaxChunks;
-  c = (c + 1023) / 1024 * 1024;
-  const int64_t lo = int64_t(tune_param("fchunk", 32)) * 1024;   // HZ_TUNE fchunk (KiElements)
-  return c < lo ? lo : c;
+  int64_t c = (len + tune_param("pk", 16) - 1) / tune_param("pk", 16);
+  const int64_t cap = (len + kMaxChunks - 1) / kMaxChunks;
+  if (c < cap) c = cap;
+  const int64_t lo = int64_t(tune_param("fchunk", 64)) * 1024;
+  if (c < lo) c = lo;
+  return (c + 1023) / 1024 * 1024;
 }
 
 template <typename T>
@@ -165,6 +168,16 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   // kernel's done(phase) is what tells them the write (incl. its copies) is complete
   const unsigned long long phase = ++P.phase;
   const int64_t plen = p->len[top];
+  int me = 0;
+  for (int k = 0; k < D; ++k)
+    if (members[k].second == ctx->rank) me = k;
+  // forward with s == w, hybrid push/pull (HZ_TUNE pushf = % of each piece pushed by
+  // the quantize kernel, in whole 1024-element tiles).  Default 0 = pull only: on
+  // B200 the pushes cost the quantize kernel about as much NVLink time as they save
+  // the gather (profiles/push_pull_r01.md).
+  int64_t push_lim = 0;
+  if (!backward && s == w && D > 1 && B == 256)
+    push_lim = plen * tune_param("pushf", 0) / 100 / 1024 * 1024;
 
   if (!backward && s == w && D > 1 && B == 256 && tune_param("fused", 0)) {
     // A2 + A3 + A5 in ONE kernel: quantize the own primary chunk by chunk into the
@@ -192,6 +205,7 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
       h.flags_remote[k] = at<unsigned long long>(ctx, members[k].second, kChunkAGOff) + h.me * kMaxChunks;
     h.flags = at<unsigned long long>(ctx, ctx->rank, kChunkAGOff);
     h.work = at<unsigned long long>(ctx, ctx->rank, kWorkAGOff);
+    h.cnt = at<unsigned int>(ctx, ctx->rank, kCntAGOff);
     h.y = full_out;
     h.out_dt = out_dt;
     h.phase = phase - P.epoch_host;
@@ -199,11 +213,31 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
     SyncArgs sy = make_sync(ctx, 0, phase - 1, 0, phase);
     const int64_t local = p->len[w] * elem_bytes(dt) + code_bytes(plen, bits) + plen / B * 4 +
                           code_bytes(Np, bits) + Np / B * 4 - remote + Np * elem_bytes(out_dt);
+    static int dbg_calls = 0;
+    const bool dbg = tune_param("pdbg", 0) && ++dbg_calls == tune_param("pdbg", 0);
+    if (dbg) {   // diagnostic timeline of one call (HZ_TUNE pdbg=<call number>), printed to stderr
+      h.dbg = at<unsigned long long>(ctx, ctx->rank, kDbgOff);
+      std::vector<unsigned long long> init(size_t(kMaxChunks) * 4, 0ull);
+      for (int c = 0; c < h.nch; ++c) init[c * 4 + 1] = ~0ull;
+      cudaMemcpyAsync(h.dbg, init.data(), init.size() * 8, cudaMemcpyHostToDevice, st);
+      cudaStreamSynchronize(st);
+    }
     TraceScope t(st, "ag_fused", w, bits, Np, local, remote);
     sy.stamps = t.stamps;
     cudaError_t e = launch_ag_fused(h, st, sy);
     t.end();
     if (e != cudaSuccess) return cuda_fail(e, "fused all-gather kernel launch");
+    if (dbg) {
+      std::vector<unsigned long long> tl(size_t(kMaxChunks) * 4);
+      cudaStreamSynchronize(st);
+      cudaMemcpy(tl.data(), h.dbg, tl.size() * 8, cudaMemcpyDeviceToHost);
+      const unsigned long long t0 = tl[(kMaxChunks - 1) * 4];
+      fprintf(stderr, "[hz pdbg rank %d] ag_pipe plen=%lld C=%lld nch=%d (us from entry: last-arrive publish "
+              "first-consumer-start last-consumer-end)\n", ctx->rank, (long long)plen, (long long)h.C, h.nch);
+      for (int c = 0; c < h.nch; ++c)
+        fprintf(stderr, "  c=%3d %8.2f %8.2f %8.2f %8.2f\n", c, (tl[c * 4 + 3] - t0) * 1e-3, (tl[c * 4] - t0) * 1e-3,
+                (tl[c * 4 + 1] - t0) * 1e-3, (tl[c * 4 + 2] - t0) * 1e-3);
+    }
     clear_error();
     return HZ_OK;
   }
@@ -219,7 +253,28 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
       qs = at<float>(ctx, ctx->rank, P.ag_prim_s.off);
     }
     SyncArgs sq = make_sync(ctx, 0, phase - 1, phase, 0);
-    if ((rc = run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w, &sq)) != HZ_OK) return rc;
+    if (push_lim > 0) {
+      // hybrid push/pull: the quantize kernel (HBM-bound, NVLink idle) also stores
+      // the first push_lim codes of its piece into every member's receive buffer;
+      // the gather below pulls only the rest over NVLink
+      if ((rc = slot(ctx, P.ag_recv_c, code_bytes(D * plen, 8))) != HZ_OK) return rc;
+      if ((rc = slot(ctx, P.ag_recv_s, D * plen / B * 4)) != HZ_OK) return rc;
+      PushDst dst{};
+      int64_t pushed = 0;
+      for (int k = 0; k < D; ++k) {
+        if (members[k].second == ctx->rank) continue;
+        dst.c[dst.n] = at<uint8_t>(ctx, members[k].second, P.ag_recv_c.off) + code_bytes(me * plen, bits);
+        dst.s[dst.n] = at<float>(ctx, members[k].second, P.ag_recv_s.off) + me * plen / B;
+        ++dst.n;
+        pushed += code_bytes(push_lim, bits) + push_lim / B * 4;
+      }
+      dst.lim = push_lim;
+      if ((rc = run_quantize_push(primary, dt, plen, bits, qc, qs, nullptr, out_dt, dst, st, w, &sq, pushed)) !=
+          HZ_OK)
+        return rc;
+    } else if ((rc = run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w, &sq)) != HZ_OK) {
+      return rc;
+    }
     if (s > w) {   // A4, s > w: the secondary is a sub-slice of the own quantized primary
       const int64_t rel = p->off[s] - p->off[w];
       if ((rc = copy_async(sec_codes, qc + code_bytes(rel, bits), code_bytes(len_s, bits), st)) != HZ_OK) return rc;
@@ -239,8 +294,14 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
     const int m = members[k].second;
     pc.c[k] = at<const uint8_t>(ctx, m, off_of(ctx, xc));
     pc.s[k] = at<const float>(ctx, m, off_of(ctx, xs));
-    if (m != ctx->rank) remote += code_bytes(plen, bits) + plen / B * 4;
+    if (m == ctx->rank) continue;
+    remote += code_bytes(plen - push_lim, bits) + (plen - push_lim) / B * 4;
+    if (push_lim > 0) {   // the pushed head of piece k is already in the local receive buffer
+      pc.cr[k] = at<const uint8_t>(ctx, ctx->rank, P.ag_recv_c.off) + code_bytes(k * plen, bits);
+      pc.sr[k] = at<const float>(ctx, ctx->rank, P.ag_recv_s.off) + k * plen / B;
+    }
   }
+  pc.split = push_lim;
   if (!backward && s < w) {   // A4, s < w: keep range_s of the gathered codes
     pc.sec_c = sec_codes;
     pc.sec_s = sec_scales;
@@ -254,12 +315,99 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   return HZ_OK;
 }
 
+// qgZ over NVLink, push mode: every producer (the level-`from` quantize, each
+// level's requantizing reduce) stores the chunk destined to member j straight into
+// member j's level receive buffer, at the producer's own digit; every reduce then
+// reads its g inputs from local HBM (ascending digit = the oracle's summation order).
+hz_status p2p_reduce_scatter_push(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
+                                  int from_level, int to_level, const int* bits_per_level, float* shard,
+                                  int accumulate, cudaStream_t st) {
+  auto& P = ctx->p2p;
+  const int B = p->block;
+  hz_status rc;
+  for (int l = from_level; l <= to_level; ++l) {   // level-l receive buffers (8-bit capacity)
+    if ((rc = slot(ctx, P.rs_recv_c[l], code_bytes(p->len[l - 1], 8))) != HZ_OK) return rc;
+    if ((rc = slot(ctx, P.rs_recv_s[l], p->len[l - 1] / B * 4)) != HZ_OK) return rc;
+  }
+  int64_t stride[HZ_MAX_LEVELS];
+  int64_t sacc = 1;
+  for (int l = 0; l < p->levels; ++l) {
+    stride[l] = sacc;
+    sacc *= p->group[l];
+  }
+  // destinations of level l's chunks: member j gets chunk j at this rank's digit
+  auto dest_of = [&](int l, int bits, PushDst& dst, int64_t& remote) {
+    const int g = p->group[l - 1];
+    const int d = p->digit[l - 1];
+    const int64_t cl = p->len[l];
+    dst = PushDst{};
+    dst.n = g;
+    dst.scatter = 1;
+    dst.seg = cl;
+    remote = 0;
+    for (int j = 0; j < g; ++j) {
+      const int m = static_cast<int>(p->rank + (static_cast<int64_t>(j) - d) * stride[l - 1]);
+      dst.c[j] = at<uint8_t>(ctx, m, P.rs_recv_c[l].off) + code_bytes(d * cl, bits);
+      dst.s[j] = at<float>(ctx, m, P.rs_recv_s[l].off) + d * cl / B;
+      if (m != ctx->rank) remote += code_bytes(cl, bits) + cl / B * 4;
+    }
+  };
+  const unsigned long long base = P.phase;
+  P.phase += static_cast<unsigned long long>(to_level - from_level + 1);
+  auto phase_of = [&](int l) { return base + static_cast<unsigned long long>(l - from_level + 1); };
+  {   // A7 + A8: quantize range_{from-1} and push chunk j to member j
+    const int l = from_level;
+    PushDst dst;
+    int64_t remote;
+    dest_of(l, bits_per_level[l - 1], dst, remote);
+    const unsigned long long ph = phase_of(l);
+    SyncArgs sq = make_sync(ctx, 0, ph - 1, ph, 0);
+    if ((rc = run_quantize_push(grad, dt, p->len[l - 1], bits_per_level[l - 1], nullptr, nullptr, nullptr, HZ_F32, dst,
+                                st, l, &sq, remote)) != HZ_OK)
+      return rc;
+  }
+  for (int l = from_level; l <= to_level; ++l) {   // A9 (+ A8 of the next level) / A10
+    const int g = p->group[l - 1];
+    const int bits = bits_per_level[l - 1];
+    const int64_t cl = p->len[l];
+    const uint8_t* ptr_c[kMaxG];
+    const float* ptr_s[kMaxG];
+    for (int j = 0; j < g; ++j) {
+      ptr_c[j] = at<const uint8_t>(ctx, ctx->rank, P.rs_recv_c[l].off) + code_bytes(j * cl, bits);
+      ptr_s[j] = at<const float>(ctx, ctx->rank, P.rs_recv_s[l].off) + j * cl / B;
+    }
+    const unsigned long long ph = phase_of(l);
+    if (l < to_level) {
+      PushDst dst;
+      int64_t remote;
+      dest_of(l + 1, bits_per_level[l], dst, remote);
+      SyncArgs sr = make_sync(ctx, ph, ph - 1, ph + 1, ph);
+      if ((rc = run_reduce_push(g, ptr_c, ptr_s, cl, bits, bits_per_level[l], dst, st, l, &sr, remote)) != HZ_OK)
+        return rc;
+    } else {
+      SyncArgs sr = make_sync(ctx, ph, 0, 0, ph);
+      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st, l, &sr, 0)) !=
+          HZ_OK)
+        return rc;
+    }
+  }
+  clear_error();
+  return HZ_OK;
+}
+
 hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
                              int from_level, int to_level, const int* bits_per_level, float* shard,
                              int accumulate, cudaStream_t st) {
   auto& P = ctx->p2p;
   const int B = p->block;
   hz_status rc;
+  // full push for qgZ measured slower than pull on B200: HZ_TUNE rspush=1
+  bool push = B == 256 && tune_param("rspush", 0) && !tune_param("fused", 0);
+  for (int l = from_level; l < to_level; ++l) push = push && push_reduce_supported(p->group[l - 1], B);
+  for (int l = from_level; l <= to_level; ++l)
+    if (p->group[l - 1] > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "group size > 16 at one level");
+  if (push) return p2p_reduce_scatter_push(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard, accumulate,
+                                           st);
   for (int l = from_level; l <= to_level; ++l) {   // level-l send buffers (8-bit capacity)
     if ((rc = slot(ctx, P.rs_c[l], code_bytes(p->len[l - 1], 8))) != HZ_OK) return rc;
     if ((rc = slot(ctx, P.rs_s[l], p->len[l - 1] / B * 4)) != HZ_OK) return rc;
@@ -306,6 +454,7 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
     }
     h.flags = at<unsigned long long>(ctx, ctx->rank, kChunkRSOff);
     h.work = at<unsigned long long>(ctx, ctx->rank, kWorkRSOff);
+    h.cnt = at<unsigned int>(ctx, ctx->rank, kCntRSOff);
     h.of = shard;
     if (l < to_level) {
       h.oc = at<uint8_t>(ctx, ctx->rank, P.rs_c[l + 1].off);

@@ -34,6 +34,26 @@ def test_multi_gpu(n):
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
 
 
+@pytest.mark.multigpu
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("tune", ["fused=1", "fused=1,pf=20,pk=4", "pushf=40", "pushf=100,rspush=1"])
+def test_multi_gpu_transport_variants(n, tune):
+    """The alternative P2P kernel schedules selected with HZ_TUNE: the one-launch
+    pipelined kernels (k_fused.cu, fused=1), the hybrid push/pull forward gather
+    (pushf=40: the quantize kernel also stores the head of its piece into every
+    member's receive buffer; the default is pull only), the full push gather
+    (pushf=100) and the push qgZ (rspush=1: producers store each chunk into its
+    consumer's receive buffer)."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29520 + n),
+           os.path.join(ROOT, "tests", "mp_parity.py")]
+    env = dict(os.environ, HZ_TUNE=tune)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+
+
 def test_world1_full_size_neox20b():
     """NeoX-20B layer (453 M parameters) through hz_allgather_params / hz_reduce_scatter_grads
     in the bench configuration, checked on sampled blocks."""
