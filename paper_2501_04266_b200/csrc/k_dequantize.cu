@@ -49,6 +49,25 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
     }
     Codes8<BITS> raw[U];
     float sc[U];
+    if constexpr (U == 4) {
+      if (log2b == 8 && (inter || (pc.n == 1 && ub + 32 * U <= nunits))) {
+        // B = 256, a full tile: its 4 blocks have 4 consecutive scales — one 16-byte
+        // (broadcast) load instead of 4 single-scale requests (peer reads are
+        // request-bound for small transfers)
+        if (!inter) jt = 0;
+        const int64_t r0 = ub * 8 - jt * pc.len;
+        const bool head = r0 < pc.split && pc.cr[jt] != nullptr;
+        const uint8_t* cb = (head ? pc.cr[jt] : pc.c[jt]) + (r0 + lane * 8) * BITS / 8;
+        const float4 s4 = __ldg(reinterpret_cast<const float4*>((head ? pc.sr[jt] : pc.s[jt]) + (r0 >> 8)));
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u].load(cb + u * 256 * BITS / 8);
+        sc[0] = s4.x;
+        sc[1] = s4.y;
+        sc[2] = s4.z;
+        sc[3] = s4.w;
+        goto decode;
+      }
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t unit = ub + u * 32 + lane;
@@ -65,6 +84,7 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
         sc[u] = __ldg((head ? pc.sr[j] : pc.s[j]) + (r >> log2b));
       }
     }
+  decode:
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t unit = ub + u * 32 + lane;

@@ -46,6 +46,20 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
   if constexpr (GT > 0) {
     Codes8<BIN> raw[U][GT][G::NSUB];
     float sc[U][GT];
+    if constexpr (B == 256 && U == 4) {
+      // main loop only (the tail uses U = 1): blk0 % 4 == 0, all steps valid; the
+      // 4 scales of an input are one 16-byte broadcast load
+#pragma unroll
+      for (int p = 0; p < GT; ++p) {
+        const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.s[p] + blk0));
+        sc[0][p] = s4.x;
+        sc[1][p] = s4.y;
+        sc[2][p] = s4.z;
+        sc[3][p] = s4.w;
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u][p][0].load(a.c[p] + ((blk0 + u) * B + ll * 8) * BIN / 8);
+      }
+    } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t blk = blk0 + u * G::BPW + lb;
@@ -62,6 +76,7 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
           for (int k = 0; k < G::NSUB; ++k) raw[u][p][k].zero();
         }
       }
+    }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
