@@ -293,11 +293,13 @@ HZ_API hz_status hz_flat_allgather(hz_ctx* ctx, const void* chunk, void* out, in
 HZ_API hz_status hz_flat_reduce_scatter(hz_ctx* ctx, const void* in, void* out_chunk,
                                  int64_t numel, hz_dtype dt, void* stream);
 
-/* Upper bound on the CTAs of every libhz kernel launch (process-wide; 0 = no bound,
- * the default: SMs x resident CTAs).  All kernels are grid-stride loops, so any
- * bound is correct; a small bound (e.g. 32-64) leaves SMs to compute kernels that
- * run concurrently on other streams (communication / computation overlap). */
-HZ_API hz_status hz_set_grid_limit(int max_ctas);
+/* SM budget of every libhz kernel launch (process-wide; 0 = all SMs, the default).
+ * Grids are sized to `sms` x the kernel's resident CTAs per SM instead of the whole
+ * GPU.  All kernels are grid-stride loops, so any budget is correct.  Intended for
+ * communication streams confined to an SM partition (a CUDA green context of
+ * `sms` SMs) while compute kernels run on the rest (tools/train_step.py --green).
+ * Errors: HZ_ERR_INVALID if sms < 0. */
+HZ_API hz_status hz_set_sm_budget(int sms);
 
 /* ------------------------------------------------------------------ tracing */
 

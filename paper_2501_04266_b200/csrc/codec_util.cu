@@ -39,14 +39,18 @@ int resident_ctas(const void* kernel) {
 
 }  // namespace
 
-std::atomic<int> g_grid_limit{0};
+std::atomic<int> g_sm_budget{0};
 
 int64_t grid_for(const void* kernel, int64_t warp_tasks) {
   const int64_t per_cta = dev::kThreads / 32;
   const int64_t need = (warp_tasks + per_cta - 1) / per_cta;
-  int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(kernel);
-  const int lim = g_grid_limit.load(std::memory_order_relaxed);
-  if (lim > 0 && cap > lim) cap = lim;
+  const int budget = g_sm_budget.load(std::memory_order_relaxed);
+  const int sms = budget > 0 && budget < sm_count() ? budget : sm_count();
+  int64_t cap = static_cast<int64_t>(sms) * resident_ctas(kernel);
+  // HZ_TUNE grid_np=k: non-persistent grids of up to k x the resident capacity
+  // (short CTAs the block scheduler can interleave with other streams' kernels)
+  static const int np = tune_param("grid_np", 0);
+  if (np > 0) cap *= np;
   const int64_t g = need < cap ? need : cap;
   return g < 1 ? 1 : g;
 }
@@ -91,9 +95,9 @@ cudaError_t launch_epoch_advance(unsigned long long* epoch, unsigned long long s
 }
 }  // namespace hz
 
-extern "C" hz_status hz_set_grid_limit(int max_ctas) {
-  if (max_ctas < 0) return hz::fail(HZ_ERR_INVALID, "max_ctas: negative");
-  hz::g_grid_limit.store(max_ctas, std::memory_order_relaxed);
+extern "C" hz_status hz_set_sm_budget(int sms) {
+  if (sms < 0) return hz::fail(HZ_ERR_INVALID, "sms: negative");
+  hz::g_sm_budget.store(sms, std::memory_order_relaxed);
   hz::clear_error();
   return HZ_OK;
 }

@@ -123,7 +123,7 @@ def adamw_params(lr, b1, b2, eps, wd, t):
 
 _sig("hz_adamw_step", [_vp, ctypes.POINTER(Partition), _vp, _vp, _vp, _vp, ctypes.POINTER(AdamWParams), _vp, _int,
                        _vp])
-_sig("hz_set_grid_limit", [_int])
+_sig("hz_set_sm_budget", [_int])
 _sig("hz_flat_allgather", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_flat_reduce_scatter", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_trace_begin", [_int, _int])
@@ -311,9 +311,9 @@ def _wrap_device_ptr(ptr, numel, dtype, device):
 
 
 # ------------------------------------------------------------------ collectives
-def set_grid_limit(max_ctas):
-    """hz_set_grid_limit: cap the CTAs of every libhz launch (0 = SMs x occupancy)."""
-    _check(_lib.hz_set_grid_limit(int(max_ctas)))
+def set_sm_budget(sms):
+    """hz_set_sm_budget: size every libhz grid for `sms` SMs (0 = all SMs)."""
+    _check(_lib.hz_set_sm_budget(int(sms)))
 
 
 def get_uid():

@@ -1,13 +1,13 @@
 #!/bin/bash
-# N3 overlap sweep: tools/train_step.py over tokens x libhz grid limits (4 and 2 GPUs).
+# N3 overlap sweep: tools/train_step.py (4 GPUs) over tokens x communication SM
+# partition (CUDA green context of K SMs for the communication stream, libhz grids
+# sized to it), with / without stream priorities.
 mkdir -p gpurun_out
-set -x
-for T in 1024 2048; do
- for lim in 0 16 32 64; do
-  modes="hz"; [ $lim = 0 ] && modes="compute,hz,flat"
-  timeout 300 python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29611 tools/train_step.py --tokens $T --grid-limit $lim --modes $modes --steps 5 2>&1 | grep '^{' >> gpurun_out/sweep4.jsonl
- done
-done
-for lim in 0 32; do
-  timeout 300 python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 tools/train_step.py --tokens 1024 --grid-limit $lim --steps 5 2>&1 | grep '^{' >> gpurun_out/sweep2.jsonl
+out=${SWEEP_OUT:-gpurun_out/overlap4.jsonl}
+for T in ${SWEEP_TOKENS:-1024 2048}; do
+  for flags in "" "--green 32" "--green 48" "--green 64" "--green 48 --prio"; do
+    modes="hz"; [ -z "$flags" ] && modes="compute,hz,flat"
+    timeout 300 python -m torch.distributed.run --nproc-per-node ${SWEEP_GPUS:-4} --master-addr 127.0.0.1 \
+      --master-port 29611 tools/train_step.py --tokens $T --modes $modes --steps 5 $flags 2>&1 | grep '^{' >> $out
+  done
 done

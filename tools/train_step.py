@@ -45,8 +45,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--modes", default="compute,hz,flat")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
-    ap.add_argument("--grid-limit", type=int, default=0,
-                    help="cap on the CTAs of every libhz kernel (leaves SMs to the GEMMs)")
+    ap.add_argument("--green", type=int, default=0,
+                    help="run the communication stream in a CUDA green context of this many SMs "
+                         "(libhz grids sized to it: hz_set_sm_budget)")
+    ap.add_argument("--prio", action="store_true",
+                    help="compute stream at high priority, communication stream at the lowest")
     args = ap.parse_args()
 
     import torch
@@ -74,7 +77,10 @@ def main():
         dist.broadcast_object_list(box, src=0)
         uid = box[0]
     ctx = hz.Context(rank, world, uid, group, local)
-    hz.set_grid_limit(args.grid_limit)
+    if args.green:
+        from tools.green_probe import green_stream
+        comm_green, green_sms = green_stream(args.green)
+        hz.set_sm_budget(green_sms)
     L = len(group)
     numel = synth.layer_numel(h)
     p = ctx.partition(numel, B, 1, 1, L)
@@ -139,8 +145,15 @@ def main():
         torch.matmul(acts["qkv"].t(), x, out=G["qkv"])
 
     flops = nl * 3 * 2 * T * 12 * h * h
-    comp = torch.cuda.current_stream()
-    comm = torch.cuda.Stream()
+    if args.prio:
+        comp = torch.cuda.Stream(priority=-2)
+        torch.cuda.set_stream(comp)
+        comm = torch.cuda.Stream(priority=0)
+    else:
+        comp = torch.cuda.current_stream()
+        comm = torch.cuda.Stream()
+    if args.green:
+        comm = comm_green
 
     def step(mode):
         if mode == "compute":
@@ -228,7 +241,8 @@ def main():
     line = {"what": "synthetic ZeRO-topo training step (layer GEMMs + sharded collectives, overlapped)",
             "config": args.config, "layers": nl, "tokens_per_gpu": T, "n_gpus": world, "hierarchy": list(group),
             "transport": "p2p" if use_p2p else ("nccl" if world > 1 else "local"),
-            "grid_limit": args.grid_limit, "results": results}
+            "green_sms": green_sms if args.green else 0, "prio": args.prio, "hz_tune": os.environ.get("HZ_TUNE", ""),
+            "results": results}
     ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
