@@ -25,6 +25,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "hz_internal.h"
 
 namespace hz {
@@ -413,6 +415,26 @@ __device__ __forceinline__ int64_t num_warps() {
 // min(ceil(warp_tasks / warps per CTA), SMs x resident CTAs of that kernel).
 int64_t grid_for(const void* kernel, int64_t warp_tasks);
 
+// Every libhz kernel launch: kThreads per CTA, no dynamic shared memory, and the
+// programmatic-stream-serialization attribute when HZ_TUNE pdl=1 (PDL; off by
+// default, see pdl_enabled) — the kernel's prologue (sync_wait) then orders it after
+// the previous kernel on the stream.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), int64_t grid, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(dev::kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 }  // namespace hz
 
 namespace hz {
@@ -453,6 +475,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 __device__ __forceinline__ void sync_wait(const SyncArgs& s) {
+  // Programmatic dependent launch (launch_k): let the next kernel on the stream be
+  // launched now (it is scheduled only once every CTA of this grid has started, so
+  // its CTAs take the SM slots this grid frees), and wait here until the previous
+  // kernel has completed and its memory is visible — the stream-order semantics,
+  // minus the launch gap.  Both are no-ops without the launch attribute.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (s.stamps && blockIdx.x == 0 && threadIdx.x == 0) s.stamps[0] = globaltimer();
   if (!(s.en & (kWaitReady | kWaitDone))) {
     if (s.stamps && blockIdx.x == 0 && threadIdx.x == 0) s.stamps[1] = globaltimer();

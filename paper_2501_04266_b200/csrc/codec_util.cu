@@ -95,6 +95,15 @@ cudaError_t launch_epoch_advance(unsigned long long* epoch, unsigned long long s
 }
 }  // namespace hz
 
+namespace hz {
+// Off by default: measured on B200 (profiles/bench_r01.md) PDL left the multi-GPU
+// step unchanged and made the N = 1 step 7 % slower (the fused round trip 51 -> 56 µs).
+bool pdl_enabled() {
+  static const bool on = tune_param("pdl", 0) != 0;
+  return on;
+}
+}  // namespace hz
+
 extern "C" hz_status hz_set_sm_budget(int sms) {
   if (sms < 0) return hz::fail(HZ_ERR_INVALID, "sms: negative");
   hz::g_sm_budget.store(sms, std::memory_order_relaxed);

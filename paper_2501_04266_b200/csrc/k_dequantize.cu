@@ -114,8 +114,7 @@ cudaError_t dequantize_u(const Pieces& pc, int64_t nunits, int log2b, void* y, c
                          const SyncArgs& sy) {
   auto kern = k_dequantize<BITS, TO, U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(pc, nunits, log2b, static_cast<TO*>(y), sy);
-  return cudaGetLastError();
+  return launch_k(kern, grid, st, pc, nunits, log2b, static_cast<TO*>(y), sy);
 }
 
 template <int BITS, typename TO>

@@ -325,8 +325,7 @@ cudaError_t ag_t(FusedAG a, cudaStream_t st, const SyncArgs& sy) {
   auto kern = k_ag_pipe<T, BITS, TO>;
   const int64_t grid = pipe_grid(reinterpret_cast<const void*>(kern));
   a.gp = producers(grid);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, sy);
-  return cudaGetLastError();
+  return launch_k(kern, grid, st, a, sy);
 }
 
 template <typename T, int BITS>
@@ -344,8 +343,7 @@ cudaError_t rs_t(FusedRS a, cudaStream_t st, const SyncArgs& sy) {
   auto kern = k_rs_pipe<T, BIN, BOUT, GT>;
   const int64_t grid = pipe_grid(reinterpret_cast<const void*>(kern));
   a.gp = producers(grid);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, sy);
-  return cudaGetLastError();
+  return launch_k(kern, grid, st, a, sy);
 }
 
 template <typename T, int BIN, int BOUT>

@@ -115,8 +115,7 @@ cudaError_t adamw_t(const float* g, float* th, float* m, float* v, void* out, in
   const int64_t n4 = n / 4;
   auto kern = k_adamw<TO, U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (n4 + 32 * U - 1) / (32 * U));
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(g, th, m, v, static_cast<TO*>(out), n4, hp, sy);
-  return cudaGetLastError();
+  return launch_k(kern, grid, st, g, th, m, v, static_cast<TO*>(out), n4, hp, sy);
 }
 
 }  // namespace
@@ -139,8 +138,7 @@ cudaError_t launch_gather_copy(const Pieces& pc, void* out, cudaStream_t st, con
   const int64_t nvec = pc.n * (pc.len / 16);
   auto kern = k_gather_copy<U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nvec + 32 * U - 1) / (32 * U));
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(pc, nvec, static_cast<uint4*>(out), sy);
-  return cudaGetLastError();
+  return launch_k(kern, grid, st, pc, nvec, static_cast<uint4*>(out), sy);
 }
 
 }  // namespace hz

@@ -159,9 +159,7 @@ cudaError_t quantize_u(const void* x, int64_t n, uint8_t* codes, float* scales, 
   constexpr int NB = U * Geo<B>::BPW;
   auto kern = k_quantize<T, B, BITS, U, OUT, P>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), nblocks / NB + 1);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(static_cast<const T*>(x), nblocks, codes, scales, sy,
-                                                         y, acc, push);
-  return cudaGetLastError();
+  return launch_k(kern, grid, st, static_cast<const T*>(x), nblocks, codes, scales, sy, y, acc, push);
 }
 
 // push variants (B = 256): codes / scales also stored into the consumers' receive

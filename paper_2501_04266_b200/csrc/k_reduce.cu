@@ -463,8 +463,7 @@ cudaError_t requant_u(const RedArgs& a, cudaStream_t st, const SyncArgs& sy, con
   constexpr int NB = U * Geo<B>::BPW;
   auto kern = k_reduce_requant<B, BIN, BOUT, GT, U, P>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), a.n / B / NB + 1);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, sy, push);
-  return cudaGetLastError();
+  return launch_k(kern, grid, st, a, sy, push);
 }
 
 // push variant (B = 256): the requantized sum goes straight into the next level's
@@ -516,8 +515,7 @@ cudaError_t f32_u(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& 
   const int64_t nunits = a.n / Wide<BIN>::E;
   auto kern = a.accumulate ? k_reduce_f32<BIN, GT, U, true> : k_reduce_f32<BIN, GT, U, false>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, log2b, sy);
-  return cudaGetLastError();
+  return launch_k(kern, grid, st, a, log2b, sy);
 }
 
 template <int BIN, int E, int GT>
@@ -526,8 +524,7 @@ cudaError_t f32_direct(const RedArgs& a, int log2b, cudaStream_t st, const SyncA
   const int64_t nunits = a.n / E;
   auto kern = a.accumulate ? k_reduce_f32_direct<BIN, E, GT, U, true> : k_reduce_f32_direct<BIN, E, GT, U, false>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, st>>>(a, log2b, sy);
-  return cudaGetLastError();
+  return launch_k(kern, grid, st, a, log2b, sy);
 }
 
 template <int BIN, int GT>

@@ -145,6 +145,53 @@ int main() {
     });
     printf("G=%3d local copy bulk C=49152 S=4 512 thr: %6.1f GB/s (read)\n", G, bytes / t5 / 1e6);
   }
+  // both directions at once: GPU0 pulls from GPU1 while GPU1 pulls from GPU0
+  {
+    void* l1b;
+    cudaStream_t s1;
+    CK(cudaSetDevice(1));
+    CK(cudaMalloc(&l1b, bytes));
+    CK(cudaStreamCreate(&s1));
+    CK(cudaFuncSetAttribute(bulk_k<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(bulk_k<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    cudaEvent_t a0, b0, a1, b1;
+    CK(cudaEventCreate(&a1));
+    CK(cudaEventCreate(&b1));
+    CK(cudaSetDevice(0));
+    CK(cudaEventCreate(&a0));
+    CK(cudaEventCreate(&b0));
+    for (int mode = 0; mode < 3; ++mode) {
+      for (int G : {32, 74, 148, 296}) {
+        float m0 = 0, m1 = 0;
+        for (int rep = 0; rep < 2; ++rep) {
+          for (int d = 0; d < 2; ++d) {
+            CK(cudaSetDevice(d));
+            cudaStream_t st = d ? s1 : s0;
+            const char* src = (const char*)(d ? l0 : l1);
+            char* dst = (char*)(d ? l1b : l0b);
+            CK(cudaEventRecord(d ? a1 : a0, st));
+            for (int i = 0; i < iters; ++i) {
+              if (mode == 0)
+                load_k<256, 8><<<G * 4, 256, 0, st>>>((const uint4*)src, (uint4*)dst, bytes / 16);
+              else if (mode == 1)
+                bulk_k<256><<<G, 256, 4 * 49152, st>>>(src, dst, bytes / 49152, 49152, 4);
+              else
+                bulk_k<512><<<G, 512, 6 * 32768, st>>>(src, dst, bytes / 32768, 32768, 6);
+            }
+            CK(cudaEventRecord(d ? b1 : b0, st));
+          }
+          CK(cudaEventSynchronize(b0));
+          CK(cudaEventSynchronize(b1));
+          CK(cudaEventElapsedTime(&m0, a0, b0));
+          CK(cudaEventElapsedTime(&m1, a1, b1));
+        }
+        const char* nm[3] = {"loads 256x8x16B (4 CTAs per G)", "bulk C=48K S=4 256 thr", "bulk C=32K S=6 512 thr"};
+        printf("bidirectional %-32s G=%3d: GPU0 %6.1f GB/s  GPU1 %6.1f GB/s\n", nm[mode], G,
+               bytes * iters / m0 / 1e6, bytes * iters / m1 / 1e6);
+      }
+    }
+    CK(cudaSetDevice(0));
+  }
   // verify last bulk copy from peer
   CK(cudaSetDevice(0));
   bulk_k<256><<<8, 256, 4 * 32768, s0>>>((const char*)l1, (char*)l0b, bytes / 32768, 32768, 4);
