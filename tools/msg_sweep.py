@@ -7,7 +7,9 @@ qwZ/hpZ all-gather (forward and backward) and qgZ reduce-scatter of one tensor o
 Timing discipline (§8(d)): 5 warm-up iterations, then ``--iters`` (>= 20) timed, each
 preceded by a device synchronize + world barrier and bracketed by CUDA events on the
 issuing stream; per-iteration times are max-reduced over ranks, then the median and
-p10/p90 are reported.  Wire bytes per rank come from one stamps-only traced call
+p10/p90 are reported; ``ms_loop`` is the per-call time of ``--iters`` calls issued
+back to back after one barrier (the steady state of a stream of collectives).
+Wire bytes per rank come from one stamps-only traced call
 (the library's ``remote_bytes``, peer bytes read per rank); flat NCCL wire bytes are
 (W-1)/W of the message.
 
@@ -133,6 +135,18 @@ def main():
                 e1.record(stream)
                 e1.synchronize()
                 times.append(e0.elapsed_time(e1))
+            # steady state: --iters calls back to back (no barrier between them), one
+            # event pair; the per-call time of a stream of collectives
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0.record(stream)
+            for _ in range(args.iters):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            loop = torch.tensor([e0.elapsed_time(e1) / args.iters], dtype=torch.float64)
+            dist.all_reduce(loop, op=dist.ReduceOp.MAX)
+            loop_ms = float(loop.item())
             t = torch.tensor(times, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t = sorted(t.tolist())
@@ -142,6 +156,7 @@ def main():
             line = {"bytes": S, "op": name, "n_gpus": world, "hierarchy": list(group),
                     "transport": args.transport if name.startswith("hz") else "nccl",
                     "ms_median": round(med, 4), "ms_p10": round(p10, 4), "ms_p90": round(p90, 4),
+                    "ms_loop": round(loop_ms, 4),
                     "algbw_GBps": round(S / (med * 1e-3) / 1e9, 1),
                     "wire_bytes_per_rank": int(wire),
                     "wire_GBps_per_rank": round(wire / (med * 1e-3) / 1e9, 1)}
