@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
     }
     Codes8<BITS> raw[U];
     float sc[U];
+    bool fast = false;
     if constexpr (U == 4) {
       if (log2b == 8 && (inter || (pc.n == 1 && ub + 32 * U <= nunits))) {
         // B = 256, a full tile: its 4 blocks have 4 consecutive scales — one 16-byte
@@ -65,13 +66,13 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
         sc[1] = s4.y;
         sc[2] = s4.z;
         sc[3] = s4.w;
-        goto decode;
+        fast = true;
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t unit = ub + u * 32 + lane;
-      if (unit < nunits) {
+      if (!fast && unit < nunits) {
         const int64_t e = unit * 8;
         int j = jt;
         if (j < 0) {
@@ -84,7 +85,6 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
         sc[u] = __ldg((head ? pc.sr[j] : pc.s[j]) + (r >> log2b));
       }
     }
-  decode:
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t unit = ub + u * 32 + lane;
