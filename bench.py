@@ -233,7 +233,9 @@ def p2p_pool_bytes(args, group):
         max_np = max(max_np, Np)
     total += 2 * len(group) * (max_np + max_np // B * 4 + 512)   # slots (may grow once)
     total += 2 * (max_np // W) * 4 + 1024                       # step-tail update slot
-    return total + (64 << 20)
+    top = max_np // (W // group[-1])                             # len_{L-1}
+    total += 2 * top * 4 + 1024                                 # allreduce + select ping-pong
+    return int(total * 1.1) + (64 << 20)                        # bump-allocator slack
 
 
 def max_over_ranks(x, world):
@@ -440,6 +442,12 @@ def run_hz(args):
     if not args.no_tail:
         tail = extra(step_tail, hz, ctx, torch, model, stream, world, args)
 
+    # A10 cross-node step both ways (default qgZ reduce-scatter vs paper-literal
+    # allreduce + select), on fp32 range_{L-1} shards
+    a10 = None
+    if world > 1 and not args.no_tail:
+        a10 = extra(cross_node_step, hz, ctx, torch, model, stream, world, args)
+
     # flat ZeRO-3 baseline on the same logical bytes (context, not timed with the step)
     flat = None
     if world > 1 and not args.no_flat:
@@ -476,6 +484,7 @@ def run_hz(args):
         "stages": stages,
         "flat_zero3_baseline": flat,
         "step_tail": tail,
+        "a10_cross_node_step": a10,
     }
     ctx.close()
     if rank == 0:
@@ -559,6 +568,49 @@ def step_tail(hz, ctx, torch, model, stream, world, args):
             "adamw_hbm_bytes_per_step": opt_elems * 30,
             "what": "AdamW on the fp32 optimizer shards + post-update all-gather of the bf16 weights into the "
                     "primaries (eager; not part of the headline metric)"}
+
+
+def cross_node_step(hz, ctx, torch, model, stream, world, args):
+    """A10, the once-per-step top-level reduction of every tensor's fp32 range_{L-1}
+    shard, two ways: the default qgZ reduce-scatter of level L (quantized, R12) and
+    the paper-literal fp32 allreduce over level L + select of range_L (P:361,
+    hz_allreduce_select).  CUDA events around K steps, max over ranks."""
+    L = ctx.levels
+    lens = [t["p"].range(L - 1)[1] for t in model.tensors]
+    src = torch.empty(max(lens), dtype=torch.float32, device=model.tensors[0]["grad"].device).normal_(0, 1e-3)
+    gL = ctx.group[L - 1]
+
+    def rs():
+        for t, n in zip(model.tensors, lens):
+            ctx.reduce_scatter_grads(t["p"], src[:n], t["shard"], model.bits, from_level=L, to_level=L, stream=stream)
+
+    def ar():
+        for t, n in zip(model.tensors, lens):
+            ctx.allreduce_select(t["p"], src[:n], t["shard"], L, L, stream=stream)
+
+    out = {}
+    for name, fn in (("qgz_reduce_scatter", rs), ("allreduce_select", ar)):
+        fn()
+        torch.cuda.synchronize()
+        barrier(world)
+        n = max(1, min(args.steps, 5))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out[name + "_ms"] = max_over_ranks(e0.elapsed_time(e1), world) / n
+    total = sum(lens)
+    bits = model.bits[L - 1]
+    out["peer_bytes_per_rank"] = {
+        "qgz_reduce_scatter": int((gL - 1) * (total // gL) * (bits / 8 + 4 / args.block)),
+        "allreduce_select": int((gL - 1) * total * 4)}
+    out["what"] = ("level-L reduction of fp32 range_{L-1} shards of every tensor: qgZ int%d reduce-scatter "
+                   "(default, R12) vs fp32 allreduce + select (P:361)" % bits)
+    del src
+    return out
 
 
 def run_e2e(hz, ctx, torch, model, stream, world, args):

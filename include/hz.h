@@ -234,6 +234,23 @@ HZ_API hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, c
                                   const int* bits_per_level, float* shard, int accumulate,
                                   void* stream);
 
+/* A10, the paper-literal cross-node step ("call Allreduce ... select the
+ * gradients matching the on-device optimizer states"; reading R12).
+ * shard_in: fp32[len_{from_level-1}] over range_{from_level-1} (device, read only).
+ * Levels from_level..to_level run in order; at level l every rank sums the g_l
+ * members' buffers element by element in ascending level digit (fp32, one
+ * rounding per add, unquantized) — an allreduce — and after the last level keeps
+ * range_{to_level}: out = fp32[len_{to_level}] (device, caller-owned).  The result
+ * is bitwise equal to oracle/collectives.allreduce_select and to an unquantized
+ * reduce-scatter over the same levels; it moves (g_l - 1) * len_{from_level-1}
+ * fp32 per level and rank, twice the reduce-scatter's bytes (the reason the
+ * default cross-node step is hz_reduce_scatter_grads).  Collective; transports:
+ * NCCL (all-gather per level communicator + ordered local sum) or P2P (peers'
+ * buffers read in place).  Errors: HZ_ERR_INVALID (levels, NULL / misaligned
+ * pointers), HZ_ERR_CUDA, HZ_ERR_NCCL. */
+HZ_API hz_status hz_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const float* shard_in,
+                                     int from_level, int to_level, float* out, void* stream);
+
 /* NVLink peer-memory transport (collective over all ranks of the context; one
  * node, world <= 8).  Allocates this rank's symmetric pool of pool_bytes,
  * exchanges CUDA IPC handles over NCCL and maps every peer's pool.  Afterwards

@@ -23,6 +23,7 @@ struct hz_ctx {
   Buf ag_c, ag_s;                      // full-layer codes / scales (all-gather)
   Buf rs_a_c, rs_a_s, rs_b_c, rs_b_s;  // ping-pong send buffers (reduce-scatter)
   Buf rs_r_c, rs_r_s;                  // receive slots (reduce-scatter)
+  Buf ar_a, ar_b, ar_g;                // allreduce + select: ping-pong fp32, gathered members
 
   // NVLink P2P transport (hz_enable_p2p): one IPC-mapped symmetric pool per rank.
   struct P2P {
@@ -42,6 +43,7 @@ struct hz_ctx {
     Slot ag_prim_c, ag_prim_s;                  // quantized primary when s != w
     Slot rs_c[HZ_MAX_LEVELS + 1], rs_s[HZ_MAX_LEVELS + 1];   // level-l send buffers
     Slot upd;                                   // updated weights of range_L (step tail)
+    Slot ar_a, ar_b;                            // allreduce + select: ping-pong fp32 buffers
     // push mode: receive buffers the producers store into over NVLink
     Slot ag_recv_c, ag_recv_s;                  // forward gather: D pieces of the primary codes
     Slot rs_recv_c[HZ_MAX_LEVELS + 1], rs_recv_s[HZ_MAX_LEVELS + 1];   // level-l: g chunks destined here
@@ -88,6 +90,10 @@ hz_status run_reduce_push(int g, const uint8_t* const* c, const float* const* s,
                           int bits_out, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
                           int64_t remote);
 hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
+hz_status run_sum(const Pieces& pc, int64_t n, float* out, cudaStream_t st, int level, const SyncArgs* sync,
+                  int64_t remote);
+hz_status p2p_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const float* in, int from_level, int to_level,
+                               float* out, cudaStream_t st);
 
 // P2P transport (p2p.cpp)
 bool in_pool(const hz_ctx* ctx, const void* p, size_t bytes);

@@ -208,6 +208,17 @@ hz_status run_adamw(const float* g, float* th, float* m, float* v, void* out, hz
   return HZ_OK;
 }
 
+hz_status run_sum(const Pieces& pc, int64_t n, float* out, cudaStream_t st, int level, const SyncArgs* sync,
+                  int64_t remote) {
+  TraceScope t(st, "allreduce_sum", level, 32, n, (pc.n + 1) * n * 4 - remote, remote);
+  SyncArgs sy = sync ? *sync : SyncArgs{};
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_sum_f32(pc, n, out, st, (sync || t.stamps) ? &sy : nullptr);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "allreduce-sum kernel launch");
+  return HZ_OK;
+}
+
 hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (bytes == 0 || dst == src) return HZ_OK;
   TraceScope t(st, "copy", 0, 0, 0, int64_t(bytes) * 2);
@@ -516,6 +527,59 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
         return rc;
     }
   }
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const float* shard_in, int from_level,
+                              int to_level, float* out, void* stream) {
+  using namespace hz;
+  hz_status rc = check_partition(ctx, p);
+  if (rc != HZ_OK) return rc;
+  const int L = ctx->levels;
+  if (from_level < 1 || from_level > L) return fail(HZ_ERR_INVALID, "from_level: must be in [1, levels]");
+  if (to_level < from_level || to_level > L) return fail(HZ_ERR_INVALID, "to_level: must be in [from_level, levels]");
+  if (!shard_in || !aligned16(shard_in)) return fail(HZ_ERR_INVALID, "shard_in: NULL or not 16-byte aligned");
+  if (!out || !aligned16(out)) return fail(HZ_ERR_INVALID, "out: NULL or not 16-byte aligned");
+  if ((rc = check_async(ctx)) != HZ_OK) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = p->len[from_level - 1];
+  const int64_t sel = p->off[to_level] - p->off[from_level - 1];
+  if (n == 0) {
+    clear_error();
+    return HZ_OK;
+  }
+  if (ctx->p2p.on) return p2p_allreduce_select(ctx, p, shard_in, from_level, to_level, out, st);
+  // NCCL transport: per level, all-gather the members' full buffers (piece j = digit
+  // j) and sum them locally in ascending digit — the oracle's order, bit for bit
+  const size_t nb = static_cast<size_t>(n) * 4;
+  if ((rc = grow(ctx->ar_a, nb)) != HZ_OK) return rc;
+  if ((rc = grow(ctx->ar_b, nb)) != HZ_OK) return rc;
+  int gmax = 1;
+  for (int l = from_level; l <= to_level; ++l) gmax = ctx->group[l - 1] > gmax ? ctx->group[l - 1] : gmax;
+  if ((rc = grow(ctx->ar_g, nb * gmax)) != HZ_OK) return rc;
+  const float* cur = shard_in;
+  float* bufs[2] = {static_cast<float*>(ctx->ar_a.p), static_cast<float*>(ctx->ar_b.p)};
+  int nxt = 0;
+  for (int l = from_level; l <= to_level; ++l) {
+    const int g = ctx->group[l - 1];
+    if (g == 1) continue;
+    float* G = static_cast<float*>(ctx->ar_g.p);
+    {
+      TraceScope t(st, "nccl_allgather", l, 32, n * g, nb * g, nb * (g - 1));
+      ncclResult_t r = ncclAllGather(cur, G, n, ncclFloat32, ctx->lvl[l - 1], st);
+      t.end();
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather(allreduce)");
+    }
+    Pieces pc{};
+    pc.n = g;
+    pc.len = n;
+    for (int j = 0; j < g; ++j) pc.c[j] = reinterpret_cast<const uint8_t*>(G + j * n);
+    if ((rc = run_sum(pc, n, bufs[nxt], st, l, nullptr, 0)) != HZ_OK) return rc;
+    cur = bufs[nxt];
+    nxt ^= 1;
+  }
+  if ((rc = copy_async(out, cur + sel, static_cast<size_t>(p->len[to_level]) * 4, st)) != HZ_OK) return rc;
   clear_error();
   return HZ_OK;
 }

@@ -118,6 +118,9 @@ struct AdamW {
 cudaError_t launch_adamw(const float* g, float* th, float* m, float* v, void* out, hz_dtype out_dt, int64_t n,
                          const AdamW& hp, cudaStream_t st, const SyncArgs* sync);
 cudaError_t launch_gather_copy(const Pieces& pc, void* out, cudaStream_t st, const SyncArgs* sync);
+// out[i] = ((c[0][i] + c[1][i]) + ...) + c[n-1][i] over fp32 pieces (Pieces::c as
+// float arrays of n elements, n % 4 == 0; the pieces may be peer-mapped)
+cudaError_t launch_sum_f32(const Pieces& pc, int64_t n, float* out, cudaStream_t st, const SyncArgs* sync);
 
 // Fused codec + NVLink collective kernels (k_fused.cu, B = 256 only).
 constexpr int kMaxChunks = 4096;   // per-chunk flags per member in the P2P pool header

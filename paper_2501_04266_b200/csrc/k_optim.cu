@@ -5,6 +5,9 @@
 //   k_gather_copy  post-update all-gather over NVLink: the members' updated
 //                  shards are read straight from their pools (interleaved tiles, as
 //                  the gather-dequantize) into the rank's primary range.
+//   k_sum_f32      one level of the paper-literal allreduce (A10 option):
+//                  out = ((x_0 + x_1) + ...) + x_{g-1}, fp32, ascending member digit
+//                  (the inputs may be peer-mapped; g == 1 is a copy).
 // Arithmetic: one IEEE rounding per operation in the oracle's order (__fmul_rn,
 // __fadd_rn, __fsub_rn, __fsqrt_rn, __fdiv_rn; no FMA).
 #include "codec.cuh"
@@ -117,6 +120,53 @@ cudaError_t adamw_u(const float* g, float* th, float* m, float* v, void* out, in
   return launch_k(kern, grid, st, g, th, m, v, static_cast<TO*>(out), n4, hp, sy);
 }
 
+template <int GT, int U>
+__global__ void __launch_bounds__(kThreads) k_sum_f32(const __grid_constant__ Pieces pc, int64_t n4,
+                                                      float4* __restrict__ out, const __grid_constant__ SyncArgs sy) {
+  sync_wait(sy);
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  const int64_t nth = static_cast<int64_t>(gridDim.x) * kThreads;
+  const int g = GT > 0 ? GT : pc.n;
+  for (int64_t base = tid; base < n4; base += nth * U) {
+    float4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * nth;
+      if (i < n4) acc[u] = reinterpret_cast<const float4*>(pc.c[0])[i];
+    }
+    for (int j = 1; j < g; ++j) {
+      float4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = base + u * nth;
+        if (i < n4) x[u] = reinterpret_cast<const float4*>(pc.c[j])[i];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[u].x = __fadd_rn(acc[u].x, x[u].x);
+        acc[u].y = __fadd_rn(acc[u].y, x[u].y);
+        acc[u].z = __fadd_rn(acc[u].z, x[u].z);
+        acc[u].w = __fadd_rn(acc[u].w, x[u].w);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * nth;
+      if (i < n4) out[i] = acc[u];
+    }
+  }
+  sync_signal(sy);
+}
+
+template <int GT>
+cudaError_t sum_t(const Pieces& pc, int64_t n, float* out, cudaStream_t st, const SyncArgs& sy) {
+  constexpr int U = 2;
+  const int64_t n4 = n / 4;
+  auto kern = k_sum_f32<GT, U>;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (n4 + 32 * U - 1) / (32 * U));
+  return launch_k(kern, grid, st, pc, n4, reinterpret_cast<float4*>(out), sy);
+}
+
 template <typename TO>
 cudaError_t adamw_t(const float* g, float* th, float* m, float* v, void* out, int64_t n, const AdamW& hp,
                     cudaStream_t st, const SyncArgs& sy) {
@@ -141,6 +191,18 @@ cudaError_t launch_adamw(const float* g, float* th, float* m, float* v, void* ou
     case HZ_F16: return adamw_t<__half>(g, th, m, v, out, n, hp, st, sy);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sum_f32(const Pieces& pc, int64_t n, float* out, cudaStream_t st, const SyncArgs* sync) {
+  const SyncArgs sy = sync ? *sync : SyncArgs{};
+  if (n == 0 && !sync) return cudaSuccess;
+  switch (pc.n) {
+    case 1: return sum_t<1>(pc, n, out, st, sy);
+    case 2: return sum_t<2>(pc, n, out, st, sy);
+    case 4: return sum_t<4>(pc, n, out, st, sy);
+    case 8: return sum_t<8>(pc, n, out, st, sy);
+    default: return sum_t<0>(pc, n, out, st, sy);
+  }
 }
 
 cudaError_t launch_gather_copy(const Pieces& pc, void* out, cudaStream_t st, const SyncArgs* sync) {

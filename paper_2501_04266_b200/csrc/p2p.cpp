@@ -515,6 +515,63 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
   return HZ_OK;
 }
 
+// A10 paper-literal option over NVLink: copy the shard into a peer-readable
+// slot, then per level every rank reads all members' buffers in place and sums them
+// in ascending digit (a full allreduce: each rank moves (g-1) * len bytes per level,
+// twice the reduce-scatter's), and finally keeps its range_to slice.
+hz_status p2p_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const float* in, int from_level, int to_level,
+                               float* out, cudaStream_t st) {
+  auto& P = ctx->p2p;
+  hz_status rc;
+  const int64_t n = p->len[from_level - 1];
+  const int64_t sel = p->off[to_level] - p->off[from_level - 1];
+  if ((rc = slot(ctx, P.ar_a, n * 4)) != HZ_OK) return rc;
+  if ((rc = slot(ctx, P.ar_b, n * 4)) != HZ_OK) return rc;
+  int64_t stride[HZ_MAX_LEVELS];
+  int64_t sacc = 1;
+  for (int l = 0; l < p->levels; ++l) {
+    stride[l] = sacc;
+    sacc *= p->group[l];
+  }
+  const size_t off[2] = {P.ar_a.off, P.ar_b.off};
+  const unsigned long long base = P.phase;
+  P.phase += static_cast<unsigned long long>(to_level - from_level + 1);
+  // copy-in (producer of phase base+1): the slot may still be read in phase base
+  {
+    Pieces pc{};
+    pc.n = 1;
+    pc.len = n;
+    pc.c[0] = reinterpret_cast<const uint8_t*>(in);
+    SyncArgs sq = make_sync(ctx, 0, base, base + 1, 0);
+    if ((rc = run_sum(pc, n, at<float>(ctx, ctx->rank, off[0]), st, from_level, &sq, 0)) != HZ_OK) return rc;
+  }
+  int cur = 0;
+  for (int l = from_level; l <= to_level; ++l) {
+    const int g = p->group[l - 1];
+    const int d = p->digit[l - 1];
+    const unsigned long long ph = base + static_cast<unsigned long long>(l - from_level + 1);
+    Pieces pc{};
+    pc.n = g;
+    pc.len = n;
+    int64_t remote = 0;
+    for (int j = 0; j < g; ++j) {
+      const int m = static_cast<int>(p->rank + (static_cast<int64_t>(j) - d) * stride[l - 1]);
+      pc.c[j] = at<const uint8_t>(ctx, m, off[cur]);
+      if (m != ctx->rank) remote += n * 4;
+    }
+    SyncArgs sr = l < to_level ? make_sync(ctx, ph, ph - 1, ph + 1, ph) : make_sync(ctx, ph, ph - 1, 0, ph);
+    if ((rc = run_sum(pc, n, at<float>(ctx, ctx->rank, off[cur ^ 1]), st, l, &sr, remote)) != HZ_OK) return rc;
+    cur ^= 1;
+  }
+  // select range_to (local; the slot's next writer waits for this rank's done flag,
+  // which follows this copy in stream order)
+  if ((rc = copy_async(out, at<float>(ctx, ctx->rank, off[cur]) + sel, static_cast<size_t>(p->len[to_level]) * 4,
+                       st)) != HZ_OK)
+    return rc;
+  clear_error();
+  return HZ_OK;
+}
+
 // Step tail over NVLink: AdamW writes the updated weights of range_L into a pool
 // slot (producer), then one copy kernel gathers the members' slots — the ranks that
 // share digits 1..w — into the primary range_w (consumer).

@@ -124,6 +124,7 @@ def adamw_params(lr, b1, b2, eps, wd, t):
 _sig("hz_adamw_step", [_vp, ctypes.POINTER(Partition), _vp, _vp, _vp, _vp, ctypes.POINTER(AdamWParams), _vp, _int,
                        _vp])
 _sig("hz_set_sm_budget", [_int])
+_sig("hz_allreduce_select", [_vp, _vp, _vp, _int, _int, _vp, _vp])
 _sig("hz_flat_allgather", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_flat_reduce_scatter", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_trace_begin", [_int, _int])
@@ -422,6 +423,14 @@ class Context:
                                             from_level, L if to_level is None else to_level, arr,
                                             _ptr(shard), int(bool(accumulate)), _stream(stream)))
         return shard
+
+    def allreduce_select(self, p, shard_in, out, from_level, to_level=None, stream=None):
+        """hz_allreduce_select: the paper-literal A10 step (fp32 allreduce over levels
+        from..to, ascending digit, then this rank's range_to slice into ``out``)."""
+        _check(_lib.hz_allreduce_select(self._h, ctypes.byref(p), _ptr(shard_in), int(from_level),
+                                        self.levels if to_level is None else int(to_level), _ptr(out),
+                                        _stream(stream)))
+        return out
 
     def adamw_step(self, p, grad_shard, master, m, v, hp, primary, stream=None):
         """hz_adamw_step: AdamW on range_L, then the post-update all-gather into primary."""

@@ -139,6 +139,27 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             except AssertionError as e:
                 errors.append(str(e))
 
+        # A10 paper-literal option: fp32 allreduce over levels frm..L, then select
+        # range_L — bitwise equal to the oracle's allreduce_select
+        for frm in sorted({1, L}):
+            p = ctx.partition(numel, B, 1, 1, L)
+            shards = {}
+            for q in range(world):
+                o, n_ = pm.range_at(q, g, Np, frm - 1)
+                shards[q] = synth.gradient_like(n_, 300 + q, block=B, specials=False)
+            want = col.allreduce_select(shards, g, Np, frm, L)
+            gin = to_dev(shards[rank])
+            gout = Guarded(p.range(L)[1], torch.float32)
+            ctx.allreduce_select(p, gin, gout.t, frm, L)
+            torch.cuda.synchronize()
+            try:
+                what = f"[{tag}] g={g} allreduce+select from level {frm}"
+                assert_bitwise(to_host(gout.t), want[rank], what)
+                gout.check(what)
+                assert_unchanged(gin, shards[rank], what)
+            except AssertionError as e:
+                errors.append(str(e))
+
         # step tail (N2): AdamW on range_L, post-update all-gather into range_w
         from oracle import optim
         for w in sorted({1, L, 0} & set(range(L + 1))):

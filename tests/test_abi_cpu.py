@@ -85,6 +85,16 @@ def test_partition_validation(hz):
         assert str(ei.value).split(": ", 1)[1].startswith(field), (kw, str(ei.value))
 
 
+def test_collective_validation_without_context(hz):
+    lib = hz.lib_handle()
+    p = hz.partition_ex(0, (2, 2), 1000)
+    # no context: rejected on the host, message names the field
+    assert lib.hz_allreduce_select(None, ctypes.byref(p), None, 1, 2, None, None) == hz.ERR_INVALID
+    assert lib.hz_last_error().startswith(b"ctx")
+    assert lib.hz_set_sm_budget(-1) == hz.ERR_INVALID
+    assert lib.hz_set_sm_budget(0) == hz.OK
+
+
 def test_codec_validation_without_gpu(hz):
     lib = hz.lib_handle()
     # rejected on the host before any CUDA call
