@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--qgz-bits", type=int, default=4)
     ap.add_argument("--block", type=int, default=256)
     ap.add_argument("--layers", type=int, default=0, help="limit the tensor count (debug only)")
+    ap.add_argument("--hierarchy", default="",
+                    help="override the hierarchy, e.g. 4 = one level over all ranks (ZeRO++-style flat "
+                         "qwZ / hpZ / qgZ) instead of the default 2,2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flat", action="store_true")
@@ -218,6 +221,15 @@ class Model:
             ctx.reduce_scatter_grads(t["p"], t["grad"], t["shard"], self.bits, stream=stream)
 
 
+def hierarchy_of(args, world):
+    if args.hierarchy:
+        g = tuple(int(x) for x in args.hierarchy.split(","))
+        if math.prod(g) != world:
+            raise SystemExit(f"--hierarchy {args.hierarchy}: product != {world} ranks")
+        return g
+    return HIERARCHY[args.config].get(world)
+
+
 def p2p_pool_bytes(args, group):
     """Symmetric pool: every tensor's hpZ secondary + the library's per-level send slots."""
     from paper_2501_04266_b200 import synth
@@ -307,7 +319,7 @@ def run_hz(args):
         dist.init_process_group("gloo")
     from paper_2501_04266_b200 import hz
 
-    group = HIERARCHY[args.config].get(world)
+    group = hierarchy_of(args, world)
     if group is None:
         raise SystemExit(f"no hierarchy for {world} GPUs")
     uid = hz.get_uid() if rank == 0 else None
@@ -728,7 +740,7 @@ def run_reference(args):
         return
     from paper_2501_04266_b200 import synth
     n = args.gpus
-    group = HIERARCHY[args.config][n]
+    group = hierarchy_of(args, n)
     numel = synth.layer_numel(synth.GPT_CONFIGS[args.config]["hidden"])
     numel = max(1, numel // n)
     for i in range(max(args.warmup, 3)):

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--modes", default="compute,hz,flat")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
+    ap.add_argument("--hierarchy", default="", help="override, e.g. 4 = ZeRO++-style one level over all ranks")
     ap.add_argument("--green", type=int, default=0,
                     help="run the communication stream in a CUDA green context of this many SMs "
                          "(libhz grids sized to it: hz_set_sm_budget)")
@@ -64,7 +65,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("gloo")
-    group = bench.HIERARCHY[args.config][world]
+    group = bench.hierarchy_of(args, world)
     cfg = synth.GPT_CONFIGS[args.config]
     h = cfg["hidden"]
     nl = args.layers or cfg["layers"]
