@@ -165,6 +165,29 @@ def ncu_traffic():
         return {}
 
 
+MIX_PROBE_ELEMS = 50358272
+MIX_PROBE_KINDS = {   # kernel kind -> probe mixes (tools/hbm_mix_probe.cu) it averages over
+    "quantize_dequantize": ("quantize_dequantize_bf16", "quantize_dequantize_f32"),
+    "dequantize": ("dequantize",),
+    "quantize": ("quantize",),
+}
+
+
+def same_mix_probe(kind, avg_elems, avg_ms):
+    """Time a plain streaming kernel with this kind's read:write byte mix takes for the
+    same element count (committed probe, profiles/hbm_mix_r01.json), and our kernel's
+    fraction of it (> 1: faster than the plain streaming kernel)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "hbm_mix_r01.json")) as f:
+            probe = json.load(f)
+        keys = MIX_PROBE_KINDS[kind]
+        us = sum(probe[k]["us"] for k in keys) / len(keys) * avg_elems / MIX_PROBE_ELEMS
+    except (OSError, ValueError, KeyError):
+        return {}
+    return {"same_mix_probe_us": us, "frac_of_same_mix_probe": us / (avg_ms * 1e3),
+            "same_mix_probe_source": "profiles/hbm_mix_r01.json (tools/hbm_mix_probe.cu)"}
+
+
 # --------------------------------------------------------------------- the step
 class Model:
     def __init__(self, hz, ctx, torch, config, rank, world, args, device):
@@ -414,6 +437,7 @@ def run_hz(args):
         roofline = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
                     "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes_per_launch": d["avg_bytes"],
                     "avg_launch_ms": d["avg_ms"], "peak_source": peak_src}
+        roofline.update(same_mix_probe(dom, d["avg_elems"], d["avg_ms"]))
         rb = d.get("avg_remote_bytes", 0)
         if rb:
             # fused NVLink kernel: the floor is the slower of local HBM bytes / HBM peak and
