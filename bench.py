@@ -46,6 +46,7 @@ HIERARCHY = {
 KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "quantize_dequantize", "reduce", "reduce_requant",
                 "quantize_push", "reduce_push", "ag_fused", "rs_fused")
 NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+NVLINK_BIDIR_PROBE_GBS = 620.0   # both GPUs of a pair pulling at once, per direction (profiles/bulk_probe_r01.txt)
 
 
 def parse():
@@ -447,6 +448,7 @@ def run_hz(args):
             roofline.update({"hbm_frac": d["GBps"] / peak, "nvlink_achieved": d["nvlink_GBps"],
                              "nvlink_peak": NVLINK_PEER_GBS, "nvlink_frac": d["nvlink_GBps"] / NVLINK_PEER_GBS,
                              "remote_bytes_per_launch": rb,
+                             "nvlink_frac_of_bidirectional_probe": d["nvlink_GBps"] / NVLINK_BIDIR_PROBE_GBS,
                              "floor_ms": max(t_hbm, t_nvl) * 1e3, "frac_of_floor": max(t_hbm, t_nvl) * 1e3 / d["avg_ms"]})
             if t_nvl > t_hbm:
                 roofline.update({"bound": "nvlink", "achieved": d["nvlink_GBps"], "peak": NVLINK_PEER_GBS,
