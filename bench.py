@@ -651,36 +651,90 @@ def cross_node_step(hz, ctx, torch, model, stream, world, args):
     return out
 
 
+def _host_registered(torch, numel, dtype):
+    """Page-locked host tensor of exactly numel elements (cudaHostRegister on a plain
+    CPU allocation; torch's pinned allocator would round each buffer up to a power
+    of two)."""
+    h = torch.empty(numel, dtype=dtype)
+    rc = torch.cuda.cudart().cudaHostRegister(h.data_ptr(), h.numel() * h.element_size(), 0)
+    if int(rc) != 0:
+        raise RuntimeError(f"cudaHostRegister failed ({rc})")
+    return h
+
+
+def _host_unregister(torch, h):
+    torch.cuda.cudart().cudaHostUnregister(h.data_ptr())
+
+
+def _pcie_probe(torch, h, d, stream):
+    """H2D alone, D2H alone and both at once on two streams: the copy floor of e2e."""
+    nb = min(h.numel() * h.element_size(), d.numel() * d.element_size())
+    hb, db = h.view(torch.uint8)[:nb], d.view(torch.uint8)[:nb]
+    hb2 = hb.clone().pin_memory() if nb <= (1 << 30) else None
+    out = {}
+    s2 = torch.cuda.Stream()
+    for name in ("h2d", "d2h", "both"):
+        best = None
+        for _ in range(3):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            with torch.cuda.stream(stream):
+                if name in ("h2d", "both"):
+                    db.copy_(hb, non_blocking=True)
+            if name in ("d2h", "both"):
+                s2.wait_event(e0)
+                with torch.cuda.stream(s2):
+                    (hb2 if (name == "both" and hb2 is not None) else hb).copy_(db, non_blocking=True)
+                stream.wait_stream(s2)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        out[name + "_GBps"] = (2 if name == "both" else 1) * nb / (best * 1e-3) / 1e9
+    out["probe_bytes"] = nb
+    return out
+
+
 def run_e2e(hz, ctx, torch, model, stream, world, args):
-    """Same step through the public API with inputs copied from pinned host memory each
-    step (primary + gradient per tensor) and the fp32 gradient shards read back."""
-    maxw = max(t["primary"].numel() for t in model.tensors)
-    maxg = max(t["grad"].numel() for t in model.tensors)
-    maxs = max(t["shard"].numel() for t in model.tensors)
-    hp = torch.empty(maxw, dtype=torch.bfloat16, pin_memory=True)
-    hg = torch.empty(maxg, dtype=torch.bfloat16, pin_memory=True)
-    hs = torch.empty(maxs, dtype=torch.float32, pin_memory=True)
-    # the host copies hold the same data as the device-resident inputs
-    hp[:model.tensors[0]["primary"].numel()].copy_(model.tensors[0]["primary"])
-    hg[:model.tensors[0]["grad"].numel()].copy_(model.tensors[0]["grad"])
-    bits = args.qwz_bits
-    h2d = sum(t["primary"].numel() * 2 + t["grad"].numel() * 2 for t in model.tensors)
-    d2h = sum(t["shard"].numel() * 4 for t in model.tensors)
+    """The same step end to end through the C-ABI with HOST buffers: hz_step_host
+    (csrc/executor.cpp) uploads every tensor's primary and gradient from page-locked
+    host memory, runs the gathers and the qgZ reduce-scatter, and downloads every fp32
+    gradient shard, the copies on the library's two copy streams overlapping each
+    other and the kernels.  Timed with CUDA events on the kernel stream (which waits
+    for the last download), back-to-back steps, max over ranks.  The host shards are
+    compared bitwise with the device-resident run's shards."""
+    L = ctx.levels
+    tens = model.tensors
+    h_p = _host_registered(torch, sum(t["primary"].numel() for t in tens), torch.bfloat16)
+    h_g = _host_registered(torch, sum(t["grad"].numel() for t in tens), torch.bfloat16)
+    h_s = _host_registered(torch, sum(t["shard"].numel() for t in tens), torch.float32)
+    free = torch.cuda.mem_get_info()[0]
+    fresh = free > h_s.numel() * 4 + (4 << 30)
+    io = []
+    op = og = os_ = 0
+    for t in tens:
+        npr, ngr, nsh = t["primary"].numel(), t["grad"].numel(), t["shard"].numel()
+        hp, hg, hs = h_p[op:op + npr], h_g[og:og + ngr], h_s[os_:os_ + nsh]
+        op, og, os_ = op + npr, og + ngr, os_ + nsh
+        hp.copy_(t["primary"])
+        hg.copy_(t["grad"])
+        io.append({"p": t["p"], "h_primary": hp, "d_primary": t["primary"], "h_grad": hg, "d_grad": t["grad"],
+                   "sec_codes": t["sec_c"], "sec_scales": t["sec_s"],
+                   "d_shard": torch.empty_like(t["shard"]) if fresh else t["shard"], "h_shard": hs})
+    h2d = sum(t["primary"].numel() * 2 + t["grad"].numel() * 2 for t in tens)
+    d2h = sum(t["shard"].numel() * 4 for t in tens)
+    sargs = ctx.step_host_args(io, model.bits)
 
     def step():
-        for i, t in enumerate(model.tensors):
-            t["primary"].copy_(hp[:t["primary"].numel()], non_blocking=True)
-            model.ctx.allgather_params(t["p"], t["primary"], t["sec_c"], t["sec_s"], model.full[i & 1],
-                                       bits=bits, stream=stream)
-        for i, t in reversed(list(enumerate(model.tensors))):
-            t["grad"].copy_(hg[:t["grad"].numel()], non_blocking=True)
-            model.ctx.allgather_params(t["p"], None, t["sec_c"], t["sec_s"], model.full[i & 1], bits=bits,
-                                       backward=True, stream=stream)
-            model.ctx.reduce_scatter_grads(t["p"], t["grad"], t["shard"], model.bits, stream=stream)
-            hs[:t["shard"].numel()].copy_(t["shard"], non_blocking=True)
+        ctx.step_host(sargs, model.full, qwz_bits=args.qwz_bits, stream=stream)
 
     step()
     torch.cuda.synchronize()
+    match = None
+    if fresh:
+        match = all(torch.equal(io[i]["h_shard"].view(torch.int32), t["shard"].cpu().view(torch.int32))
+                    for i, t in enumerate(tens))
     barrier(world)
     n = max(1, min(args.steps, 5))
     e0 = torch.cuda.Event(enable_timing=True)
@@ -691,8 +745,16 @@ def run_e2e(hz, ctx, torch, model, stream, world, args):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world) / n
+    probe = _pcie_probe(torch, h_s, io[0]["d_shard"] if fresh else model.full[0], stream)
+    floor_ms = max(h2d / (probe["h2d_GBps"] * 1e9), d2h / (probe["d2h_GBps"] * 1e9),
+                   (h2d + d2h) / (probe["both_GBps"] * 1e9)) * 1e3
+    for h in (h_p, h_g, h_s):
+        _host_unregister(torch, h)
     return {"value": world * model.logical_bytes / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": "hz_step_host (C-ABI, host buffers; copies on two library streams overlapping the kernels)",
+            "host_shards_equal_device_run": match,
+            "pcie_probe": probe, "pcie_floor_ms": floor_ms, "frac_of_pcie_floor": floor_ms / ms}
 
 
 # ------------------------------------------------------------------ CPU oracle

@@ -301,6 +301,49 @@ HZ_API hz_status hz_adamw_step(hz_ctx* ctx, const hz_partition_t* p, const float
                                float* master, float* m, float* v, const hz_adamw_t* hp,
                                void* primary, hz_dtype dt, void* stream);
 
+/* Host-staged step executor: one step of the hot path with its inputs and results
+ * in HOST memory (the end-to-end form of SURVEY §8(d)'s step; the per-layer phase
+ * order of P:275 / S:359 with one micro-batch, GA = 1).  For n tensors t[0..n-1]:
+ *   forward : i = 0..n-1   copy t[i].h_primary -> t[i].d_primary (dt[len_w]),
+ *                          hz_allgather_params(forward, qwz_bits) -> full_out[i % 2];
+ *   backward: i = n-1..0   copy t[i].h_grad -> t[i].d_grad (dt[Np]),
+ *                          hz_allgather_params(backward) -> full_out[i % 2],
+ *                          hz_reduce_scatter_grads(levels 1..L, qgz_bits) -> t[i].d_shard,
+ *                          copy t[i].d_shard -> t[i].h_shard (fp32[len_L]).
+ * The copies run on two library-owned streams (host->device and device->host), the
+ * kernels on `stream`; per-tensor events order them, so the PCIe transfers of the
+ * two directions overlap each other and the kernels.  `stream` finally waits for
+ * every device->host copy: once `stream` passes this call, every h_shard holds the
+ * step's fp32 gradient shard (bitwise the result of the device-resident calls).
+ * The host->device copies of a call wait only for the previous call's kernels, so
+ * back-to-back calls upload the next step's inputs while this step's shards are
+ * still being read back.
+ * Ownership: the caller owns every buffer.  h_* should be page-locked
+ * (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous; they must
+ * not be modified (h_primary, h_grad) or read (h_shard) before `stream` passes the
+ * call.  d_primary / d_grad are staging buffers the executor writes; the caller
+ * must not use them on other streams meanwhile.  sec_codes / sec_scales: the hpZ
+ * secondary of range_s (P2P transport: from hz_sym_alloc).  full_out0/1: device
+ * out_dt[max Np] gathered-layer buffers, alternating between tensors.
+ * Errors: HZ_ERR_INVALID (n < 1, NULL pointers, a partition of another context,
+ * misaligned device pointers; message names the tensor and field; nothing is
+ * enqueued), HZ_ERR_CUDA, HZ_ERR_NCCL; errors of the underlying calls are passed
+ * through (work already enqueued for earlier tensors stays enqueued). */
+typedef struct {
+  const hz_partition_t* p;
+  const void* h_primary; /* host dt[len_w] (range_w) */
+  void* d_primary;       /* device dt[len_w] */
+  const void* h_grad;    /* host dt[Np] */
+  void* d_grad;          /* device dt[Np] */
+  uint8_t* sec_codes;    /* device, range_s codes (len_s*qwz_bits/8 bytes) */
+  float* sec_scales;     /* device, range_s scales (len_s/block fp32) */
+  float* d_shard;        /* device fp32[len_L] */
+  float* h_shard;        /* host fp32[len_L] */
+} hz_tensor_io;
+HZ_API hz_status hz_step_host(hz_ctx* ctx, int n, const hz_tensor_io* t, hz_dtype dt, int qwz_bits,
+                              const int* qgz_bits, void* full_out0, void* full_out1, hz_dtype out_dt,
+                              void* stream);
+
 /* Flat ZeRO-3 baseline (Table VII/VIII row "ZeRO-3"): plain ncclAllGather of
  * the rank's bf16/fp16/fp32 chunk (numel/world elements, rank order) into
  * out[numel], and plain ncclReduceScatter(sum) of in[numel] into

@@ -48,6 +48,15 @@ struct hz_ctx {
     Slot ag_recv_c, ag_recv_s;                  // forward gather: D pieces of the primary codes
     Slot rs_recv_c[HZ_MAX_LEVELS + 1], rs_recv_s[HZ_MAX_LEVELS + 1];   // level-l: g chunks destined here
   } p2p;
+
+  // Host-staged step executor (hz_step_host, executor.cpp): copy streams and events,
+  // created on first use.
+  struct Exec {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev;        // 3 per tensor: primary in, grad in, shard ready
+    cudaEvent_t kernels_done = nullptr; // the previous call's last kernel
+    cudaEvent_t d2h_done = nullptr;
+  } exec;
 };
 
 namespace hz {
@@ -104,6 +113,7 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
                              int from_level, int to_level, const int* bits_per_level, float* shard,
                              int accumulate, cudaStream_t st);
 void p2p_release(hz_ctx* ctx);
+void exec_release(hz_ctx* ctx);   // executor.cpp
 hz_status p2p_adamw_gather(hz_ctx* ctx, const hz_partition_t* p, const float* g, float* th, float* m, float* v,
                            const AdamW& hp, void* primary, hz_dtype dt, cudaStream_t st);
 hz_status run_adamw(const float* g, float* th, float* m, float* v, void* out, hz_dtype dt, int64_t n,

@@ -305,11 +305,12 @@ hz_status hz_finalize(hz_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   p2p_release(ctx);
+  exec_release(ctx);
   for (int l = 0; l < HZ_MAX_LEVELS; ++l)
     if (ctx->lvl[l]) ncclCommDestroy(ctx->lvl[l]);
   if (ctx->world_comm) ncclCommDestroy(ctx->world_comm);
   for (auto* b : {&ctx->ag_c, &ctx->ag_s, &ctx->rs_a_c, &ctx->rs_a_s, &ctx->rs_b_c, &ctx->rs_b_s,
-                  &ctx->rs_r_c, &ctx->rs_r_s})
+                  &ctx->rs_r_c, &ctx->rs_r_s, &ctx->ar_a, &ctx->ar_b, &ctx->ar_g})
     free_buf(*b);
   delete ctx;
   clear_error();

@@ -126,6 +126,23 @@ _sig("hz_adamw_step", [_vp, ctypes.POINTER(Partition), _vp, _vp, _vp, _vp, ctype
 _sig("hz_set_sm_budget", [_int])
 _sig("hz_allreduce_select", [_vp, _vp, _vp, _int, _int, _vp, _vp])
 _sig("hz_flat_allgather", [_vp, _vp, _vp, _i64, _int, _vp])
+
+
+class StepHostArgs:
+    """Marshalled hz_step_host arguments (keeps the partitions and tensors alive)."""
+
+    def __init__(self, io, n, dt, bits, keep):
+        self.io, self.n, self.dt, self.bits, self._keep = io, n, dt, bits, keep
+
+
+class TensorIO(ctypes.Structure):
+    """hz_tensor_io: one tensor of an hz_step_host call (host + device buffers)."""
+    _fields_ = [("p", ctypes.POINTER(Partition)), ("h_primary", _vp), ("d_primary", _vp), ("h_grad", _vp),
+                ("d_grad", _vp), ("sec_codes", _vp), ("sec_scales", _vp), ("d_shard", _vp), ("h_shard", _vp)]
+
+
+_sig("hz_step_host", [_vp, _int, ctypes.POINTER(TensorIO), _int, _int, ctypes.POINTER(ctypes.c_int), _vp, _vp,
+                      _int, _vp])
 _sig("hz_flat_reduce_scatter", [_vp, _vp, _vp, _i64, _int, _vp])
 _sig("hz_trace_begin", [_int, _int])
 _sig("hz_trace_end", [])
@@ -437,6 +454,30 @@ class Context:
         _check(_lib.hz_adamw_step(self._h, ctypes.byref(p), _ptr(grad_shard), _ptr(master), _ptr(m), _ptr(v),
                                   ctypes.byref(hp), _ptr(primary), _dtype_code(primary), _stream(stream)))
         return primary
+
+    def step_host(self, tensors, full_out, qwz_bits=8, qgz_bits=None, stream=None):
+        """hz_step_host: one step (forward gather, backward gather, qgZ of every tensor)
+        with host inputs and host fp32 shards.  ``tensors``: list of dicts with keys
+        p, h_primary, d_primary, h_grad, d_grad, sec_codes, sec_scales, d_shard, h_shard
+        (torch tensors; h_* pinned CPU tensors).  ``full_out``: two device buffers.
+        Build the argument array once with :meth:`step_host_args` and pass it back to
+        reuse it across steps."""
+        args = tensors if isinstance(tensors, StepHostArgs) else self.step_host_args(tensors, qgz_bits)
+        _check(_lib.hz_step_host(self._h, args.n, args.io, args.dt, qwz_bits, args.bits, _ptr(full_out[0]),
+                                 _ptr(full_out[1]), _dtype_code(full_out[0]), _stream(stream)))
+
+    def step_host_args(self, tensors, qgz_bits=None):
+        L = self.levels
+        bpl = list(qgz_bits) if qgz_bits is not None else [4] * L
+        bpl = bpl + [4] * (L - len(bpl))
+        io = (TensorIO * len(tensors))()
+        for k, t in enumerate(tensors):
+            io[k].p = ctypes.pointer(t["p"])
+            for f in ("h_primary", "d_primary", "h_grad", "d_grad", "sec_codes", "sec_scales", "d_shard",
+                      "h_shard"):
+                setattr(io[k], f, _ptr(t[f]))
+        return StepHostArgs(io, len(tensors), _dtype_code(tensors[0]["d_primary"]), (ctypes.c_int * L)(*bpl),
+                            tensors)
 
     def flat_allgather(self, chunk, out, stream=None):
         _check(_lib.hz_flat_allgather(self._h, _ptr(chunk), _ptr(out), out.numel(),

@@ -256,6 +256,8 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             errors.append(str(e))
         del graph
 
+        errors += check_step_host(ctx, hz, rank, world, g, sec_buffers, tag, B)
+
         # flat ZeRO-3 baseline collectives (plain NCCL)
         n = world * 4096
         x = torch.arange(n, dtype=torch.float32, device="cuda") + rank
@@ -274,6 +276,64 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             errors.append(str(e))
     finally:
         ctx.close()
+    return errors
+
+
+def check_step_host(ctx, hz, rank, world, g, sec_buffers, tag, B, sizes=(150_001, 70_000, 4097)):
+    """hz_step_host (host-staged executor): three tensors of different sizes, two
+    back-to-back calls with different host inputs and host shard buffers, no sync
+    in between (the second call's uploads overlap the first call's downloads).
+    Every host shard must equal the oracle's qgZ shard of its own call's inputs, and
+    the gathered buffers the oracle's forward gather of the last two tensors."""
+    errors = []
+    L = len(g)
+    parts = [ctx.partition(n, B, 1, 1, L) for n in sizes]
+    Nmax = max(p.padded_numel for p in parts)
+    full = [torch.empty(Nmax, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    dev = []
+    for p in parts:
+        sl = p.range(1)[1]
+        sc, ss = sec_buffers(sl, sl // B)
+        dev.append({"p": p, "d_primary": torch.empty(p.range(1)[1], dtype=torch.bfloat16, device="cuda"),
+                    "d_grad": torch.empty(p.padded_numel, dtype=torch.bfloat16, device="cuda"),
+                    "sec_codes": sc, "sec_scales": ss,
+                    "d_shard": torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")})
+    calls = []
+    for c in range(2):
+        io, want = [], []
+        for k, (n, p, d) in enumerate(zip(sizes, parts, dev)):
+            Np = p.padded_numel
+            fr = np.zeros(Np, np.float32)
+            fr[:n] = synth.params_like(n, 300 + 10 * c + k, block=B)
+            fr = fr.astype(ml_dtypes.bfloat16)
+            gr = {}
+            for r in range(world):
+                x = np.zeros(Np, np.float32)
+                x[:n] = synth.gradient_like(n, 900 + 100 * c + 10 * k + r, block=B)
+                gr[r] = x.astype(ml_dtypes.bfloat16)
+            off, ln = p.range(1)
+            prim = {r: fr[pm.range_at(r, g, Np, 1)[0]:sum(pm.range_at(r, g, Np, 1))] for r in range(world)}
+            h_primary = torch.from_numpy(fr[off:off + ln].view(np.uint16).copy()).view(torch.bfloat16).pin_memory()
+            h_grad = torch.from_numpy(gr[rank].view(np.uint16).copy()).view(torch.bfloat16).pin_memory()
+            h_shard = torch.full((p.range(L)[1],), float("nan"), dtype=torch.float32).pin_memory()
+            io.append(dict(d, h_primary=h_primary, h_grad=h_grad, h_shard=h_shard))
+            want.append((col.allgather_forward(prim, g, Np, B, 1, 1, bits=8)[0][rank],
+                         col.reduce_scatter(gr, g, Np, B, 1, L, {l: 4 for l in range(1, L + 1)})[rank]))
+        calls.append((ctx.step_host_args(io, [4] * L), io, want))
+    st = torch.cuda.current_stream()
+    for args, _, _ in calls:
+        ctx.step_host(args, full, qwz_bits=8, stream=st)
+    torch.cuda.synchronize()
+    try:
+        for c, (_, io, want) in enumerate(calls):
+            for k, t in enumerate(io):
+                assert_bitwise(t["h_shard"].numpy(), want[k][1], f"[{tag}] g={g} step_host call {c} tensor {k} shard")
+        last = calls[-1][2]
+        for k in (0, 1):   # full_out[k % 2] last written by tensor k's backward gather (tensors run n-1..0)
+            Np = parts[k].padded_numel
+            assert_bitwise(to_host(full[k][:Np]), last[k][0], f"[{tag}] g={g} step_host gathered tensor {k}")
+    except AssertionError as e:
+        errors.append(str(e))
     return errors
 
 
