@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--qwz-bits", type=int, default=8)
     ap.add_argument("--qgz-bits", type=int, default=4)
     ap.add_argument("--block", type=int, default=256)
+    ap.add_argument("--roles", default="1,1",
+                    help="w,s role levels (primary, hpZ secondary); 1,1 = the paper's ZeRO-topo (setting T); "
+                         "L,1 or L,2 = ZeRO++ inside the hierarchy (setting Z); s=0 keeps a replicated secondary")
     ap.add_argument("--layers", type=int, default=0, help="limit the tensor count (debug only)")
     ap.add_argument("--hierarchy", default="",
                     help="override the hierarchy, e.g. 4 = one level over all ranks (ZeRO++-style flat "
@@ -73,7 +76,9 @@ def parse():
     ap.add_argument("--no-trace", action="store_true", help="no per-launch events (overhead check)")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
                     help="capture one step in a CUDA graph and time graph replays (--no-graph: eager)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    args.w, args.s = (int(x) for x in args.roles.split(","))
+    return args
 
 
 def dist_env():
@@ -204,9 +209,9 @@ class Model:
         max_np = 0
         self.p2p = ctx.p2p
         for i, (name, numel) in enumerate(tensors):
-            p = ctx.partition(numel, B, w=1, s=1, gl=L)
+            p = ctx.partition(numel, B, w=args.w, s=args.s, gl=L)
             Np = p.padded_numel
-            off_w, len_w = p.range(1)
+            off_w, len_w = p.range(args.w)
             seed = 2000 + 97 * rank + i
             full_p = synth.torch_normal(Np, 7000 + i, 0.02, torch.bfloat16, device, outlier_every=0)
             full_p[numel:] = 0                                       # zero padding (O2)
@@ -214,7 +219,7 @@ class Model:
             del full_p
             grad = synth.torch_normal(Np, seed, 1e-3, torch.bfloat16, device)
             grad[numel:] = 0
-            _, len_s = p.range(1)
+            _, len_s = p.range(args.s)
             _, len_l = p.range(L)
             t = {
                 "name": name, "numel": numel, "p": p, "primary": primary, "grad": grad,
@@ -264,8 +269,11 @@ def p2p_pool_bytes(args, group):
     max_np = 0
     for _, numel in synth.model_tensors(args.config):
         Np = -(-numel // unit) * unit
-        len_s = Np // group[0]
+        len_s = Np // math.prod(group[:args.s])
+        len_w = Np // math.prod(group[:args.w])
         total += len_s * args.qwz_bits // 8 + len_s // B * 4 + 512
+        if args.s != args.w:                                      # quantized-primary slot
+            total += len_w * args.qwz_bits // 8 + len_w // B * 4 + 512
         max_np = max(max_np, Np)
     total += 2 * len(group) * (max_np + max_np // B * 4 + 512)   # slots (may grow once)
     total += 2 * (max_np // W) * 4 + 1024                       # step-tail update slot
@@ -346,6 +354,8 @@ def run_hz(args):
     group = hierarchy_of(args, world)
     if group is None:
         raise SystemExit(f"no hierarchy for {world} GPUs")
+    if not (1 <= args.w <= len(group) and 0 <= args.s <= len(group)):
+        raise SystemExit(f"--roles {args.roles}: need 1 <= w <= L and 0 <= s <= L (L = {len(group)})")
     uid = hz.get_uid() if rank == 0 else None
     if world > 1:
         import torch.distributed as dist
@@ -506,7 +516,7 @@ def run_hz(args):
         "data": "synthetic (seeded torch.Generator on device: params N(0,0.02^2), grads N(0,1e-6) with 1/1024 x64 outliers)",
         "config": {
             "workload": f"{args.config}: {len(model.tensors)} flat per-tensor buffers ({model.logical_bytes // 6:,} params), "
-                        f"setting T (w=1, s=1, gl=L), GA=1",
+                        f"{'setting T' if (args.w, args.s) == (1, 1) else 'roles'} (w={args.w}, s={args.s}, gl=L), GA=1",
             "hierarchy": list(group), "block": args.block, "qwz_bits": args.qwz_bits, "qgz_bits": args.qgz_bits,
             "io": "bf16 params/grads in, bf16 gathered layers out, fp32 scales, fp32 gradient shard",
             "l2": "inputs larger than L2 (each step streams several GB); no flush",
@@ -524,9 +534,13 @@ def run_hz(args):
         "step_tail": tail,
         "a10_cross_node_step": a10,
     }
-    ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
+    # a CUDA graph that captured NCCL calls must be destroyed before its communicators
+    # (ncclCommDestroy waits for the graph's resources otherwise)
+    del graph
+    torch.cuda.synchronize()
+    ctx.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -730,6 +744,7 @@ def run_e2e(hz, ctx, torch, model, stream, world, args):
         ctx.step_host(sargs, model.full, qwz_bits=args.qwz_bits, stream=stream)
 
     step()
+    model.step(stream)        # device-resident step on the same inputs: reference shards in t["shard"]
     torch.cuda.synchronize()
     match = None
     if fresh:
@@ -858,6 +873,11 @@ def run_reference(args):
 
 def main():
     args = parse()
+    wd = float(os.environ.get("HZ_BENCH_WATCHDOG", "0"))
+    if wd > 0:
+        # debug aid: dump every thread's Python stack and exit if the run exceeds wd seconds
+        import faulthandler
+        faulthandler.dump_traceback_later(wd, exit=True)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch_under_torchrun(args)
     if args.impl == "reference":

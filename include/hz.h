@@ -197,7 +197,10 @@ HZ_API hz_status hz_get_uid(hz_uid* out);
 HZ_API hz_status hz_init(hz_ctx** out, int rank, int world, const hz_uid* uid, int levels,
                   const int* group, int cuda_device, size_t workspace_bytes);
 
-/* Destroys the communicators and frees the workspace.  NULL is a no-op. */
+/* Destroys the communicators and frees the workspace.  NULL is a no-op.  CUDA graphs
+ * that captured this context's NCCL-transport calls must be destroyed first (NCCL
+ * keeps graph-owned resources on the communicators; destroying them under a live
+ * graph blocks). */
 HZ_API hz_status hz_finalize(hz_ctx* ctx);
 
 /* hz_partition_ex for the context's rank and hierarchy. */

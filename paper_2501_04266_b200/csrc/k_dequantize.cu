@@ -67,6 +67,22 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
         sc[2] = s4.z;
         sc[3] = s4.w;
         fast = true;
+      } else if (inter || (pc.n == 1 && ub + 32 * U <= nunits)) {
+        // any other block size, a full tile (1024 elements starting at a multiple of
+        // 1024): its NS = max(1, 1024/B) scales are consecutive — lane k < NS loads
+        // scale k (one request for the tile), every lane takes its unit's scale by
+        // shuffle.  (B >= 1024: the tile lies inside one block, NS = 1.)
+        if (!inter) jt = 0;
+        const int64_t r0 = ub * 8 - jt * pc.len;
+        const bool head = r0 < pc.split && pc.cr[jt] != nullptr;
+        const uint8_t* cb = (head ? pc.cr[jt] : pc.c[jt]) + (r0 + lane * 8) * BITS / 8;
+        const int ns = log2b >= 10 ? 1 : (1024 >> log2b);
+        const float mine = __ldg((head ? pc.sr[jt] : pc.s[jt]) + (r0 >> log2b) + (lane < ns ? lane : ns - 1));
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u].load(cb + u * 256 * BITS / 8);
+#pragma unroll
+        for (int u = 0; u < U; ++u) sc[u] = __shfl_sync(0xffffffffu, mine, (u * 256 + lane * 8) >> log2b);
+        fast = true;
       }
     }
 #pragma unroll

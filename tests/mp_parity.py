@@ -425,6 +425,12 @@ def run(rank, world, local, bcast=None):
             if bcast is not None:
                 uid = bcast(uid)
             errors += check_hierarchy(hz, rank, world, g, uid, local, p2p=p2p)
+    # other block sizes through the fused P2P gather (its tile-scale fast path differs for B != 256)
+    for B in (64, 1024):
+        uid = hz.get_uid() if rank == 0 else None
+        if bcast is not None:
+            uid = bcast(uid)
+        errors += check_hierarchy(hz, rank, world, HIERARCHIES[world][0], uid, local, numel=90_001, B=B, p2p=True)
     # bench configuration at GPT-1.3B layer size, first hierarchy of this world size
     numel = synth.layer_numel(synth.GPT_CONFIGS["gpt1.3b"]["hidden"])
     for p2p in (False, True):
