@@ -93,6 +93,9 @@ def test_collective_validation_without_context(hz):
     assert lib.hz_last_error().startswith(b"ctx")
     assert lib.hz_set_sm_budget(-1) == hz.ERR_INVALID
     assert lib.hz_set_sm_budget(0) == hz.OK
+    bits = (ctypes.c_int * 2)(4, 4)
+    assert lib.hz_step_host(None, 1, None, hz.BF16, 8, bits, None, None, hz.BF16, None) == hz.ERR_INVALID
+    assert lib.hz_last_error().startswith(b"ctx")
 
 
 def test_codec_validation_without_gpu(hz):

@@ -65,3 +65,37 @@ def test_world1_full_size_neox20b():
     errors = mp_parity.check_full_size(hz, 0, 1, (1,), hz.get_uid(), 0, numel, p2p=False)
     assert not errors, "\n".join(errors)
     torch.cuda.empty_cache()
+
+
+def test_step_host_validation():
+    """hz_step_host rejects bad arguments on the host, naming the tensor and field,
+    and enqueues nothing."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2501_04266_b200 import hz
+    ctx = hz.Context(0, 1, hz.get_uid(), (1,), 0)
+    try:
+        p = ctx.partition(4096, 256, 1, 1, 1)
+        d = lambda n, dt: torch.empty(n, dtype=dt, device="cuda")
+        t = {"p": p, "h_primary": torch.empty(4096, dtype=torch.bfloat16).pin_memory(),
+             "d_primary": d(p.range(1)[1], torch.bfloat16),
+             "h_grad": torch.empty(p.padded_numel, dtype=torch.bfloat16).pin_memory(),
+             "d_grad": d(p.padded_numel, torch.bfloat16), "sec_codes": d(p.range(1)[1], torch.uint8),
+             "sec_scales": d(p.range(1)[1] // 256, torch.float32), "d_shard": d(p.range(1)[1], torch.float32),
+             "h_shard": None}
+        full = [d(p.padded_numel, torch.bfloat16) for _ in range(2)]
+        with pytest.raises(hz.HZError) as ei:
+            ctx.step_host([t], full)
+        assert ei.value.status == hz.ERR_INVALID and "t[0].h_shard" in str(ei.value)
+        t["h_shard"] = torch.empty(p.range(1)[1], dtype=torch.float32).pin_memory()
+        with pytest.raises(hz.HZError) as ei:
+            ctx.step_host([t], full, qwz_bits=5)
+        assert "qwz_bits" in str(ei.value)
+        bad = dict(t, d_grad=t["d_grad"][1:])                      # misaligned device pointer
+        with pytest.raises(hz.HZError) as ei:
+            ctx.step_host([t, bad], full)
+        assert "t[1].d_grad" in str(ei.value)
+        ctx.step_host([t], full)                                   # valid call still works
+        torch.cuda.synchronize()
+    finally:
+        ctx.close()
