@@ -410,16 +410,19 @@ def run_hz(args):
         torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    e0, e1 = ev[0], ev[-1]
     e0.record(stream)
-    for _ in range(args.steps):
+    for k in range(args.steps):
         if graph is not None:
             graph.replay()
         else:
             model.step(stream)
-    e1.record(stream)
+        ev[k + 1].record(stream)
     torch.cuda.synchronize()
+    per_step = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps))
+    pct = {f"p{q}": max_over_ranks(per_step[min(len(per_step) - 1, int(round(q / 100 * (len(per_step) - 1))))], world)
+           for q in (10, 50, 90)}
     if graph is not None and transport == "p2p":
         ctx.p2p_replayed(args.steps)
     barrier(world)
@@ -511,7 +514,7 @@ def run_hz(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "ms_per_step_pct": pct, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded torch.Generator on device: params N(0,0.02^2), grads N(0,1e-6) with 1/1024 x64 outliers)",
         "config": {
