@@ -43,7 +43,8 @@ HIERARCHY = {
     "gpt6.7b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
     "neox20b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
 }
-KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "quantize_dequantize", "reduce", "reduce_requant",
+KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "gather_quantize", "quantize_dequantize", "reduce",
+                "reduce_requant",
                 "quantize_push", "reduce_push", "ag_fused", "rs_fused")
 NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 NVLINK_BIDIR_PROBE_GBS = 620.0   # both GPUs of a pair pulling at once, per direction (profiles/bulk_probe_r01.txt)
@@ -62,6 +63,9 @@ def parse():
     ap.add_argument("--roles", default="1,1",
                     help="w,s role levels (primary, hpZ secondary); 1,1 = the paper's ZeRO-topo (setting T); "
                          "L,1 or L,2 = ZeRO++ inside the hierarchy (setting Z); s=0 keeps a replicated secondary")
+    ap.add_argument("--pipelined", action=argparse.BooleanOptionalAction, default=True,
+                    help="issue the step through hz_allgather_params_next / hz_backward_step (adjacent layers "
+                         "paired in one launch on the P2P transport); --no-pipelined: one call per collective")
     ap.add_argument("--layers", type=int, default=0, help="limit the tensor count (debug only)")
     ap.add_argument("--hierarchy", default="",
                     help="override the hierarchy, e.g. 4 = one level over all ranks (ZeRO++-style flat "
@@ -240,14 +244,33 @@ class Model:
         return self.torch.empty(numel, dtype=dtype, device=device)
 
     def step(self, stream):
-        ctx, bits = self.ctx, self.args.qwz_bits
-        for i, t in enumerate(self.tensors):                         # forward: qwZ + hpZ
-            ctx.allgather_params(t["p"], t["primary"], t["sec_c"], t["sec_s"], self.full[i & 1], bits=bits,
-                                 stream=stream)
-        for i, t in reversed(list(enumerate(self.tensors))):        # backward: gather from secondary, qgZ
-            ctx.allgather_params(t["p"], None, t["sec_c"], t["sec_s"], self.full[i & 1], bits=bits,
-                                 backward=True, stream=stream)
-            ctx.reduce_scatter_grads(t["p"], t["grad"], t["shard"], self.bits, stream=stream)
+        ctx, bits, T = self.ctx, self.args.qwz_bits, self.tensors
+        if not self.args.pipelined:
+            for i, t in enumerate(T):                                # forward: qwZ + hpZ
+                ctx.allgather_params(t["p"], t["primary"], t["sec_c"], t["sec_s"], self.full[i & 1], bits=bits,
+                                     stream=stream)
+            for i, t in reversed(list(enumerate(T))):               # backward: gather from secondary, qgZ
+                ctx.allgather_params(t["p"], None, t["sec_c"], t["sec_s"], self.full[i & 1], bits=bits,
+                                     backward=True, stream=stream)
+                ctx.reduce_scatter_grads(t["p"], t["grad"], t["shard"], self.bits, stream=stream)
+            return
+        # the same calls in a training step's issue order, adjacent layers paired
+        # (hz_allgather_params_next / hz_backward_step: one launch per pair on the P2P transport)
+        n = len(T)
+        for i, t in enumerate(T):                                    # forward: gather i, prefetch quantize i+1
+            nx = T[i + 1] if i + 1 < n else None
+            ctx.allgather_params_next(t["p"], t["primary"], t["sec_c"], t["sec_s"], self.full[i & 1], bits=bits,
+                                      p_next=nx["p"] if nx else None, next_primary=nx["primary"] if nx else None,
+                                      next_sec_codes=nx["sec_c"] if nx else None,
+                                      next_sec_scales=nx["sec_s"] if nx else None, stream=stream)
+        t = T[n - 1]
+        ctx.allgather_params(t["p"], None, t["sec_c"], t["sec_s"], self.full[(n - 1) & 1], bits=bits, backward=True,
+                             stream=stream)
+        for i in range(n - 1, -1, -1):                               # backward: qgZ of i || gather of i-1
+            t, pv = T[i], (T[i - 1] if i > 0 else None)
+            ctx.backward_step(t["p"], t["grad"], t["shard"], self.bits, p_prev=pv["p"] if pv else None,
+                              prev_sec_codes=pv["sec_c"] if pv else None, prev_sec_scales=pv["sec_s"] if pv else None,
+                              prev_full_out=self.full[(i - 1) & 1] if pv else None, prev_bits=bits, stream=stream)
 
 
 def hierarchy_of(args, world):
@@ -526,6 +549,7 @@ def run_hz(args):
             "parallelism": f"dp{world} hierarchical ({'x'.join(map(str, group))})",
             "transport": transport,
             "cuda_graph": graph is not None,
+            "pipelined": args.pipelined,
         },
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -222,6 +222,38 @@ HZ_API hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int b
                               uint8_t* sec_codes, float* sec_scales,
                               void* full_out, hz_dtype out_dt, void* stream);
 
+/* Forward gather with the next layer's quantize prefetched (qwZ, same result as
+ * hz_allgather_params forward for layer p): the gather + dequantize of layer p and
+ * the quantize of layer p_next's primary (next_primary, dt[len_w of p_next]) into its
+ * secondary buffers (next_sec_codes / next_sec_scales, int8 codes + fp32 scales of
+ * range_s) run in ONE kernel (P2P transport: the NVLink-bound gather and the
+ * HBM-bound quantize overlap; one launch and one cross-GPU synchronisation fewer).
+ * The next call for layer p_next (hz_allgather_params or _next, with the same primary
+ * and secondary pointers, and no other collective call in between) then skips its
+ * quantize.  The caller must not modify next_primary in between.  p_next == NULL:
+ * exactly hz_allgather_params(forward).  Not fusable (NCCL transport, s != w, block
+ * != 256, bits != 8, out_dt != bf16): the prefetch is skipped and the next call
+ * quantizes itself — results are bitwise identical either way.  Errors as
+ * hz_allgather_params; p_next / next_* fields are named in the message. */
+HZ_API hz_status hz_allgather_params_next(hz_ctx* ctx, const hz_partition_t* p, const void* primary, hz_dtype dt,
+                                          int bits, uint8_t* sec_codes, float* sec_scales, void* full_out,
+                                          hz_dtype out_dt, const hz_partition_t* p_next, const void* next_primary,
+                                          uint8_t* next_sec_codes, float* next_sec_scales, void* stream);
+
+/* Backward step of a layer pair: the qgZ reduce-scatter of layer p's gradient
+ * (exactly hz_reduce_scatter_grads with the same arguments) and the backward
+ * all-gather of the previous layer p_prev from its secondary (exactly
+ * hz_allgather_params(backward = 1, bits = prev_bits) into prev_full_out) — the
+ * order a training step issues them in (layer i's gradients are reduced while layer
+ * i-1's weights are gathered for its backward).  P2P transport, B = 256, bf16
+ * output: the gather and the level-`from` quantize run in ONE kernel; otherwise the
+ * gather then the reduce-scatter.  p_prev == NULL: exactly hz_reduce_scatter_grads. */
+HZ_API hz_status hz_backward_step(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
+                                  int from_level, int to_level, const int* bits_per_level, float* shard,
+                                  int accumulate, const hz_partition_t* p_prev, uint8_t* prev_sec_codes,
+                                  float* prev_sec_scales, int prev_bits, void* prev_full_out,
+                                  hz_dtype prev_out_dt, void* stream);
+
 /* qgZ hierarchical all-to-all reduce-scatter (O9; Table VIII).
  * grad: dt[len_{from_level-1}] over the rank's range_{from_level-1}
  *   (from_level == 1: the full padded gradient dt[Np]).

@@ -51,7 +51,7 @@ const char* const kSymbols[] = {
     "hz_trace_read",       "hz_plan_allgather",      "hz_plan_reduce_scatter",
     "hz_enable_p2p",       "hz_p2p_enabled",         "hz_sym_alloc",
     "hz_p2p_capture_begin", "hz_p2p_capture_end",    "hz_p2p_replayed",
-    "hz_adamw_step",       "hz_set_sm_budget",     "hz_allreduce_select", "hz_step_host",
+    "hz_adamw_step",       "hz_set_sm_budget",     "hz_allreduce_select", "hz_step_host", "hz_allgather_params_next", "hz_backward_step",
 };
 }  // namespace
 }  // namespace hz

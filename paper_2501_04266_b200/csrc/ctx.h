@@ -36,6 +36,11 @@ struct hz_ctx {
     unsigned long long epoch_host = 0;          // value *epoch will hold once enqueued work ran
     unsigned long long capture_start = 0;       // phase at hz_p2p_capture_begin
     unsigned long long span = 0;                // phases of the last captured graph
+    // prefetched quantize (hz_allgather_params_next): the next layer's primary was
+    // quantized into pre_codes in phase pre_phase by the previous call's dual kernel
+    unsigned long long pre_phase = 0;
+    const void* pre_codes = nullptr;
+    const void* pre_primary = nullptr;
     bool capturing = false;
     struct Slot {
       size_t off = 0, cap = 0;
@@ -98,6 +103,9 @@ hz_status run_quantize_push(const void* x, hz_dtype dt, int64_t n, int bits, uin
 hz_status run_reduce_push(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
                           int bits_out, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
                           int64_t remote);
+hz_status run_gather_quantize(const Pieces& pc, int64_t n, int bits, void* y, hz_dtype odt, const void* x,
+                              hz_dtype dt, int64_t nq, int qbits, uint8_t* c, float* s, cudaStream_t st,
+                              const SyncArgs& sync, int64_t remote_bytes);
 hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
 hz_status run_sum(const Pieces& pc, int64_t n, float* out, cudaStream_t st, int level, const SyncArgs* sync,
                   int64_t remote);
@@ -106,12 +114,30 @@ hz_status p2p_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const float
 
 // P2P transport (p2p.cpp)
 bool in_pool(const hz_ctx* ctx, const void* p, size_t bytes);
+// the next layer's quantize fused into this layer's forward gather (k_gather_quantize)
+struct NextQ {
+  const hz_partition_t* p;
+  const void* primary;
+  uint8_t* codes;
+  float* scales;
+};
+// the previous layer's backward gather fused into this layer's level-`from` quantize
+struct PrevG {
+  const hz_partition_t* p;
+  uint8_t* sec_codes;
+  float* sec_scales;
+  int bits;
+  void* full_out;
+  hz_dtype out_dt;
+};
+bool p2p_next_fusable(const hz_ctx* ctx, const hz_partition_t* p, int bits, hz_dtype out_dt, const NextQ& nx);
 hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, const void* primary,
                         hz_dtype dt, int bits, uint8_t* sec_codes, float* sec_scales, void* full_out,
-                        hz_dtype out_dt, cudaStream_t st);
+                        hz_dtype out_dt, cudaStream_t st, const NextQ* next);
+bool p2p_prev_fusable(const hz_ctx* ctx, const hz_partition_t* p, int from_level, const PrevG& pg);
 hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
                              int from_level, int to_level, const int* bits_per_level, float* shard,
-                             int accumulate, cudaStream_t st);
+                             int accumulate, cudaStream_t st, const PrevG* prev = nullptr);
 void p2p_release(hz_ctx* ctx);
 void exec_release(hz_ctx* ctx);   // executor.cpp
 hz_status p2p_adamw_gather(hz_ctx* ctx, const hz_partition_t* p, const float* g, float* th, float* m, float* v,

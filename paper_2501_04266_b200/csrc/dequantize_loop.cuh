@@ -1,0 +1,106 @@
+// The gather+dequantize loop of k_dequantize (see k_dequantize.cu), shared with the
+// dual kernel of k_quantize.cu (k_gather_quantize): warp `warp` of `nwarps` processes
+// its grid-stride share of the layer.  Internal header.
+#pragma once
+
+#include "codec.cuh"
+
+namespace hz {
+namespace dev {
+
+template <int BITS, typename TO, int U>
+__device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits, int log2b, TO* __restrict__ y,
+                                                int64_t warp, int64_t nwarps) {
+  const int lane = threadIdx.x & 31;
+  const bool copy_sec = pc.sec_c != nullptr;
+  // Pieces interleaved by warp tile (32*U units): consecutive tiles alternate between
+  // pieces, so local (HBM) and peer (NVLink) tiles are in flight at the same time
+  // instead of one half of the layer after the other.
+  const bool inter = pc.n > 1 && (pc.len % (256 * U)) == 0;
+  const int64_t tiles_per_piece = pc.len / (256 * U);
+  for (int64_t base = warp * 32 * U; base < nunits; base += nwarps * 32 * U) {
+    int64_t ub = base;            // first unit of this warp tile in the layer
+    int jt = -1;                  // its piece, when interleaved
+    if (inter) {
+      const int64_t tile = base / (32 * U);
+      jt = static_cast<int>(tile % pc.n);
+      ub = jt * (pc.len / 8) + (tile / pc.n) * (32 * U);
+      (void)tiles_per_piece;
+    }
+    Codes8<BITS> raw[U];
+    float sc[U];
+    bool fast = false;
+    if constexpr (U == 4) {
+      if (log2b == 8 && (inter || (pc.n == 1 && ub + 32 * U <= nunits))) {
+        // B = 256, a full tile: its 4 blocks have 4 consecutive scales — one 16-byte
+        // (broadcast) load instead of 4 single-scale requests (peer reads are
+        // request-bound for small transfers)
+        if (!inter) jt = 0;
+        const int64_t r0 = ub * 8 - jt * pc.len;
+        const bool head = r0 < pc.split && pc.cr[jt] != nullptr;
+        const uint8_t* cb = (head ? pc.cr[jt] : pc.c[jt]) + (r0 + lane * 8) * BITS / 8;
+        const float4 s4 = __ldg(reinterpret_cast<const float4*>((head ? pc.sr[jt] : pc.s[jt]) + (r0 >> 8)));
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u].load(cb + u * 256 * BITS / 8);
+        sc[0] = s4.x;
+        sc[1] = s4.y;
+        sc[2] = s4.z;
+        sc[3] = s4.w;
+        fast = true;
+      } else if (inter || (pc.n == 1 && ub + 32 * U <= nunits)) {
+        // any other block size, a full tile (1024 elements starting at a multiple of
+        // 1024): its NS = max(1, 1024/B) scales are consecutive — lane k < NS loads
+        // scale k (one request for the tile), every lane takes its unit's scale by
+        // shuffle.  (B >= 1024: the tile lies inside one block, NS = 1.)
+        if (!inter) jt = 0;
+        const int64_t r0 = ub * 8 - jt * pc.len;
+        const bool head = r0 < pc.split && pc.cr[jt] != nullptr;
+        const uint8_t* cb = (head ? pc.cr[jt] : pc.c[jt]) + (r0 + lane * 8) * BITS / 8;
+        const int ns = log2b >= 10 ? 1 : (1024 >> log2b);
+        const float mine = __ldg((head ? pc.sr[jt] : pc.s[jt]) + (r0 >> log2b) + (lane < ns ? lane : ns - 1));
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u].load(cb + u * 256 * BITS / 8);
+#pragma unroll
+        for (int u = 0; u < U; ++u) sc[u] = __shfl_sync(0xffffffffu, mine, (u * 256 + lane * 8) >> log2b);
+        fast = true;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t unit = ub + u * 32 + lane;
+      if (!fast && unit < nunits) {
+        const int64_t e = unit * 8;
+        int j = jt;
+        if (j < 0) {
+          j = 0;
+          for (int q = 1; q < pc.n; ++q) j += e >= q * pc.len;   // piece of this unit
+        }
+        const int64_t r = e - j * pc.len;
+        const bool head = r < pc.split && pc.cr[j] != nullptr;   // pushed head: local receive buffer
+        raw[u].load((head ? pc.cr[j] : pc.c[j]) + r * BITS / 8);
+        sc[u] = __ldg((head ? pc.sr[j] : pc.s[j]) + (r >> log2b));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t unit = ub + u * 32 + lane;
+      if (unit < nunits) {
+        float c[8], v[8];
+        raw[u].decode(c);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __fmul_rn(c[i], sc[u]);
+        Out8<TO>::store(y + unit * 8, v);
+        if (copy_sec) {
+          const int64_t e = unit * 8;
+          if (e >= pc.sec_lo && e < pc.sec_hi) {
+            raw[u].store(pc.sec_c + (e - pc.sec_lo) * BITS / 8);
+            if (((e - pc.sec_lo) & ((int64_t(1) << log2b) - 1)) == 0) pc.sec_s[(e - pc.sec_lo) >> log2b] = sc[u];
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace hz

@@ -142,6 +142,20 @@ hz_status run_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block
   return HZ_OK;
 }
 
+hz_status run_gather_quantize(const Pieces& pc, int64_t n, int bits, void* y, hz_dtype odt, const void* x,
+                              hz_dtype dt, int64_t nq, int qbits, uint8_t* c, float* s, cudaStream_t st,
+                              const SyncArgs& sync, int64_t remote_bytes) {
+  const int64_t g_bytes = code_bytes(n, bits) + n / 256 * 4 + n * elem_bytes(odt) - remote_bytes;
+  const int64_t q_bytes = nq * elem_bytes(dt) + code_bytes(nq, qbits) + nq / 256 * 4;
+  TraceScope t(st, "gather_quantize", 0, bits, n + nq, g_bytes + q_bytes, remote_bytes);
+  SyncArgs sy = sync;
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_gather_quantize(pc, n, y, x, dt, nq, qbits, c, s, st, sy);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "gather+quantize kernel launch");
+  return HZ_OK;
+}
+
 hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
                      int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
                      cudaStream_t st, int level, const SyncArgs* sync, int64_t remote_bytes) {
@@ -324,9 +338,9 @@ hz_status hz_partition(const hz_ctx* ctx, int64_t numel, int block, int w, int s
   return partition(ctx->rank, ctx->levels, ctx->group, numel, block, w, s, gl, out);
 }
 
-hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward,
-                              const void* primary, hz_dtype dt, int bits, uint8_t* sec_codes,
-                              float* sec_scales, void* full_out, hz_dtype out_dt, void* stream) {
+static hz_status check_allgather(const hz_ctx* ctx, const hz_partition_t* p, int backward, const void* primary,
+                                 hz_dtype dt, int bits, const uint8_t* sec_codes, const float* sec_scales,
+                                 const void* full_out, hz_dtype out_dt) {
   using namespace hz;
   hz_status st0 = check_partition(ctx, p);
   if (st0 != HZ_OK) return st0;
@@ -338,6 +352,46 @@ hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward
   if (!sec_codes || !aligned16(sec_codes)) return fail(HZ_ERR_INVALID, "sec_codes: NULL or not 16-byte aligned");
   if (!sec_scales || !aligned16(sec_scales)) return fail(HZ_ERR_INVALID, "sec_scales: NULL or not 16-byte aligned");
   if (!full_out || !aligned16(full_out)) return fail(HZ_ERR_INVALID, "full_out: NULL or not 16-byte aligned");
+  return HZ_OK;
+}
+
+static hz_status allgather_impl(hz_ctx* ctx, const hz_partition_t* p, int backward, const void* primary,
+                                hz_dtype dt, int bits, uint8_t* sec_codes, float* sec_scales, void* full_out,
+                                hz_dtype out_dt, void* stream, const hz::NextQ* nextq);
+
+hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward,
+                              const void* primary, hz_dtype dt, int bits, uint8_t* sec_codes,
+                              float* sec_scales, void* full_out, hz_dtype out_dt, void* stream) {
+  return allgather_impl(ctx, p, backward, primary, dt, bits, sec_codes, sec_scales, full_out, out_dt, stream,
+                        nullptr);
+}
+
+hz_status hz_allgather_params_next(hz_ctx* ctx, const hz_partition_t* p, const void* primary, hz_dtype dt,
+                                   int bits, uint8_t* sec_codes, float* sec_scales, void* full_out,
+                                   hz_dtype out_dt, const hz_partition_t* p_next, const void* next_primary,
+                                   uint8_t* next_sec_codes, float* next_sec_scales, void* stream) {
+  using namespace hz;
+  if (!p_next) return allgather_impl(ctx, p, 0, primary, dt, bits, sec_codes, sec_scales, full_out, out_dt, stream,
+                                     nullptr);
+  hz_status rc = check_partition(ctx, p_next);
+  if (rc != HZ_OK) return fail(rc, std::string("p_next: ") + hz_last_error());
+  if (p_next->block != p->block) return fail(HZ_ERR_INVALID, "p_next: block differs from p");
+  if (!next_primary || !aligned16(next_primary))
+    return fail(HZ_ERR_INVALID, "next_primary: NULL or not 16-byte aligned");
+  if (!next_sec_codes || !aligned16(next_sec_codes))
+    return fail(HZ_ERR_INVALID, "next_sec_codes: NULL or not 16-byte aligned");
+  if (!next_sec_scales || !aligned16(next_sec_scales))
+    return fail(HZ_ERR_INVALID, "next_sec_scales: NULL or not 16-byte aligned");
+  NextQ nx{p_next, next_primary, next_sec_codes, next_sec_scales};
+  return allgather_impl(ctx, p, 0, primary, dt, bits, sec_codes, sec_scales, full_out, out_dt, stream, &nx);
+}
+
+static hz_status allgather_impl(hz_ctx* ctx, const hz_partition_t* p, int backward, const void* primary,
+                                hz_dtype dt, int bits, uint8_t* sec_codes, float* sec_scales, void* full_out,
+                                hz_dtype out_dt, void* stream, const hz::NextQ* nextq) {
+  using namespace hz;
+  hz_status st0 = check_allgather(ctx, p, backward, primary, dt, bits, sec_codes, sec_scales, full_out, out_dt);
+  if (st0 != HZ_OK) return st0;
   st0 = check_async(ctx);
   if (st0 != HZ_OK) return st0;
 
@@ -350,7 +404,7 @@ hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward
     return HZ_OK;
   }
   if (ctx->p2p.on)   // NVLink peer-memory transport: fused gather + dequantize
-    return p2p_allgather(ctx, p, backward, primary, dt, bits, sec_codes, sec_scales, full_out, out_dt, st);
+    return p2p_allgather(ctx, p, backward, primary, dt, bits, sec_codes, sec_scales, full_out, out_dt, st, nextq);
   hz_status rc;
   if ((rc = grow(ctx->ag_c, code_bytes(Np, bits))) != HZ_OK) return rc;
   if ((rc = grow(ctx->ag_s, Np / B * 4)) != HZ_OK) return rc;
@@ -426,10 +480,8 @@ hz_status hz_allgather_params(hz_ctx* ctx, const hz_partition_t* p, int backward
   return HZ_OK;
 }
 
-hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const void* grad,
-                                  hz_dtype dt, int from_level, int to_level,
-                                  const int* bits_per_level, float* shard, int accumulate,
-                                  void* stream) {
+static hz_status check_reduce_scatter(const hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
+                                      int from_level, int to_level, const int* bits_per_level, const float* shard) {
   using namespace hz;
   hz_status rc = check_partition(ctx, p);
   if (rc != HZ_OK) return rc;
@@ -443,6 +495,41 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
   if (!dtype_ok(dt)) return fail(HZ_ERR_INVALID, "dt: unknown dtype");
   if (!grad || !aligned16(grad)) return fail(HZ_ERR_INVALID, "grad: NULL or not 16-byte aligned");
   if (!shard || !aligned16(shard)) return fail(HZ_ERR_INVALID, "shard: NULL or not 16-byte aligned");
+  return HZ_OK;
+}
+
+hz_status hz_backward_step(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt, int from_level,
+                           int to_level, const int* bits_per_level, float* shard, int accumulate,
+                           const hz_partition_t* p_prev, uint8_t* prev_sec_codes, float* prev_sec_scales,
+                           int prev_bits, void* prev_full_out, hz_dtype prev_out_dt, void* stream) {
+  using namespace hz;
+  hz_status rc = check_reduce_scatter(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard);
+  if (rc != HZ_OK) return rc;
+  if (!p_prev)
+    return hz_reduce_scatter_grads(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard, accumulate, stream);
+  if ((rc = check_allgather(ctx, p_prev, 1, nullptr, HZ_BF16, prev_bits, prev_sec_codes, prev_sec_scales,
+                            prev_full_out, prev_out_dt)) != HZ_OK)
+    return fail(rc, std::string("prev: ") + hz_last_error());
+  if ((rc = check_async(ctx)) != HZ_OK) return rc;
+  PrevG pg{p_prev, prev_sec_codes, prev_sec_scales, prev_bits, prev_full_out, prev_out_dt};
+  if (ctx->p2p.on && p->len[from_level - 1] > 0 && p_prev->padded_numel > 0 &&
+      p2p_prev_fusable(ctx, p, from_level, pg))
+    return p2p_reduce_scatter(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard, accumulate,
+                              static_cast<cudaStream_t>(stream), &pg);
+  // not fusable (NCCL transport, other block sizes / dtypes): the two calls in order
+  if ((rc = hz_allgather_params(ctx, p_prev, 1, nullptr, HZ_BF16, prev_bits, prev_sec_codes, prev_sec_scales,
+                                prev_full_out, prev_out_dt, stream)) != HZ_OK)
+    return rc;
+  return hz_reduce_scatter_grads(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard, accumulate, stream);
+}
+
+hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const void* grad,
+                                  hz_dtype dt, int from_level, int to_level,
+                                  const int* bits_per_level, float* shard, int accumulate,
+                                  void* stream) {
+  using namespace hz;
+  hz_status rc = check_reduce_scatter(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard);
+  if (rc != HZ_OK) return rc;
   if ((rc = check_async(ctx)) != HZ_OK) return rc;
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);

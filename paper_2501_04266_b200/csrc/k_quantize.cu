@@ -12,7 +12,7 @@
 // divisions run once per block (quantize_store), and the main loop has no bounds
 // checks so every shuffle is convergent; the last partial iteration (< NB
 // blocks) goes through a checked tail path.  Grid-stride over SMs x resident CTAs.
-#include "codec.cuh"
+#include "dequantize_loop.cuh"
 
 namespace hz {
 namespace {
@@ -33,31 +33,17 @@ struct OutOf<2> { using E = EmitOut<__half>; };
 template <>
 struct OutOf<3> { using E = EmitF32; };
 
-template <typename T, int B, int BITS, int U, int OUT, class P = NoPush>
-__global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, int64_t nblocks,
-                                                       uint8_t* __restrict__ codes,
-                                                       float* __restrict__ scales,
-                                                       const __grid_constant__ SyncArgs sy,
-                                                       void* __restrict__ y, int acc,
-                                                       const __grid_constant__ P push) {
+// The quantize loop: warp `warp` of `nwarps` processes its grid-stride share of the
+// blocks (main loop without bounds checks, then the checked tail on the last warp).
+template <typename T, int B, int BITS, int U, int OUT, class P, class Emit>
+__device__ __forceinline__ void quantize_loop(const T* __restrict__ x, int64_t nblocks, uint8_t* __restrict__ codes,
+                                              float* __restrict__ scales, Emit& emit, void* __restrict__ y, int acc,
+                                              const P& push, int64_t warp, int64_t nwarps) {
   using G = Geo<B>;
-  using Emit = typename OutOf<OUT>::E;
-  __shared__ float4 stage[OUT == 3 ? kThreads / 32 : 1][OUT == 3 ? 64 : 1];
-  Emit emit;
-  if constexpr (OUT == 1 || OUT == 2) {
-    emit.y = static_cast<decltype(emit.y)>(y);
-  } else if constexpr (OUT == 3) {
-    emit.y = static_cast<float*>(y);
-    emit.stage = stage[threadIdx.x >> 5];
-    emit.acc = acc;
-  }
-  sync_wait(sy);   // P2P mode: every rank is done reading what this call overwrites
   constexpr int NB = U * G::BPW;
   const int lane = threadIdx.x & 31;
   const int lb = lane / G::LPB;
   const int ll = lane % G::LPB;
-  const int64_t warp = global_warp();
-  const int64_t nwarps = num_warps();
   const int64_t nfull = nblocks / NB;
 
   for (int64_t it = warp; it < nfull; it += nwarps) {
@@ -145,6 +131,28 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
       }
     }
   }
+}
+
+template <typename T, int B, int BITS, int U, int OUT, class P = NoPush>
+__global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, int64_t nblocks,
+                                                       uint8_t* __restrict__ codes,
+                                                       float* __restrict__ scales,
+                                                       const __grid_constant__ SyncArgs sy,
+                                                       void* __restrict__ y, int acc,
+                                                       const __grid_constant__ P push) {
+  using G = Geo<B>;
+  using Emit = typename OutOf<OUT>::E;
+  __shared__ float4 stage[OUT == 3 ? kThreads / 32 : 1][OUT == 3 ? 64 : 1];
+  Emit emit;
+  if constexpr (OUT == 1 || OUT == 2) {
+    emit.y = static_cast<decltype(emit.y)>(y);
+  } else if constexpr (OUT == 3) {
+    emit.y = static_cast<float*>(y);
+    emit.stage = stage[threadIdx.x >> 5];
+    emit.acc = acc;
+  }
+  sync_wait(sy);   // P2P mode: every rank is done reading what this call overwrites
+  quantize_loop<T, B, BITS, U, OUT, P>(x, nblocks, codes, scales, emit, y, acc, push, global_warp(), num_warps());
   sync_signal(sy);   // P2P mode: codes of this phase are ready for the peers
 }
 
@@ -229,6 +237,47 @@ cudaError_t quantize_d(const void* x, int64_t n, int bits, int block, uint8_t* c
   return cudaErrorInvalidValue;
 }
 
+// k_gather_quantize (P2P transport, B = 256): the gather+dequantize of one phase
+// (NVLink-bound: peer code reads) and the quantize of the next phase (HBM-bound),
+// two independent jobs, in ONE launch, so that the link and HBM streams overlap
+// and one launch / one cross-GPU synchronisation disappears per pair.  Forward:
+// gather layer k || quantize layer k+1's primary (the prefetch of
+// hz_allgather_params_next); backward: gather layer i-1 || quantize layer i's
+// gradient for its reduce-scatter (hz_backward_fused).  Every warp does its
+// grid-stride share of both jobs; odd CTAs gather first and even CTAs quantize
+// first, so at any time about half the warps stream each resource (HZ_TUNE gq=1:
+// every CTA gathers first).  Arithmetic per element is exactly the two kernels'.
+template <typename T, int QBITS, int GBITS, typename TO>
+__global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_constant__ Pieces pc, int64_t nunits,
+                                                               TO* __restrict__ y, const T* __restrict__ x,
+                                                               int64_t nblocks, uint8_t* __restrict__ codes,
+                                                               float* __restrict__ scales, int order,
+                                                               const __grid_constant__ SyncArgs sy) {
+  sync_wait(sy);
+  NoEmit emit;
+  const int64_t warp = global_warp(), nwarps = num_warps();
+  if (order == 0 && (blockIdx.x & 1) == 0) {
+    quantize_loop<T, 256, QBITS, kU, 0, NoPush>(x, nblocks, codes, scales, emit, nullptr, 0, NoPush{}, warp, nwarps);
+    dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps);
+  } else {
+    dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps);
+    quantize_loop<T, 256, QBITS, kU, 0, NoPush>(x, nblocks, codes, scales, emit, nullptr, 0, NoPush{}, warp, nwarps);
+  }
+  sync_signal(sy);
+}
+
+template <typename T, int QBITS>
+cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const void* x, int64_t n_q, uint8_t* codes,
+                              float* scales, cudaStream_t st, const SyncArgs& sy) {
+  auto kern = k_gather_quantize<T, QBITS, 8, __nv_bfloat16>;
+  const int64_t nunits = n_gather / 8;
+  const int64_t nblocks = n_q / 256;
+  const int64_t tasks = std::max<int64_t>((nunits + 32 * kU - 1) / (32 * kU), nblocks / (kU * Geo<256>::BPW) + 1);
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks);
+  return launch_k(kern, grid, st, pc, nunits, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x), nblocks,
+                  codes, scales, tune_param("gq", 0), sy);
+}
+
 }  // namespace
 
 bool roundtrip_supported(int block) { return block == 256; }
@@ -282,6 +331,31 @@ cudaError_t launch_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int
     case HZ_F32: return quantize_d<float>(x, n, bits, block, codes, scales, st, sy);
     case HZ_BF16: return quantize_d<__nv_bfloat16>(x, n, bits, block, codes, scales, st, sy);
     case HZ_F16: return quantize_d<__half>(x, n, bits, block, codes, scales, st, sy);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hz
+
+namespace hz {
+
+bool gather_quantize_supported(int block, int gather_bits, hz_dtype out_dt) {
+  return block == 256 && gather_bits == 8 && out_dt == HZ_BF16;
+}
+
+cudaError_t launch_gather_quantize(const Pieces& pc, int64_t n_gather, void* y, const void* x, hz_dtype dt,
+                                   int64_t n_q, int qbits, uint8_t* codes, float* scales, cudaStream_t st,
+                                   const SyncArgs& sy) {
+  switch (dt) {
+    case HZ_F32:
+      return qbits == 8 ? gather_quantize_t<float, 8>(pc, n_gather, y, x, n_q, codes, scales, st, sy)
+                        : gather_quantize_t<float, 4>(pc, n_gather, y, x, n_q, codes, scales, st, sy);
+    case HZ_BF16:
+      return qbits == 8 ? gather_quantize_t<__nv_bfloat16, 8>(pc, n_gather, y, x, n_q, codes, scales, st, sy)
+                        : gather_quantize_t<__nv_bfloat16, 4>(pc, n_gather, y, x, n_q, codes, scales, st, sy);
+    case HZ_F16:
+      return qbits == 8 ? gather_quantize_t<__half, 8>(pc, n_gather, y, x, n_q, codes, scales, st, sy)
+                        : gather_quantize_t<__half, 4>(pc, n_gather, y, x, n_q, codes, scales, st, sy);
   }
   return cudaErrorInvalidValue;
 }

@@ -148,9 +148,17 @@ bool in_pool(const hz_ctx* ctx, const void* p, size_t bytes) {
   return ctx->p2p.on && c >= ctx->p2p.pool + kPoolHeader && c + bytes <= ctx->p2p.pool + ctx->p2p.bytes;
 }
 
+bool p2p_next_fusable(const hz_ctx* ctx, const hz_partition_t* p, int bits, hz_dtype out_dt, const NextQ& nx) {
+  const hz_partition_t* q = nx.p;
+  return ctx->p2p.on && q && p->s == p->w && q->s == q->w && p->block == 256 && q->block == 256 &&
+         gather_quantize_supported(256, bits, out_dt) && q->len[q->w] > 0 &&
+         in_pool(ctx, nx.codes, code_bytes(q->len[q->s], bits)) && in_pool(ctx, nx.scales, q->len[q->s] / 256 * 4) &&
+         tune_param("pushf", 0) == 0 && tune_param("fused", 0) == 0 && tune_param("nofuse", 0) == 0;
+}
+
 hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, const void* primary,
                         hz_dtype dt, int bits, uint8_t* sec_codes, float* sec_scales, void* full_out,
-                        hz_dtype out_dt, cudaStream_t st) {
+                        hz_dtype out_dt, cudaStream_t st, const NextQ* next) {
   auto& P = ctx->p2p;
   const int64_t Np = p->padded_numel;
   const int B = p->block;
@@ -166,7 +174,13 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   // every call is a phase, even without peers to read from: it may write a
   // secondary that peers read in a later backward phase (s > w), and the final
   // kernel's done(phase) is what tells them the write (incl. its copies) is complete
-  const unsigned long long phase = ++P.phase;
+  // this layer's primary already quantized by the previous call's dual kernel (the
+  // prefetch of hz_allgather_params_next), in phase pre_phase, with no phase since
+  const bool pre = !backward && s == w && P.pre_phase != 0 && P.pre_phase == P.phase &&
+                   P.pre_codes == sec_codes && P.pre_primary == primary;
+  P.pre_phase = 0;
+  P.pre_codes = P.pre_primary = nullptr;
+  const unsigned long long phase = pre ? P.phase : ++P.phase;
   const int64_t plen = p->len[top];
   int me = 0;
   for (int k = 0; k < D; ++k)
@@ -272,7 +286,7 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
       if ((rc = run_quantize_push(primary, dt, plen, bits, qc, qs, nullptr, out_dt, dst, st, w, &sq, pushed)) !=
           HZ_OK)
         return rc;
-    } else if ((rc = run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w, &sq)) != HZ_OK) {
+    } else if (!pre && (rc = run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w, &sq)) != HZ_OK) {
       return rc;
     }
     if (s > w) {   // A4, s > w: the secondary is a sub-slice of the own quantized primary
@@ -307,6 +321,23 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
     pc.sec_s = sec_scales;
     pc.sec_lo = p->off[s];
     pc.sec_hi = p->off[s] + len_s;
+  }
+  if (!backward && next && p2p_next_fusable(ctx, p, bits, out_dt, *next)) {
+    // gather this layer (phase) || quantize the next layer's primary (phase + 1) in one
+    // launch.  Waits: the members' codes of this phase are ready, and every rank is
+    // done with every phase before it (nobody still reads the next layer's secondary,
+    // last read in an earlier backward phase).  Signals done(phase), ready(phase + 1).
+    const unsigned long long nph = ++P.phase;
+    const hz_partition_t* q = next->p;
+    SyncArgs sd = make_sync(ctx, phase, phase - 1, nph, phase);
+    if ((rc = run_gather_quantize(pc, Np, bits, full_out, out_dt, next->primary, dt, q->len[q->w], bits, next->codes,
+                                  next->scales, st, sd, remote)) != HZ_OK)
+      return rc;
+    P.pre_phase = nph;
+    P.pre_codes = next->codes;
+    P.pre_primary = next->primary;
+    clear_error();
+    return HZ_OK;
   }
   SyncArgs sd = backward ? make_sync(ctx, 0, phase - 1, 0, phase) : make_sync(ctx, phase, 0, 0, phase);
   if ((rc = run_gather_dequantize(pc, Np, bits, B, full_out, out_dt, st, 0, &sd, remote)) != HZ_OK)
@@ -395,12 +426,41 @@ hz_status p2p_reduce_scatter_push(hz_ctx* ctx, const hz_partition_t* p, const vo
   return HZ_OK;
 }
 
+bool p2p_prev_fusable(const hz_ctx* ctx, const hz_partition_t* p, int from_level, const PrevG& pg) {
+  const hz_partition_t* q = pg.p;
+  return ctx->p2p.on && q && p->block == 256 && q->block == 256 && p->len[from_level - 1] > 0 &&
+         gather_quantize_supported(256, pg.bits, pg.out_dt) &&
+         in_pool(ctx, pg.sec_codes, code_bytes(q->len[q->s], pg.bits)) &&
+         in_pool(ctx, pg.sec_scales, q->len[q->s] / 256 * 4) && static_cast<int>(cumulative_members(q, q->s).size()) <=
+                                                                   kMaxWorld &&
+         tune_param("rspush", 0) == 0 && tune_param("fused", 0) == 0 && tune_param("nofuse", 0) == 0;
+}
+
 hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
                              int from_level, int to_level, const int* bits_per_level, float* shard,
-                             int accumulate, cudaStream_t st) {
+                             int accumulate, cudaStream_t st, const PrevG* prev) {
   auto& P = ctx->p2p;
   const int B = p->block;
   hz_status rc;
+  P.pre_phase = 0;
+  // the previous layer's backward gather (phase gph) fused into this call's first
+  // quantize (hz_backward_step; the caller checked p2p_prev_fusable)
+  unsigned long long gph = 0;
+  Pieces gpc{};
+  int64_t gremote = 0;
+  if (prev) {
+    gph = ++P.phase;
+    const hz_partition_t* q = prev->p;
+    const auto members = cumulative_members(q, q->s);
+    gpc.n = static_cast<int>(members.size());
+    gpc.len = q->len[q->s];
+    for (int k = 0; k < gpc.n; ++k) {
+      const int m = members[k].second;
+      gpc.c[k] = at<const uint8_t>(ctx, m, off_of(ctx, prev->sec_codes));
+      gpc.s[k] = at<const float>(ctx, m, off_of(ctx, prev->sec_scales));
+      if (m != ctx->rank) gremote += code_bytes(gpc.len, prev->bits) + gpc.len / 256 * 4;
+    }
+  }
   // full push for qgZ measured slower than pull on B200: HZ_TUNE rspush=1
   bool push = B == 256 && tune_param("rspush", 0) && !tune_param("fused", 0);
   for (int l = from_level; l < to_level; ++l) push = push && push_reduce_supported(p->group[l - 1], B);
@@ -474,6 +534,18 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
     t.end();
     if (e != cudaSuccess) return cuda_fail(e, "fused reduce-scatter kernel launch");
     first = l + 1;
+  } else if (prev) {
+    // previous layer's backward gather (phase gph) || A7 of this layer (phase gph + 1):
+    // waits until every rank is done with every phase before gph (the secondaries
+    // are complete, nobody reads the send buffer any more); signals done(gph) and
+    // ready(gph + 1) for the level-`from` reduce below
+    const unsigned long long ph = phase_of(from_level);
+    SyncArgs sq = make_sync(ctx, 0, gph - 1, ph, gph);
+    if ((rc = run_gather_quantize(gpc, prev->p->padded_numel, prev->bits, prev->full_out, prev->out_dt, grad, dt,
+                                  p->len[from_level - 1], bits_per_level[from_level - 1],
+                                  at<uint8_t>(ctx, ctx->rank, P.rs_c[from_level].off),
+                                  at<float>(ctx, ctx->rank, P.rs_s[from_level].off), st, sq, gremote)) != HZ_OK)
+      return rc;
   } else {
     // A7: quantize the input range_{from-1} into this rank's level-`from` send buffer
     const unsigned long long ph = phase_of(from_level);

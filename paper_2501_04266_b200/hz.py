@@ -111,6 +111,10 @@ _sig("hz_allgather_params", [_vp, ctypes.POINTER(Partition), _int, _vp, _int, _i
                              _int, _vp])
 _sig("hz_reduce_scatter_grads", [_vp, ctypes.POINTER(Partition), _vp, _int, _int, _int,
                                  ctypes.POINTER(ctypes.c_int), _vp, _int, _vp])
+_sig("hz_allgather_params_next", [_vp, ctypes.POINTER(Partition), _vp, _int, _int, _vp, _vp, _vp, _int,
+                                  ctypes.POINTER(Partition), _vp, _vp, _vp, _vp])
+_sig("hz_backward_step", [_vp, ctypes.POINTER(Partition), _vp, _int, _int, _int, ctypes.POINTER(ctypes.c_int), _vp,
+                          _int, ctypes.POINTER(Partition), _vp, _vp, _int, _vp, _int, _vp])
 class AdamWParams(ctypes.Structure):
     _fields_ = [(n, ctypes.c_float) for n in ("b1", "omb1", "b2", "omb2", "lr_wd", "sqrt_bc2", "eps", "step")]
 
@@ -429,6 +433,32 @@ class Context:
                                         _ptr(sec_scales), _ptr(full_out), _dtype_code(full_out),
                                         _stream(stream)))
         return full_out
+
+    def allgather_params_next(self, p, primary, sec_codes, sec_scales, full_out, bits=8, p_next=None,
+                              next_primary=None, next_sec_codes=None, next_sec_scales=None, stream=None):
+        """hz_allgather_params_next: forward gather of ``p`` with the quantize of the next
+        layer's primary (``p_next``) prefetched into the same launch."""
+        _check(_lib.hz_allgather_params_next(
+            self._h, ctypes.byref(p), _ptr(primary), _dtype_code(primary), bits, _ptr(sec_codes), _ptr(sec_scales),
+            _ptr(full_out), _dtype_code(full_out), ctypes.byref(p_next) if p_next is not None else None,
+            _ptr(next_primary), _ptr(next_sec_codes), _ptr(next_sec_scales), _stream(stream)))
+        return full_out
+
+    def backward_step(self, p, grad, shard, bits_per_level=None, p_prev=None, prev_sec_codes=None,
+                      prev_sec_scales=None, prev_full_out=None, prev_bits=8, from_level=1, to_level=None,
+                      accumulate=False, stream=None):
+        """hz_backward_step: qgZ reduce-scatter of ``p``'s gradient and the backward gather
+        of the previous layer ``p_prev`` (fused in one launch where possible)."""
+        L = self.levels
+        bpl = list(bits_per_level) if bits_per_level is not None else [4] * L
+        bpl = bpl + [4] * (L - len(bpl))
+        arr = (ctypes.c_int * L)(*bpl)
+        _check(_lib.hz_backward_step(
+            self._h, ctypes.byref(p), _ptr(grad), _dtype_code(grad), from_level, L if to_level is None else to_level,
+            arr, _ptr(shard), int(bool(accumulate)), ctypes.byref(p_prev) if p_prev is not None else None,
+            _ptr(prev_sec_codes), _ptr(prev_sec_scales), prev_bits, _ptr(prev_full_out),
+            _dtype_code(prev_full_out) if prev_full_out is not None else BF16, _stream(stream)))
+        return shard
 
     def reduce_scatter_grads(self, p, grad, shard, bits_per_level=None, from_level=1,
                              to_level=None, accumulate=False, stream=None):

@@ -257,6 +257,7 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
         del graph
 
         errors += check_step_host(ctx, hz, rank, world, g, sec_buffers, tag, B)
+        errors += check_pipelined(ctx, hz, rank, world, g, sec_buffers, tag, B, p2p)
 
         # flat ZeRO-3 baseline collectives (plain NCCL)
         n = world * 4096
@@ -276,6 +277,81 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             errors.append(str(e))
     finally:
         ctx.close()
+    return errors
+
+
+def check_pipelined(ctx, hz, rank, world, g, sec_buffers, tag, B, p2p, sizes=(150_001, 70_000, 4097, 9000)):
+    """hz_allgather_params_next / hz_backward_step (adjacent layers paired; on the P2P
+    transport with B = 256 one dual kernel per pair): two back-to-back steps over four
+    tensors (setting T, plus one tensor with s != w, which is not fusable and takes
+    the two-call path), every gathered layer, secondary and shard bitwise against the
+    oracle; with P2P and B = 256 the trace must show the dual kernels."""
+    errors = []
+    L = len(g)
+    roles = [(1, 1), (1, 1), (L, max(L - 1, 0)), (1, 1)]
+    parts = [ctx.partition(n, B, w, s, L) for n, (w, s) in zip(sizes, roles)]
+    T = []
+    for k, (n, p) in enumerate(zip(sizes, parts)):
+        Np = p.padded_numel
+        sl = p.range(p.s)[1]
+        sc, ss = sec_buffers(sl, sl // B)
+        T.append({"p": p, "n": n, "primary": torch.empty(p.range(p.w)[1], dtype=torch.bfloat16, device="cuda"),
+                  "grad": torch.empty(Np, dtype=torch.bfloat16, device="cuda"), "sec_c": sc, "sec_s": ss,
+                  "fwd": torch.empty(Np, dtype=torch.bfloat16, device="cuda"),
+                  "bwd": torch.empty(Np, dtype=torch.bfloat16, device="cuda"),
+                  "shard": torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")})
+    if p2p:
+        hz.trace_begin(capacity=4096, events=False, stamps=True)
+    for step in range(2):
+        want = []
+        for k, t in enumerate(T):
+            p, n, Np = t["p"], t["n"], t["p"].padded_numel
+            fr = np.zeros(Np, np.float32)
+            fr[:n] = synth.params_like(n, 500 + 10 * step + k, block=B)
+            fr = fr.astype(ml_dtypes.bfloat16)
+            gr = {}
+            for r in range(world):
+                x = np.zeros(Np, np.float32)
+                x[:n] = synth.gradient_like(n, 1500 + 100 * step + 10 * k + r, block=B)
+                gr[r] = x.astype(ml_dtypes.bfloat16)
+            off, ln = p.range(p.w)
+            t["primary"].copy_(to_dev(fr[off:off + ln]))
+            t["grad"].copy_(to_dev(gr[rank]))
+            prim = {r: fr[pm.range_at(r, g, Np, p.w)[0]:sum(pm.range_at(r, g, Np, p.w))] for r in range(world)}
+            f, sec = col.allgather_forward(prim, g, Np, B, p.w, p.s, bits=8)
+            want.append((f[rank], sec[rank], col.reduce_scatter(gr, g, Np, B, 1, L, {l: 4 for l in range(1, L + 1)})[rank]))
+        torch.cuda.synchronize()
+        n = len(T)
+        for k, t in enumerate(T):
+            nx = T[k + 1] if k + 1 < n else None
+            ctx.allgather_params_next(t["p"], t["primary"], t["sec_c"], t["sec_s"], t["fwd"], bits=8,
+                                      p_next=nx["p"] if nx else None, next_primary=nx["primary"] if nx else None,
+                                      next_sec_codes=nx["sec_c"] if nx else None,
+                                      next_sec_scales=nx["sec_s"] if nx else None)
+        ctx.allgather_params(T[-1]["p"], None, T[-1]["sec_c"], T[-1]["sec_s"], T[-1]["bwd"], bits=8, backward=True)
+        for k in range(n - 1, -1, -1):
+            t, pv = T[k], (T[k - 1] if k > 0 else None)
+            ctx.backward_step(t["p"], t["grad"], t["shard"], [4] * L, p_prev=pv["p"] if pv else None,
+                              prev_sec_codes=pv["sec_c"] if pv else None, prev_sec_scales=pv["sec_s"] if pv else None,
+                              prev_full_out=pv["bwd"] if pv else None, prev_bits=8)
+        torch.cuda.synchronize()
+        try:
+            for k, t in enumerate(T):
+                what = f"[{tag}] g={g} pipelined step {step} tensor {k} (w,s)={roles[k]}"
+                assert_bitwise(to_host(t["fwd"]), want[k][0], what + " forward layer")
+                assert_bitwise(to_host(t["bwd"]), want[k][0], what + " backward layer")
+                assert_bitwise(to_host(t["sec_c"]), quant.wire_codes(want[k][1][0], 8), what + " secondary codes")
+                assert_bitwise(to_host(t["sec_s"]), want[k][1][1], what + " secondary scales")
+                assert_bitwise(to_host(t["shard"]), want[k][2], what + " qgZ shard")
+        except AssertionError as e:
+            errors.append(str(e))
+    if p2p:
+        hz.trace_end()
+        kinds = [r["kind"] for r in hz.trace_read()]
+        # per step: forward pairs (0,1) fused; (1,2) not (tensor 2 has s != w); backward pairs
+        # (3,2), (2,1), (1,0): the gather side is any layout -> all three fused
+        if B == 256 and not os.environ.get("HZ_TUNE") and kinds.count("gather_quantize") != 2 * 4:
+            errors.append(f"[{tag}] g={g} pipelined: expected 8 gather_quantize launches, trace {kinds}")
     return errors
 
 
