@@ -256,7 +256,15 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
   sync_wait(sy);
   NoEmit emit;
   const int64_t warp = global_warp(), nwarps = num_warps();
-  if (order == 0 && (blockIdx.x & 1) == 0) {
+  if (order >= 2) {   // role split: CTAs [0, order - 2) gather only, the rest quantize only
+    const int64_t gcta = order - 2;
+    const int64_t wpc = kThreads / 32;
+    if (blockIdx.x < gcta)
+      dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, gcta * wpc);
+    else
+      quantize_loop<T, 256, QBITS, kU, 0, NoPush>(x, nblocks, codes, scales, emit, nullptr, 0, NoPush{},
+                                                  warp - gcta * wpc, nwarps - gcta * wpc);
+  } else if (order == 0 && (blockIdx.x & 1) == 0) {
     quantize_loop<T, 256, QBITS, kU, 0, NoPush>(x, nblocks, codes, scales, emit, nullptr, 0, NoPush{}, warp, nwarps);
     dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps);
   } else {
@@ -274,8 +282,17 @@ cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const
   const int64_t nblocks = n_q / 256;
   const int64_t tasks = std::max<int64_t>((nunits + 32 * kU - 1) / (32 * kU), nblocks / (kU * Geo<256>::BPW) + 1);
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks);
+  // HZ_TUNE gq: 0 = every warp does both jobs, odd CTAs gather first (default); 1 = all
+  // gather first; 2 = role split with gqf percent of the CTAs gathering
+  int order = tune_param("gq", 0);
+  if (order == 2 && grid < 2) order = 0;
+  if (order == 2) {
+    int64_t gc = grid * tune_param("gqf", 50) / 100;
+    gc = std::min<int64_t>(std::max<int64_t>(gc, 1), grid - 1);
+    order = static_cast<int>(2 + gc);
+  }
   return launch_k(kern, grid, st, pc, nunits, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x), nblocks,
-                  codes, scales, tune_param("gq", 0), sy);
+                  codes, scales, order, sy);
 }
 
 }  // namespace
