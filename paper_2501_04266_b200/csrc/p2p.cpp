@@ -143,6 +143,22 @@ std::vector<std::pair<int64_t, int>> cumulative_members(const hz_partition_t* p,
 
 }  // namespace
 
+// A prefetched quantize (hz_allgather_params_next) whose layer is not gathered next
+// leaves its phase without a `done`; complete it before any other phase starts: a
+// one-CTA kernel signalling done(pre_phase) — nobody reads those codes, and every
+// earlier read of this rank is complete in stream order.
+hz_status flush_prefetch(hz_ctx* ctx, cudaStream_t st) {
+  auto& P = ctx->p2p;
+  if (!P.pre_phase) return HZ_OK;
+  const unsigned long long ph = P.pre_phase;
+  P.pre_phase = 0;
+  P.pre_codes = P.pre_primary = nullptr;
+  Pieces pc{};
+  pc.n = 1;
+  SyncArgs s = make_sync(ctx, 0, 0, 0, ph);
+  return run_gather_dequantize(pc, 0, 8, 256, nullptr, HZ_BF16, st, 0, &s, 0);
+}
+
 bool in_pool(const hz_ctx* ctx, const void* p, size_t bytes) {
   const char* c = static_cast<const char*>(p);
   return ctx->p2p.on && c >= ctx->p2p.pool + kPoolHeader && c + bytes <= ctx->p2p.pool + ctx->p2p.bytes;
@@ -178,8 +194,12 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   // prefetch of hz_allgather_params_next), in phase pre_phase, with no phase since
   const bool pre = !backward && s == w && P.pre_phase != 0 && P.pre_phase == P.phase &&
                    P.pre_codes == sec_codes && P.pre_primary == primary;
-  P.pre_phase = 0;
-  P.pre_codes = P.pre_primary = nullptr;
+  if (pre) {
+    P.pre_phase = 0;
+    P.pre_codes = P.pre_primary = nullptr;
+  } else if ((rc = flush_prefetch(ctx, st)) != HZ_OK) {
+    return rc;
+  }
   const unsigned long long phase = pre ? P.phase : ++P.phase;
   const int64_t plen = p->len[top];
   int me = 0;
@@ -442,7 +462,7 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
   auto& P = ctx->p2p;
   const int B = p->block;
   hz_status rc;
-  P.pre_phase = 0;
+  if ((rc = flush_prefetch(ctx, st)) != HZ_OK) return rc;
   // the previous layer's backward gather (phase gph) fused into this call's first
   // quantize (hz_backward_step; the caller checked p2p_prev_fusable)
   unsigned long long gph = 0;
@@ -595,6 +615,7 @@ hz_status p2p_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const float
                                float* out, cudaStream_t st) {
   auto& P = ctx->p2p;
   hz_status rc;
+  if ((rc = flush_prefetch(ctx, st)) != HZ_OK) return rc;
   const int64_t n = p->len[from_level - 1];
   const int64_t sel = p->off[to_level] - p->off[from_level - 1];
   if ((rc = slot(ctx, P.ar_a, n * 4)) != HZ_OK) return rc;
@@ -654,6 +675,7 @@ hz_status p2p_adamw_gather(hz_ctx* ctx, const hz_partition_t* p, const float* g,
   const int64_t lenL = p->len[L];
   const int64_t eb = elem_bytes(dt);
   hz_status rc;
+  if ((rc = flush_prefetch(ctx, st)) != HZ_OK) return rc;
   if ((rc = slot(ctx, P.upd, lenL * 4)) != HZ_OK) return rc;   // fp32 capacity
   const unsigned long long phase = ++P.phase;
   char* mine = at<char>(ctx, ctx->rank, P.upd.off);
@@ -785,6 +807,9 @@ hz_status hz_p2p_capture_begin(hz_ctx* ctx) {
   if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
   if (!ctx->p2p.on) return fail(HZ_ERR_INVALID, "ctx: P2P not enabled");
   if (ctx->p2p.capturing) return fail(HZ_ERR_INVALID, "ctx: capture already begun");
+  if (ctx->p2p.pre_phase)
+    return fail(HZ_ERR_INVALID, "ctx: a prefetched quantize (hz_allgather_params_next) is pending; gather that "
+                                "layer before beginning a capture");
   ctx->p2p.capturing = true;
   ctx->p2p.capture_start = ctx->p2p.phase;
   clear_error();
@@ -796,6 +821,8 @@ hz_status hz_p2p_capture_end(hz_ctx* ctx, void* stream, unsigned long long* span
   if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
   auto& P = ctx->p2p;
   if (!P.capturing) return fail(HZ_ERR_INVALID, "ctx: no capture in progress");
+  hz_status rc = flush_prefetch(ctx, static_cast<cudaStream_t>(stream));   // inside the graph
+  if (rc != HZ_OK) return rc;
   P.capturing = false;
   P.span = P.phase - P.capture_start;
   P.phase = P.capture_start;   // nothing captured has run yet

@@ -26,7 +26,11 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--step1", action="store_true",
                     help="one world-1 step of one tensor through the collective API (fused round trips)")
+    ap.add_argument("--pair", action="store_true",
+                    help="world-1 P2P context: the adjacent-layer dual kernel (k_gather_quantize) forward and backward")
     args = ap.parse_args()
+    if args.pair:
+        return pair(args)
     if args.step1:
         return step1(args)
 
@@ -144,6 +148,47 @@ def step1(args):
         gbs = byts / (ms * 1e-3) / 1e9
         print(json.dumps({"kernel": name, "numel": Np, "us": round(ms * 1e3, 2), "bytes": byts,
                           "GBps": round(gbs, 1), "frac_of_copy_peak": round(gbs / peak, 3)}), flush=True)
+    ctx.close()
+
+
+def pair(args):
+    """World-1 context with the P2P transport on, one GPT-1.3B layer pair: the dual
+    kernel of hz_allgather_params_next (gather layer a || quantize layer b's primary,
+    int8) and of hz_backward_step (gather layer a || quantize the gradient, int4, then
+    the fp32 reduce).  The gather reads local codes here (no peers), so this is the
+    kernel's HBM side; --once for ncu."""
+    import torch
+    from paper_2501_04266_b200 import hz, synth
+    ctx = hz.Context(0, 1, hz.get_uid(), (1,), 0)
+    numel = synth.layer_numel(2048)
+    p = ctx.partition(numel, 256, 1, 1, 1)
+    Np = p.padded_numel
+    ctx.enable_p2p(4 * Np + (64 << 20))
+    prim = [synth.torch_normal(Np, 1 + i, 0.02, torch.bfloat16, "cuda", outlier_every=0) for i in range(2)]
+    grad = synth.torch_normal(Np, 11, 1e-3, torch.bfloat16, "cuda")
+    sec_c = [ctx.sym_alloc(Np, torch.uint8) for _ in range(2)]
+    sec_s = [ctx.sym_alloc(Np // 256, torch.float32) for _ in range(2)]
+    out = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
+    shard = torch.empty(Np, dtype=torch.float32, device="cuda")
+    ctx.allgather_params(p, prim[0], sec_c[0], sec_s[0], out)
+    fwd = lambda: ctx.allgather_params_next(p, prim[0], sec_c[0], sec_s[0], out, p_next=p, next_primary=prim[1],
+                                            next_sec_codes=sec_c[1], next_sec_scales=sec_s[1])
+    bwd = lambda: ctx.backward_step(p, grad, shard, [4], p_prev=p, prev_sec_codes=sec_c[0], prev_sec_scales=sec_s[0],
+                                    prev_full_out=out)
+    for name, fn in (("pair_fwd", fwd), ("pair_bwd", bwd)):
+        fn()
+        torch.cuda.synchronize()
+        if args.once:
+            continue
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        print(json.dumps({"call": name, "numel": Np, "us": round(e0.elapsed_time(e1) / args.iters * 1e3, 2)}),
+              flush=True)
     ctx.close()
 
 
