@@ -43,7 +43,8 @@ HIERARCHY = {
     "gpt6.7b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
     "neox20b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
 }
-KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "gather_quantize", "quantize_dequantize", "reduce",
+KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "gather_quantize", "dequantize_roundtrip",
+                "quantize_dequantize", "reduce",
                 "reduce_requant",
                 "quantize_push", "reduce_push", "ag_fused", "rs_fused")
 NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md); 900 nominal
@@ -180,6 +181,9 @@ MIX_PROBE_KINDS = {   # kernel kind -> probe mixes (tools/hbm_mix_probe.cu) it a
     "quantize_dequantize": ("quantize_dequantize_bf16", "quantize_dequantize_f32"),
     "dequantize": ("dequantize",),
     "quantize": ("quantize",),
+    # world-1 backward pair: dequantize of layer i-1 + qgZ round trip of layer i (equal sizes
+    # except the embedding, so the per-element average of the two mixes)
+    "dequantize_roundtrip": ("dequantize", "quantize_dequantize_f32"),
 }
 
 

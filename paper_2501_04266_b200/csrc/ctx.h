@@ -105,7 +105,7 @@ hz_status run_reduce_push(int g, const uint8_t* const* c, const float* const* s,
                           int64_t remote);
 hz_status run_gather_quantize(const Pieces& pc, int64_t n, int bits, void* y, hz_dtype odt, const void* x,
                               hz_dtype dt, int64_t nq, int qbits, uint8_t* c, float* s, cudaStream_t st,
-                              const SyncArgs& sync, int64_t remote_bytes);
+                              const SyncArgs& sync, int64_t remote_bytes, float* qy = nullptr, int acc = 0);
 hz_status copy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
 hz_status run_sum(const Pieces& pc, int64_t n, float* out, cudaStream_t st, int level, const SyncArgs* sync,
                   int64_t remote);

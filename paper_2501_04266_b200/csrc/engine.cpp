@@ -25,6 +25,8 @@
 
 namespace hz {
 
+int tune_param(const char* name, int dflt);
+
 hz_status cuda_fail(cudaError_t e, const char* what) {
   return fail(HZ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -144,13 +146,13 @@ hz_status run_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block
 
 hz_status run_gather_quantize(const Pieces& pc, int64_t n, int bits, void* y, hz_dtype odt, const void* x,
                               hz_dtype dt, int64_t nq, int qbits, uint8_t* c, float* s, cudaStream_t st,
-                              const SyncArgs& sync, int64_t remote_bytes) {
+                              const SyncArgs& sync, int64_t remote_bytes, float* qy, int acc) {
   const int64_t g_bytes = code_bytes(n, bits) + n / 256 * 4 + n * elem_bytes(odt) - remote_bytes;
-  const int64_t q_bytes = nq * elem_bytes(dt) + code_bytes(nq, qbits) + nq / 256 * 4;
-  TraceScope t(st, "gather_quantize", 0, bits, n + nq, g_bytes + q_bytes, remote_bytes);
+  const int64_t q_bytes = nq * elem_bytes(dt) + (qy ? nq * 4 * (acc ? 2 : 1) : code_bytes(nq, qbits) + nq / 256 * 4);
+  TraceScope t(st, qy ? "dequantize_roundtrip" : "gather_quantize", 0, bits, n + nq, g_bytes + q_bytes, remote_bytes);
   SyncArgs sy = sync;
   sy.stamps = t.stamps;
-  cudaError_t e = launch_gather_quantize(pc, n, y, x, dt, nq, qbits, c, s, st, sy);
+  cudaError_t e = launch_gather_quantize(pc, n, y, x, dt, nq, qbits, c, s, qy, acc, st, sy);
   t.end();
   if (e != cudaSuccess) return cuda_fail(e, "gather+quantize kernel launch");
   return HZ_OK;
@@ -516,6 +518,27 @@ hz_status hz_backward_step(hz_ctx* ctx, const hz_partition_t* p, const void* gra
       p2p_prev_fusable(ctx, p, from_level, pg))
     return p2p_reduce_scatter(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard, accumulate,
                               static_cast<cudaStream_t>(stream), &pg);
+  if (!ctx->p2p.on && from_level == to_level && ctx->group[from_level - 1] == 1 && roundtrip_supported(p->block) &&
+      p_prev->block == 256 && p_prev->len[p_prev->s] == p_prev->padded_numel && p_prev->padded_numel > 0 &&
+      p->len[from_level - 1] > 0 && gather_quantize_supported(256, prev_bits, prev_out_dt) &&
+      tune_param("pair1", 0) == 1) {
+    // no exchange on either side (one-member groups): the previous layer's backward
+    // gather is the dequantize of its secondary and this layer's qgZ the round trip of
+    // its gradient — both HBM streams, one launch instead of two.  Off by default
+    // (HZ_TUNE pair1=1): measured at N = 1, GPT-1.3B, 3.295 vs 3.270 ms per step — two
+    // HBM-bound streams gain nothing from sharing a launch (profiles/pairing_r01/)
+    Pieces pc{};
+    pc.n = 1;
+    pc.len = p_prev->padded_numel;
+    pc.c[0] = prev_sec_codes;
+    pc.s[0] = prev_sec_scales;
+    if ((rc = run_gather_quantize(pc, p_prev->padded_numel, prev_bits, prev_full_out, prev_out_dt, grad, dt,
+                                  p->len[from_level - 1], bits_per_level[from_level - 1], nullptr, nullptr,
+                                  static_cast<cudaStream_t>(stream), SyncArgs{}, 0, shard, accumulate)) != HZ_OK)
+      return rc;
+    clear_error();
+    return HZ_OK;
+  }
   // not fusable (NCCL transport, other block sizes / dtypes): the two calls in order
   if ((rc = hz_allgather_params(ctx, p_prev, 1, nullptr, HZ_BF16, prev_bits, prev_sec_codes, prev_sec_scales,
                                 prev_full_out, prev_out_dt, stream)) != HZ_OK)

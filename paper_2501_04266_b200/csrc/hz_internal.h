@@ -78,9 +78,11 @@ cudaError_t launch_quantize_roundtrip(const void* x, hz_dtype dt, int64_t n, int
 // Dual kernel (k_quantize.cu): gather+dequantize of pc (n_gather elements, 8-bit codes,
 // bf16 out, B = 256) and quantize of x (n_q elements, qbits) in one launch.
 bool gather_quantize_supported(int block, int gather_bits, hz_dtype out_dt);
+// qy != nullptr: the quantize job is the fp32 round trip of a one-member level (x_hat
+// into qy, += when acc; codes / scales not stored).
 cudaError_t launch_gather_quantize(const Pieces& pc, int64_t n_gather, void* y, const void* x, hz_dtype dt,
-                                   int64_t n_q, int qbits, uint8_t* codes, float* scales, cudaStream_t st,
-                                   const SyncArgs& sy);
+                                   int64_t n_q, int qbits, uint8_t* codes, float* scales, float* qy, int acc,
+                                   cudaStream_t st, const SyncArgs& sy);
 cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, int64_t n, int bits,
                               int block, void* y, hz_dtype out_dt, cudaStream_t st);
 cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,

@@ -247,14 +247,24 @@ cudaError_t quantize_d(const void* x, int64_t n, int bits, int block, uint8_t* c
 // grid-stride share of both jobs; odd CTAs gather first and even CTAs quantize
 // first, so at any time about half the warps stream each resource (HZ_TUNE gq=1:
 // every CTA gathers first).  Arithmetic per element is exactly the two kernels'.
-template <typename T, int QBITS, int GBITS, typename TO>
+template <typename T, int QBITS, int GBITS, typename TO, int QOUT>
 __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_constant__ Pieces pc, int64_t nunits,
                                                                TO* __restrict__ y, const T* __restrict__ x,
                                                                int64_t nblocks, uint8_t* __restrict__ codes,
-                                                               float* __restrict__ scales, int order,
+                                                               float* __restrict__ scales, float* __restrict__ qy,
+                                                               int acc, int order,
                                                                const __grid_constant__ SyncArgs sy) {
+  // QOUT 3: the quantize job is the round trip of a one-member level (fp32 x_hat into
+  // qy, += when acc; codes not stored) — the world-1 backward pair
+  __shared__ float4 stage[QOUT == 3 ? kThreads / 32 : 1][QOUT == 3 ? 64 : 1];
+  using Emit = typename OutOf<QOUT>::E;
+  Emit emit;
+  if constexpr (QOUT == 3) {
+    emit.y = qy;
+    emit.stage = stage[threadIdx.x >> 5];
+    emit.acc = acc;
+  }
   sync_wait(sy);
-  NoEmit emit;
   const int64_t warp = global_warp(), nwarps = num_warps();
   if (order >= 2) {   // role split: CTAs [0, order - 2) gather only, the rest quantize only
     const int64_t gcta = order - 2;
@@ -262,22 +272,22 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
     if (blockIdx.x < gcta)
       dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, gcta * wpc);
     else
-      quantize_loop<T, 256, QBITS, kU, 0, NoPush>(x, nblocks, codes, scales, emit, nullptr, 0, NoPush{},
-                                                  warp - gcta * wpc, nwarps - gcta * wpc);
+      quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{},
+                                                     warp - gcta * wpc, nwarps - gcta * wpc);
   } else if (order == 0 && (blockIdx.x & 1) == 0) {
-    quantize_loop<T, 256, QBITS, kU, 0, NoPush>(x, nblocks, codes, scales, emit, nullptr, 0, NoPush{}, warp, nwarps);
+    quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps);
     dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps);
   } else {
     dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps);
-    quantize_loop<T, 256, QBITS, kU, 0, NoPush>(x, nblocks, codes, scales, emit, nullptr, 0, NoPush{}, warp, nwarps);
+    quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps);
   }
   sync_signal(sy);
 }
 
-template <typename T, int QBITS>
+template <typename T, int QBITS, int QOUT>
 cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const void* x, int64_t n_q, uint8_t* codes,
-                              float* scales, cudaStream_t st, const SyncArgs& sy) {
-  auto kern = k_gather_quantize<T, QBITS, 8, __nv_bfloat16>;
+                              float* scales, float* qy, int acc, cudaStream_t st, const SyncArgs& sy) {
+  auto kern = k_gather_quantize<T, QBITS, 8, __nv_bfloat16, QOUT>;
   const int64_t nunits = n_gather / 8;
   const int64_t nblocks = n_q / 256;
   const int64_t tasks = std::max<int64_t>((nunits + 32 * kU - 1) / (32 * kU), nblocks / (kU * Geo<256>::BPW) + 1);
@@ -292,7 +302,17 @@ cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const
     order = static_cast<int>(2 + gc);
   }
   return launch_k(kern, grid, st, pc, nunits, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x), nblocks,
-                  codes, scales, order, sy);
+                  codes, scales, qy, acc, order, sy);
+}
+
+template <typename T>
+cudaError_t gather_quantize_d(const Pieces& pc, int64_t n_gather, void* y, const void* x, int64_t n_q, int qbits,
+                              uint8_t* codes, float* scales, float* qy, int acc, cudaStream_t st, const SyncArgs& sy) {
+  if (qy)
+    return qbits == 8 ? gather_quantize_t<T, 8, 3>(pc, n_gather, y, x, n_q, codes, scales, qy, acc, st, sy)
+                      : gather_quantize_t<T, 4, 3>(pc, n_gather, y, x, n_q, codes, scales, qy, acc, st, sy);
+  return qbits == 8 ? gather_quantize_t<T, 8, 0>(pc, n_gather, y, x, n_q, codes, scales, nullptr, 0, st, sy)
+                    : gather_quantize_t<T, 4, 0>(pc, n_gather, y, x, n_q, codes, scales, nullptr, 0, st, sy);
 }
 
 }  // namespace
@@ -361,18 +381,13 @@ bool gather_quantize_supported(int block, int gather_bits, hz_dtype out_dt) {
 }
 
 cudaError_t launch_gather_quantize(const Pieces& pc, int64_t n_gather, void* y, const void* x, hz_dtype dt,
-                                   int64_t n_q, int qbits, uint8_t* codes, float* scales, cudaStream_t st,
-                                   const SyncArgs& sy) {
+                                   int64_t n_q, int qbits, uint8_t* codes, float* scales, float* qy, int acc,
+                                   cudaStream_t st, const SyncArgs& sy) {
   switch (dt) {
-    case HZ_F32:
-      return qbits == 8 ? gather_quantize_t<float, 8>(pc, n_gather, y, x, n_q, codes, scales, st, sy)
-                        : gather_quantize_t<float, 4>(pc, n_gather, y, x, n_q, codes, scales, st, sy);
+    case HZ_F32: return gather_quantize_d<float>(pc, n_gather, y, x, n_q, qbits, codes, scales, qy, acc, st, sy);
     case HZ_BF16:
-      return qbits == 8 ? gather_quantize_t<__nv_bfloat16, 8>(pc, n_gather, y, x, n_q, codes, scales, st, sy)
-                        : gather_quantize_t<__nv_bfloat16, 4>(pc, n_gather, y, x, n_q, codes, scales, st, sy);
-    case HZ_F16:
-      return qbits == 8 ? gather_quantize_t<__half, 8>(pc, n_gather, y, x, n_q, codes, scales, st, sy)
-                        : gather_quantize_t<__half, 4>(pc, n_gather, y, x, n_q, codes, scales, st, sy);
+      return gather_quantize_d<__nv_bfloat16>(pc, n_gather, y, x, n_q, qbits, codes, scales, qy, acc, st, sy);
+    case HZ_F16: return gather_quantize_d<__half>(pc, n_gather, y, x, n_q, qbits, codes, scales, qy, acc, st, sy);
   }
   return cudaErrorInvalidValue;
 }

@@ -54,6 +54,18 @@ def test_multi_gpu_transport_variants(n, tune):
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
 
 
+def test_world1_pair1_variant():
+    """World 1 with HZ_TUNE pair1=1: hz_backward_step runs the previous layer's dequantize
+    and this layer's qgZ round trip as one dual kernel (off by default); same results."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr", "127.0.0.1", "--master-port", "29519", os.path.join(ROOT, "tests", "mp_parity.py")]
+    env = dict(os.environ, HZ_TUNE="pair1=1")
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+
+
 def test_world1_full_size_neox20b():
     """NeoX-20B layer (453 M parameters) through hz_allgather_params / hz_reduce_scatter_grads
     in the bench configuration, checked on sampled blocks."""
