@@ -414,6 +414,7 @@ __device__ __forceinline__ int64_t num_warps() {
 // host-side grid sizing (codec_util.cu): grid-stride kernels get
 // min(ceil(warp_tasks / warps per CTA), SMs x resident CTAs of that kernel).
 int64_t grid_for(const void* kernel, int64_t warp_tasks);
+int sm_count();   // SMs of the current device (cached)
 
 // Every libhz kernel launch: kThreads per CTA, no dynamic shared memory, and the
 // programmatic-stream-serialization attribute when HZ_TUNE pdl=1 (PDL; off by

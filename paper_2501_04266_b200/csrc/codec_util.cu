@@ -7,7 +7,6 @@
 #include "codec.cuh"
 
 namespace hz {
-namespace {
 
 int sm_count() {
   static int cached[64] = {0};
@@ -21,6 +20,8 @@ int sm_count() {
   }
   return cached[dev];
 }
+
+namespace {
 
 int resident_ctas(const void* kernel) {
   static std::mutex mu;

@@ -8,9 +8,11 @@
 namespace hz {
 namespace dev {
 
+// Warp tiles [tile0, tile1) of the layer only (32*U units each; default: all of them).
 template <int BITS, typename TO, int U>
 __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits, int log2b, TO* __restrict__ y,
-                                                int64_t warp, int64_t nwarps) {
+                                                int64_t warp, int64_t nwarps, int64_t tile0 = 0,
+                                                int64_t tile1 = INT64_MAX) {
   const int lane = threadIdx.x & 31;
   const bool copy_sec = pc.sec_c != nullptr;
   // Pieces interleaved by warp tile (32*U units): consecutive tiles alternate between
@@ -18,7 +20,8 @@ __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits
   // instead of one half of the layer after the other.
   const bool inter = pc.n > 1 && (pc.len % (256 * U)) == 0;
   const int64_t tiles_per_piece = pc.len / (256 * U);
-  for (int64_t base = warp * 32 * U; base < nunits; base += nwarps * 32 * U) {
+  const int64_t end = tile1 < (nunits + 32 * U - 1) / (32 * U) ? tile1 * 32 * U : nunits;
+  for (int64_t base = (tile0 + warp) * 32 * U; base < end; base += nwarps * 32 * U) {
     int64_t ub = base;            // first unit of this warp tile in the layer
     int jt = -1;                  // its piece, when interleaved
     if (inter) {

@@ -36,9 +36,12 @@ struct OutOf<3> { using E = EmitF32; };
 // The quantize loop: warp `warp` of `nwarps` processes its grid-stride share of the
 // blocks (main loop without bounds checks, then the checked tail on the last warp).
 template <typename T, int B, int BITS, int U, int OUT, class P, class Emit>
+// Iterations [it0, it1) of the main loop only (U*BPW blocks each; default: all); the
+// tail belongs to the range that ends at the last iteration.
 __device__ __forceinline__ void quantize_loop(const T* __restrict__ x, int64_t nblocks, uint8_t* __restrict__ codes,
                                               float* __restrict__ scales, Emit& emit, void* __restrict__ y, int acc,
-                                              const P& push, int64_t warp, int64_t nwarps) {
+                                              const P& push, int64_t warp, int64_t nwarps, int64_t it0 = 0,
+                                              int64_t it1 = INT64_MAX) {
   using G = Geo<B>;
   constexpr int NB = U * G::BPW;
   const int lane = threadIdx.x & 31;
@@ -46,7 +49,8 @@ __device__ __forceinline__ void quantize_loop(const T* __restrict__ x, int64_t n
   const int ll = lane % G::LPB;
   const int64_t nfull = nblocks / NB;
 
-  for (int64_t it = warp; it < nfull; it += nwarps) {
+  const int64_t itend = it1 < nfull ? it1 : nfull;
+  for (int64_t it = it0 + warp; it < itend; it += nwarps) {
     const int64_t blk0 = it * NB;
     In8<T> raw[U][G::NSUB];
 #pragma unroll
@@ -73,7 +77,7 @@ __device__ __forceinline__ void quantize_loop(const T* __restrict__ x, int64_t n
 
   // tail: the last nblocks % NB blocks, one warp step at a time, bounds-checked
   const int64_t tail0 = nfull * NB;
-  if (tail0 < nblocks && warp == nwarps - 1) {
+  if (tail0 < nblocks && warp == nwarps - 1 && it1 >= nfull) {
     for (int64_t b0 = tail0; b0 < nblocks; b0 += G::BPW) {
       const int64_t blk = b0 + lb;
       const bool valid = blk < nblocks;
@@ -247,12 +251,12 @@ cudaError_t quantize_d(const void* x, int64_t n, int bits, int block, uint8_t* c
 // grid-stride share of both jobs; odd CTAs gather first and even CTAs quantize
 // first, so at any time about half the warps stream each resource (HZ_TUNE gq=1:
 // every CTA gathers first).  Arithmetic per element is exactly the two kernels'.
-template <typename T, int QBITS, int GBITS, typename TO, int QOUT>
+template <typename T, int QBITS, int GBITS, typename TO, int QOUT, bool CHUNKED>
 __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_constant__ Pieces pc, int64_t nunits,
                                                                TO* __restrict__ y, const T* __restrict__ x,
                                                                int64_t nblocks, uint8_t* __restrict__ codes,
                                                                float* __restrict__ scales, float* __restrict__ qy,
-                                                               int acc, int order,
+                                                               int acc, int order, int chunks,
                                                                const __grid_constant__ SyncArgs sy) {
   // QOUT 3: the quantize job is the round trip of a one-member level (fp32 x_hat into
   // qy, += when acc; codes not stored) — the world-1 backward pair
@@ -274,6 +278,20 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
     else
       quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{},
                                                      warp - gcta * wpc, nwarps - gcta * wpc);
+  } else if (CHUNKED) {
+    // both jobs cut into `chunks` consecutive pieces; every warp alternates between
+    // them (odd CTAs gather first), so the link and HBM streams stay mixed to the end
+    const int64_t ta = (nunits + 32 * kU - 1) / (32 * kU);
+    const int64_t tb = nblocks / (kU * Geo<256>::BPW);
+    const bool gfirst = blockIdx.x & 1;
+    for (int c = 0; c < chunks; ++c) {
+      const int64_t a0 = ta * c / chunks, a1 = ta * (c + 1) / chunks;
+      const int64_t b0 = tb * c / chunks, b1 = c + 1 == chunks ? INT64_MAX : tb * (c + 1) / chunks;
+      if (gfirst) dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps, a0, a1);
+      quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps,
+                                                     b0, b1);
+      if (!gfirst) dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps, a0, a1);
+    }
   } else if (order == 0 && (blockIdx.x & 1) == 0) {
     quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps);
     dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps);
@@ -287,7 +305,17 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
 template <typename T, int QBITS, int QOUT>
 cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const void* x, int64_t n_q, uint8_t* codes,
                               float* scales, float* qy, int acc, cudaStream_t st, const SyncArgs& sy) {
-  auto kern = k_gather_quantize<T, QBITS, 8, __nv_bfloat16, QOUT>;
+  // chunks of the interleaved schedule (HZ_TUNE gqc; default by size): one pass when a
+  // warp has few gather tiles (GPT-1.3B layer, ~10 per warp: the chunked kernel's extra
+  // registers cost more than the balance gains, 3.80 vs 4.20 ms), 4 chunks from ~32 tiles
+  // per warp on (GPT-6.7B layer: 19.28 -> 17.76 ms per step at N = 2)
+  int chunks = tune_param("gqc", 0);
+  if (chunks <= 0) {
+    const int64_t per_warp = (n_gather / 8 + 32 * kU - 1) / (32 * kU) / (int64_t(sm_count()) * 32);
+    chunks = per_warp >= 32 ? 4 : 1;
+  }
+  auto kern = chunks > 1 ? k_gather_quantize<T, QBITS, 8, __nv_bfloat16, QOUT, true>
+                         : k_gather_quantize<T, QBITS, 8, __nv_bfloat16, QOUT, false>;
   const int64_t nunits = n_gather / 8;
   const int64_t nblocks = n_q / 256;
   const int64_t tasks = std::max<int64_t>((nunits + 32 * kU - 1) / (32 * kU), nblocks / (kU * Geo<256>::BPW) + 1);
@@ -301,8 +329,9 @@ cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const
     gc = std::min<int64_t>(std::max<int64_t>(gc, 1), grid - 1);
     order = static_cast<int>(2 + gc);
   }
+  // HZ_TUNE gqc: chunks of the interleaved schedule (order 0)
   return launch_k(kern, grid, st, pc, nunits, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x), nblocks,
-                  codes, scales, qy, acc, order, sy);
+                  codes, scales, qy, acc, order, chunks, sy);
 }
 
 template <typename T>
