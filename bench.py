@@ -20,6 +20,12 @@ step touches several GB (> 126 MB L2), so no L2 flush is needed between steps.
 value = logical bytes of all ranks / time, logical bytes per tensor per rank =
 2*psi (forward gathered bf16) + 2*psi (backward gathered bf16) + 2*psi (bf16
 gradient in): 6*psi.  Weak scaling: per-rank work is fixed as N grows.
+
+The calls are issued in a training step's order with adjacent layers paired
+(--pipelined, default): hz_allgather_params_next gathers layer k and prefetches
+the quantize of layer k+1 in the same launch; hz_backward_step reduce-scatters
+layer i while gathering layer i-1 (one dual kernel on the NVLink transport).
+--no-pipelined issues one call per collective.
 """
 
 import argparse

@@ -96,6 +96,13 @@ def test_collective_validation_without_context(hz):
     bits = (ctypes.c_int * 2)(4, 4)
     assert lib.hz_step_host(None, 1, None, hz.BF16, 8, bits, None, None, hz.BF16, None) == hz.ERR_INVALID
     assert lib.hz_last_error().startswith(b"ctx")
+    # the paired-layer entry points validate like the calls they pair
+    assert lib.hz_allgather_params_next(None, ctypes.byref(p), None, hz.BF16, 8, None, None, None, hz.BF16, None,
+                                        None, None, None, None) == hz.ERR_INVALID
+    assert lib.hz_last_error().startswith(b"ctx")
+    assert lib.hz_backward_step(None, ctypes.byref(p), None, hz.BF16, 1, 2, bits, None, 0, None, None, None, 8, None,
+                                hz.BF16, None) == hz.ERR_INVALID
+    assert lib.hz_last_error().startswith(b"ctx")
 
 
 def test_codec_validation_without_gpu(hz):
