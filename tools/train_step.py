@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--modes", default="compute,hz,flat")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
+    ap.add_argument("--pair", action=argparse.BooleanOptionalAction, default=True,
+                    help="forward gathers through hz_allgather_params_next (next layer's quantize in the same launch)")
     ap.add_argument("--hierarchy", default="", help="override, e.g. 4 = ZeRO++-style one level over all ranks")
     ap.add_argument("--green", type=int, default=0,
                     help="run the communication stream in a CUDA green context of this many SMs "
@@ -168,7 +170,14 @@ def main():
 
         def ag(i, backward):
             t = layers[i]
-            if mode == "hz":
+            if mode == "hz" and not backward and args.pair:
+                # forward: gather layer i and prefetch the quantize of layer i+1 in one launch
+                nx = layers[i + 1] if i + 1 < nl else None
+                ctx.allgather_params_next(p, t["primary"], t["sec_c"], t["sec_s"], gathered[i & 1], bits=8,
+                                          p_next=p if nx else None, next_primary=nx["primary"] if nx else None,
+                                          next_sec_codes=nx["sec_c"] if nx else None,
+                                          next_sec_scales=nx["sec_s"] if nx else None, stream=comm)
+            elif mode == "hz":
                 ctx.allgather_params(p, None if backward else t["primary"], t["sec_c"], t["sec_s"], gathered[i & 1],
                                      bits=8, backward=backward, stream=comm)
             else:
@@ -242,7 +251,7 @@ def main():
     line = {"what": "synthetic ZeRO-topo training step (layer GEMMs + sharded collectives, overlapped)",
             "config": args.config, "layers": nl, "tokens_per_gpu": T, "n_gpus": world, "hierarchy": list(group),
             "transport": "p2p" if use_p2p else ("nccl" if world > 1 else "local"),
-            "green_sms": green_sms if args.green else 0, "prio": args.prio, "hz_tune": os.environ.get("HZ_TUNE", ""),
+            "green_sms": green_sms if args.green else 0, "prio": args.prio, "pair": args.pair, "hz_tune": os.environ.get("HZ_TUNE", ""),
             "results": results}
     ctx.close()
     if rank == 0:
