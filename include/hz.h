@@ -51,8 +51,10 @@
  *   - Return value: HZ_OK, or an error code with a message naming the offending
  *     argument available from hz_last_error() (thread-local).  Nothing is
  *     enqueued when validation fails.
- *   - Collective calls (hz_init, hz_allgather_params, hz_reduce_scatter_grads,
- *     hz_finalize) must be issued by every rank in the same order (NCCL rule).
+ *   - Collective calls (hz_init, hz_allgather_params, hz_allgather_params_next,
+ *     hz_reduce_scatter_grads, hz_backward_step, hz_allreduce_select,
+ *     hz_adamw_step, hz_step_host, hz_finalize) must be issued by every rank in
+ *     the same order with the same arguments' shapes (NCCL rule).
  *   - Non-finite inputs are a precondition violation; results are
  *     unspecified for them.
  */
