@@ -347,6 +347,10 @@ HZ_API hz_status hz_adamw_step(hz_ctx* ctx, const hz_partition_t* p, const float
  *                          hz_allgather_params(backward) -> full_out[i % 2],
  *                          hz_reduce_scatter_grads(levels 1..L, qgz_bits) -> t[i].d_shard,
  *                          copy t[i].d_shard -> t[i].h_shard (fp32[len_L]).
+ * The kernels are issued as the paired calls of a training step
+ * (hz_allgather_params_next with layer i+1 as next; hz_backward_step with layer i-1
+ * as prev), so on the P2P transport adjacent layers share launches; the results are
+ * those of the single calls above, bitwise.
  * The copies run on two library-owned streams (host->device and device->host), the
  * kernels on `stream`; per-tensor events order them, so the PCIe transfers of the
  * two directions overlap each other and the kernels.  `stream` finally waits for

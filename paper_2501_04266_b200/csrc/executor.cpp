@@ -14,7 +14,8 @@
 // uploads wait only for the previous call's kernels (its staging buffers were
 // read by them), not for its downloads: back-to-back steps keep both PCIe
 // directions busy.  The kernel stream waits for the last download at the end, so
-// the call is stream-ordered on `stream` like every other entry point.
+// the call is stream-ordered on `stream` like every other entry point.  The kernels
+// are issued as the paired calls (hz_allgather_params_next / hz_backward_step).
 #include <string>
 
 #include "ctx.h"
@@ -120,21 +121,29 @@ extern "C" hz_status hz_step_host(hz_ctx* ctx, int n, const hz_tensor_io* t, hz_
   }
 
   void* full[2] = {full_out0, full_out1};
-  // forward: qwZ + hpZ gather of every tensor as its primary arrives
+  // forward: gather layer i with the quantize of layer i+1 prefetched into the same
+  // launch (hz_allgather_params_next), as soon as both primaries are on the GPU
+  HZ_X(cudaStreamWaitEvent(st, ex.ev[0], 0), "hz_step_host: wait primary");
   for (int i = 0; i < n; ++i) {
-    HZ_X(cudaStreamWaitEvent(st, ex.ev[3 * i], 0), "hz_step_host: wait primary");
-    rc = hz_allgather_params(ctx, t[i].p, 0, t[i].d_primary, dt, qwz_bits, t[i].sec_codes, t[i].sec_scales,
-                             full[i & 1], out_dt, stream);
+    const bool nx = i + 1 < n;
+    if (nx) HZ_X(cudaStreamWaitEvent(st, ex.ev[3 * (i + 1)], 0), "hz_step_host: wait primary");
+    rc = hz_allgather_params_next(ctx, t[i].p, t[i].d_primary, dt, qwz_bits, t[i].sec_codes, t[i].sec_scales,
+                                  full[i & 1], out_dt, nx ? t[i + 1].p : nullptr, nx ? t[i + 1].d_primary : nullptr,
+                                  nx ? t[i + 1].sec_codes : nullptr, nx ? t[i + 1].sec_scales : nullptr, stream);
     if (rc != HZ_OK) return rc;
   }
-  // backward: gather from the secondary, qgZ reduce-scatter, download the shard
+  // backward: layer i's qgZ with layer i-1's gather from its secondary (hz_backward_step),
+  // then the download of layer i's shard
+  rc = hz_allgather_params(ctx, t[n - 1].p, 1, nullptr, dt, qwz_bits, t[n - 1].sec_codes, t[n - 1].sec_scales,
+                           full[(n - 1) & 1], out_dt, stream);
+  if (rc != HZ_OK) return rc;
   for (int i = n - 1; i >= 0; --i) {
     const hz_partition_t* p = t[i].p;
-    rc = hz_allgather_params(ctx, p, 1, nullptr, dt, qwz_bits, t[i].sec_codes, t[i].sec_scales, full[i & 1],
-                             out_dt, stream);
-    if (rc != HZ_OK) return rc;
     HZ_X(cudaStreamWaitEvent(st, ex.ev[3 * i + 1], 0), "hz_step_host: wait gradient");
-    rc = hz_reduce_scatter_grads(ctx, p, t[i].d_grad, dt, 1, L, qgz_bits, t[i].d_shard, 0, stream);
+    const bool pv = i > 0;
+    rc = hz_backward_step(ctx, p, t[i].d_grad, dt, 1, L, qgz_bits, t[i].d_shard, 0, pv ? t[i - 1].p : nullptr,
+                          pv ? t[i - 1].sec_codes : nullptr, pv ? t[i - 1].sec_scales : nullptr, qwz_bits,
+                          pv ? full[(i - 1) & 1] : nullptr, out_dt, stream);
     if (rc != HZ_OK) return rc;
     HZ_X(cudaEventRecord(ex.ev[3 * i + 2], st), "hz_step_host: cudaEventRecord");
     HZ_X(cudaStreamWaitEvent(ex.d2h, ex.ev[3 * i + 2], 0), "hz_step_host: wait shard");
