@@ -514,6 +514,7 @@ hz_status hz_backward_step(hz_ctx* ctx, const hz_partition_t* p, const void* gra
     return fail(rc, std::string("prev: ") + hz_last_error());
   if ((rc = check_async(ctx)) != HZ_OK) return rc;
   PrevG pg{p_prev, prev_sec_codes, prev_sec_scales, prev_bits, prev_full_out, prev_out_dt};
+  if (prev_full_out == grad) return fail(HZ_ERR_INVALID, "prev_full_out: aliases grad");
   if (ctx->p2p.on && p->len[from_level - 1] > 0 && p_prev->padded_numel > 0 &&
       p2p_prev_fusable(ctx, p, from_level, pg))
     return p2p_reduce_scatter(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard, accumulate,

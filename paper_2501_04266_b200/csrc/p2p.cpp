@@ -342,7 +342,8 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
     pc.sec_lo = p->off[s];
     pc.sec_hi = p->off[s] + len_s;
   }
-  if (!backward && next && p2p_next_fusable(ctx, p, bits, out_dt, *next)) {
+  if (!backward && next && next->codes != sec_codes && next->scales != sec_scales &&
+      p2p_next_fusable(ctx, p, bits, out_dt, *next)) {
     // gather this layer (phase) || quantize the next layer's primary (phase + 1) in one
     // launch.  Waits: the members' codes of this phase are ready, and every rank is
     // done with every phase before it (nobody still reads the next layer's secondary,
