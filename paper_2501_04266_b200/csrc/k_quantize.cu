@@ -251,7 +251,7 @@ cudaError_t quantize_d(const void* x, int64_t n, int bits, int block, uint8_t* c
 // grid-stride share of both jobs; odd CTAs gather first and even CTAs quantize
 // first, so at any time about half the warps stream each resource (HZ_TUNE gq=1:
 // every CTA gathers first).  Arithmetic per element is exactly the two kernels'.
-template <typename T, int QBITS, int GBITS, typename TO, int QOUT, bool CHUNKED>
+template <typename T, int QBITS, int GBITS, typename TO, int QOUT, bool CHUNKED, int GU = kU>
 __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_constant__ Pieces pc, int64_t nunits,
                                                                TO* __restrict__ y, const T* __restrict__ x,
                                                                int64_t nblocks, uint8_t* __restrict__ codes,
@@ -274,29 +274,29 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
     const int64_t gcta = order - 2;
     const int64_t wpc = kThreads / 32;
     if (blockIdx.x < gcta)
-      dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, gcta * wpc);
+      dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, gcta * wpc);
     else
       quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{},
                                                      warp - gcta * wpc, nwarps - gcta * wpc);
   } else if (CHUNKED) {
     // both jobs cut into `chunks` consecutive pieces; every warp alternates between
     // them (odd CTAs gather first), so the link and HBM streams stay mixed to the end
-    const int64_t ta = (nunits + 32 * kU - 1) / (32 * kU);
+    const int64_t ta = (nunits + 32 * GU - 1) / (32 * GU);
     const int64_t tb = nblocks / (kU * Geo<256>::BPW);
     const bool gfirst = blockIdx.x & 1;
     for (int c = 0; c < chunks; ++c) {
       const int64_t a0 = ta * c / chunks, a1 = ta * (c + 1) / chunks;
       const int64_t b0 = tb * c / chunks, b1 = c + 1 == chunks ? INT64_MAX : tb * (c + 1) / chunks;
-      if (gfirst) dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps, a0, a1);
+      if (gfirst) dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, nwarps, a0, a1);
       quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps,
                                                      b0, b1);
-      if (!gfirst) dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps, a0, a1);
+      if (!gfirst) dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, nwarps, a0, a1);
     }
   } else if (order == 0 && (blockIdx.x & 1) == 0) {
     quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps);
-    dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps);
+    dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, nwarps);
   } else {
-    dequantize_loop<GBITS, TO, kU>(pc, nunits, 8, y, warp, nwarps);
+    dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, nwarps);
     quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps);
   }
   sync_signal(sy);
@@ -314,8 +314,11 @@ cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const
     const int64_t per_warp = (n_gather / 8 + 32 * kU - 1) / (32 * kU) / (int64_t(sm_count()) * 32);
     chunks = per_warp >= 32 ? 4 : 1;
   }
+  // HZ_TUNE gqu=8: 8 gather units in flight per lane (one-pass codes-only variant)
   auto kern = chunks > 1 ? k_gather_quantize<T, QBITS, 8, __nv_bfloat16, QOUT, true>
                          : k_gather_quantize<T, QBITS, 8, __nv_bfloat16, QOUT, false>;
+  if constexpr (QOUT == 0)
+    if (chunks == 1 && tune_param("gqu", kU) == 8) kern = k_gather_quantize<T, QBITS, 8, __nv_bfloat16, 0, false, 8>;
   const int64_t nunits = n_gather / 8;
   const int64_t nblocks = n_q / 256;
   const int64_t tasks = std::max<int64_t>((nunits + 32 * kU - 1) / (32 * kU), nblocks / (kU * Geo<256>::BPW) + 1);

@@ -77,6 +77,6 @@ def test_no_local_memory(resources):
 def test_dual_kernel_default_variant_fits_64_registers(resources):
     """The one-pass k_gather_quantize (the default below 32 gather tiles per warp) keeps
     the 64 registers of the kernels it merges (4 CTAs of 256 threads per SM)."""
-    one_pass = [r for f, r in resources.items() if "k_gather_quantize" in f and "Li0ELb0E" in f]
+    one_pass = [r for f, r in resources.items() if "k_gather_quantize" in f and "Li0ELb0ELi4E" in f]
     assert one_pass
     assert all(r["REG"] <= 64 and r.get("STACK", 0) == 0 for r in one_pass), one_pass
