@@ -331,6 +331,23 @@ def barrier(world):
         dist.barrier()
 
 
+def step_model(recs, steps, hbm_peak, nvl_peak=NVLINK_PEER_GBS, nvl_bidir=NVLINK_BIDIR_PROBE_GBS):
+    """the modeled minimum of one step = the sum over the step's
+    launches of each launch's roofline time, max(local HBM bytes / HBM peak, peer bytes /
+    NVLink peak) (NCCL calls: bytes sent / NVLink peak) — every kernel at its roofline,
+    back to back, no synchronisation.  Returned per step, with the NVLink term also taken
+    at the bidirectional peer-read probe (both GPUs of a group pull at once)."""
+    t, tb = 0.0, 0.0
+    for r in recs:
+        b, rem = float(r["bytes"]), float(r.get("remote_bytes", 0) or 0)
+        if r["kind"].startswith("nccl"):
+            b, rem = 0.0, b
+        t += max(b / (hbm_peak * 1e9), rem / (nvl_peak * 1e9))
+        tb += max(b / (hbm_peak * 1e9), rem / (nvl_bidir * 1e9))
+    return {"model_ms": t / steps * 1e3, "model_ms_bidir_probe": tb / steps * 1e3,
+            "hbm_peak_GBps": hbm_peak, "nvlink_peak_GBps": nvl_peak, "nvlink_bidir_probe_GBps": nvl_bidir}
+
+
 def summarize_trace(recs, steps):
     kinds = {}
     for r in recs:
@@ -467,6 +484,11 @@ def run_hz(args):
     recs = hz.trace_read()
     # with a graph the trace holds one step's launches (events re-recorded by every replay)
     stages = summarize_trace(recs, 1 if graph is not None else args.steps)
+    peak0, _ = measured_peaks()
+    smodel = step_model(recs, 1 if graph is not None else args.steps, peak0) if recs else None
+    if smodel:
+        smodel["frac_of_model"] = smodel["model_ms"] / ms_per_step
+        smodel["frac_of_model_bidir_probe"] = smodel["model_ms_bidir_probe"] / ms_per_step
     gpu_launches = sum(1 for r in recs if r["kind"] in KERNEL_KINDS) * (args.steps if graph is not None else 1)
     value = world * model.logical_bytes / (ms_per_step * 1e-3) / 1e9
 
@@ -567,6 +589,7 @@ def run_hz(args):
         "gpu_launches": gpu_launches,
         "clocks": clocks,
         "stages": stages,
+        "step_model": smodel,
         "flat_zero3_baseline": flat,
         "step_tail": tail,
         "a10_cross_node_step": a10,

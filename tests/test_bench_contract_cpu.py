@@ -39,3 +39,16 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_step_model_sums_launch_rooflines():
+    """bench.step_model: per launch max(HBM bytes / HBM peak, peer bytes / NVLink peak),
+    NCCL calls on the link only, summed and divided by the steps the trace covers."""
+    sys.path.insert(0, ROOT)
+    import bench
+    recs = [{"kind": "quantize", "bytes": 6e9, "remote_bytes": 0},             # 1 ms at 6000 GB/s
+            {"kind": "gather_dequantize", "bytes": 3e9, "remote_bytes": 1.5e9},  # max(0.5, 2.0) ms at 750
+            {"kind": "nccl_allgather", "bytes": 0.75e9, "remote_bytes": 0}]      # 1 ms on the link
+    m = bench.step_model(recs, 2, 6000.0, nvl_peak=750.0, nvl_bidir=500.0)
+    assert abs(m["model_ms"] - (1.0 + 2.0 + 1.0) / 2) < 1e-9
+    assert abs(m["model_ms_bidir_probe"] - (1.0 + 3.0 + 1.5) / 2) < 1e-9
