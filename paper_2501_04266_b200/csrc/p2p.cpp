@@ -22,6 +22,15 @@
 // signal `ready`, consumers wait for `ready` and signal `done` (codec.cuh).
 // All P2P calls of one context must be issued on one stream, in the same order
 // on every rank (the NCCL discipline).
+//
+// Paired layers (hz_allgather_params_next / hz_backward_step): one dual kernel
+// (k_gather_quantize) runs a gather of phase a and a quantize of phase a+1.  It waits
+// for ready >= a (the gathered codes) and done >= a-1 (every rank finished every
+// earlier phase, so nobody still reads what the quantize overwrites: the next layer's
+// secondary, last read in an earlier backward phase, or the qgZ send slot, last read
+// by the previous layer's reduce) and signals done = a and ready = a+1.  A prefetched
+// quantize whose layer is not gathered next (another call comes first) leaves phase
+// a+1 without a `done`; flush_prefetch completes it before the next phase starts.
 #include <algorithm>
 #include <cstring>
 #include <string>
