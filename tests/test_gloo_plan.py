@@ -1,4 +1,4 @@
-"""Multi-process CPU tests of the N>1 host logic (gloo, world size 2 and 4).
+"""Multi-process CPU tests of the N>1 host logic (gloo, world size 2, 4 and 8).
 
 Each process is one rank.  It asks libhz for its partition (hz_partition_ex) and
 its communication plans (hz_plan_allgather / hz_plan_reduce_scatter — the plans
@@ -184,3 +184,8 @@ def test_gloo_world2():
 
 def test_gloo_world4():
     _run(4, [(2, 2), (4,), (2, 1, 2)])
+
+
+def test_gloo_world8():
+    """The bench's eight-GPU hierarchies ((2,4) for GPT-1.3B, (2,2,2) for 6.7B / 20B)."""
+    _run(8, [(2, 4), (2, 2, 2)])
