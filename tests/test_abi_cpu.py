@@ -126,3 +126,25 @@ def test_codec_validation_without_gpu(hz):
     assert lib.hz_finalize(None) == hz.OK
     assert lib.hz_trace_begin(0, 3) == hz.ERR_INVALID
     assert lib.hz_trace_begin(16, 0) == hz.ERR_INVALID
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    """No CPU fallback: the binding raises ImportError when libhz.so is missing."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = tmp_path / "paper_2501_04266_b200"
+    pkg.mkdir()
+    src = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2501_04266_b200")
+    for f in ("__init__.py", "hz.py"):
+        shutil.copy(os.path.join(src, f), pkg / f)
+    code = ("import sys\n"
+            "try:\n"
+            "    from paper_2501_04266_b200 import hz\n"
+            "except ImportError as e:\n"
+            "    print('ImportError', e); sys.exit(0)\n"
+            "sys.exit(1)\n")
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=tmp_path, timeout=120,
+                       env=dict(os.environ, PYTHONPATH=str(tmp_path)))
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "no CPU fallback" in p.stdout
