@@ -148,3 +148,15 @@ def test_binding_fails_loudly_without_the_library(tmp_path):
                        env=dict(os.environ, PYTHONPATH=str(tmp_path)))
     assert p.returncode == 0, p.stdout + p.stderr
     assert "no CPU fallback" in p.stdout
+
+
+def test_product_package_never_touches_the_oracle():
+    """The oracle is test infrastructure: nothing in the product package (binding,
+    build, synthetic inputs, CUDA / C++ sources) imports or includes it."""
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2501_04266_b200")
+    pat = re.compile(r"^\s*(import\s+oracle|from\s+oracle|#\s*include\s+\S*oracle)", re.M)
+    for dirpath, _, files in os.walk(root):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                with open(os.path.join(dirpath, f)) as fh:
+                    assert not pat.search(fh.read()), os.path.join(dirpath, f)
