@@ -84,7 +84,9 @@ typedef enum {
   HZ_ERR_CUDA = 2,        /* CUDA runtime / launch error */
   HZ_ERR_NCCL = 3,        /* NCCL error (incl. asynchronous errors of earlier calls) */
   HZ_ERR_NONFINITE = 4,   /* reserved for debug builds */
-  HZ_ERR_UNSUPPORTED = 5  /* valid request this build does not implement */
+  HZ_ERR_UNSUPPORTED = 5, /* valid request this build does not implement */
+  HZ_ERR_ABORTED = 6      /* the context was aborted (a cross-GPU wait timed out, or
+                             hz_abort); only hz_finalize is allowed afterwards */
 } hz_status;
 
 typedef enum { HZ_F32 = 0, HZ_BF16 = 1, HZ_F16 = 2 } hz_dtype;
@@ -104,6 +106,12 @@ typedef struct {
   int32_t digit[HZ_MAX_LEVELS];  /* d_l(rank) at index l-1 */
   int64_t off[HZ_MAX_LEVELS + 1];/* off_l, l = 0..L (elements) */
   int64_t len[HZ_MAX_LEVELS + 1];/* len_l, l = 0..L (elements) */
+  /* qgZ hop grouping ("1-hop all-to-all", reading R15): the reduce-scatter
+   * runs one all-to-all per hop; hop k covers levels hop_last[k-1]+1 .. hop_last[k]
+   * (hop_last[-1] = 0).  nhops == 0: one hop per level (the default written by
+   * hz_partition / hz_partition_ex).  Set with hz_partition_set_hops. */
+  int32_t nhops;
+  int32_t hop_last[HZ_MAX_LEVELS];
 } hz_partition_t;
 
 /* Library version string, e.g. "hz 0.1 sm_100a". Never NULL. */
@@ -125,6 +133,21 @@ HZ_API const char* hz_symbol_name(int i);
 HZ_API hz_status hz_partition_ex(int rank, int levels, const int* group, int64_t numel,
                           int block, int w, int s, int gl, hz_partition_t* out);
 
+/* Merged-level qgZ (the 1-hop all-to-all reduce-scatter; "the
+ * hop grouping is a parameter"; reading R15).  Sets p's hop grouping: nhops in
+ * [1, levels], hop_last strictly ascending, hop_last[nhops-1] == levels; nhops == 0
+ * (hop_last ignored) restores one hop per level.  A hop over levels a..b is ONE
+ * all-to-all over the prod_{l=a..b} g_l ranks that share every digit outside a..b:
+ * the member whose digits are (d_a..d_b) receives the chunk of range_{a-1} at
+ * sum_{l=a..b} d_l*len_l (its range_b — the ownership map is unchanged, O3), and
+ * each rank sums the members' dequantized chunks in ascending rank order, fp32, no
+ * FMA.  One quantization per hop: fewer requantizations than per-level hops (the
+ * error P:122 designs against), more peers per all-to-all.  Every qgZ entry point
+ * (hz_reduce_scatter_grads, hz_backward_step, hz_step_host) and
+ * hz_plan_reduce_scatter follow the grouping; their from_level / to_level must fall
+ * on hop boundaries.  Pure host function.  Errors: HZ_ERR_INVALID. */
+HZ_API hz_status hz_partition_set_hops(hz_partition_t* p, int nhops, const int* hop_last);
+
 /* Communication plan of one rank: the exact NCCL operations hz_allgather_params /
  * hz_reduce_scatter_grads issue, in order (the engine issues its calls from
  * these plans).  Pure host functions; used by the CPU (gloo) tests to check
@@ -133,10 +156,13 @@ HZ_API hz_status hz_partition_ex(int rank, int levels, const int* group, int64_t
  *     (send_off, elems) into range_{l-1} (recv_off), over the g_l members;
  *     all-gather top = w (forward) or s (backward) down to 1, levels with
  *     g_l = 1 omitted (O7/O8, Table VII).
- *   HZ_PLAN_SENDRECV: level-l exchange with the member of level digit `peer`
- *     (global rank peer_rank): send chunk `peer` of range_{l-1} (send_off,
- *     elems) and receive that member's chunk for range_l (recv_off); peers in
- *     ascending digit, levels from..to (O9, Table VIII).
+ *   HZ_PLAN_SENDRECV: exchange of the hop over levels level..level_last with
+ *     the member of merged digit `peer` (global rank peer_rank; its index in
+ *     ascending rank order within the hop group): send that member's chunk of
+ *     range_{level-1} (send_off, elems) and receive its chunk for range_{level_last}
+ *     (recv_off); peers in ascending merged digit, hops from..to (O9, Table
+ *     VIII).  With one hop per level, level_last == level and peer is the level
+ *     digit.
  * Offsets are global element offsets of the padded layer; code_bytes /
  * scale_bytes are the bytes of one piece / chunk.  *n_out = number of steps
  * (all of them, even when max is smaller; copies min(max, n)). */
@@ -144,8 +170,9 @@ typedef enum { HZ_PLAN_ALLGATHER = 1, HZ_PLAN_SENDRECV = 2 } hz_plan_op;
 
 typedef struct {
   int32_t op;         /* hz_plan_op */
-  int32_t level;      /* 1..L */
-  int32_t group;      /* g_level */
+  int32_t level;      /* 1..L (SENDRECV: first level of the hop) */
+  int32_t level_last; /* SENDRECV: last level of the hop; ALLGATHER: == level */
+  int32_t group;      /* members of the exchange (g_level, or the hop's product) */
   int32_t peer;       /* SENDRECV: peer's level digit (its level-communicator rank); else -1 */
   int32_t peer_rank;  /* SENDRECV: peer's global rank; else -1 */
   int32_t bits;       /* code width */
@@ -302,6 +329,35 @@ HZ_API hz_status hz_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const
 HZ_API hz_status hz_enable_p2p(hz_ctx* ctx, size_t pool_bytes);
 HZ_API hz_status hz_p2p_enabled(const hz_ctx* ctx, int* out);
 
+/* Virtual world: `world` contexts (ranks 0..world-1 of hierarchy `group`) in THIS
+ * process on ONE GPU, with the P2P transport enabled and every rank's "peer" pool
+ * being another context's allocation (pool_bytes each; no IPC, no NCCL).  The same
+ * exchange kernels, flags and phase protocol run as on `world` GPUs; additionally
+ * every synchronised launch is ordered on the host after the launches that signal
+ * what it waits for (CUDA events), so the contexts must be driven concurrently from
+ * one host thread each (one stream each), issuing the same call sequence per rank —
+ * a call blocks its thread until the ranks it waits for have issued their side.
+ * Intended for testing the multi-rank path on one GPU (tests/vworld.py).  Not
+ * supported in a virtual world: NCCL-transport and flat calls, graph capture.
+ * 1 <= world <= 8.  out: array of `world` context pointers; each is finalised with
+ * hz_finalize (the pools are freed with the last one; finalise every context after
+ * all their work, every context's thread must be done).  Errors: HZ_ERR_INVALID,
+ * HZ_ERR_UNSUPPORTED (world > 8), HZ_ERR_CUDA. */
+HZ_API hz_status hz_init_virtual(hz_ctx** out, int world, int levels, const int* group, int cuda_device,
+                                 size_t pool_bytes);
+
+/* Failure handling of the P2P transport.  A kernel waits for its peers'
+ * phase flags at most `seconds` (default 600 s, so checkpoint saves or evaluation on
+ * one rank do not break the others); a longer wait, or hz_abort (from any host thread,
+ * e.g. a watchdog), aborts the context: every waiting kernel returns without work or
+ * signals (no sticky CUDA error, no hung GPU) and every later call except hz_finalize
+ * returns HZ_ERR_ABORTED.  Peers of an aborted rank time out in turn.  hz_check
+ * returns HZ_ERR_ABORTED / HZ_ERR_NCCL (asynchronous errors of any of the context's
+ * NCCL communicators, which are then aborted) or HZ_OK without enqueuing anything. */
+HZ_API hz_status hz_set_wait_timeout(hz_ctx* ctx, double seconds);
+HZ_API hz_status hz_abort(hz_ctx* ctx);
+HZ_API hz_status hz_check(const hz_ctx* ctx);
+
 /* CUDA-graph support for the P2P transport.  The cross-GPU phase numbers are
  * stored in the kernels relative to a device-side epoch, so a captured step can
  * be replayed: bracket the capture of one step with hz_p2p_capture_begin /
@@ -334,6 +390,12 @@ HZ_API hz_status hz_sym_alloc(hz_ctx* ctx, size_t bytes, void** out);
 typedef struct {
   float b1, omb1, b2, omb2, lr_wd, sqrt_bc2, eps, step;
 } hz_adamw_t;
+/* The hz_adamw_t of step t >= 1 (reading R19): every constant computed in double
+ * and rounded once to fp32 (omb1 = 1-b1, omb2 = 1-b2, lr_wd = lr*weight_decay,
+ * sqrt_bc2 = sqrt(1-b2^t), step = lr/(1-b1^t)).  Pure host function.
+ * Errors: HZ_ERR_INVALID (NULL out, t < 1, b1 / b2 outside [0, 1)). */
+HZ_API hz_status hz_adamw_params(double lr, double b1, double b2, double eps, double weight_decay, int64_t t,
+                                 hz_adamw_t* out);
 HZ_API hz_status hz_adamw_step(hz_ctx* ctx, const hz_partition_t* p, const float* grad_shard,
                                float* master, float* m, float* v, const hz_adamw_t* hp,
                                void* primary, hz_dtype dt, void* stream);
@@ -406,8 +468,9 @@ HZ_API hz_status hz_set_sm_budget(int sms);
 
 /* Per-launch device timing of the library's own work: CUDA events around each
  * kernel / NCCL group on its stream and/or in-kernel device-clock stamps.
- * hz_trace_begin(cap, flags) starts recording up to cap records (process-wide);
- * hz_trace_end() stops.  hz_trace_read
+ * hz_trace_begin(cap, flags) starts recording up to cap records of the calling
+ * host thread's launches (per thread, so that the contexts of a virtual world, one
+ * thread each, trace separately); hz_trace_end() stops.  hz_trace_read
  * synchronises the recorded events and copies up to max records.  kind is a
  * static string ("quantize", "dequantize", "reduce", "reduce_requant",
  * "nccl_allgather", "nccl_alltoall", "nccl_flat", "copy"). bytes = algorithmic
@@ -423,7 +486,8 @@ typedef struct {
   float wait_ms;   /* P2P kernels: time CTA 0 spent waiting for peers (device clock); else -1 */
   float work_ms;   /* P2P kernels: after-wait to last CTA arrival (device clock); else -1 */
   float publish_ms;/* P2P kernels: last CTA's fence + flag stores (device clock); else -1 */
-  float stamp_ms;  /* kernels, HZ_TRACE_STAMPS: CTA 0 entry to last CTA exit (device clock); else -1 */
+  float stamp_ms;  /* kernels, HZ_TRACE_STAMPS: CTA 0 entry to the last CTA's exit, including
+                      the P2P flag publication (device clock); else -1 */
 } hz_trace_rec;
 
 #define HZ_TRACE_EVENTS 1  /* CUDA event pair around every launch (adds stream operations) */

@@ -30,7 +30,7 @@ import ml_dtypes
 import numpy as np
 
 from . import quant
-from .partition import world_of, digits, range_at, exchange_group
+from .partition import world_of, digits, range_at, exchange_group, hop_group
 
 
 class Ledger:
@@ -192,6 +192,47 @@ def reduce_scatter(inputs, g, Np, block, from_level, to_level, bits_per_level,
         P = new
     if accum is not None:                                                # A10
         return {r: (accum[r].astype(np.float32) + P[r]).astype(np.float32) for r in range(W)}
+    return P
+
+
+def reduce_scatter_hops(inputs, g, Np, block, hops, bits, accum=None, trace=None):
+    """O9 with the hop grouping as a parameter ("the hop grouping is a
+    parameter"; the "1-hop all-to-all based Reduce-scatter" inside the node).
+
+    hops: consecutive level ranges [(a, b), ...] covering the levels to reduce, e.g.
+    [(1, 2), (3, 3)] on 2x2x2 = one all-to-all over the 4 ranks of a node-level group,
+    then one over level 3.  For a hop a..b, each member m of r's hop group (ranks that
+    share every digit outside a..b, ascending rank) quantizes (``bits``; None = pass
+    through) the piece of its P_m^(a-1) that r owns after the hop — range_b(r), which
+    lies at off_b(r) - off_{a-1} in the common range_{a-1} — and r sums the members'
+    dequantized pieces in ascending rank, fp32, one rounding per add (R10, R11).
+    One quantization per hop and contributor: the requantizations between levels of
+    one hop disappear.  With one hop per level this is ``reduce_scatter``.
+    inputs[r] covers range_{a_0 - 1}(r); returns {r: fp32 over range_{b_last}(r)},
+    added to accum[r] when given (A10).  trace[(b, r)] = scales used (error pins)."""
+    W = world_of(g)
+    P = {r: quant.to_f32(inputs[r]) for r in range(W)}
+    for a, b in hops:
+        new = {}
+        for r in range(W):
+            base, _ = range_at(r, g, Np, a - 1)
+            off, ln = range_at(r, g, Np, b)
+            chunks = [P[m][off - base:off - base + ln] for m in hop_group(r, g, a, b)]
+            if bits is None:
+                acc = None
+                for xh in chunks:
+                    acc = xh.copy() if acc is None else (acc + xh).astype(np.float32)
+                used = []
+            else:
+                coded = [quant.quantize(ch, bits, block) for ch in chunks]
+                acc = reduce_coded(coded, block)
+                used = [sc for _, sc in coded]
+            new[r] = acc
+            if trace is not None:
+                trace[(b, r)] = used
+        P = new
+    if accum is not None:
+        return {r: (np.asarray(accum[r], np.float32) + P[r]).astype(np.float32) for r in range(W)}
     return P
 
 

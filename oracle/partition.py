@@ -79,6 +79,16 @@ def exchange_group(r, g, level):
     return members
 
 
+def hop_group(r, g, a, b):
+    """Ranks sharing every digit outside levels a..b with r, in ascending rank order
+    (= ascending merged digit, d_a least significant): the members of one merged-level
+    qgZ all-to-all ("1-hop"; reading R15)."""
+    ds = digits(r, g)
+    W = world_of(g)
+    keep = [k for k in range(len(g)) if not a - 1 <= k <= b - 1]
+    return [q for q in range(W) if all(digits(q, g)[k] == ds[k] for k in keep)]
+
+
 def cumulative_group(r, g, level):
     """Ranks sharing every digit above ``level`` with r (size prod_{k<=level} g_k)."""
     ds = digits(r, g)

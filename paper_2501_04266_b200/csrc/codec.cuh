@@ -19,6 +19,10 @@
 //     low bits of 0x4B400000 reads as 1.5*2^23 + k; subtracting the exact bias
 //     gives the integer code exactly (replaces I2F).
 //   * x_hat = __fmul_rn(code, scale); sums use __fadd_rn in ascending input order.
+// Loads: inputs only this GPU writes (the primary, the gradient) use the read-only
+// path (__ldg); codes and scales, which may be a peer's IPC-mapped memory written by
+// that peer while this kernel's grid is alive, use coherent L2 loads (__ldcg,
+// ld.global.cg: no L1 allocation), ordered after the phase wait (codec.cuh bottom).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -117,7 +121,7 @@ struct Codes8;
 template <>
 struct Codes8<8> {
   uint2 r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const uint2*>(p)); }
   __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<uint2*>(p) = r; }
   __device__ __forceinline__ void zero() { r = make_uint2(0u, 0u); }
   // exact float value of each code
@@ -140,7 +144,7 @@ struct Codes8<8> {
 template <>
 struct Codes8<4> {
   unsigned r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const unsigned*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const unsigned*>(p)); }
   __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<unsigned*>(p) = r; }
   __device__ __forceinline__ void zero() { r = 0u; }
   __device__ __forceinline__ void decode(float (&c)[8]) const {
@@ -170,7 +174,7 @@ struct Codes4;
 template <>
 struct Codes4<8> {
   unsigned r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const unsigned*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const unsigned*>(p)); }
   __device__ __forceinline__ void decode(float (&c)[4]) const {
     const unsigned x = r ^ 0x80808080u;
 #pragma unroll
@@ -182,7 +186,7 @@ template <>
 struct Codes4<4> {
   unsigned short r;
   __device__ __forceinline__ void load(const uint8_t* p) {
-    r = __ldg(reinterpret_cast<const unsigned short*>(p));
+    r = __ldcg(reinterpret_cast<const unsigned short*>(p));
   }
   __device__ __forceinline__ void decode(float (&c)[4]) const {
     const unsigned x = static_cast<unsigned>(r) ^ 0x8888u;   // nibble ^ 8 = code + 8
@@ -274,46 +278,10 @@ struct NoEmit {
   __device__ __forceinline__ void operator()(int64_t, int, const float (&)[8]) const {}
 };
 
-// Push targets (PushDst, hz_internal.h): NoPush compiles to nothing.
-struct NoPush {
-  static constexpr bool on = false;
-  template <int BITS>
-  __device__ __forceinline__ void put(int64_t, const Codes8<BITS>&) const {}
-  template <int B>
-  __device__ __forceinline__ void put_scale(int64_t, float) const {}
-};
-
-struct Push {
-  static constexpr bool on = true;
-  PushDst d;
-  template <int BITS>
-  __device__ __forceinline__ void put(int64_t e, const Codes8<BITS>& v) const {
-    if (d.scatter) {
-      const int j = static_cast<int>(e / d.seg);
-      const int64_t r = e - j * d.seg;
-      if (d.lim <= 0 || r < d.lim) v.store(d.c[j] + r * BITS / 8);
-    } else if (d.lim <= 0 || e < d.lim) {
-      for (int j = 0; j < d.n; ++j) v.store(d.c[j] + e * BITS / 8);
-    }
-  }
-  template <int B>
-  __device__ __forceinline__ void put_scale(int64_t blk, float s) const {
-    if (d.scatter) {
-      const int64_t sb = d.seg / B;
-      const int j = static_cast<int>(blk / sb);
-      const int64_t r = blk - j * sb;
-      if (d.lim <= 0 || r * B < d.lim) d.s[j][r] = s;
-    } else if (d.lim <= 0 || blk * B < d.lim) {
-      for (int j = 0; j < d.n; ++j) d.s[j][blk] = s;
-    }
-  }
-};
-
-template <int B, int BITS, int U, class Emit = NoEmit, class P = NoPush>
+template <int B, int BITS, int U, class Emit = NoEmit>
 __device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB][8], const float (&am)[U],
                                                int64_t blk0, int lane, uint8_t* __restrict__ codes,
-                                               float* __restrict__ scales, const Emit& emit = Emit{},
-                                               const P& push = P{}) {
+                                               float* __restrict__ scales, const Emit& emit = Emit{}) {
   using G = Geo<B>;
   constexpr int NB = U * G::BPW;
   static_assert(NB <= 32, "one block per lane at most");
@@ -327,11 +295,8 @@ __device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB]
   }
   float scale, inv;
   quant_params<BITS>(mine, scale, inv);
-  // codes == nullptr (round trip / push only): no local code / scale stores
+  // codes == nullptr (round trip of a one-member level): no code / scale stores
   if (codes && lane < NB) scales[blk0 + lane] = scale;
-  if constexpr (P::on) {
-    if (lane < NB) push.template put_scale<B>(blk0 + lane, scale);
-  }
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const float iv = __shfl_sync(kFull, inv, u * G::BPW + lb);
@@ -342,11 +307,10 @@ __device__ __forceinline__ void quantize_store(const float (&v)[U][Geo<B>::NSUB]
       unsigned b[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) b[i] = qbits(v[u][k][i], iv);
-      if (codes || P::on) {
+      if (codes) {
         Codes8<BITS> out;
         out.set(b);
-        if (codes) out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
-        if constexpr (P::on) push.template put<BITS>(blk * B + k * G::SUBSTRIDE + ll * 8, out);
+        out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
       }
       if constexpr (Emit::on) {
         float xh[8];
@@ -445,17 +409,24 @@ namespace hz {
 int tune_param(const char* name, int dflt);
 }  // namespace hz
 
+
 // ======================================================================= P2P sync
-// Cross-GPU phase synchronisation for the NVLink peer-memory transport (engine
-// P2P mode).  Every collective phase has a global number (same on all ranks).
-// Flags live in each rank's IPC-mapped pool header: ready[q] / done[q] = the last
-// phase rank q signalled to this rank.  A kernel may
+// Cross-GPU phase synchronisation for the NVLink peer-memory transport (p2p.cpp).
+// Every collective phase has a global number (the same on all ranks, which issue
+// the same call sequence).  Flags live in each rank's IPC-mapped pool header:
+// ready[q] / done[q] = the last phase rank q signalled to this rank (monotone).
+// A kernel may
 //   * wait (prologue, thread 0 of every CTA, ld.acquire.sys spin) until
-//     ready[q] >= wait_ready and done[q] >= wait_done for every rank q;
-//   * signal (epilogue, last CTA to finish, after __threadfence_system) by a
-//     st.release.sys of sig_ready / sig_done into every rank's flag slot for
-//     this rank.
-// A spin longer than ~20 s traps (a dead peer must not hang the GPU).
+//     ready[q] >= wait_ready for the ranks q of wr_mask (the members whose buffers
+//     it reads) and done[q] >= wait_done for wd_mask (the ranks that read what it
+//     overwrites) — level-local: no other rank is waited for;
+//   * signal (epilogue, last CTA to finish, fence.acq_rel.sys + relaxed system-scope
+//     stores) sig_ready to sr_mask and sig_done to sd_mask.
+// A wait longer than timeout_ns, or a nonzero *abort (mapped host memory: set by
+// another timed-out wait of this context, or by hz_abort on the host), aborts: the
+// CTA returns without doing its work or signalling, *abort is set to 1, and the host
+// reports HZ_ERR_ABORTED on the context's next call.  A dead or stalled peer
+// therefore neither hangs the GPU nor leaves a sticky CUDA error.
 namespace hz {
 namespace dev {
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -463,8 +434,10 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -475,48 +448,61 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-__device__ __forceinline__ void sync_wait(const SyncArgs& s) {
+// Returns false when the context is aborted (the whole CTA must return at once).
+__device__ __forceinline__ bool sync_wait(const SyncArgs& s) {
   // Programmatic dependent launch (launch_k): let the next kernel on the stream be
-  // launched now (it is scheduled only once every CTA of this grid has started, so
-  // its CTAs take the SM slots this grid frees), and wait here until the previous
-  // kernel has completed and its memory is visible — the stream-order semantics,
-  // minus the launch gap.  Both are no-ops without the launch attribute.
+  // launched now and wait here until the previous kernel has completed and its memory
+  // is visible — the stream-order semantics minus the launch gap.  Both are no-ops
+  // without the launch attribute.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (s.stamps && blockIdx.x == 0 && threadIdx.x == 0) s.stamps[0] = globaltimer();
-  if (!(s.en & (kWaitReady | kWaitDone))) {
+  if (!(s.wr_mask | s.wd_mask)) {
     if (s.stamps && blockIdx.x == 0 && threadIdx.x == 0) s.stamps[1] = globaltimer();
-    return;
+    return true;
   }
+  __shared__ int ok;
   if (threadIdx.x == 0) {
     const unsigned long long t0 = globaltimer();
     const unsigned long long e = s.epoch ? *s.epoch : 0ull;
-    const unsigned long long wr = (s.en & kWaitReady) ? s.wait_ready + e : 0ull;
-    const unsigned long long wd = (s.en & kWaitDone) ? s.wait_done + e : 0ull;
-    for (int q = 0; q < s.world; ++q) {
-      while ((wr && ld_acquire_sys(s.ready_local + q) < wr) ||
-             (wd && ld_acquire_sys(s.done_local + q) < wd)) {
-        if (globaltimer() - t0 > 20000000000ull) __trap();
+    const unsigned long long wr = s.wait_ready + e, wd = s.wait_done + e;
+    int good = s.abort ? ld_volatile_u32(s.abort) == 0u : 1;
+    unsigned it = 0;
+    for (int q = 0; q < kMaxWorld && good; ++q) {
+      const bool r = (s.wr_mask >> q) & 1u, d = (s.wd_mask >> q) & 1u;
+      while ((r && ld_acquire_sys(s.ready_local + q) < wr) || (d && ld_acquire_sys(s.done_local + q) < wd)) {
+        if ((++it & 127u) == 0u) {
+          if (s.abort && ld_volatile_u32(s.abort) != 0u) {
+            good = 0;
+            break;
+          }
+          if (globaltimer() - t0 > s.timeout_ns) {
+            if (s.abort) atomicExch(s.abort, 1u);
+            good = 0;
+            break;
+          }
+        }
       }
     }
+    ok = good;
     if (s.stamps && blockIdx.x == 0) s.stamps[1] = globaltimer();
   }
   __syncthreads();
+  return ok != 0;
 }
 
 // Kernel epilogue: trace stamp of the last CTA to finish (stamps[2], with its own
-// arrival counter in stamps[4]) and, in P2P mode, the phase publication.
+// arrival counter in stamps[4]) and, in P2P mode, the phase publication (stamps[3]).
 __device__ __forceinline__ void sync_signal(const SyncArgs& s) {
-  const bool sig = (s.en & (kSigReady | kSigDone)) != 0;
+  const bool sig = (s.sr_mask | s.sd_mask) != 0u;
   if (!sig && !s.stamps) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     // gpu-scope release per CTA (peers read this GPU's memory through its L2, the
     // point of coherence for gpu scope); the last CTA then publishes with a
-    // system-scope release, cumulative over everything it has observed.  Kernels
-    // that stored into peer memory fence at system scope.
-    if (s.sysfence) __threadfence_system();
-    else __threadfence();
+    // system-scope acq_rel fence, cumulative over everything it has observed
+    // (the arrival counter), followed by relaxed system-scope flag stores.
+    __threadfence();
     if (s.stamps && atomicAdd(s.stamps + 4, 1ull) == gridDim.x - 1ull) {
       s.stamps[2] = globaltimer();
       s.stamps[4] = 0ull;   // graph replays reuse the slot
@@ -524,21 +510,11 @@ __device__ __forceinline__ void sync_signal(const SyncArgs& s) {
     if (sig && atomicAdd(s.counter, 1u) == gridDim.x - 1) {
       *s.counter = 0u;
       const unsigned long long e = s.epoch ? *s.epoch : 0ull;
-      const unsigned long long sr = (s.en & kSigReady) ? s.sig_ready + e : 0ull;
-      const unsigned long long sd = (s.en & kSigDone) ? s.sig_done + e : 0ull;
-      if (s.mode == 0) {
-        __threadfence_system();
-        for (int q = 0; q < s.world; ++q) {
-          if (sr) st_release_sys(s.ready_remote[q], sr);
-          if (sd) st_release_sys(s.done_remote[q], sd);
-        }
-      } else {
-        if (s.mode == 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
-        else if (s.mode == 2) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        for (int q = 0; q < s.world; ++q) {
-          if (sr) st_relaxed_sys(s.ready_remote[q], sr);
-          if (sd) st_relaxed_sys(s.done_remote[q], sd);
-        }
+      const unsigned long long sr = s.sig_ready + e, sd = s.sig_done + e;
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int q = 0; q < kMaxWorld; ++q) {
+        if ((s.sr_mask >> q) & 1u) st_relaxed_sys(s.ready_remote[q], sr);
+        if ((s.sd_mask >> q) & 1u) st_relaxed_sys(s.done_remote[q], sd);
       }
       if (s.stamps) s.stamps[3] = globaltimer();
     }

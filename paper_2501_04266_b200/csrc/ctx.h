@@ -5,9 +5,14 @@
 #include <nccl.h>
 
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "hz_internal.h"
+
+namespace hz {
+struct VWorld;   // vworld.cpp
+}
 
 struct hz_ctx {
   int rank = 0, world = 1, levels = 0, device = 0;
@@ -15,6 +20,10 @@ struct hz_ctx {
   int digit[HZ_MAX_LEVELS] = {0};
   ncclComm_t world_comm = nullptr;
   ncclComm_t lvl[HZ_MAX_LEVELS] = {nullptr};
+  // merged qgZ hops over levels a..b (a < b), split lazily: hop_comm[a-1][b-1]
+  ncclComm_t hop_comm[HZ_MAX_LEVELS][HZ_MAX_LEVELS] = {{nullptr}};
+  bool nccl_dead = false;           // communicators aborted after an asynchronous error
+  std::string nccl_err;
   struct Buf {
     void* p = nullptr;
     size_t cap = 0;
@@ -25,7 +34,7 @@ struct hz_ctx {
   Buf rs_r_c, rs_r_s;                  // receive slots (reduce-scatter)
   Buf ar_a, ar_b, ar_g;                // allreduce + select: ping-pong fp32, gathered members
 
-  // NVLink P2P transport (hz_enable_p2p): one IPC-mapped symmetric pool per rank.
+  // NVLink P2P transport (hz_enable_p2p / hz_init_virtual): one symmetric pool per rank.
   struct P2P {
     bool on = false;
     char* pool = nullptr;                       // local base
@@ -36,12 +45,16 @@ struct hz_ctx {
     unsigned long long epoch_host = 0;          // value *epoch will hold once enqueued work ran
     unsigned long long capture_start = 0;       // phase at hz_p2p_capture_begin
     unsigned long long span = 0;                // phases of the last captured graph
+    bool capturing = false;
     // prefetched quantize (hz_allgather_params_next): the next layer's primary was
-    // quantized into pre_codes in phase pre_phase by the previous call's dual kernel
+    // quantized into pre_codes in phase pre_phase by the previous call's dual kernel,
+    // with pre_bits / pre_dt / pre_len elements
     unsigned long long pre_phase = 0;
     const void* pre_codes = nullptr;
     const void* pre_primary = nullptr;
-    bool capturing = false;
+    int pre_bits = 0;
+    hz_dtype pre_dt = HZ_BF16;
+    int64_t pre_len = 0;
     struct Slot {
       size_t off = 0, cap = 0;
     };
@@ -49,9 +62,16 @@ struct hz_ctx {
     Slot rs_c[HZ_MAX_LEVELS + 1], rs_s[HZ_MAX_LEVELS + 1];   // level-l send buffers
     Slot upd;                                   // updated weights of range_L (step tail)
     Slot ar_a, ar_b;                            // allreduce + select: ping-pong fp32 buffers
-    // push mode: receive buffers the producers store into over NVLink
-    Slot ag_recv_c, ag_recv_s;                  // forward gather: D pieces of the primary codes
-    Slot rs_recv_c[HZ_MAX_LEVELS + 1], rs_recv_s[HZ_MAX_LEVELS + 1];   // level-l: g chunks destined here
+    // level-local synchronisation (host bookkeeping, p2p.cpp): the ranks this rank
+    // reads from (its `done` signals go to them) and, per pool buffer, the ranks that
+    // read this rank's copy of it (a writer of the buffer waits for their `done`)
+    unsigned nbr = 0;
+    std::unordered_map<size_t, unsigned> readers;
+    // abort word in mapped page-locked host memory (device pointer for the kernels)
+    unsigned* abort_host = nullptr;
+    unsigned* abort_dev = nullptr;
+    unsigned long long timeout_ns = 600ull * 1000000000ull;
+    hz::VWorld* vw = nullptr;                   // virtual world (hz_init_virtual), else null
   } p2p;
 
   // Host-staged step executor (hz_step_host, executor.cpp): copy streams and events,
@@ -66,19 +86,12 @@ struct hz_ctx {
 
 namespace hz {
 
-// header of the symmetric pool: ready[8] u64 | done[8] u64 | counter u32 | epoch u64 |
-// pipelined-kernel ticket counters | per-chunk flags of the pipelined all-gather
-// [8][kMaxChunks] and reduce-scatter [16][kMaxChunks] | per-chunk producer arrival
-// counters (u32 [kMaxChunks] each)
+// header of the symmetric pool: ready[8] u64 | done[8] u64 | arrival counter u32 |
+// phase epoch u64
 constexpr size_t kReadyOff = 0, kDoneOff = 64, kCounterOff = 128, kEpochOff = 192;
-constexpr size_t kWorkAGOff = 256, kWorkRSOff = 320;
-constexpr size_t kChunkAGOff = 4096;
-constexpr size_t kChunkRSOff = kChunkAGOff + size_t(kMaxWorld) * kMaxChunks * 8;
-constexpr size_t kCntAGOff = kChunkRSOff + size_t(kMaxG) * kMaxChunks * 8;
-constexpr size_t kCntRSOff = kCntAGOff + size_t(kMaxChunks) * 4;
-constexpr size_t kDbgOff = kCntRSOff + size_t(kMaxChunks) * 4;   // HZ_TUNE pdbg timelines [kMaxChunks][4]
-constexpr size_t kPoolHeader = kDbgOff + size_t(kMaxChunks) * 32;
+constexpr size_t kPoolHeader = 4096;
 
+int tune_param(const char* name, int dflt);   // HZ_TUNE overrides (codec_util.cu)
 hz_status cuda_fail(cudaError_t e, const char* what);
 hz_status nccl_fail(ncclResult_t r, const char* what);
 hz_status grow(hz_ctx::Buf& b, size_t need);
@@ -96,13 +109,6 @@ hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int6
                      int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
                      cudaStream_t st, int level, const SyncArgs* sync = nullptr,
                      int64_t remote_bytes = 0);
-// push kernels (P2P): `remote` = bytes stored into peer memory per launch
-hz_status run_quantize_push(const void* x, hz_dtype dt, int64_t n, int bits, uint8_t* c, float* s, void* y,
-                            hz_dtype odt, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
-                            int64_t remote);
-hz_status run_reduce_push(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
-                          int bits_out, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
-                          int64_t remote);
 hz_status run_gather_quantize(const Pieces& pc, int64_t n, int bits, void* y, hz_dtype odt, const void* x,
                               hz_dtype dt, int64_t nq, int qbits, uint8_t* c, float* s, cudaStream_t st,
                               const SyncArgs& sync, int64_t remote_bytes, float* qy = nullptr, int acc = 0);
@@ -139,6 +145,14 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
                              int from_level, int to_level, const int* bits_per_level, float* shard,
                              int accumulate, cudaStream_t st, const PrevG* prev = nullptr);
 void p2p_release(hz_ctx* ctx);
+hz_status p2p_alloc_abort(hz_ctx* ctx);
+hz_status p2p_check(const hz_ctx* ctx);        // HZ_ERR_ABORTED once the context is aborted
+hz_status check_async(const hz_ctx* ctx);      // asynchronous NCCL errors of every communicator (engine.cpp)
+// virtual world (vworld.cpp): host-side ordering of one synchronised launch
+hz_status vw_wait(hz_ctx* ctx, const SyncArgs& s, cudaStream_t st);
+hz_status vw_signal(hz_ctx* ctx, const SyncArgs& s, cudaStream_t st);
+void vw_abort(hz_ctx* ctx);
+void vw_release(hz_ctx* ctx);
 void exec_release(hz_ctx* ctx);   // executor.cpp
 hz_status p2p_adamw_gather(hz_ctx* ctx, const hz_partition_t* p, const float* g, float* th, float* m, float* v,
                            const AdamW& hp, void* primary, hz_dtype dt, cudaStream_t st);

@@ -40,9 +40,8 @@ __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits
         // request-bound for small transfers)
         if (!inter) jt = 0;
         const int64_t r0 = ub * 8 - jt * pc.len;
-        const bool head = r0 < pc.split && pc.cr[jt] != nullptr;
-        const uint8_t* cb = (head ? pc.cr[jt] : pc.c[jt]) + (r0 + lane * 8) * BITS / 8;
-        const float4 s4 = __ldg(reinterpret_cast<const float4*>((head ? pc.sr[jt] : pc.s[jt]) + (r0 >> 8)));
+        const uint8_t* cb = pc.c[jt] + (r0 + lane * 8) * BITS / 8;
+        const float4 s4 = __ldcg(reinterpret_cast<const float4*>(pc.s[jt] + (r0 >> 8)));
 #pragma unroll
         for (int u = 0; u < U; ++u) raw[u].load(cb + u * 256 * BITS / 8);
         sc[0] = s4.x;
@@ -57,10 +56,9 @@ __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits
         // shuffle.  (B >= 1024: the tile lies inside one block, NS = 1.)
         if (!inter) jt = 0;
         const int64_t r0 = ub * 8 - jt * pc.len;
-        const bool head = r0 < pc.split && pc.cr[jt] != nullptr;
-        const uint8_t* cb = (head ? pc.cr[jt] : pc.c[jt]) + (r0 + lane * 8) * BITS / 8;
+        const uint8_t* cb = pc.c[jt] + (r0 + lane * 8) * BITS / 8;
         const int ns = log2b >= 10 ? 1 : (1024 >> log2b);
-        const float mine = __ldg((head ? pc.sr[jt] : pc.s[jt]) + (r0 >> log2b) + (lane < ns ? lane : ns - 1));
+        const float mine = __ldcg(pc.s[jt] + (r0 >> log2b) + (lane < ns ? lane : ns - 1));
 #pragma unroll
         for (int u = 0; u < U; ++u) raw[u].load(cb + u * 256 * BITS / 8);
 #pragma unroll
@@ -79,9 +77,8 @@ __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits
           for (int q = 1; q < pc.n; ++q) j += e >= q * pc.len;   // piece of this unit
         }
         const int64_t r = e - j * pc.len;
-        const bool head = r < pc.split && pc.cr[j] != nullptr;   // pushed head: local receive buffer
-        raw[u].load((head ? pc.cr[j] : pc.c[j]) + r * BITS / 8);
-        sc[u] = __ldg((head ? pc.sr[j] : pc.s[j]) + (r >> log2b));
+        raw[u].load(pc.c[j] + r * BITS / 8);
+        sc[u] = __ldcg(pc.s[j] + (r >> log2b));
       }
     }
 #pragma unroll

@@ -18,8 +18,11 @@
 // (= destination digit j) is a contiguous slice of both arrays, so the
 // all-to-all is grouped ncclSend/ncclRecv of slices; the own chunk is read in
 // place by the reduce kernel and never enters NCCL.
+#include <cmath>
 #include <cstring>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "ctx.h"
 
@@ -69,13 +72,66 @@ void free_buf(hz_ctx::Buf& b) {
   b.cap = 0;
 }
 
+}  // namespace
+
+// Asynchronous NCCL errors of ANY communicator of the context (world, levels, merged
+// hops: the level communicators carry the traffic) and the P2P abort word.  On an
+// NCCL error every communicator is aborted (ncclCommAbort: no later call can hang on
+// a dead peer) and every later call reports HZ_ERR_NCCL.
 hz_status check_async(const hz_ctx* ctx) {
-  ncclResult_t r = ncclSuccess;
-  if (ctx->world_comm && ncclCommGetAsyncError(ctx->world_comm, &r) == ncclSuccess &&
-      r != ncclSuccess && r != ncclInProgress)
-    return nccl_fail(r, "asynchronous NCCL error from an earlier call");
+  hz_status rc = p2p_check(ctx);
+  if (rc != HZ_OK) return rc;
+  hz_ctx* c = const_cast<hz_ctx*>(ctx);
+  if (c->nccl_dead) return fail(HZ_ERR_NCCL, "NCCL communicators were aborted after an asynchronous error: " + c->nccl_err);
+  std::vector<ncclComm_t*> comms;
+  if (c->world_comm) comms.push_back(&c->world_comm);
+  for (auto& x : c->lvl)
+    if (x) comms.push_back(&x);
+  for (auto& row : c->hop_comm)
+    for (auto& x : row)
+      if (x) comms.push_back(&x);
+  for (ncclComm_t* cm : comms) {
+    ncclResult_t r = ncclSuccess;
+    if (ncclCommGetAsyncError(*cm, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress) {
+      c->nccl_err = ncclGetErrorString(r);
+      for (ncclComm_t* k : comms) {
+        ncclCommAbort(*k);
+        *k = nullptr;
+      }
+      c->nccl_dead = true;
+      return fail(HZ_ERR_NCCL, "asynchronous NCCL error from an earlier call (communicators aborted): " + c->nccl_err);
+    }
+  }
   return HZ_OK;
 }
+
+// Communicator of the merged hop over levels a..b (a == b: the level communicator),
+// split from the world communicator on first use — a collective call, made by every
+// rank at the same point of the same call sequence.  Comm rank = merged digit.
+hz_status hop_comm(hz_ctx* ctx, int a, int b, ncclComm_t* out) {
+  if (a == b) {
+    *out = ctx->lvl[a - 1];
+    return HZ_OK;
+  }
+  ncclComm_t& c = ctx->hop_comm[a - 1][b - 1];
+  if (!c) {
+    int stride = 1, color = ctx->rank, key = 0, kstride = 1;
+    for (int l = 1; l <= ctx->levels; ++l) {
+      if (l >= a && l <= b) {
+        color -= ctx->digit[l - 1] * stride;
+        key += ctx->digit[l - 1] * kstride;
+        kstride *= ctx->group[l - 1];
+      }
+      stride *= ctx->group[l - 1];
+    }
+    ncclResult_t r = ncclCommSplit(ctx->world_comm, color, key, &c, nullptr);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclCommSplit(merged hop)");
+  }
+  *out = c;
+  return HZ_OK;
+}
+
+namespace {
 
 hz_status check_partition(const hz_ctx* ctx, const hz_partition_t* p) {
   if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
@@ -87,6 +143,10 @@ hz_status check_partition(const hz_ctx* ctx, const hz_partition_t* p) {
   if (!block_ok(p->block)) return fail(HZ_ERR_INVALID, "p.block: must be a power of two in [32, 2048]");
   if (p->padded_numel % (int64_t(p->world) * 4 * p->block))
     return fail(HZ_ERR_INVALID, "p.padded_numel: not a multiple of world*4*block");
+  if (p->nhops < 0 || p->nhops > p->levels) return fail(HZ_ERR_INVALID, "p.nhops: must be in [0, levels]");
+  for (int k = 0, prev = 0; k < p->nhops; prev = p->hop_last[k], ++k)
+    if (p->hop_last[k] <= prev || p->hop_last[k] > p->levels || (k + 1 == p->nhops && p->hop_last[k] != p->levels))
+      return fail(HZ_ERR_INVALID, "p.hop_last: must be strictly ascending and end at level L");
   return HZ_OK;
 }
 
@@ -172,31 +232,6 @@ hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int6
                                 (sync || t.stamps) ? &sy : nullptr);
   t.end();
   if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
-  return HZ_OK;
-}
-
-hz_status run_quantize_push(const void* x, hz_dtype dt, int64_t n, int bits, uint8_t* c, float* s, void* y,
-                            hz_dtype odt, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
-                            int64_t remote) {
-  const int64_t local = n * elem_bytes(dt) + (c ? code_bytes(n, bits) + n / 256 * 4 : 0) + (y ? n * elem_bytes(odt) : 0);
-  TraceScope t(st, "quantize_push", level, bits, n, local, remote);
-  SyncArgs sy = sync ? *sync : SyncArgs{};
-  sy.stamps = t.stamps;
-  cudaError_t e = launch_quantize_push(x, dt, n, bits, c, s, y, odt, dst, st, &sy);
-  t.end();
-  if (e != cudaSuccess) return cuda_fail(e, "quantize-push kernel launch");
-  return HZ_OK;
-}
-
-hz_status run_reduce_push(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
-                          int bits_out, const PushDst& dst, cudaStream_t st, int level, const SyncArgs* sync,
-                          int64_t remote) {
-  TraceScope t(st, "reduce_push", level, bits_in, n, g * (code_bytes(n, bits_in) + n / 256 * 4), remote);
-  SyncArgs sy = sync ? *sync : SyncArgs{};
-  sy.stamps = t.stamps;
-  cudaError_t e = launch_reduce_push(g, c, s, n, bits_in, bits_out, dst, st, &sy);
-  t.end();
-  if (e != cudaSuccess) return cuda_fail(e, "reduce-push kernel launch");
   return HZ_OK;
 }
 
@@ -324,6 +359,9 @@ hz_status hz_finalize(hz_ctx* ctx) {
   exec_release(ctx);
   for (int l = 0; l < HZ_MAX_LEVELS; ++l)
     if (ctx->lvl[l]) ncclCommDestroy(ctx->lvl[l]);
+  for (auto& row : ctx->hop_comm)
+    for (auto& c : row)
+      if (c) ncclCommDestroy(c);
   if (ctx->world_comm) ncclCommDestroy(ctx->world_comm);
   for (auto* b : {&ctx->ag_c, &ctx->ag_s, &ctx->rs_a_c, &ctx->rs_a_s, &ctx->rs_b_c, &ctx->rs_b_s,
                   &ctx->rs_r_c, &ctx->rs_r_s, &ctx->ar_a, &ctx->ar_b, &ctx->ar_g})
@@ -497,7 +535,8 @@ static hz_status check_reduce_scatter(const hz_ctx* ctx, const hz_partition_t* p
   if (!dtype_ok(dt)) return fail(HZ_ERR_INVALID, "dt: unknown dtype");
   if (!grad || !aligned16(grad)) return fail(HZ_ERR_INVALID, "grad: NULL or not 16-byte aligned");
   if (!shard || !aligned16(shard)) return fail(HZ_ERR_INVALID, "shard: NULL or not 16-byte aligned");
-  return HZ_OK;
+  std::vector<Hop> hops;
+  return hops_of(p, from_level, to_level, &hops);
 }
 
 hz_status hz_backward_step(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt, int from_level,
@@ -578,8 +617,14 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
   uint8_t* r_c = static_cast<uint8_t*>(ctx->rs_r_c.p);
   float* r_s = static_cast<float*>(ctx->rs_r_s.p);
 
-  if (from_level == to_level && ctx->group[from_level - 1] == 1 && roundtrip_supported(B)) {
-    // A7 + A9 fused: a single level whose group has one member exchanges nothing, so
+  std::vector<Hop> hops;
+  if ((rc = hops_of(p, from_level, to_level, &hops)) != HZ_OK) return rc;
+  std::vector<int> ranks;
+  std::vector<int64_t> rel;
+  int me = 0;
+  hop_members(p, hops[0].a, hops[0].b, &ranks, &rel, &me);
+  if (hops.size() == 1 && ranks.size() == 1 && roundtrip_supported(B)) {
+    // A7 + A9 fused: a single hop whose group has one member exchanges nothing, so
     // the shard is the round trip of the own gradient: one kernel, codes never reread.
     // (the gradient's codes are never read by anyone here, so they are not stored)
     if ((rc = run_roundtrip(grad, dt, base_len, bits_per_level[from_level - 1], B, nullptr, nullptr, shard, HZ_F32,
@@ -588,54 +633,53 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
     clear_error();
     return HZ_OK;
   }
-  // A7: quantize the whole input range_{from-1}; chunk j of it goes to digit j.
+  // A7: quantize the whole input range_{from-1}; the chunk of member j goes to j.
   if ((rc = run_quantize(grad, dt, base_len, bits_per_level[from_level - 1], B, a_c, a_s, st,
                          from_level)) != HZ_OK)
     return rc;
   std::vector<hz_comm_step> plan;
   if ((rc = plan_reduce_scatter(p, from_level, to_level, bits_per_level, &plan)) != HZ_OK) return rc;
   size_t next = 0;
-  for (int l = from_level; l <= to_level; ++l) {
-    const int g = ctx->group[l - 1];
-    const int d = ctx->digit[l - 1];
-    const int bits = bits_per_level[l - 1];
-    const int64_t cl = p->len[l];
+  for (size_t h = 0; h < hops.size(); ++h) {
+    const Hop& hp = hops[h];
+    hop_members(p, hp.a, hp.b, &ranks, &rel, &me);
+    const int g = static_cast<int>(ranks.size());
+    const int bits = bits_per_level[hp.a - 1];
+    const int64_t cl = p->len[hp.b];
     const int64_t cb = code_bytes(cl, bits);
     const int64_t cs = cl / B;
+    if (g > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "more than 16 ranks in one qgZ hop");
     const uint8_t* ptr_c[kMaxG];
     const float* ptr_s[kMaxG];
-    if (g > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "group size > 16 at one level");
-    if (g > 1) {   // A8: all-to-all within the level-l exchange group, from the plan
-      TraceScope t(st, "nccl_alltoall", l, bits, cl, (g - 1) * (cb + cs * 4));
+    if (g > 1) {   // A8: all-to-all within the hop group, from the plan
+      ncclComm_t comm = nullptr;
+      if ((rc = hop_comm(ctx, hp.a, hp.b, &comm)) != HZ_OK) return rc;
+      TraceScope t(st, "nccl_alltoall", hp.b, bits, cl, (g - 1) * (cb + cs * 4));
       HZ_NCCL(ncclGroupStart(), "ncclGroupStart");
-      for (; next < plan.size() && plan[next].level == l; ++next) {
+      for (; next < plan.size() && plan[next].level == hp.a; ++next) {
         const hz_comm_step& s = plan[next];
         const int j = s.peer;
-        const int64_t rel = s.send_off - p->off[l - 1];   // chunk j of this rank's range_{l-1}
-        HZ_NCCL(ncclSend(a_c + code_bytes(rel, bits), s.code_bytes, ncclUint8, j, ctx->lvl[l - 1], st),
-                "ncclSend(codes)");
-        HZ_NCCL(ncclRecv(r_c + j * cb, s.code_bytes, ncclUint8, j, ctx->lvl[l - 1], st), "ncclRecv(codes)");
-        HZ_NCCL(ncclSend(a_s + rel / B, s.scale_bytes / 4, ncclFloat32, j, ctx->lvl[l - 1], st),
-                "ncclSend(scales)");
-        HZ_NCCL(ncclRecv(r_s + j * cs, s.scale_bytes / 4, ncclFloat32, j, ctx->lvl[l - 1], st),
-                "ncclRecv(scales)");
+        const int64_t relj = s.send_off - p->off[hp.a - 1];   // member j's chunk of this rank's range_{a-1}
+        HZ_NCCL(ncclSend(a_c + code_bytes(relj, bits), s.code_bytes, ncclUint8, j, comm, st), "ncclSend(codes)");
+        HZ_NCCL(ncclRecv(r_c + j * cb, s.code_bytes, ncclUint8, j, comm, st), "ncclRecv(codes)");
+        HZ_NCCL(ncclSend(a_s + relj / B, s.scale_bytes / 4, ncclFloat32, j, comm, st), "ncclSend(scales)");
+        HZ_NCCL(ncclRecv(r_s + j * cs, s.scale_bytes / 4, ncclFloat32, j, comm, st), "ncclRecv(scales)");
       }
       HZ_NCCL(ncclGroupEnd(), "ncclGroupEnd");
       t.end();
     }
     for (int j = 0; j < g; ++j) {
-      ptr_c[j] = j == d ? a_c + j * cb : r_c + j * cb;
-      ptr_s[j] = j == d ? a_s + j * cs : r_s + j * cs;
+      ptr_c[j] = j == me ? a_c + code_bytes(rel[me], bits) : r_c + j * cb;
+      ptr_s[j] = j == me ? a_s + rel[me] / B : r_s + j * cs;
     }
-    if (l < to_level) {   // A9 fused with the next level's requantization
-      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, bits_per_level[l], b_c, b_s, nullptr, 0, st,
-                           l)) != HZ_OK)
+    if (h + 1 < hops.size()) {   // A9 fused with the next hop's requantization
+      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, bits_per_level[hops[h + 1].a - 1], b_c, b_s, nullptr, 0, st,
+                           hp.b)) != HZ_OK)
         return rc;
       std::swap(a_c, b_c);
       std::swap(a_s, b_s);
-    } else {              // A9/A10: final fp32 shard, optionally accumulated
-      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st,
-                           l)) != HZ_OK)
+    } else {                     // A9/A10: final fp32 shard, optionally accumulated
+      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st, hp.b)) != HZ_OK)
         return rc;
     }
   }
@@ -692,6 +736,27 @@ hz_status hz_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const float*
     nxt ^= 1;
   }
   if ((rc = copy_async(out, cur + sel, static_cast<size_t>(p->len[to_level]) * 4, st)) != HZ_OK) return rc;
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_adamw_params(double lr, double b1, double b2, double eps, double weight_decay, int64_t t,
+                          hz_adamw_t* out) {
+  using namespace hz;
+  if (!out) return fail(HZ_ERR_INVALID, "out: NULL");
+  if (t < 1) return fail(HZ_ERR_INVALID, "t: must be >= 1");
+  if (!(b1 >= 0.0 && b1 < 1.0)) return fail(HZ_ERR_INVALID, "b1: must be in [0, 1)");
+  if (!(b2 >= 0.0 && b2 < 1.0)) return fail(HZ_ERR_INVALID, "b2: must be in [0, 1)");
+  // reading R19: every constant computed in double, rounded once to fp32
+  const double td = static_cast<double>(t);
+  out->b1 = static_cast<float>(b1);
+  out->omb1 = static_cast<float>(1.0 - b1);
+  out->b2 = static_cast<float>(b2);
+  out->omb2 = static_cast<float>(1.0 - b2);
+  out->lr_wd = static_cast<float>(lr * weight_decay);
+  out->sqrt_bc2 = static_cast<float>(std::sqrt(1.0 - std::pow(b2, td)));
+  out->eps = static_cast<float>(eps);
+  out->step = static_cast<float>(lr / (1.0 - std::pow(b1, td)));
   clear_error();
   return HZ_OK;
 }

@@ -24,22 +24,22 @@ int64_t code_bytes(int64_t n, int bits);   // n * bits / 8
 // ------------------------------------------------------------- P2P phase sync
 // (see codec.cuh for the protocol).  A zero-initialised SyncArgs means "no sync".
 constexpr int kMaxWorld = 8;
-constexpr unsigned kWaitReady = 1u, kWaitDone = 2u, kSigReady = 4u, kSigDone = 8u;
 struct SyncArgs {
-  unsigned long long* ready_local;
-  unsigned long long* done_local;
-  unsigned long long* ready_remote[kMaxWorld];
+  unsigned long long* ready_local;               // this rank's flags: ready[q] / done[q] =
+  unsigned long long* done_local;                // the last phase rank q signalled to this rank
+  unsigned long long* ready_remote[kMaxWorld];   // &ready[me] / &done[me] in rank q's pool
   unsigned long long* done_remote[kMaxWorld];
-  unsigned int* counter;
-  int world;
-  // phase thresholds relative to *epoch (the device-side phase offset advanced by
-  // every replay of a captured CUDA graph); `en` says which of them are active
-  unsigned long long wait_ready, wait_done, sig_ready, sig_done;
+  unsigned int* counter;                         // last-CTA arrival counter (pool header)
   const unsigned long long* epoch;
-  unsigned en;   // kWaitReady | kWaitDone | kSigReady | kSigDone
-  unsigned long long* stamps;   // optional [8]: entry, after wait, last-CTA arrival, flags sent (ns), counter
-  int mode;                     // publication fence variant (HZ_TUNE p2p_sig; 0 = fence.sc.sys)
-  int sysfence;                 // per-CTA fence at system scope (kernels that store into peer memory)
+  unsigned int* abort;             // mapped host word: nonzero = the context is aborted
+  unsigned long long timeout_ns;   // a wait longer than this aborts (sets *abort = 1)
+  // wait until ready[q] >= wait_ready for q in wr_mask and done[q] >= wait_done for q
+  // in wd_mask; signal sig_ready to the ranks of sr_mask and sig_done to sd_mask.
+  // Phase numbers are relative to *epoch (the device-side offset advanced by every
+  // replay of a captured CUDA graph).
+  unsigned long long wait_ready, wait_done, sig_ready, sig_done;
+  unsigned wr_mask, wd_mask, sr_mask, sd_mask;
+  unsigned long long* stamps;      // optional [8]: entry, after wait, last-CTA arrival, flags sent (ns), counter
 };
 
 // Pieces of a gathered layer for the fused gather+dequantize kernel: piece j
@@ -55,11 +55,6 @@ struct Pieces {
   uint8_t* sec_c;
   float* sec_s;
   int64_t sec_lo, sec_hi;
-  // hybrid push/pull: elements [0, split) of piece j come from cr[j] / sr[j] (local
-  // receive buffer) when cr[j] is set
-  const uint8_t* cr[kMaxWorld];
-  const float* sr[kMaxWorld];
-  int64_t split;
 };
 
 // ----------------------------------------------------------------- kernels
@@ -89,29 +84,6 @@ cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int 
                                      hz_dtype out_dt, cudaStream_t st, const SyncArgs* sync);
 constexpr int kMaxG = 16;
 
-// Push destinations of the P2P push kernels (quantize / requantize that store their
-// codes straight into the consumers' receive buffers over NVLink).  The codes and
-// scales of element e go, besides the local buffers (if any), to every c[j] + e
-// (mirror), or only to segment j = e / seg at c[j] + (e - j*seg) (scatter).
-struct PushDst {
-  uint8_t* c[kMaxG];
-  float* s[kMaxG];
-  int64_t seg;      // scatter segment in elements (a multiple of the block)
-  int n;
-  int scatter;
-  int64_t lim;      // > 0: only elements whose offset (within the segment) is < lim
-};
-// Push variants (P2P transport, block 256): codes / scales also (or only, when
-// codes == nullptr) stored to `dst` (peer receive buffers); y (optional) = the own
-// round trip x_hat.  The per-CTA release fences at system scope.
-cudaError_t launch_quantize_push(const void* x, hz_dtype dt, int64_t n, int bits, uint8_t* codes, float* scales,
-                                 void* y, hz_dtype out_dt, const PushDst& dst, cudaStream_t st,
-                                 const SyncArgs* sync);
-bool push_reduce_supported(int g, int block);
-cudaError_t launch_reduce_push(int g, const uint8_t* const* codes, const float* const* scales, int64_t n,
-                               int bits_in, int bits_out, const PushDst& dst, cudaStream_t st,
-                               const SyncArgs* sync);
-
 cudaError_t launch_epoch_advance(unsigned long long* epoch, unsigned long long span, cudaStream_t st);
 cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
                           int64_t n, int bits_in, int block, int bits_out, uint8_t* out_codes,
@@ -130,54 +102,6 @@ cudaError_t launch_gather_copy(const Pieces& pc, void* out, cudaStream_t st, con
 // float arrays of n elements, n % 4 == 0; the pieces may be peer-mapped)
 cudaError_t launch_sum_f32(const Pieces& pc, int64_t n, float* out, cudaStream_t st, const SyncArgs* sync);
 
-// Fused codec + NVLink collective kernels (k_fused.cu, B = 256 only).
-constexpr int kMaxChunks = 4096;   // per-chunk flags per member in the P2P pool header
-struct FusedAGArgs {
-  const void* x;
-  hz_dtype dt;
-  int bits;
-  uint8_t* qc;
-  float* qs;
-  const uint8_t* pc[kMaxWorld];
-  const float* ps[kMaxWorld];
-  int D, me;
-  int64_t plen, C;
-  int nch;
-  unsigned long long* flags;
-  unsigned long long* flags_remote[kMaxWorld];
-  unsigned long long* work;
-  unsigned int* cnt;      // per-chunk producer arrival counters (local, zero between launches)
-  unsigned long long* dbg;   // optional per-chunk timeline (HZ_TUNE pdbg)
-  void* y;
-  hz_dtype out_dt;
-  unsigned long long phase;
-  const unsigned long long* epoch;
-};
-struct FusedRSArgs {
-  const void* x;
-  hz_dtype dt;
-  int bits_in, bits_out, acc;
-  uint8_t* qc;
-  float* qs;
-  const uint8_t* mc[kMaxG];
-  const float* ms[kMaxG];
-  int g, d;
-  int64_t cl, C;
-  int ncl;
-  unsigned long long* flags;
-  unsigned long long* flags_remote[kMaxG];
-  unsigned long long* work;
-  unsigned int* cnt;
-  float* of;
-  uint8_t* oc;
-  float* os;
-  unsigned long long phase;
-  const unsigned long long* epoch;
-};
-bool fused_rs_supported(int g);
-cudaError_t launch_ag_fused(const FusedAGArgs& a, cudaStream_t st, const SyncArgs& sy);
-cudaError_t launch_rs_fused(const FusedRSArgs& a, cudaStream_t st, const SyncArgs& sy);
-
 // ------------------------------------------------------------------ tracing
 struct TraceScope {
   // Records a start event on construction and an end event + record on end().
@@ -195,6 +119,14 @@ struct TraceScope {
 // ----------------------------------------------------------------- partition
 hz_status partition(int rank, int levels, const int* group, int64_t numel, int block, int w,
                     int s, int gl, hz_partition_t* out);
+
+// qgZ hops (partition.cpp): levels a..b exchanged in one all-to-all
+struct Hop {
+  int a, b;
+};
+hz_status hops_of(const hz_partition_t* p, int from_level, int to_level, std::vector<Hop>* out);
+void hop_members(const hz_partition_t* p, int a, int b, std::vector<int>* ranks, std::vector<int64_t>* rel,
+                 int* me);
 
 // -------------------------------------------------------------------- plans
 hz_status plan_allgather(const hz_partition_t* p, int backward, int bits, std::vector<hz_comm_step>* out);

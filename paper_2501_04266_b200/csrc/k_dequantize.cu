@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
                                                          int64_t nunits, int log2b,
                                                          TO* __restrict__ y,
                                                          const __grid_constant__ SyncArgs sy) {
-  sync_wait(sy);
+  if (!sync_wait(sy)) return;
   dequantize_loop<BITS, TO, U>(pc, nunits, log2b, y, global_warp(), num_warps());
   sync_signal(sy);
 }

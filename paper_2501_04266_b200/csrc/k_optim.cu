@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kThreads) k_adamw(const float* __restrict__ g,
                                                     float* __restrict__ m, float* __restrict__ v,
                                                     TO* __restrict__ out, int64_t n4, AdamW hp,
                                                     const __grid_constant__ SyncArgs sy) {
-  sync_wait(sy);
+  if (!sync_wait(sy)) return;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
   const int64_t nth = static_cast<int64_t>(gridDim.x) * kThreads;
   for (int64_t base = tid; base < n4; base += nth * U) {
@@ -86,7 +86,7 @@ template <int U>
 __global__ void __launch_bounds__(kThreads) k_gather_copy(const __grid_constant__ Pieces pc, int64_t nvec,
                                                           uint4* __restrict__ out,
                                                           const __grid_constant__ SyncArgs sy) {
-  sync_wait(sy);
+  if (!sync_wait(sy)) return;
   const int lane = threadIdx.x & 31;
   const int64_t warp = global_warp();
   const int64_t nwarps = num_warps();
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_copy(const __grid_constant_
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t q = vb + u * 32 + lane;
-      if (q < per) r[u] = reinterpret_cast<const uint4*>(pc.c[j])[q];
+      if (q < per) r[u] = __ldcg(reinterpret_cast<const uint4*>(pc.c[j]) + q);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -123,7 +123,7 @@ cudaError_t adamw_u(const float* g, float* th, float* m, float* v, void* out, in
 template <int GT, int U>
 __global__ void __launch_bounds__(kThreads) k_sum_f32(const __grid_constant__ Pieces pc, int64_t n4,
                                                       float4* __restrict__ out, const __grid_constant__ SyncArgs sy) {
-  sync_wait(sy);
+  if (!sync_wait(sy)) return;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
   const int64_t nth = static_cast<int64_t>(gridDim.x) * kThreads;
   const int g = GT > 0 ? GT : pc.n;
@@ -132,14 +132,14 @@ __global__ void __launch_bounds__(kThreads) k_sum_f32(const __grid_constant__ Pi
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + u * nth;
-      if (i < n4) acc[u] = reinterpret_cast<const float4*>(pc.c[0])[i];
+      if (i < n4) acc[u] = __ldcg(reinterpret_cast<const float4*>(pc.c[0]) + i);
     }
     for (int j = 1; j < g; ++j) {
       float4 x[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t i = base + u * nth;
-        if (i < n4) x[u] = reinterpret_cast<const float4*>(pc.c[j])[i];
+        if (i < n4) x[u] = __ldcg(reinterpret_cast<const float4*>(pc.c[j]) + i);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {

@@ -35,12 +35,12 @@ struct OutOf<3> { using E = EmitF32; };
 
 // The quantize loop: warp `warp` of `nwarps` processes its grid-stride share of the
 // blocks (main loop without bounds checks, then the checked tail on the last warp).
-template <typename T, int B, int BITS, int U, int OUT, class P, class Emit>
+template <typename T, int B, int BITS, int U, int OUT, class Emit>
 // Iterations [it0, it1) of the main loop only (U*BPW blocks each; default: all); the
 // tail belongs to the range that ends at the last iteration.
 __device__ __forceinline__ void quantize_loop(const T* __restrict__ x, int64_t nblocks, uint8_t* __restrict__ codes,
                                               float* __restrict__ scales, Emit& emit, void* __restrict__ y, int acc,
-                                              const P& push, int64_t warp, int64_t nwarps, int64_t it0 = 0,
+                                              int64_t warp, int64_t nwarps, int64_t it0 = 0,
                                               int64_t it1 = INT64_MAX) {
   using G = Geo<B>;
   constexpr int NB = U * G::BPW;
@@ -72,7 +72,7 @@ __device__ __forceinline__ void quantize_loop(const T* __restrict__ x, int64_t n
       }
       am[u] = group_max<G::LPB>(m);
     }
-    quantize_store<B, BITS, U, Emit, P>(v, am, blk0, lane, codes, scales, emit, push);
+    quantize_store<B, BITS, U, Emit>(v, am, blk0, lane, codes, scales, emit);
   }
 
   // tail: the last nblocks % NB blocks, one warp step at a time, bounds-checked
@@ -104,11 +104,10 @@ __device__ __forceinline__ void quantize_loop(const T* __restrict__ x, int64_t n
         unsigned b[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) b[i] = qbits(v[k][i], inv);
-        if (valid && (codes || P::on)) {
+        if (valid && codes) {
           Codes8<BITS> out;
           out.set(b);
-          if (codes) out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
-          if constexpr (P::on) push.template put<BITS>(blk * B + k * G::SUBSTRIDE + ll * 8, out);
+          out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
         }
         if constexpr (OUT == 1 || OUT == 2) {
           if (valid) {
@@ -130,20 +129,16 @@ __device__ __forceinline__ void quantize_loop(const T* __restrict__ x, int64_t n
         }
       }
       if (valid && codes && ll == 0) scales[blk] = scale;
-      if constexpr (P::on) {
-        if (valid && ll == 0) push.template put_scale<B>(blk, scale);
-      }
     }
   }
 }
 
-template <typename T, int B, int BITS, int U, int OUT, class P = NoPush>
+template <typename T, int B, int BITS, int U, int OUT>
 __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, int64_t nblocks,
                                                        uint8_t* __restrict__ codes,
                                                        float* __restrict__ scales,
                                                        const __grid_constant__ SyncArgs sy,
-                                                       void* __restrict__ y, int acc,
-                                                       const __grid_constant__ P push) {
+                                                       void* __restrict__ y, int acc) {
   using G = Geo<B>;
   using Emit = typename OutOf<OUT>::E;
   __shared__ float4 stage[OUT == 3 ? kThreads / 32 : 1][OUT == 3 ? 64 : 1];
@@ -155,8 +150,8 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
     emit.stage = stage[threadIdx.x >> 5];
     emit.acc = acc;
   }
-  sync_wait(sy);   // P2P mode: every rank is done reading what this call overwrites
-  quantize_loop<T, B, BITS, U, OUT, P>(x, nblocks, codes, scales, emit, y, acc, push, global_warp(), num_warps());
+  if (!sync_wait(sy)) return;   // P2P mode: the readers of what this call overwrites are done
+  quantize_loop<T, B, BITS, U, OUT>(x, nblocks, codes, scales, emit, y, acc, global_warp(), num_warps());
   sync_signal(sy);   // P2P mode: codes of this phase are ready for the peers
 }
 
@@ -164,28 +159,14 @@ constexpr int kU = 4;   // warp steps per warp iteration
 // B > 256: NSUB = B/256 loads per step already; B < 256: NB = U*BPW <= 32
 constexpr int uq(int B) { return B > 256 ? 1 : kU; }
 
-template <typename T, int B, int BITS, int U, int OUT = 0, class P = NoPush>
+template <typename T, int B, int BITS, int U, int OUT = 0>
 cudaError_t quantize_u(const void* x, int64_t n, uint8_t* codes, float* scales, cudaStream_t st,
-                       const SyncArgs& sy, void* y = nullptr, int acc = 0, const P& push = P{}) {
+                       const SyncArgs& sy, void* y = nullptr, int acc = 0) {
   const int64_t nblocks = n / B;
   constexpr int NB = U * Geo<B>::BPW;
-  auto kern = k_quantize<T, B, BITS, U, OUT, P>;
+  auto kern = k_quantize<T, B, BITS, U, OUT>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), nblocks / NB + 1);
-  return launch_k(kern, grid, st, static_cast<const T*>(x), nblocks, codes, scales, sy, y, acc, push);
-}
-
-// push variants (B = 256): codes / scales also stored into the consumers' receive
-// buffers; y (optional) receives the own data's round trip x_hat
-template <typename T, int BITS>
-cudaError_t push_t(const void* x, int64_t n, uint8_t* codes, float* scales, void* y, hz_dtype out_dt,
-                   const Push& push, cudaStream_t st, const SyncArgs& sy) {
-  if (!y) return quantize_u<T, 256, BITS, kU, 0, Push>(x, n, codes, scales, st, sy, nullptr, 0, push);
-  switch (out_dt) {
-    case HZ_BF16: return quantize_u<T, 256, BITS, kU, 1, Push>(x, n, codes, scales, st, sy, y, 0, push);
-    case HZ_F16: return quantize_u<T, 256, BITS, kU, 2, Push>(x, n, codes, scales, st, sy, y, 0, push);
-    case HZ_F32: return quantize_u<T, 256, BITS, kU, 3, Push>(x, n, codes, scales, st, sy, y, 0, push);
-  }
-  return cudaErrorInvalidValue;
+  return launch_k(kern, grid, st, static_cast<const T*>(x), nblocks, codes, scales, sy, y, acc);
 }
 
 template <typename T, int BITS>
@@ -268,7 +249,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
     emit.stage = stage[threadIdx.x >> 5];
     emit.acc = acc;
   }
-  sync_wait(sy);
+  if (!sync_wait(sy)) return;
   const int64_t warp = global_warp(), nwarps = num_warps();
   if (order >= 2) {   // role split: CTAs [0, order - 2) gather only, the rest quantize only
     const int64_t gcta = order - 2;
@@ -276,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
     if (blockIdx.x < gcta)
       dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, gcta * wpc);
     else
-      quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{},
+      quantize_loop<T, 256, QBITS, kU, QOUT>(x, nblocks, codes, scales, emit, qy, acc,
                                                      warp - gcta * wpc, nwarps - gcta * wpc);
   } else if (CHUNKED) {
     // both jobs cut into `chunks` consecutive pieces; every warp alternates between
@@ -288,16 +269,16 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
       const int64_t a0 = ta * c / chunks, a1 = ta * (c + 1) / chunks;
       const int64_t b0 = tb * c / chunks, b1 = c + 1 == chunks ? INT64_MAX : tb * (c + 1) / chunks;
       if (gfirst) dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, nwarps, a0, a1);
-      quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps,
+      quantize_loop<T, 256, QBITS, kU, QOUT>(x, nblocks, codes, scales, emit, qy, acc, warp, nwarps,
                                                      b0, b1);
       if (!gfirst) dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, nwarps, a0, a1);
     }
   } else if (order == 0 && (blockIdx.x & 1) == 0) {
-    quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps);
+    quantize_loop<T, 256, QBITS, kU, QOUT>(x, nblocks, codes, scales, emit, qy, acc, warp, nwarps);
     dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, nwarps);
   } else {
     dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, warp, nwarps);
-    quantize_loop<T, 256, QBITS, kU, QOUT, NoPush>(x, nblocks, codes, scales, emit, qy, acc, NoPush{}, warp, nwarps);
+    quantize_loop<T, 256, QBITS, kU, QOUT>(x, nblocks, codes, scales, emit, qy, acc, warp, nwarps);
   }
   sync_signal(sy);
 }
@@ -367,27 +348,6 @@ cudaError_t launch_quantize_roundtrip(const void* x, hz_dtype dt, int64_t n, int
     case HZ_F16:
       return bits == 8 ? roundtrip_t<__half, 8>(x, n, codes, scales, y, out_dt, acc, st, sy)
                        : roundtrip_t<__half, 4>(x, n, codes, scales, y, out_dt, acc, st, sy);
-  }
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_quantize_push(const void* x, hz_dtype dt, int64_t n, int bits, uint8_t* codes, float* scales,
-                                 void* y, hz_dtype out_dt, const PushDst& dst, cudaStream_t st,
-                                 const SyncArgs* sync) {
-  SyncArgs sy = sync ? *sync : SyncArgs{};
-  sy.sysfence = 1;
-  Push push{};
-  push.d = dst;
-  switch (dt) {
-    case HZ_F32:
-      return bits == 8 ? push_t<float, 8>(x, n, codes, scales, y, out_dt, push, st, sy)
-                       : push_t<float, 4>(x, n, codes, scales, y, out_dt, push, st, sy);
-    case HZ_BF16:
-      return bits == 8 ? push_t<__nv_bfloat16, 8>(x, n, codes, scales, y, out_dt, push, st, sy)
-                       : push_t<__nv_bfloat16, 4>(x, n, codes, scales, y, out_dt, push, st, sy);
-    case HZ_F16:
-      return bits == 8 ? push_t<__half, 8>(x, n, codes, scales, y, out_dt, push, st, sy)
-                       : push_t<__half, 4>(x, n, codes, scales, y, out_dt, push, st, sy);
   }
   return cudaErrorInvalidValue;
 }

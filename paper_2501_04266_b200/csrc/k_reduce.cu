@@ -51,7 +51,7 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
       // 4 scales of an input are one 16-byte broadcast load
 #pragma unroll
       for (int p = 0; p < GT; ++p) {
-        const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.s[p] + blk0));
+        const float4 s4 = __ldcg(reinterpret_cast<const float4*>(a.s[p] + blk0));
         sc[0][p] = s4.x;
         sc[1][p] = s4.y;
         sc[2][p] = s4.z;
@@ -70,7 +70,7 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
 #pragma unroll
           for (int k = 0; k < G::NSUB; ++k)
             raw[u][p][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
-          sc[u][p] = __ldg(a.s[p] + blk);
+          sc[u][p] = __ldcg(a.s[p] + blk);
         } else {
 #pragma unroll
           for (int k = 0; k < G::NSUB; ++k) raw[u][p][k].zero();
@@ -106,7 +106,7 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
 #pragma unroll
           for (int k = 0; k < G::NSUB; ++k)
             raw[u][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
-          sc[u] = __ldg(a.s[p] + blk);
+          sc[u] = __ldcg(a.s[p] + blk);
         } else {
 #pragma unroll
           for (int k = 0; k < G::NSUB; ++k) raw[u][k].zero();
@@ -131,12 +131,11 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
 // Main loop: warp iterations of U full steps (NB = U*BPW blocks), no bounds checks,
 // quantize_store epilogue (one division per block).  Tail (< NB blocks): one
 // checked step at a time by the last warp.
-template <int B, int BIN, int BOUT, int GT, int U, class P = NoPush>
+template <int B, int BIN, int BOUT, int GT, int U>
 __global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_constant__ RedArgs a,
-                                                             const __grid_constant__ SyncArgs sy,
-                                                             const __grid_constant__ P push) {
+                                                             const __grid_constant__ SyncArgs sy) {
   using G = Geo<B>;
-  sync_wait(sy);   // P2P: peers' chunks ready, and nobody still reads our output slot
+  if (!sync_wait(sy)) return;   // P2P: peers' chunks ready, and nobody still reads our output slot
   constexpr int NB = U * G::BPW;
   const int lane = threadIdx.x & 31;
   const int lb = lane / G::LPB;
@@ -163,7 +162,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_consta
         for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(acc[u][k][i]));
       am[u] = group_max<G::LPB>(m);
     }
-    quantize_store<B, BOUT, U, NoEmit, P>(acc, am, blk0, lane, a.oc, a.os, NoEmit{}, push);
+    quantize_store<B, BOUT, U, NoEmit>(acc, am, blk0, lane, a.oc, a.os, NoEmit{});
   }
 
   const int64_t tail0 = nfull * NB;
@@ -189,13 +188,9 @@ __global__ void __launch_bounds__(kThreads) k_reduce_requant(const __grid_consta
           for (int i = 0; i < 8; ++i) bq[i] = qbits(acc[0][k][i], inv);
           Codes8<BOUT> out;
           out.set(bq);
-          if (a.oc) out.store(a.oc + (blk * B + k * G::SUBSTRIDE + ll * 8) * BOUT / 8);
-          if constexpr (P::on) push.template put<BOUT>(blk * B + k * G::SUBSTRIDE + ll * 8, out);
+          out.store(a.oc + (blk * B + k * G::SUBSTRIDE + ll * 8) * BOUT / 8);
         }
-        if (ll == 0 && a.oc) a.os[blk] = scale;
-        if constexpr (P::on) {
-          if (ll == 0) push.template put_scale<B>(blk, scale);
-        }
+        if (ll == 0) a.os[blk] = scale;
       }
     }
   }
@@ -215,7 +210,7 @@ template <>
 struct Wide<8> {
   static constexpr int E = 8;
   uint2 r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const uint2*>(p)); }
   __device__ __forceinline__ void decode(float (&c)[E]) const {
     Codes8<8> x;
     x.r = r;
@@ -226,7 +221,7 @@ template <>
 struct Wide<4> {
   static constexpr int E = 16;
   uint2 r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const uint2*>(p)); }
   __device__ __forceinline__ void decode(float (&c)[E]) const {
     Codes8<4> lo, hi;
     lo.r = r.x;
@@ -248,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
   constexpr int E = Wide<BIN>::E;
   constexpr int G = E / 4;                         // float4 granules per lane per unit
   __shared__ float4 stage[kThreads / 32][32 * G];
-  sync_wait(sy);
+  if (!sync_wait(sy)) return;
   const int lane = threadIdx.x & 31;
   float4* st = stage[threadIdx.x >> 5];
   const int64_t warp = global_warp();
@@ -281,7 +276,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
           raw[u][p].r = make_uint2(0u, 0u);
           if (unit < nunits) {
             raw[u][p].load(a.c[p] + unit * 8);
-            sc[u][p] = __ldg(a.s[p] + ((unit * E) >> log2b));
+            sc[u][p] = __ldcg(a.s[p] + ((unit * E) >> log2b));
           }
         }
       }
@@ -309,7 +304,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
           raw[u].r = make_uint2(0u, 0u);
           if (unit < nunits) {
             raw[u].load(a.c[p] + unit * 8);
-            sc[u] = __ldg(a.s[p] + ((unit * E) >> log2b));
+            sc[u] = __ldcg(a.s[p] + ((unit * E) >> log2b));
           }
         }
 #pragma unroll
@@ -356,127 +351,17 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
   sync_signal(sy);
 }
 
-// Direct-store variant: E (4 or 8) consecutive elements per lane, E/4 float4 stores
-// per lane at lane-contiguous addresses (no shared-memory staging).  Narrower code
-// loads (E*BIN/8 bytes per lane); kept for the HZ_TUNE rf_e sweep.
-template <int BIN, int E>
-struct Narrow {
-  static constexpr int NB = E * BIN / 8;   // code bytes per lane
-  unsigned r;
-  __device__ __forceinline__ void load(const uint8_t* p) {
-    if constexpr (NB == 2) r = __ldg(reinterpret_cast<const unsigned short*>(p));
-    else r = __ldg(reinterpret_cast<const unsigned*>(p));
-  }
-  __device__ __forceinline__ void decode(float (&c)[E]) const {
-    if constexpr (BIN == 8) {
-      const unsigned x = r ^ 0x80808080u;
-#pragma unroll
-      for (int i = 0; i < E; ++i) c[i] = __fsub_rn(byte_as_magic(x, i), kMagic + 128.f);
-    } else {
-      const unsigned x = r ^ 0x88888888u;
-      const unsigned ev = x & 0x0F0F0F0Fu;
-      const unsigned od = (x >> 4) & 0x0F0F0F0Fu;
-#pragma unroll
-      for (int i = 0; i < E / 2; ++i) {
-        c[2 * i] = __fsub_rn(byte_as_magic(ev, i), kMagic + 8.f);
-        c[2 * i + 1] = __fsub_rn(byte_as_magic(od, i), kMagic + 8.f);
-      }
-    }
-  }
-};
-
-template <int BIN, int E, int GT, int U, bool ACC>
-__global__ void __launch_bounds__(kThreads) k_reduce_f32_direct(const __grid_constant__ RedArgs a, int log2b,
-                                                                const __grid_constant__ SyncArgs sy) {
-  static_assert(BIN == 8 ? E == 4 : (E == 4 || E == 8), "unit width");
-  sync_wait(sy);
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = global_warp();
-  const int64_t nwarps = num_warps();
-  const int64_t nunits = a.n / E;
-  constexpr int GP = GT > 0 ? GT : 1;
-  for (int64_t base = warp * 32 * U; base < nunits; base += nwarps * 32 * U) {
-    float acc[U][E];
-    float4 old[ACC ? U : 1][E / 4];
-    Narrow<BIN, E> raw[U][GP];
-    float sc[U][GP];
-    const int np = GT > 0 ? GT : a.g;
-    for (int p0 = 0; p0 < np; p0 += GP) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t unit = base + u * 32 + lane;
-#pragma unroll
-        for (int q = 0; q < GP; ++q) {
-          sc[u][q] = 0.f;
-          raw[u][q].r = 0u;
-          if (unit < nunits) {
-            raw[u][q].load(a.c[p0 + q] + unit * Narrow<BIN, E>::NB);
-            sc[u][q] = __ldg(a.s[p0 + q] + ((unit * E) >> log2b));
-          }
-        }
-        if (ACC && p0 == 0 && unit < nunits) {
-#pragma unroll
-          for (int k = 0; k < E / 4; ++k) old[u][k] = reinterpret_cast<const float4*>(a.of)[unit * (E / 4) + k];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int q = 0; q < GP; ++q) {
-          float c[E];
-          raw[u][q].decode(c);
-#pragma unroll
-          for (int i = 0; i < E; ++i) {
-            const float xh = __fmul_rn(c[i], sc[u][q]);
-            acc[u][i] = (p0 + q) == 0 ? xh : __fadd_rn(acc[u][i], xh);
-          }
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t unit = base + u * 32 + lane;
-      if (unit < nunits) {
-#pragma unroll
-        for (int k = 0; k < E / 4; ++k) {
-          float4 o = make_float4(acc[u][4 * k], acc[u][4 * k + 1], acc[u][4 * k + 2], acc[u][4 * k + 3]);
-          if constexpr (ACC) {
-            o.x = __fadd_rn(old[u][k].x, o.x);
-            o.y = __fadd_rn(old[u][k].y, o.y);
-            o.z = __fadd_rn(old[u][k].z, o.z);
-            o.w = __fadd_rn(old[u][k].w, o.w);
-          }
-          reinterpret_cast<float4*>(a.of)[unit * (E / 4) + k] = o;
-        }
-      }
-    }
-  }
-  sync_signal(sy);
-}
-
 // ---------------------------------------------------------------------- launch
 constexpr int kUR = 4;   // warp steps per warp iteration (requant)
 constexpr int kUF = 2;   // 8-byte code units in flight per lane per input (fp32 out)
 constexpr int ur(int B) { return B > 256 ? 1 : kUR; }
 
-template <int B, int BIN, int BOUT, int GT, int U, class P = NoPush>
-cudaError_t requant_u(const RedArgs& a, cudaStream_t st, const SyncArgs& sy, const P& push = P{}) {
+template <int B, int BIN, int BOUT, int GT, int U>
+cudaError_t requant_u(const RedArgs& a, cudaStream_t st, const SyncArgs& sy) {
   constexpr int NB = U * Geo<B>::BPW;
-  auto kern = k_reduce_requant<B, BIN, BOUT, GT, U, P>;
+  auto kern = k_reduce_requant<B, BIN, BOUT, GT, U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), a.n / B / NB + 1);
-  return launch_k(kern, grid, st, a, sy, push);
-}
-
-// push variant (B = 256): the requantized sum goes straight into the next level's
-// receive buffers (scatter by destination)
-template <int BIN, int BOUT>
-cudaError_t requant_push(const RedArgs& a, const Push& push, cudaStream_t st, const SyncArgs& sy) {
-  switch (a.g) {
-    case 1: return requant_u<256, BIN, BOUT, 1, kUR, Push>(a, st, sy, push);
-    case 2: return requant_u<256, BIN, BOUT, 2, kUR, Push>(a, st, sy, push);
-    case 4: return requant_u<256, BIN, BOUT, 4, kUR, Push>(a, st, sy, push);
-    case 8: return requant_u<256, BIN, BOUT, 8, kUR, Push>(a, st, sy, push);
-  }
-  return cudaErrorInvalidValue;
+  return launch_k(kern, grid, st, a, sy);
 }
 
 template <int B, int BIN, int BOUT, int GT>
@@ -518,23 +403,8 @@ cudaError_t f32_u(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& 
   return launch_k(kern, grid, st, a, log2b, sy);
 }
 
-template <int BIN, int E, int GT>
-cudaError_t f32_direct(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& sy) {
-  constexpr int U = 4;
-  const int64_t nunits = a.n / E;
-  auto kern = a.accumulate ? k_reduce_f32_direct<BIN, E, GT, U, true> : k_reduce_f32_direct<BIN, E, GT, U, false>;
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
-  return launch_k(kern, grid, st, a, log2b, sy);
-}
-
 template <int BIN, int GT>
 cudaError_t f32_t(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& sy) {
-  if constexpr (GT > 0 && GT <= 2) {   // HZ_TUNE rf_e: 4, 8 = direct-store variants
-    const int e = tune_param("rf_e", 0);
-    if (e == 4) return f32_direct<BIN, 4, GT>(a, log2b, st, sy);
-    if constexpr (BIN == 4)
-      if (e == 8) return f32_direct<BIN, 8, GT>(a, log2b, st, sy);
-  }
   if constexpr (GT > 0 && GT <= 2) {   // HZ_TUNE rf_u: 1, 2, 4
     switch (tune_param("rf_u", kUF)) {
       case 1: return f32_u<BIN, GT, 1>(a, log2b, st, sy);
@@ -557,26 +427,6 @@ cudaError_t f32_g(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& 
 }
 
 }  // namespace
-
-bool push_reduce_supported(int g, int block) { return block == 256 && (g == 1 || g == 2 || g == 4 || g == 8); }
-
-cudaError_t launch_reduce_push(int g, const uint8_t* const* codes, const float* const* scales, int64_t n,
-                               int bits_in, int bits_out, const PushDst& dst, cudaStream_t st,
-                               const SyncArgs* sync) {
-  SyncArgs sy = sync ? *sync : SyncArgs{};
-  sy.sysfence = 1;
-  RedArgs a{};
-  for (int p = 0; p < g; ++p) {
-    a.c[p] = codes[p];
-    a.s[p] = scales[p];
-  }
-  a.g = g;
-  a.n = n;
-  Push push{};
-  push.d = dst;
-  if (bits_in == 8) return bits_out == 8 ? requant_push<8, 8>(a, push, st, sy) : requant_push<8, 4>(a, push, st, sy);
-  return bits_out == 8 ? requant_push<4, 8>(a, push, st, sy) : requant_push<4, 4>(a, push, st, sy);
-}
 
 cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
                           int64_t n, int bits_in, int block, int bits_out, uint8_t* out_codes,

@@ -1,36 +1,52 @@
-// NVLink peer-memory transport (hz_enable_p2p): the per-level collectives are
-// fused into the codec kernels instead of being staged through NCCL.
+// NVLink peer-memory transport (hz_enable_p2p; hz_init_virtual): the per-level
+// collectives are fused into the codec kernels instead of being staged through NCCL.
 //
-// Every rank owns one symmetric pool (cudaMalloc + cudaIpcGetMemHandle; the
-// handles are exchanged with one ncclAllGather and opened with
-// cudaIpcOpenMemHandle), so a buffer at pool offset X on this rank is at offset
-// X in every peer's pool.  Allocations (hz_sym_alloc and the library's slots)
-// are bump allocations made in the same order on every rank, hence symmetric.
+// Every rank owns one symmetric pool (cudaMalloc + cudaIpcGetMemHandle; the handles
+// are exchanged with one ncclAllGather and opened with cudaIpcOpenMemHandle), so a
+// buffer at pool offset X on this rank is at offset X in every peer's pool.
+// Allocations (hz_sym_alloc and the library's slots) are bump allocations made in
+// the same order on every rank, hence symmetric.
 //
 // qwZ/hpZ all-gather (O7/O8): the owner quantizes its primary into a pool buffer
 // (the caller's pool-allocated secondary when s == w); each rank then runs ONE
-// gather+dequantize kernel whose pieces are the members' codes, read straight
-// over NVLink — the gathered codes never land in HBM.  Backward: the same kernel
-// over the members' secondaries.
-// qgZ reduce-scatter (O9): level l's send buffer (quantize output, or the
-// previous level's requantized sum) lives in the pool; the level-l reduce kernel
-// reads chunk d_l of every group member's send buffer over NVLink and sums in
-// ascending digit order — the all-to-all and the dequant+sum are one kernel.
+// gather+dequantize kernel whose pieces are the members' codes, read straight over
+// NVLink — the gathered codes never land in HBM.  Backward: the same kernel over
+// the members' secondaries.
+// qgZ reduce-scatter (O9): a hop's send buffer (the quantize output, or the previous
+// hop's requantized sum) lives in the pool; the hop's reduce kernel reads the chunk
+// destined to this rank from every member's send buffer over NVLink and sums in
+// ascending member order — the all-to-all and the dequant+sum are one kernel.
 //
-// Ordering: every phase has a global number; producers wait until all ranks are
-// done with the previous phase (no one still reads what they overwrite) and
-// signal `ready`, consumers wait for `ready` and signal `done` (codec.cuh).
-// All P2P calls of one context must be issued on one stream, in the same order
-// on every rank (the NCCL discipline).
+// Ordering (codec.cuh): every call is one or more numbered phases, the same numbers
+// on every rank.  Synchronisation is level-local (the devices involved in an
+// exchange do not scale with the job):
+//   * a kernel that READS peers' buffers produced in the same phase waits for
+//     `ready >= phase` from exactly those peers (the gather members, the hop group);
+//   * a kernel that OVERWRITES a pool buffer waits for `done >= phase-1` from the
+//     ranks that read this rank's copy of that buffer in earlier calls (`readers`);
+//   * a backward gather reads secondaries written in an earlier phase and waits for
+//     `done >= phase-1` from its members (every rank finished every earlier phase);
+//   * the kernel that completes a phase signals `done(phase)` to `nbr`, the ranks this
+//     rank reads from (and, from a forward gather on, the members of its backward
+//     gather): `done[q] >= v` at a rank certifies that q finished all its reads and
+//     writes of phases <= v.  Producers signal `ready(phase)` to the readers of what
+//     they wrote.
+// So a pair exchange waits only for the pair, whatever the other ranks do.  All P2P
+// calls of one context must be issued on one stream, in the same order on every rank
+// (the NCCL discipline).
 //
 // Paired layers (hz_allgather_params_next / hz_backward_step): one dual kernel
 // (k_gather_quantize) runs a gather of phase a and a quantize of phase a+1.  It waits
-// for ready >= a (the gathered codes) and done >= a-1 (every rank finished every
-// earlier phase, so nobody still reads what the quantize overwrites: the next layer's
-// secondary, last read in an earlier backward phase, or the qgZ send slot, last read
-// by the previous layer's reduce) and signals done = a and ready = a+1.  A prefetched
-// quantize whose layer is not gathered next (another call comes first) leaves phase
-// a+1 without a `done`; flush_prefetch completes it before the next phase starts.
+// for its gather's condition and for `done >= a-1` from the readers of what the
+// quantize overwrites, and signals done(a) and ready(a+1).  A prefetched quantize
+// whose layer is not gathered next (another call comes first) leaves phase a+1
+// without a `done`; flush_prefetch completes it before the next phase starts.
+//
+// Virtual world (hz_init_virtual, vworld.cpp): W contexts in one process on one GPU,
+// whose peer pools are each other's allocations.  The same kernels and flags run;
+// in addition every launch is ordered on the host after the launches that signal
+// what it waits for (CUDA events), so the W streams cannot deadlock on shared
+// hardware queues or SMs.
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -38,10 +54,6 @@
 #include <vector>
 
 #include "ctx.h"
-
-namespace hz {
-int tune_param(const char* name, int dflt);
-}
 
 namespace hz {
 namespace {
@@ -72,18 +84,6 @@ hz_status slot(hz_ctx* ctx, hz_ctx::P2P::Slot& sl, size_t bytes) {
   return rc;
 }
 
-// pipelined-kernel chunk: about len / pk (HZ_TUNE pk, default 16) elements, a
-// multiple of 1024 (4 blocks of 256), >= fchunk KiElements (default 64), and few
-// enough chunks for the per-member flag arrays
-int64_t chunk_elems(int64_t len) {
-  int64_t c = (len + tune_param("pk", 16) - 1) / tune_param("pk", 16);
-  const int64_t cap = (len + kMaxChunks - 1) / kMaxChunks;
-  if (c < cap) c = cap;
-  const int64_t lo = int64_t(tune_param("fchunk", 64)) * 1024;
-  if (c < lo) c = lo;
-  return (c + 1023) / 1024 * 1024;
-}
-
 template <typename T>
 T* at(hz_ctx* ctx, int q, size_t off) {
   return reinterpret_cast<T*>(ctx->p2p.peer[q] + off);
@@ -93,8 +93,29 @@ size_t off_of(const hz_ctx* ctx, const void* local) {
   return static_cast<size_t>(static_cast<const char*>(local) - ctx->p2p.pool);
 }
 
-SyncArgs make_sync(hz_ctx* ctx, unsigned long long wait_ready, unsigned long long wait_done,
-                   unsigned long long sig_ready, unsigned long long sig_done) {
+unsigned mask_of(const std::vector<int>& ranks, int me) {
+  unsigned m = 0;
+  for (int r : ranks)
+    if (r != me) m |= 1u << r;
+  return m;
+}
+
+// readers of this rank's copy of the pool buffer at `local` (earlier calls)
+unsigned readers_of(const hz_ctx* ctx, const void* local) {
+  auto it = ctx->p2p.readers.find(off_of(ctx, local));
+  return it == ctx->p2p.readers.end() ? 0u : it->second;
+}
+
+void add_readers(hz_ctx* ctx, const void* local, unsigned m) { ctx->p2p.readers[off_of(ctx, local)] |= m; }
+
+// Phase arguments are absolute phase numbers; the kernel sees them relative to the
+// device epoch (graph replays advance it).  A zero mask disables that wait / signal.
+struct Phases {
+  unsigned long long wr = 0, wd = 0, sr = 0, sd = 0;
+  unsigned wr_mask = 0, wd_mask = 0, sr_mask = 0, sd_mask = 0;
+};
+
+SyncArgs make_sync(hz_ctx* ctx, const Phases& ph) {
   auto& P = ctx->p2p;
   SyncArgs s{};
   s.ready_local = reinterpret_cast<unsigned long long*>(P.pool + kReadyOff);
@@ -104,58 +125,70 @@ SyncArgs make_sync(hz_ctx* ctx, unsigned long long wait_ready, unsigned long lon
     s.done_remote[q] = reinterpret_cast<unsigned long long*>(P.peer[q] + kDoneOff) + ctx->rank;
   }
   s.counter = reinterpret_cast<unsigned int*>(P.pool + kCounterOff);
-  s.world = ctx->world;
-  // thresholds are stored relative to the device epoch the kernel will see
-  // (arguments: absolute phase numbers, 0 = none; phase numbers are > epoch_host)
-  const unsigned long long e = P.epoch_host;
-  s.en = (wait_ready ? kWaitReady : 0u) | (wait_done ? kWaitDone : 0u) | (sig_ready ? kSigReady : 0u) |
-         (sig_done ? kSigDone : 0u);
-  s.wait_ready = wait_ready - e;
-  s.wait_done = wait_done - e;
-  s.sig_ready = sig_ready - e;
-  s.sig_done = sig_done - e;
   s.epoch = reinterpret_cast<const unsigned long long*>(P.pool + kEpochOff);
-  s.mode = tune_param("p2p_sig", 1);   // fence.acq_rel.sys + relaxed.sys flag stores
+  s.abort = P.abort_dev;
+  s.timeout_ns = P.timeout_ns;
+  const unsigned long long e = P.epoch_host;
+  s.wait_ready = ph.wr - e;
+  s.wait_done = ph.wd - e;
+  s.sig_ready = ph.sr - e;
+  s.sig_done = ph.sd - e;
+  s.wr_mask = ph.wr_mask;
+  s.wd_mask = ph.wd_mask;
+  s.sr_mask = ph.sr_mask;
+  s.sd_mask = ph.sd_mask;
   return s;
 }
 
+// One synchronised launch: in a virtual world the host first orders the stream after
+// the signals this kernel waits for, and records its own signals afterwards.
+template <class F>
+hz_status synced(hz_ctx* ctx, const SyncArgs& s, cudaStream_t st, F&& launch) {
+  hz_status rc;
+  if (ctx->p2p.vw && (rc = vw_wait(ctx, s, st)) != HZ_OK) return rc;
+  if ((rc = launch()) != HZ_OK) return rc;
+  if (ctx->p2p.vw) return vw_signal(ctx, s, st);
+  return HZ_OK;
+}
+
 // Members of this rank's cumulative group of `level` (ranks that share every digit
-// above `level`), as (off_level within range_0, rank), sorted by offset: piece k
-// of the gathered layer is owned by the k-th entry.
+// above `level`), as (off_level within range_0, rank), sorted by offset: piece k of
+// the gathered layer is owned by the k-th entry.
 std::vector<std::pair<int64_t, int>> cumulative_members(const hz_partition_t* p, int level) {
-  int64_t stride[HZ_MAX_LEVELS];
-  int64_t st = 1;
-  for (int l = 0; l < p->levels; ++l) {
-    stride[l] = st;
-    st *= p->group[l];
-  }
-  int64_t base = p->rank;
-  int64_t D = 1;
-  for (int l = 0; l < level; ++l) {
-    base -= p->digit[l] * stride[l];
-    D *= p->group[l];
-  }
+  std::vector<int> ranks;
+  std::vector<int64_t> rel;
   std::vector<std::pair<int64_t, int>> out;
-  for (int64_t idx = 0; idx < D; ++idx) {
-    int64_t rem = idx, r = base, off = 0;
-    for (int l = 0; l < level; ++l) {
-      const int d = static_cast<int>(rem % p->group[l]);
-      rem /= p->group[l];
-      r += d * stride[l];
-      off += d * p->len[l + 1];
-    }
-    out.emplace_back(off, static_cast<int>(r));
+  if (level < 1) {
+    out.emplace_back(0, p->rank);
+    return out;
   }
+  hop_members(p, 1, level, &ranks, &rel, nullptr);
+  for (size_t k = 0; k < ranks.size(); ++k) out.emplace_back(rel[k], ranks[k]);
   std::sort(out.begin(), out.end());
   return out;
 }
 
+unsigned mask_of(const std::vector<std::pair<int64_t, int>>& mem, int me) {
+  unsigned m = 0;
+  for (const auto& x : mem)
+    if (x.second != me) m |= 1u << x.second;
+  return m;
+}
+
 }  // namespace
+
+hz_status p2p_check(const hz_ctx* ctx) {
+  const auto& P = ctx->p2p;
+  if (P.abort_host && *reinterpret_cast<volatile unsigned*>(P.abort_host))
+    return fail(HZ_ERR_ABORTED, "context aborted: a cross-GPU wait timed out or hz_abort was called "
+                                "(only hz_finalize is allowed now)");
+  return HZ_OK;
+}
 
 // A prefetched quantize (hz_allgather_params_next) whose layer is not gathered next
 // leaves its phase without a `done`; complete it before any other phase starts: a
-// one-CTA kernel signalling done(pre_phase) — nobody reads those codes, and every
-// earlier read of this rank is complete in stream order.
+// one-CTA kernel signalling done(pre_phase) — nobody reads those codes in that phase,
+// and every earlier read of this rank is complete in stream order.
 hz_status flush_prefetch(hz_ctx* ctx, cudaStream_t st) {
   auto& P = ctx->p2p;
   if (!P.pre_phase) return HZ_OK;
@@ -164,8 +197,11 @@ hz_status flush_prefetch(hz_ctx* ctx, cudaStream_t st) {
   P.pre_codes = P.pre_primary = nullptr;
   Pieces pc{};
   pc.n = 1;
-  SyncArgs s = make_sync(ctx, 0, 0, 0, ph);
-  return run_gather_dequantize(pc, 0, 8, 256, nullptr, HZ_BF16, st, 0, &s, 0);
+  Phases f;
+  f.sd = ph;
+  f.sd_mask = P.nbr;
+  SyncArgs s = make_sync(ctx, f);
+  return synced(ctx, s, st, [&] { return run_gather_dequantize(pc, 0, 8, 256, nullptr, HZ_BF16, st, 0, &s, 0); });
 }
 
 bool in_pool(const hz_ctx* ctx, const void* p, size_t bytes) {
@@ -178,7 +214,7 @@ bool p2p_next_fusable(const hz_ctx* ctx, const hz_partition_t* p, int bits, hz_d
   return ctx->p2p.on && q && p->s == p->w && q->s == q->w && p->block == 256 && q->block == 256 &&
          gather_quantize_supported(256, bits, out_dt) && q->len[q->w] > 0 &&
          in_pool(ctx, nx.codes, code_bytes(q->len[q->s], bits)) && in_pool(ctx, nx.scales, q->len[q->s] / 256 * 4) &&
-         tune_param("pushf", 0) == 0 && tune_param("fused", 0) == 0 && tune_param("nofuse", 0) == 0;
+         tune_param("nofuse", 0) == 0;
 }
 
 hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, const void* primary,
@@ -196,94 +232,27 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   const auto members = cumulative_members(p, top);
   const int D = static_cast<int>(members.size());
   if (D > kMaxWorld) return fail(HZ_ERR_UNSUPPORTED, "P2P gather over more than 8 ranks");
-  // every call is a phase, even without peers to read from: it may write a
-  // secondary that peers read in a later backward phase (s > w), and the final
-  // kernel's done(phase) is what tells them the write (incl. its copies) is complete
+  const unsigned gmask = mask_of(members, ctx->rank);                         // read in this call
+  const unsigned smask = mask_of(cumulative_members(p, s), ctx->rank);        // backward group
   // this layer's primary already quantized by the previous call's dual kernel (the
-  // prefetch of hz_allgather_params_next), in phase pre_phase, with no phase since
-  const bool pre = !backward && s == w && P.pre_phase != 0 && P.pre_phase == P.phase &&
-                   P.pre_codes == sec_codes && P.pre_primary == primary;
+  // prefetch of hz_allgather_params_next), in phase pre_phase, with no phase since,
+  // from the same primary with the same code width, dtype and length
+  const bool pre = !backward && s == w && P.pre_phase != 0 && P.pre_phase == P.phase && P.pre_codes == sec_codes &&
+                   P.pre_primary == primary && P.pre_bits == bits && P.pre_dt == dt && P.pre_len == p->len[w];
   if (pre) {
     P.pre_phase = 0;
     P.pre_codes = P.pre_primary = nullptr;
   } else if ((rc = flush_prefetch(ctx, st)) != HZ_OK) {
     return rc;
   }
+  // every call is a phase, even without peers to read from: it may write a secondary
+  // that peers read in a later backward phase, and its done(phase) tells them so
   const unsigned long long phase = pre ? P.phase : ++P.phase;
+  // the members read this rank's buffers from now on, and will gather its secondary
+  // in the backward: they get this rank's `done` signals
+  P.nbr |= gmask | smask;
   const int64_t plen = p->len[top];
-  int me = 0;
-  for (int k = 0; k < D; ++k)
-    if (members[k].second == ctx->rank) me = k;
-  // forward with s == w, hybrid push/pull (HZ_TUNE pushf = % of each piece pushed by
-  // the quantize kernel, in whole 1024-element tiles).  Default 0 = pull only: on
-  // B200 the pushes cost the quantize kernel about as much NVLink time as they save
-  // the gather (profiles/push_pull_r01.md).
-  int64_t push_lim = 0;
-  if (!backward && s == w && D > 1 && B == 256)
-    push_lim = plen * tune_param("pushf", 0) / 100 / 1024 * 1024;
 
-  if (!backward && s == w && D > 1 && B == 256 && tune_param("fused", 0)) {
-    // A2 + A3 + A5 in ONE kernel: quantize the own primary chunk by chunk into the
-    // (peer-readable) secondary, publish each chunk, and dequantize every member's
-    // chunks as they become ready — NVLink transfers overlap the quantization.
-    FusedAGArgs h{};
-    h.x = primary;
-    h.dt = dt;
-    h.bits = bits;
-    h.qc = sec_codes;
-    h.qs = sec_scales;
-    h.D = D;
-    h.plen = plen;
-    h.C = chunk_elems(plen);
-    h.nch = static_cast<int>((plen + h.C - 1) / h.C);
-    int64_t remote = 0;
-    for (int k = 0; k < D; ++k) {
-      const int m = members[k].second;
-      if (m == ctx->rank) h.me = k;
-      h.pc[k] = at<const uint8_t>(ctx, m, off_of(ctx, sec_codes));
-      h.ps[k] = at<const float>(ctx, m, off_of(ctx, sec_scales));
-      if (m != ctx->rank) remote += code_bytes(plen, bits) + plen / B * 4;
-    }
-    for (int k = 0; k < D; ++k)
-      h.flags_remote[k] = at<unsigned long long>(ctx, members[k].second, kChunkAGOff) + h.me * kMaxChunks;
-    h.flags = at<unsigned long long>(ctx, ctx->rank, kChunkAGOff);
-    h.work = at<unsigned long long>(ctx, ctx->rank, kWorkAGOff);
-    h.cnt = at<unsigned int>(ctx, ctx->rank, kCntAGOff);
-    h.y = full_out;
-    h.out_dt = out_dt;
-    h.phase = phase - P.epoch_host;
-    h.epoch = at<const unsigned long long>(ctx, ctx->rank, kEpochOff);
-    SyncArgs sy = make_sync(ctx, 0, phase - 1, 0, phase);
-    const int64_t local = p->len[w] * elem_bytes(dt) + code_bytes(plen, bits) + plen / B * 4 +
-                          code_bytes(Np, bits) + Np / B * 4 - remote + Np * elem_bytes(out_dt);
-    static int dbg_calls = 0;
-    const bool dbg = tune_param("pdbg", 0) && ++dbg_calls == tune_param("pdbg", 0);
-    if (dbg) {   // diagnostic timeline of one call (HZ_TUNE pdbg=<call number>), printed to stderr
-      h.dbg = at<unsigned long long>(ctx, ctx->rank, kDbgOff);
-      std::vector<unsigned long long> init(size_t(kMaxChunks) * 4, 0ull);
-      for (int c = 0; c < h.nch; ++c) init[c * 4 + 1] = ~0ull;
-      cudaMemcpyAsync(h.dbg, init.data(), init.size() * 8, cudaMemcpyHostToDevice, st);
-      cudaStreamSynchronize(st);
-    }
-    TraceScope t(st, "ag_fused", w, bits, Np, local, remote);
-    sy.stamps = t.stamps;
-    cudaError_t e = launch_ag_fused(h, st, sy);
-    t.end();
-    if (e != cudaSuccess) return cuda_fail(e, "fused all-gather kernel launch");
-    if (dbg) {
-      std::vector<unsigned long long> tl(size_t(kMaxChunks) * 4);
-      cudaStreamSynchronize(st);
-      cudaMemcpy(tl.data(), h.dbg, tl.size() * 8, cudaMemcpyDeviceToHost);
-      const unsigned long long t0 = tl[(kMaxChunks - 1) * 4];
-      fprintf(stderr, "[hz pdbg rank %d] ag_pipe plen=%lld C=%lld nch=%d (us from entry: last-arrive publish "
-              "first-consumer-start last-consumer-end)\n", ctx->rank, (long long)plen, (long long)h.C, h.nch);
-      for (int c = 0; c < h.nch; ++c)
-        fprintf(stderr, "  c=%3d %8.2f %8.2f %8.2f %8.2f\n", c, (tl[c * 4 + 3] - t0) * 1e-3, (tl[c * 4] - t0) * 1e-3,
-                (tl[c * 4 + 1] - t0) * 1e-3, (tl[c * 4 + 2] - t0) * 1e-3);
-    }
-    clear_error();
-    return HZ_OK;
-  }
   const uint8_t* xc;
   const float* xs;
   if (!backward) {
@@ -295,29 +264,21 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
       qc = at<uint8_t>(ctx, ctx->rank, P.ag_prim_c.off);
       qs = at<float>(ctx, ctx->rank, P.ag_prim_s.off);
     }
-    SyncArgs sq = make_sync(ctx, 0, phase - 1, phase, 0);
-    if (push_lim > 0) {
-      // hybrid push/pull: the quantize kernel (HBM-bound, NVLink idle) also stores
-      // the first push_lim codes of its piece into every member's receive buffer;
-      // the gather below pulls only the rest over NVLink
-      if ((rc = slot(ctx, P.ag_recv_c, code_bytes(D * plen, 8))) != HZ_OK) return rc;
-      if ((rc = slot(ctx, P.ag_recv_s, D * plen / B * 4)) != HZ_OK) return rc;
-      PushDst dst{};
-      int64_t pushed = 0;
-      for (int k = 0; k < D; ++k) {
-        if (members[k].second == ctx->rank) continue;
-        dst.c[dst.n] = at<uint8_t>(ctx, members[k].second, P.ag_recv_c.off) + code_bytes(me * plen, bits);
-        dst.s[dst.n] = at<float>(ctx, members[k].second, P.ag_recv_s.off) + me * plen / B;
-        ++dst.n;
-        pushed += code_bytes(push_lim, bits) + push_lim / B * 4;
-      }
-      dst.lim = push_lim;
-      if ((rc = run_quantize_push(primary, dt, plen, bits, qc, qs, nullptr, out_dt, dst, st, w, &sq, pushed)) !=
+    if (!pre) {
+      // A2: overwrites qc (read by the gather members of earlier calls) and, in this
+      // call, the secondary (read by the backward group)
+      Phases f;
+      f.wd = phase - 1;
+      f.wd_mask = readers_of(ctx, qc) | readers_of(ctx, sec_codes);
+      f.sr = phase;
+      f.sr_mask = gmask;
+      SyncArgs sq = make_sync(ctx, f);
+      if ((rc = synced(ctx, sq, st, [&] { return run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w, &sq); })) !=
           HZ_OK)
         return rc;
-    } else if (!pre && (rc = run_quantize(primary, dt, p->len[w], bits, B, qc, qs, st, w, &sq)) != HZ_OK) {
-      return rc;
     }
+    add_readers(ctx, qc, gmask);
+    add_readers(ctx, sec_codes, smask);
     if (s > w) {   // A4, s > w: the secondary is a sub-slice of the own quantized primary
       const int64_t rel = p->off[s] - p->off[w];
       if ((rc = copy_async(sec_codes, qc + code_bytes(rel, bits), code_bytes(len_s, bits), st)) != HZ_OK) return rc;
@@ -337,14 +298,8 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
     const int m = members[k].second;
     pc.c[k] = at<const uint8_t>(ctx, m, off_of(ctx, xc));
     pc.s[k] = at<const float>(ctx, m, off_of(ctx, xs));
-    if (m == ctx->rank) continue;
-    remote += code_bytes(plen - push_lim, bits) + (plen - push_lim) / B * 4;
-    if (push_lim > 0) {   // the pushed head of piece k is already in the local receive buffer
-      pc.cr[k] = at<const uint8_t>(ctx, ctx->rank, P.ag_recv_c.off) + code_bytes(k * plen, bits);
-      pc.sr[k] = at<const float>(ctx, ctx->rank, P.ag_recv_s.off) + k * plen / B;
-    }
+    if (m != ctx->rank) remote += code_bytes(plen, bits) + plen / B * 4;
   }
-  pc.split = push_lim;
   if (!backward && s < w) {   // A4, s < w: keep range_s of the gathered codes
     pc.sec_c = sec_codes;
     pc.sec_s = sec_scales;
@@ -354,104 +309,50 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   if (!backward && next && next->codes != sec_codes && next->scales != sec_scales &&
       p2p_next_fusable(ctx, p, bits, out_dt, *next)) {
     // gather this layer (phase) || quantize the next layer's primary (phase + 1) in one
-    // launch.  Waits: the members' codes of this phase are ready, and every rank is
-    // done with every phase before it (nobody still reads the next layer's secondary,
-    // last read in an earlier backward phase).  Signals done(phase), ready(phase + 1).
+    // launch.  Waits: the members' codes of this phase are ready, and the readers of
+    // the next layer's secondary (earlier calls) are done.  Signals done(phase) and
+    // ready(phase + 1) to the next layer's gather members.
     const unsigned long long nph = ++P.phase;
     const hz_partition_t* q = next->p;
-    SyncArgs sd = make_sync(ctx, phase, phase - 1, nph, phase);
-    if ((rc = run_gather_quantize(pc, Np, bits, full_out, out_dt, next->primary, dt, q->len[q->w], bits, next->codes,
-                                  next->scales, st, sd, remote)) != HZ_OK)
+    const unsigned nmask = mask_of(cumulative_members(q, q->w), ctx->rank);
+    Phases f;
+    f.wr = phase;
+    f.wr_mask = gmask;
+    f.wd = phase - 1;
+    f.wd_mask = readers_of(ctx, next->codes);
+    f.sd = phase;
+    f.sd_mask = P.nbr;
+    f.sr = nph;
+    f.sr_mask = nmask;
+    SyncArgs sd = make_sync(ctx, f);
+    if ((rc = synced(ctx, sd, st, [&] {
+           return run_gather_quantize(pc, Np, bits, full_out, out_dt, next->primary, dt, q->len[q->w], bits,
+                                      next->codes, next->scales, st, sd, remote);
+         })) != HZ_OK)
       return rc;
     P.pre_phase = nph;
     P.pre_codes = next->codes;
     P.pre_primary = next->primary;
+    P.pre_bits = bits;
+    P.pre_dt = dt;
+    P.pre_len = q->len[q->w];
     clear_error();
     return HZ_OK;
   }
-  SyncArgs sd = backward ? make_sync(ctx, 0, phase - 1, 0, phase) : make_sync(ctx, phase, 0, 0, phase);
-  if ((rc = run_gather_dequantize(pc, Np, bits, B, full_out, out_dt, st, 0, &sd, remote)) != HZ_OK)
+  Phases f;
+  if (backward) {   // secondaries written in earlier phases: the members finished them
+    f.wd = phase - 1;
+    f.wd_mask = gmask;
+  } else {
+    f.wr = phase;
+    f.wr_mask = gmask;
+  }
+  f.sd = phase;
+  f.sd_mask = P.nbr;
+  SyncArgs sd = make_sync(ctx, f);
+  if ((rc = synced(ctx, sd, st, [&] { return run_gather_dequantize(pc, Np, bits, B, full_out, out_dt, st, 0, &sd, remote); })) !=
+      HZ_OK)
     return rc;
-  clear_error();
-  return HZ_OK;
-}
-
-// qgZ over NVLink, push mode: every producer (the level-`from` quantize, each
-// level's requantizing reduce) stores the chunk destined to member j straight into
-// member j's level receive buffer, at the producer's own digit; every reduce then
-// reads its g inputs from local HBM (ascending digit = the oracle's summation order).
-hz_status p2p_reduce_scatter_push(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
-                                  int from_level, int to_level, const int* bits_per_level, float* shard,
-                                  int accumulate, cudaStream_t st) {
-  auto& P = ctx->p2p;
-  const int B = p->block;
-  hz_status rc;
-  for (int l = from_level; l <= to_level; ++l) {   // level-l receive buffers (8-bit capacity)
-    if ((rc = slot(ctx, P.rs_recv_c[l], code_bytes(p->len[l - 1], 8))) != HZ_OK) return rc;
-    if ((rc = slot(ctx, P.rs_recv_s[l], p->len[l - 1] / B * 4)) != HZ_OK) return rc;
-  }
-  int64_t stride[HZ_MAX_LEVELS];
-  int64_t sacc = 1;
-  for (int l = 0; l < p->levels; ++l) {
-    stride[l] = sacc;
-    sacc *= p->group[l];
-  }
-  // destinations of level l's chunks: member j gets chunk j at this rank's digit
-  auto dest_of = [&](int l, int bits, PushDst& dst, int64_t& remote) {
-    const int g = p->group[l - 1];
-    const int d = p->digit[l - 1];
-    const int64_t cl = p->len[l];
-    dst = PushDst{};
-    dst.n = g;
-    dst.scatter = 1;
-    dst.seg = cl;
-    remote = 0;
-    for (int j = 0; j < g; ++j) {
-      const int m = static_cast<int>(p->rank + (static_cast<int64_t>(j) - d) * stride[l - 1]);
-      dst.c[j] = at<uint8_t>(ctx, m, P.rs_recv_c[l].off) + code_bytes(d * cl, bits);
-      dst.s[j] = at<float>(ctx, m, P.rs_recv_s[l].off) + d * cl / B;
-      if (m != ctx->rank) remote += code_bytes(cl, bits) + cl / B * 4;
-    }
-  };
-  const unsigned long long base = P.phase;
-  P.phase += static_cast<unsigned long long>(to_level - from_level + 1);
-  auto phase_of = [&](int l) { return base + static_cast<unsigned long long>(l - from_level + 1); };
-  {   // A7 + A8: quantize range_{from-1} and push chunk j to member j
-    const int l = from_level;
-    PushDst dst;
-    int64_t remote;
-    dest_of(l, bits_per_level[l - 1], dst, remote);
-    const unsigned long long ph = phase_of(l);
-    SyncArgs sq = make_sync(ctx, 0, ph - 1, ph, 0);
-    if ((rc = run_quantize_push(grad, dt, p->len[l - 1], bits_per_level[l - 1], nullptr, nullptr, nullptr, HZ_F32, dst,
-                                st, l, &sq, remote)) != HZ_OK)
-      return rc;
-  }
-  for (int l = from_level; l <= to_level; ++l) {   // A9 (+ A8 of the next level) / A10
-    const int g = p->group[l - 1];
-    const int bits = bits_per_level[l - 1];
-    const int64_t cl = p->len[l];
-    const uint8_t* ptr_c[kMaxG];
-    const float* ptr_s[kMaxG];
-    for (int j = 0; j < g; ++j) {
-      ptr_c[j] = at<const uint8_t>(ctx, ctx->rank, P.rs_recv_c[l].off) + code_bytes(j * cl, bits);
-      ptr_s[j] = at<const float>(ctx, ctx->rank, P.rs_recv_s[l].off) + j * cl / B;
-    }
-    const unsigned long long ph = phase_of(l);
-    if (l < to_level) {
-      PushDst dst;
-      int64_t remote;
-      dest_of(l + 1, bits_per_level[l], dst, remote);
-      SyncArgs sr = make_sync(ctx, ph, ph - 1, ph + 1, ph);
-      if ((rc = run_reduce_push(g, ptr_c, ptr_s, cl, bits, bits_per_level[l], dst, st, l, &sr, remote)) != HZ_OK)
-        return rc;
-    } else {
-      SyncArgs sr = make_sync(ctx, ph, 0, 0, ph);
-      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st, l, &sr, 0)) !=
-          HZ_OK)
-        return rc;
-    }
-  }
   clear_error();
   return HZ_OK;
 }
@@ -461,9 +362,8 @@ bool p2p_prev_fusable(const hz_ctx* ctx, const hz_partition_t* p, int from_level
   return ctx->p2p.on && q && p->block == 256 && q->block == 256 && p->len[from_level - 1] > 0 &&
          gather_quantize_supported(256, pg.bits, pg.out_dt) &&
          in_pool(ctx, pg.sec_codes, code_bytes(q->len[q->s], pg.bits)) &&
-         in_pool(ctx, pg.sec_scales, q->len[q->s] / 256 * 4) && static_cast<int>(cumulative_members(q, q->s).size()) <=
-                                                                   kMaxWorld &&
-         tune_param("rspush", 0) == 0 && tune_param("fused", 0) == 0 && tune_param("nofuse", 0) == 0;
+         in_pool(ctx, pg.sec_scales, q->len[q->s] / 256 * 4) &&
+         static_cast<int>(cumulative_members(q, q->s).size()) <= kMaxWorld && tune_param("nofuse", 0) == 0;
 }
 
 hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
@@ -472,16 +372,36 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
   auto& P = ctx->p2p;
   const int B = p->block;
   hz_status rc;
+  std::vector<Hop> hops;
+  if ((rc = hops_of(p, from_level, to_level, &hops)) != HZ_OK) return rc;
+  const int H = static_cast<int>(hops.size());
+  // members of every hop (ascending rank), the offset of each member's chunk in the
+  // hop's input range, and this rank's index
+  std::vector<std::vector<int>> hr(H);
+  std::vector<std::vector<int64_t>> hrel(H);
+  std::vector<int> hme(H, 0);
+  std::vector<unsigned> hmask(H, 0u);
+  for (int h = 0; h < H; ++h) {
+    hop_members(p, hops[h].a, hops[h].b, &hr[h], &hrel[h], &hme[h]);
+    if (static_cast<int>(hr[h].size()) > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "more than 16 ranks in one qgZ hop");
+    hmask[h] = mask_of(hr[h], ctx->rank);
+  }
   if ((rc = flush_prefetch(ctx, st)) != HZ_OK) return rc;
+  for (const Hop& h : hops) {   // hop send buffers (8-bit capacity), indexed by the first level
+    if ((rc = slot(ctx, P.rs_c[h.a], code_bytes(p->len[h.a - 1], 8))) != HZ_OK) return rc;
+    if ((rc = slot(ctx, P.rs_s[h.a], p->len[h.a - 1] / B * 4)) != HZ_OK) return rc;
+  }
   // the previous layer's backward gather (phase gph) fused into this call's first
   // quantize (hz_backward_step; the caller checked p2p_prev_fusable)
   unsigned long long gph = 0;
   Pieces gpc{};
   int64_t gremote = 0;
+  unsigned pmask = 0;
   if (prev) {
     gph = ++P.phase;
     const hz_partition_t* q = prev->p;
     const auto members = cumulative_members(q, q->s);
+    pmask = mask_of(members, ctx->rank);
     gpc.n = static_cast<int>(members.size());
     gpc.len = q->len[q->s];
     for (int k = 0; k < gpc.n; ++k) {
@@ -491,125 +411,87 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
       if (m != ctx->rank) gremote += code_bytes(gpc.len, prev->bits) + gpc.len / 256 * 4;
     }
   }
-  // full push for qgZ measured slower than pull on B200: HZ_TUNE rspush=1
-  bool push = B == 256 && tune_param("rspush", 0) && !tune_param("fused", 0);
-  for (int l = from_level; l < to_level; ++l) push = push && push_reduce_supported(p->group[l - 1], B);
-  for (int l = from_level; l <= to_level; ++l)
-    if (p->group[l - 1] > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "group size > 16 at one level");
-  if (push) return p2p_reduce_scatter_push(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard, accumulate,
-                                           st);
-  for (int l = from_level; l <= to_level; ++l) {   // level-l send buffers (8-bit capacity)
-    if ((rc = slot(ctx, P.rs_c[l], code_bytes(p->len[l - 1], 8))) != HZ_OK) return rc;
-    if ((rc = slot(ctx, P.rs_s[l], p->len[l - 1] / B * 4)) != HZ_OK) return rc;
-  }
-  int64_t stride[HZ_MAX_LEVELS];
-  int64_t sacc = 1;
-  for (int l = 0; l < p->levels; ++l) {
-    stride[l] = sacc;
-    sacc *= p->group[l];
-  }
   const unsigned long long base = P.phase;
-  P.phase += static_cast<unsigned long long>(to_level - from_level + 1);
-  auto phase_of = [&](int l) { return base + static_cast<unsigned long long>(l - from_level + 1); };
+  P.phase += static_cast<unsigned long long>(H);
+  auto phase_of = [&](int h) { return base + static_cast<unsigned long long>(h + 1); };
+  for (int h = 0; h < H; ++h) P.nbr |= hmask[h];
+  P.nbr |= pmask;
 
-  int first = from_level;   // first level handled by the per-level kernels below
-  if (B == 256 && fused_rs_supported(p->group[from_level - 1]) && tune_param("fused", 0)) {
-    // A7 + A8 + A9 of the first level in ONE kernel: quantize the own input chunk by
-    // chunk (destinations interleaved), publish each chunk to its destination, and
-    // reduce the members' chunks destined here as they become ready.
-    const int l = from_level;
-    const int g = p->group[l - 1];
-    const int d = p->digit[l - 1];
-    const int bits = bits_per_level[l - 1];
-    const int64_t cl = p->len[l];
-    const unsigned long long ph = phase_of(l);
-    FusedRSArgs h{};
-    h.x = grad;
-    h.dt = dt;
-    h.bits_in = bits;
-    h.bits_out = l < to_level ? bits_per_level[l] : 0;
-    h.acc = l < to_level ? 0 : accumulate;
-    h.qc = at<uint8_t>(ctx, ctx->rank, P.rs_c[l].off);
-    h.qs = at<float>(ctx, ctx->rank, P.rs_s[l].off);
-    h.g = g;
-    h.d = d;
-    h.cl = cl;
-    h.C = chunk_elems(cl);
-    h.ncl = static_cast<int>((cl + h.C - 1) / h.C);
-    for (int j = 0; j < g; ++j) {
-      const int m = static_cast<int>(p->rank + (static_cast<int64_t>(j) - d) * stride[l - 1]);
-      h.mc[j] = at<const uint8_t>(ctx, m, P.rs_c[l].off) + code_bytes(d * cl, bits);
-      h.ms[j] = at<const float>(ctx, m, P.rs_s[l].off) + d * cl / B;
-      h.flags_remote[j] = at<unsigned long long>(ctx, m, kChunkRSOff) + d * kMaxChunks;
-    }
-    h.flags = at<unsigned long long>(ctx, ctx->rank, kChunkRSOff);
-    h.work = at<unsigned long long>(ctx, ctx->rank, kWorkRSOff);
-    h.cnt = at<unsigned int>(ctx, ctx->rank, kCntRSOff);
-    h.of = shard;
-    if (l < to_level) {
-      h.oc = at<uint8_t>(ctx, ctx->rank, P.rs_c[l + 1].off);
-      h.os = at<float>(ctx, ctx->rank, P.rs_s[l + 1].off);
-    }
-    h.phase = ph - P.epoch_host;
-    h.epoch = at<const unsigned long long>(ctx, ctx->rank, kEpochOff);
-    SyncArgs sy = l < to_level ? make_sync(ctx, 0, ph - 1, ph + 1, ph) : make_sync(ctx, 0, ph - 1, 0, ph);
-    const int64_t n_in = p->len[l - 1];
-    const int64_t remote = (g - 1) * (code_bytes(cl, bits) + cl / B * 4);
-    const int64_t out = h.bits_out ? code_bytes(cl, h.bits_out) + cl / B * 4 : cl * 4 * (h.acc ? 2 : 1);
-    const int64_t local = n_in * elem_bytes(dt) + code_bytes(n_in, bits) + n_in / B * 4 +
-                          g * (code_bytes(cl, bits) + cl / B * 4) - remote + out;
-    TraceScope t(st, "rs_fused", l, bits, n_in, local, remote);
-    sy.stamps = t.stamps;
-    cudaError_t e = launch_rs_fused(h, st, sy);
-    t.end();
-    if (e != cudaSuccess) return cuda_fail(e, "fused reduce-scatter kernel launch");
-    first = l + 1;
-  } else if (prev) {
+  uint8_t* c0 = at<uint8_t>(ctx, ctx->rank, P.rs_c[hops[0].a].off);
+  float* s0 = at<float>(ctx, ctx->rank, P.rs_s[hops[0].a].off);
+  const unsigned rb0 = readers_of(ctx, c0);
+  add_readers(ctx, c0, hmask[0]);
+  if (prev) {
     // previous layer's backward gather (phase gph) || A7 of this layer (phase gph + 1):
-    // waits until every rank is done with every phase before gph (the secondaries
-    // are complete, nobody reads the send buffer any more); signals done(gph) and
-    // ready(gph + 1) for the level-`from` reduce below
-    const unsigned long long ph = phase_of(from_level);
-    SyncArgs sq = make_sync(ctx, 0, gph - 1, ph, gph);
-    if ((rc = run_gather_quantize(gpc, prev->p->padded_numel, prev->bits, prev->full_out, prev->out_dt, grad, dt,
-                                  p->len[from_level - 1], bits_per_level[from_level - 1],
-                                  at<uint8_t>(ctx, ctx->rank, P.rs_c[from_level].off),
-                                  at<float>(ctx, ctx->rank, P.rs_s[from_level].off), st, sq, gremote)) != HZ_OK)
+    // the previous layer's members finished every earlier phase (their secondaries are
+    // complete) and the readers of the send buffer are done; signals done(gph) and
+    // ready(gph + 1) to the first hop
+    Phases f;
+    f.wd = gph - 1;
+    f.wd_mask = pmask | rb0;
+    f.sd = gph;
+    f.sd_mask = P.nbr;
+    f.sr = phase_of(0);
+    f.sr_mask = hmask[0];
+    SyncArgs sq = make_sync(ctx, f);
+    if ((rc = synced(ctx, sq, st, [&] {
+           return run_gather_quantize(gpc, prev->p->padded_numel, prev->bits, prev->full_out, prev->out_dt, grad, dt,
+                                      p->len[from_level - 1], bits_per_level[from_level - 1], c0, s0, st, sq, gremote);
+         })) != HZ_OK)
       return rc;
   } else {
-    // A7: quantize the input range_{from-1} into this rank's level-`from` send buffer
-    const unsigned long long ph = phase_of(from_level);
-    SyncArgs sq = make_sync(ctx, 0, ph - 1, ph, 0);
-    if ((rc = run_quantize(grad, dt, p->len[from_level - 1], bits_per_level[from_level - 1], B,
-                           at<uint8_t>(ctx, ctx->rank, P.rs_c[from_level].off),
-                           at<float>(ctx, ctx->rank, P.rs_s[from_level].off), st, from_level, &sq)) != HZ_OK)
+    // A7: quantize the input range_{from-1} into this rank's first send buffer
+    Phases f;
+    f.wd = phase_of(0) - 1;
+    f.wd_mask = rb0;
+    f.sr = phase_of(0);
+    f.sr_mask = hmask[0];
+    SyncArgs sq = make_sync(ctx, f);
+    if ((rc = synced(ctx, sq, st, [&] {
+           return run_quantize(grad, dt, p->len[from_level - 1], bits_per_level[from_level - 1], B, c0, s0, st,
+                               from_level, &sq);
+         })) != HZ_OK)
       return rc;
   }
-  for (int l = first; l <= to_level; ++l) {
-    const int g = p->group[l - 1];
-    const int d = p->digit[l - 1];
-    const int bits = bits_per_level[l - 1];
-    const int64_t cl = p->len[l];
-    if (g > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "group size > 16 at one level");
+  for (int h = 0; h < H; ++h) {
+    const Hop& hp = hops[h];
+    const int g = static_cast<int>(hr[h].size());
+    const int bits = bits_per_level[hp.a - 1];
+    const int64_t cl = p->len[hp.b];
+    const int64_t my_rel = hrel[h][hme[h]];   // where this rank's chunk lies in every member's buffer
     const uint8_t* ptr_c[kMaxG];
     const float* ptr_s[kMaxG];
-    for (int j = 0; j < g; ++j) {   // A8+A9: chunk d of member j's send buffer, over NVLink
-      const int m = static_cast<int>(p->rank + (static_cast<int64_t>(j) - d) * stride[l - 1]);
-      ptr_c[j] = at<const uint8_t>(ctx, m, P.rs_c[l].off) + code_bytes(d * cl, bits);
-      ptr_s[j] = at<const float>(ctx, m, P.rs_s[l].off) + d * cl / B;
+    for (int j = 0; j < g; ++j) {   // A8+A9: this rank's chunk of member j's send buffer, over NVLink
+      ptr_c[j] = at<const uint8_t>(ctx, hr[h][j], P.rs_c[hp.a].off) + code_bytes(my_rel, bits);
+      ptr_s[j] = at<const float>(ctx, hr[h][j], P.rs_s[hp.a].off) + my_rel / B;
     }
-    const unsigned long long ph = phase_of(l);
+    const unsigned long long ph = phase_of(h);
     const int64_t remote = (g - 1) * (code_bytes(cl, bits) + cl / B * 4);
-    if (l < to_level) {
-      SyncArgs sr = make_sync(ctx, ph, ph - 1, ph + 1, ph);
-      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, bits_per_level[l],
-                           at<uint8_t>(ctx, ctx->rank, P.rs_c[l + 1].off),
-                           at<float>(ctx, ctx->rank, P.rs_s[l + 1].off), nullptr, 0, st, l, &sr, remote)) != HZ_OK)
+    Phases f;
+    f.wr = ph;
+    f.wr_mask = hmask[h];
+    f.sd = ph;
+    f.sd_mask = P.nbr;
+    if (h + 1 < H) {
+      uint8_t* oc = at<uint8_t>(ctx, ctx->rank, P.rs_c[hops[h + 1].a].off);
+      float* os = at<float>(ctx, ctx->rank, P.rs_s[hops[h + 1].a].off);
+      f.wd = ph - 1;
+      f.wd_mask = readers_of(ctx, oc);
+      add_readers(ctx, oc, hmask[h + 1]);
+      f.sr = ph + 1;
+      f.sr_mask = hmask[h + 1];
+      SyncArgs sr = make_sync(ctx, f);
+      if ((rc = synced(ctx, sr, st, [&] {
+             return run_reduce(g, ptr_c, ptr_s, cl, bits, B, bits_per_level[hops[h + 1].a - 1], oc, os, nullptr, 0, st,
+                               hp.b, &sr, remote);
+           })) != HZ_OK)
         return rc;
     } else {
-      SyncArgs sr = make_sync(ctx, ph, 0, 0, ph);
-      if ((rc = run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st, l, &sr, remote)) !=
-          HZ_OK)
+      SyncArgs sr = make_sync(ctx, f);
+      if ((rc = synced(ctx, sr, st, [&] {
+             return run_reduce(g, ptr_c, ptr_s, cl, bits, B, 0, nullptr, nullptr, shard, accumulate, st, hp.b, &sr,
+                               remote);
+           })) != HZ_OK)
         return rc;
     }
   }
@@ -630,44 +512,61 @@ hz_status p2p_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const float
   const int64_t sel = p->off[to_level] - p->off[from_level - 1];
   if ((rc = slot(ctx, P.ar_a, n * 4)) != HZ_OK) return rc;
   if ((rc = slot(ctx, P.ar_b, n * 4)) != HZ_OK) return rc;
-  int64_t stride[HZ_MAX_LEVELS];
-  int64_t sacc = 1;
-  for (int l = 0; l < p->levels; ++l) {
-    stride[l] = sacc;
-    sacc *= p->group[l];
+  std::vector<unsigned> lmask(HZ_MAX_LEVELS + 2, 0u);
+  std::vector<std::vector<int>> lr(HZ_MAX_LEVELS + 2);
+  for (int l = from_level; l <= to_level; ++l) {
+    std::vector<int64_t> rel;
+    hop_members(p, l, l, &lr[l], &rel, nullptr);
+    lmask[l] = mask_of(lr[l], ctx->rank);
+    P.nbr |= lmask[l];
   }
   const size_t off[2] = {P.ar_a.off, P.ar_b.off};
   const unsigned long long base = P.phase;
   P.phase += static_cast<unsigned long long>(to_level - from_level + 1);
-  // copy-in (producer of phase base+1): the slot may still be read in phase base
-  {
+  {   // copy-in (producer of phase base+1)
     Pieces pc{};
     pc.n = 1;
     pc.len = n;
     pc.c[0] = reinterpret_cast<const uint8_t*>(in);
-    SyncArgs sq = make_sync(ctx, 0, base, base + 1, 0);
-    if ((rc = run_sum(pc, n, at<float>(ctx, ctx->rank, off[0]), st, from_level, &sq, 0)) != HZ_OK) return rc;
+    float* dst = at<float>(ctx, ctx->rank, off[0]);
+    Phases f;
+    f.wd = base;
+    f.wd_mask = readers_of(ctx, dst);
+    f.sr = base + 1;
+    f.sr_mask = lmask[from_level];
+    SyncArgs sq = make_sync(ctx, f);
+    if ((rc = synced(ctx, sq, st, [&] { return run_sum(pc, n, dst, st, from_level, &sq, 0); })) != HZ_OK) return rc;
   }
   int cur = 0;
   for (int l = from_level; l <= to_level; ++l) {
-    const int g = p->group[l - 1];
-    const int d = p->digit[l - 1];
+    const int g = static_cast<int>(lr[l].size());
     const unsigned long long ph = base + static_cast<unsigned long long>(l - from_level + 1);
     Pieces pc{};
     pc.n = g;
     pc.len = n;
     int64_t remote = 0;
     for (int j = 0; j < g; ++j) {
-      const int m = static_cast<int>(p->rank + (static_cast<int64_t>(j) - d) * stride[l - 1]);
-      pc.c[j] = at<const uint8_t>(ctx, m, off[cur]);
-      if (m != ctx->rank) remote += n * 4;
+      pc.c[j] = at<const uint8_t>(ctx, lr[l][j], off[cur]);
+      if (lr[l][j] != ctx->rank) remote += n * 4;
     }
-    SyncArgs sr = l < to_level ? make_sync(ctx, ph, ph - 1, ph + 1, ph) : make_sync(ctx, ph, ph - 1, 0, ph);
-    if ((rc = run_sum(pc, n, at<float>(ctx, ctx->rank, off[cur ^ 1]), st, l, &sr, remote)) != HZ_OK) return rc;
+    float* dst = at<float>(ctx, ctx->rank, off[cur ^ 1]);
+    Phases f;
+    f.wr = ph;
+    f.wr_mask = lmask[l];
+    f.wd = ph - 1;
+    f.wd_mask = readers_of(ctx, dst);
+    add_readers(ctx, at<float>(ctx, ctx->rank, off[cur]), lmask[l]);
+    f.sd = ph;
+    f.sd_mask = P.nbr;
+    if (l < to_level) {
+      f.sr = ph + 1;
+      f.sr_mask = lmask[l + 1];
+    }
+    SyncArgs sr = make_sync(ctx, f);
+    if ((rc = synced(ctx, sr, st, [&] { return run_sum(pc, n, dst, st, l, &sr, remote); })) != HZ_OK) return rc;
     cur ^= 1;
   }
-  // select range_to (local; the slot's next writer waits for this rank's done flag,
-  // which follows this copy in stream order)
+  // select range_to (local; the slot's next writer waits for this rank's readers)
   if ((rc = copy_async(out, at<float>(ctx, ctx->rank, off[cur]) + sel, static_cast<size_t>(p->len[to_level]) * 4,
                        st)) != HZ_OK)
     return rc;
@@ -687,68 +586,93 @@ hz_status p2p_adamw_gather(hz_ctx* ctx, const hz_partition_t* p, const float* g,
   hz_status rc;
   if ((rc = flush_prefetch(ctx, st)) != HZ_OK) return rc;
   if ((rc = slot(ctx, P.upd, lenL * 4)) != HZ_OK) return rc;   // fp32 capacity
-  const unsigned long long phase = ++P.phase;
-  char* mine = at<char>(ctx, ctx->rank, P.upd.off);
-  SyncArgs sq = make_sync(ctx, 0, phase - 1, phase, 0);
-  if ((rc = run_adamw(g, th, m, v, mine, dt, lenL, hp, st, &sq)) != HZ_OK) return rc;
-  // members: vary digits w+1..L, keep digits 1..w
-  int64_t stride[HZ_MAX_LEVELS];
-  int64_t sacc = 1;
-  for (int l = 0; l < L; ++l) {
-    stride[l] = sacc;
-    sacc *= p->group[l];
-  }
-  int64_t base = p->rank, D = 1;
-  for (int l = w; l < L; ++l) {
-    base -= p->digit[l] * stride[l];
-    D *= p->group[l];
-  }
-  if (D > kMaxWorld) return fail(HZ_ERR_UNSUPPORTED, "P2P gather over more than 8 ranks");
+  // members: vary digits w+1..L, keep digits 1..w; piece order = offset in range_w
+  std::vector<int> hr;
+  std::vector<int64_t> rel;
   std::vector<std::pair<int64_t, int>> mem;
-  for (int64_t idx = 0; idx < D; ++idx) {
-    int64_t rem = idx, r = base, off = 0;
-    for (int l = w; l < L; ++l) {
-      const int d = static_cast<int>(rem % p->group[l]);
-      rem /= p->group[l];
-      r += d * stride[l];
-      off += d * p->len[l + 1];
-    }
-    mem.emplace_back(off, static_cast<int>(r));
+  if (w < L) {
+    hop_members(p, w + 1, L, &hr, &rel, nullptr);
+    for (size_t k = 0; k < hr.size(); ++k) mem.emplace_back(rel[k], hr[k]);
+    std::sort(mem.begin(), mem.end());
+  } else {
+    mem.emplace_back(0, ctx->rank);
   }
-  std::sort(mem.begin(), mem.end());
+  std::vector<int> ranks;
+  for (const auto& x : mem) ranks.push_back(x.second);
+  const int D = static_cast<int>(ranks.size());
+  if (D > kMaxWorld) return fail(HZ_ERR_UNSUPPORTED, "P2P gather over more than 8 ranks");
+  const unsigned mmask = mask_of(ranks, ctx->rank);
+  const unsigned long long phase = ++P.phase;
+  P.nbr |= mmask;
+  char* mine = at<char>(ctx, ctx->rank, P.upd.off);
+  {
+    Phases f;
+    f.wd = phase - 1;
+    f.wd_mask = readers_of(ctx, mine);
+    f.sr = phase;
+    f.sr_mask = mmask;
+    SyncArgs sq = make_sync(ctx, f);
+    if ((rc = synced(ctx, sq, st, [&] { return run_adamw(g, th, m, v, mine, dt, lenL, hp, st, &sq); })) != HZ_OK)
+      return rc;
+  }
+  add_readers(ctx, mine, mmask);
   Pieces pc{};
-  pc.n = static_cast<int>(D);
+  pc.n = D;
   pc.len = lenL * eb;   // bytes
   int64_t remote = 0;
-  for (int k = 0; k < pc.n; ++k) {
-    pc.c[k] = at<const uint8_t>(ctx, mem[k].second, P.upd.off);
-    if (mem[k].second != ctx->rank) remote += pc.len;
+  for (int k = 0; k < D; ++k) {
+    pc.c[k] = at<const uint8_t>(ctx, ranks[k], P.upd.off);
+    if (ranks[k] != ctx->rank) remote += pc.len;
   }
-  SyncArgs sd = make_sync(ctx, phase, 0, 0, phase);
-  TraceScope t(st, "gather_copy", w, 16, lenL * D, D * pc.len * 2 - remote, remote);
-  sd.stamps = t.stamps;
-  cudaError_t e = launch_gather_copy(pc, primary, st, &sd);
-  t.end();
-  if (e != cudaSuccess) return cuda_fail(e, "post-update gather kernel launch");
-  clear_error();
-  return HZ_OK;
+  Phases f;
+  f.wr = phase;
+  f.wr_mask = mmask;
+  f.sd = phase;
+  f.sd_mask = P.nbr;
+  SyncArgs sd = make_sync(ctx, f);
+  return synced(ctx, sd, st, [&]() -> hz_status {
+    TraceScope t(st, "gather_copy", w, 16, lenL * D, D * pc.len * 2 - remote, remote);
+    SyncArgs s2 = sd;
+    s2.stamps = t.stamps;
+    cudaError_t e = launch_gather_copy(pc, primary, st, &s2);
+    t.end();
+    if (e != cudaSuccess) return cuda_fail(e, "post-update gather kernel launch");
+    clear_error();
+    return HZ_OK;
+  });
 }
 
 void p2p_release(hz_ctx* ctx) {
   auto& P = ctx->p2p;
-  if (!P.pool) return;
-  // every rank must be done with every peer's pool before anyone unmaps / frees
-  int* flag = nullptr;
-  if (cudaMalloc(&flag, sizeof(int)) == cudaSuccess) {
-    ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, ctx->world_comm, nullptr);
-    cudaStreamSynchronize(nullptr);
-    cudaFree(flag);
+  if (P.vw) {   // virtual world: pools are freed with the last context
+    vw_release(ctx);
+  } else if (P.pool) {
+    // every rank must be done with every peer's pool before anyone unmaps / frees
+    int* flag = nullptr;
+    if (ctx->world_comm && cudaMalloc(&flag, sizeof(int)) == cudaSuccess) {
+      ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, ctx->world_comm, nullptr);
+      cudaStreamSynchronize(nullptr);
+      cudaFree(flag);
+    }
+    for (int q = 0; q < ctx->world; ++q)
+      if (q != ctx->rank && P.peer[q]) cudaIpcCloseMemHandle(P.peer[q]);
+    cudaFree(P.pool);
   }
-  for (int q = 0; q < ctx->world; ++q)
-    if (q != ctx->rank && P.peer[q]) cudaIpcCloseMemHandle(P.peer[q]);
-  cudaFree(P.pool);
+  if (P.abort_host) cudaFreeHost(P.abort_host);
   cudaGetLastError();
   P = hz_ctx::P2P{};
+}
+
+hz_status p2p_alloc_abort(hz_ctx* ctx) {
+  auto& P = ctx->p2p;
+  void* h = nullptr;
+  P2P_CUDA(cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable), "abort word cudaHostAlloc");
+  std::memset(h, 0, 64);
+  void* d = nullptr;
+  P2P_CUDA(cudaHostGetDevicePointer(&d, h, 0), "abort word cudaHostGetDevicePointer");
+  P.abort_host = static_cast<unsigned*>(h);
+  P.abort_dev = static_cast<unsigned*>(d);
+  return HZ_OK;
 }
 
 }  // namespace hz
@@ -763,6 +687,8 @@ hz_status hz_enable_p2p(hz_ctx* ctx, size_t pool_bytes) {
   auto& P = ctx->p2p;
   const size_t total = align_up(kPoolHeader + pool_bytes, size_t(2) << 20);
   P2P_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  hz_status rc = p2p_alloc_abort(ctx);
+  if (rc != HZ_OK) return rc;
   P2P_CUDA(cudaMalloc(&P.pool, total), "P2P pool cudaMalloc");
   P.bytes = total;
   P.used = kPoolHeader;
@@ -812,10 +738,40 @@ hz_status hz_p2p_enabled(const hz_ctx* ctx, int* out) {
   return HZ_OK;
 }
 
+hz_status hz_set_wait_timeout(hz_ctx* ctx, double seconds) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  if (!(seconds > 0.0) || seconds > 1e7) return fail(HZ_ERR_INVALID, "seconds: must be in (0, 1e7]");
+  ctx->p2p.timeout_ns = static_cast<unsigned long long>(seconds * 1e9);
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_abort(hz_ctx* ctx) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  if (ctx->p2p.abort_host) *reinterpret_cast<volatile unsigned*>(ctx->p2p.abort_host) = 2u;
+  if (ctx->p2p.vw) vw_abort(ctx);
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_check(const hz_ctx* ctx) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  hz_status rc = p2p_check(ctx);
+  if (rc != HZ_OK) return rc;
+  rc = check_async(ctx);
+  if (rc != HZ_OK) return rc;
+  clear_error();
+  return HZ_OK;
+}
+
 hz_status hz_p2p_capture_begin(hz_ctx* ctx) {
   using namespace hz;
   if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
   if (!ctx->p2p.on) return fail(HZ_ERR_INVALID, "ctx: P2P not enabled");
+  if (ctx->p2p.vw) return fail(HZ_ERR_UNSUPPORTED, "ctx: graph capture is not supported in a virtual world");
   if (ctx->p2p.capturing) return fail(HZ_ERR_INVALID, "ctx: capture already begun");
   if (ctx->p2p.pre_phase)
     return fail(HZ_ERR_INVALID, "ctx: a prefetched quantize (hz_allgather_params_next) is pending; gather that "

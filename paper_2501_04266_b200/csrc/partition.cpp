@@ -10,6 +10,7 @@
 // consecutive pieces of its common range_{l-1} in ascending digit order, so
 // every all-gather output and every reduce-scatter chunk is contiguous.
 #include <string>
+#include <vector>
 
 #include "hz_internal.h"
 
@@ -64,4 +65,82 @@ hz_status partition(int rank, int levels, const int* group, int64_t numel, int b
   return HZ_OK;
 }
 
+// qgZ hop grouping (R15): the hops of p inside levels from..to.
+hz_status hops_of(const hz_partition_t* p, int from_level, int to_level, std::vector<Hop>* out) {
+  out->clear();
+  if (p->nhops <= 0) {
+    for (int l = from_level; l <= to_level; ++l) out->push_back(Hop{l, l});
+    return HZ_OK;
+  }
+  int a = 1;
+  for (int k = 0; k < p->nhops; ++k) {
+    const int b = p->hop_last[k];
+    if (a >= from_level && b <= to_level) {
+      out->push_back(Hop{a, b});
+    } else if ((a < from_level && b >= from_level) || (a <= to_level && b > to_level)) {
+      return fail(HZ_ERR_INVALID, "from_level/to_level: must fall on hop boundaries of p (hop levels " +
+                                      std::to_string(a) + ".." + std::to_string(b) + ")");
+    }
+    a = b + 1;
+  }
+  return HZ_OK;
+}
+
+// Members of p's rank in the hop over levels a..b, ascending rank (= ascending merged
+// digit j = sum_{l=a..b} d_l * prod_{k=a}^{l-1} g_k), with rel = off_b(member) -
+// off_{a-1}: where the member's chunk lies in range_{a-1}.
+void hop_members(const hz_partition_t* p, int a, int b, std::vector<int>* ranks, std::vector<int64_t>* rel,
+                 int* me) {
+  int64_t stride[HZ_MAX_LEVELS];
+  int64_t st = 1;
+  for (int l = 0; l < p->levels; ++l) {
+    stride[l] = st;
+    st *= p->group[l];
+  }
+  int64_t base = p->rank;
+  int64_t G = 1;
+  for (int l = a; l <= b; ++l) {
+    base -= p->digit[l - 1] * stride[l - 1];
+    G *= p->group[l - 1];
+  }
+  ranks->clear();
+  rel->clear();
+  for (int64_t j = 0; j < G; ++j) {
+    int64_t rem = j, r = base, off = 0;
+    for (int l = a; l <= b; ++l) {
+      const int64_t d = rem % p->group[l - 1];
+      rem /= p->group[l - 1];
+      r += d * stride[l - 1];
+      off += d * p->len[l];
+    }
+    if (r == p->rank && me) *me = static_cast<int>(j);
+    ranks->push_back(static_cast<int>(r));
+    rel->push_back(off);
+  }
+}
+
 }  // namespace hz
+
+extern "C" hz_status hz_partition_set_hops(hz_partition_t* p, int nhops, const int* hop_last) {
+  using namespace hz;
+  if (!p) return fail(HZ_ERR_INVALID, "p: NULL");
+  if (nhops == 0) {
+    p->nhops = 0;
+    for (int k = 0; k < HZ_MAX_LEVELS; ++k) p->hop_last[k] = 0;
+    clear_error();
+    return HZ_OK;
+  }
+  if (nhops < 0 || nhops > p->levels) return fail(HZ_ERR_INVALID, "nhops: must be in [0, levels]");
+  if (!hop_last) return fail(HZ_ERR_INVALID, "hop_last: NULL");
+  int prev = 0;
+  for (int k = 0; k < nhops; ++k) {
+    if (hop_last[k] <= prev || hop_last[k] > p->levels)
+      return fail(HZ_ERR_INVALID, "hop_last[" + std::to_string(k) + "]: must be strictly ascending in [1, levels]");
+    prev = hop_last[k];
+  }
+  if (prev != p->levels) return fail(HZ_ERR_INVALID, "hop_last: the last hop must end at level L");
+  p->nhops = nhops;
+  for (int k = 0; k < HZ_MAX_LEVELS; ++k) p->hop_last[k] = k < nhops ? hop_last[k] : 0;
+  clear_error();
+  return HZ_OK;
+}

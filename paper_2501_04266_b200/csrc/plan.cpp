@@ -7,9 +7,10 @@
 //   all-gather (O7/O8, Table VII): for l = top..1 with g_l > 1:
 //       ALLGATHER(level l, piece = range_l (len_l elems), into range_{l-1})
 //     top = w (forward) or s (backward).
-//   reduce-scatter (O9, Table VIII): for l = from..to with g_l > 1, for
-//     every peer digit j != d_l in ascending order:
-//       SENDRECV(level l, peer j, send chunk j of range_{l-1}, receive range_l)
+//   reduce-scatter (O9, Table VIII): for every hop a..b of p's grouping
+//     inside from..to (one hop per level by default), for every member j != me of
+//     the hop group in ascending merged digit (= ascending rank):
+//       SENDRECV(hop a..b, peer j, send member j's chunk of range_{a-1}, receive range_b)
 #include <string>
 #include <vector>
 
@@ -28,6 +29,7 @@ hz_status plan_allgather(const hz_partition_t* p, int backward, int bits, std::v
     hz_comm_step st{};
     st.op = HZ_PLAN_ALLGATHER;
     st.level = l;
+    st.level_last = l;
     st.group = g;
     st.peer = -1;
     st.peer_rank = -1;
@@ -50,31 +52,32 @@ hz_status plan_reduce_scatter(const hz_partition_t* p, int from_level, int to_le
   if (to_level < from_level || to_level > L) return fail(HZ_ERR_INVALID, "to_level: must be in [from_level, levels]");
   if (!bits_per_level) return fail(HZ_ERR_INVALID, "bits_per_level: NULL");
   out->clear();
-  int64_t stride[HZ_MAX_LEVELS];
-  int64_t s = 1;
-  for (int l = 0; l < L; ++l) {
-    stride[l] = s;
-    s *= p->group[l];
-  }
-  for (int l = from_level; l <= to_level; ++l) {
-    const int bits = bits_per_level[l - 1];
-    if (!bits_ok(bits)) return fail(HZ_ERR_INVALID, "bits_per_level[" + std::to_string(l - 1) + "]: must be 4 or 8");
-    const int g = p->group[l - 1];
-    const int d = p->digit[l - 1];
-    for (int j = 0; j < g; ++j) {
-      if (j == d) continue;
+  std::vector<Hop> hops;
+  hz_status rc = hops_of(p, from_level, to_level, &hops);
+  if (rc != HZ_OK) return rc;
+  std::vector<int> ranks;
+  std::vector<int64_t> rel;
+  for (const Hop& h : hops) {
+    const int bits = bits_per_level[h.a - 1];
+    if (!bits_ok(bits)) return fail(HZ_ERR_INVALID, "bits_per_level[" + std::to_string(h.a - 1) + "]: must be 4 or 8");
+    int me = 0;
+    hop_members(p, h.a, h.b, &ranks, &rel, &me);
+    const int G = static_cast<int>(ranks.size());
+    for (int j = 0; j < G; ++j) {
+      if (j == me) continue;
       hz_comm_step st{};
       st.op = HZ_PLAN_SENDRECV;
-      st.level = l;
-      st.group = g;
+      st.level = h.a;
+      st.level_last = h.b;
+      st.group = G;
       st.peer = j;
-      st.peer_rank = static_cast<int32_t>(p->rank + (static_cast<int64_t>(j) - d) * stride[l - 1]);
+      st.peer_rank = ranks[j];
       st.bits = bits;
-      st.elems = p->len[l];
-      st.send_off = p->off[l - 1] + j * p->len[l];
-      st.recv_off = p->off[l];
-      st.code_bytes = code_bytes(p->len[l], bits);
-      st.scale_bytes = p->len[l] / p->block * 4;
+      st.elems = p->len[h.b];
+      st.send_off = p->off[h.a - 1] + rel[j];
+      st.recv_off = p->off[h.b];
+      st.code_bytes = code_bytes(p->len[h.b], bits);
+      st.scale_bytes = p->len[h.b] / p->block * 4;
       out->push_back(st);
     }
   }

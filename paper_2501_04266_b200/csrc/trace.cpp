@@ -23,14 +23,16 @@ struct Rec {
   cudaStream_t st;
 };
 
-std::mutex g_mu;
-bool g_on = false;
-std::vector<Rec> g_recs;
-std::vector<cudaEvent_t> g_pool;
-size_t g_used = 0;
-unsigned long long* g_stamps = nullptr;   // device [capacity][8]
-bool g_events = true;
-size_t g_cap = 0;
+// per host thread: the contexts of a virtual world run one per thread and trace
+// separately (the mutex only guards against a reader on the same thread's state)
+thread_local std::mutex g_mu;
+thread_local bool g_on = false;
+thread_local std::vector<Rec> g_recs;
+thread_local std::vector<cudaEvent_t> g_pool;
+thread_local size_t g_used = 0;
+thread_local unsigned long long* g_stamps = nullptr;   // device [capacity][8]
+thread_local bool g_events = true;
+thread_local size_t g_cap = 0;
 
 void destroy_pool() {
   for (auto e : g_pool) cudaEventDestroy(e);
@@ -154,10 +156,13 @@ hz_status hz_trace_read(hz_trace_rec* out, int max, int* n_out) {
     out[n].stamp_ms = -1.f;
     const unsigned long long* t = st.size() >= 8 * (i + 1) ? &st[8 * i] : nullptr;
     if (t && t[0] && t[1] && t[2] >= t[1]) {
+      // duration = entry to the end of the flag publication when the kernel published
+      // (t[3]), else to the last CTA's arrival
+      const bool pub = t[3] >= t[2] && t[3] != 0;
       out[n].wait_ms = static_cast<float>(t[1] - t[0]) * 1e-6f;
       out[n].work_ms = static_cast<float>(t[2] - t[1]) * 1e-6f;
-      out[n].stamp_ms = static_cast<float>(t[2] - t[0]) * 1e-6f;
-      out[n].publish_ms = t[3] >= t[2] ? static_cast<float>(t[3] - t[2]) * 1e-6f : -1.f;
+      out[n].stamp_ms = static_cast<float>((pub ? t[3] : t[2]) - t[0]) * 1e-6f;
+      out[n].publish_ms = pub ? static_cast<float>(t[3] - t[2]) * 1e-6f : -1.f;
     }
     ++n;
   }

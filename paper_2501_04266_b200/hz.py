@@ -22,9 +22,9 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 MAX_LEVELS = 4
 F32, BF16, F16 = 0, 1, 2
-OK, ERR_INVALID, ERR_CUDA, ERR_NCCL, ERR_NONFINITE, ERR_UNSUPPORTED = range(6)
+OK, ERR_INVALID, ERR_CUDA, ERR_NCCL, ERR_NONFINITE, ERR_UNSUPPORTED, ERR_ABORTED = range(7)
 _STATUS = {1: "HZ_ERR_INVALID", 2: "HZ_ERR_CUDA", 3: "HZ_ERR_NCCL", 4: "HZ_ERR_NONFINITE",
-           5: "HZ_ERR_UNSUPPORTED"}
+           5: "HZ_ERR_UNSUPPORTED", 6: "HZ_ERR_ABORTED"}
 
 
 class HZError(RuntimeError):
@@ -41,10 +41,29 @@ class Partition(ctypes.Structure):
         ("gl", ctypes.c_int32),
         ("group", ctypes.c_int32 * MAX_LEVELS), ("digit", ctypes.c_int32 * MAX_LEVELS),
         ("off", ctypes.c_int64 * (MAX_LEVELS + 1)), ("len", ctypes.c_int64 * (MAX_LEVELS + 1)),
+        ("nhops", ctypes.c_int32), ("hop_last", ctypes.c_int32 * MAX_LEVELS),
     ]
 
     def range(self, level):
         return int(self.off[level]), int(self.len[level])
+
+    def set_hops(self, hop_last):
+        """hz_partition_set_hops: qgZ hop grouping, e.g. (2, 3) on a 3-level hierarchy =
+        levels 1..2 in one all-to-all, then level 3; None / () = one hop per level."""
+        hl = list(hop_last or ())
+        arr = (ctypes.c_int * max(len(hl), 1))(*hl)
+        _check(_lib.hz_partition_set_hops(ctypes.byref(self), len(hl), arr))
+        return self
+
+    def hops(self):
+        """The hop grouping as a list of (first level, last level)."""
+        if self.nhops == 0:
+            return [(l, l) for l in range(1, self.levels + 1)]
+        out, a = [], 1
+        for k in range(self.nhops):
+            out.append((a, int(self.hop_last[k])))
+            a = int(self.hop_last[k]) + 1
+        return out
 
     def as_dict(self):
         L = self.levels
@@ -53,6 +72,7 @@ class Partition(ctypes.Structure):
             "levels": L, "world": self.world, "rank": self.rank, "w": self.w, "s": self.s,
             "gl": self.gl, "group": list(self.group[:L]), "digit": list(self.digit[:L]),
             "off": list(self.off[:L + 1]), "len": list(self.len[:L + 1]),
+            "nhops": self.nhops, "hop_last": list(self.hop_last[:self.nhops]),
         }
 
 
@@ -69,7 +89,8 @@ class TraceRec(ctypes.Structure):
 
 
 class CommStep(ctypes.Structure):
-    _fields_ = [("op", ctypes.c_int32), ("level", ctypes.c_int32), ("group", ctypes.c_int32),
+    _fields_ = [("op", ctypes.c_int32), ("level", ctypes.c_int32), ("level_last", ctypes.c_int32),
+                ("group", ctypes.c_int32),
                 ("peer", ctypes.c_int32), ("peer_rank", ctypes.c_int32), ("bits", ctypes.c_int32),
                 ("elems", ctypes.c_int64), ("send_off", ctypes.c_int64), ("recv_off", ctypes.c_int64),
                 ("code_bytes", ctypes.c_int64), ("scale_bytes", ctypes.c_int64)]
@@ -119,10 +140,16 @@ class AdamWParams(ctypes.Structure):
     _fields_ = [(n, ctypes.c_float) for n in ("b1", "omb1", "b2", "omb2", "lr_wd", "sqrt_bc2", "eps", "step")]
 
 
+_sig("hz_adamw_params", [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                         _i64, ctypes.POINTER(AdamWParams)])
+
+
 def adamw_params(lr, b1, b2, eps, wd, t):
-    """hz_adamw_t of step t (t >= 1): host scalars rounded once to fp32 (reading R19)."""
-    import math
-    return AdamWParams(b1, 1.0 - b1, b2, 1.0 - b2, lr * wd, math.sqrt(1.0 - b2 ** t), eps, lr / (1.0 - b1 ** t))
+    """hz_adamw_params: the hz_adamw_t of step t (t >= 1), computed by the library
+    (reading R19: double, rounded once to fp32)."""
+    hp = AdamWParams()
+    _check(_lib.hz_adamw_params(float(lr), float(b1), float(b2), float(eps), float(wd), int(t), ctypes.byref(hp)))
+    return hp
 
 
 _sig("hz_adamw_step", [_vp, ctypes.POINTER(Partition), _vp, _vp, _vp, _vp, ctypes.POINTER(AdamWParams), _vp, _int,
@@ -152,6 +179,11 @@ _sig("hz_trace_begin", [_int, _int])
 _sig("hz_trace_end", [])
 _sig("hz_trace_read", [ctypes.POINTER(TraceRec), _int, ctypes.POINTER(ctypes.c_int)])
 _sig("hz_enable_p2p", [_vp, ctypes.c_size_t])
+_sig("hz_init_virtual", [ctypes.POINTER(_vp), _int, _int, ctypes.POINTER(ctypes.c_int), _int, ctypes.c_size_t])
+_sig("hz_set_wait_timeout", [_vp, ctypes.c_double])
+_sig("hz_abort", [_vp])
+_sig("hz_check", [_vp])
+_sig("hz_partition_set_hops", [ctypes.POINTER(Partition), _int, ctypes.POINTER(ctypes.c_int)])
 _sig("hz_p2p_enabled", [_vp, ctypes.POINTER(ctypes.c_int)])
 _sig("hz_sym_alloc", [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)])
 _sig("hz_p2p_capture_begin", [_vp])
@@ -190,6 +222,27 @@ def _ptr(t):
     return t.data_ptr()
 
 
+def _need(t, name, numel=None, dtypes=None):
+    """Host-side guard for a tensor argument (the C side cannot know buffer sizes):
+    a contiguous CUDA tensor of an accepted dtype with at least ``numel`` elements.
+    Raw integer pointers and None pass through unchecked."""
+    if t is None or isinstance(t, int):
+        return
+    if not t.is_cuda:
+        raise HZError(ERR_INVALID, f"{name}: not a CUDA tensor")
+    if not t.is_contiguous():
+        raise HZError(ERR_INVALID, f"{name}: not contiguous")
+    if dtypes is not None and t.dtype not in dtypes:
+        raise HZError(ERR_INVALID, f"{name}: dtype {t.dtype} not in {dtypes}")
+    if numel is not None and t.numel() < numel:
+        raise HZError(ERR_INVALID, f"{name}: {t.numel()} elements, needs {numel}")
+
+
+def _float_dtypes():
+    import torch
+    return (torch.float32, torch.bfloat16, torch.float16)
+
+
 def _dtype_code(t):
     import torch
     return {torch.float32: F32, torch.bfloat16: BF16, torch.float16: F16}[t.dtype]
@@ -210,12 +263,15 @@ def _groups(group):
 
 
 # ---------------------------------------------------------------- host-only API
-def partition_ex(rank, group, numel, block=256, w=1, s=1, gl=None):
-    """hz_partition_ex: the O1-O3 map for one rank (pure host, no GPU)."""
+def partition_ex(rank, group, numel, block=256, w=1, s=1, gl=None, hops=None):
+    """hz_partition_ex: the O1-O3 map for one rank (pure host, no GPU); ``hops``: the
+    qgZ hop grouping as hz_partition_set_hops's hop_last list (None = per level)."""
     arr, L = _groups(group)
     p = Partition()
     _check(_lib.hz_partition_ex(rank, L, arr, numel, block, w, s, L if gl is None else gl,
                                 ctypes.byref(p)))
+    if hops:
+        p.set_hops(hops)
     return p
 
 
@@ -370,6 +426,25 @@ class Context:
                             workspace_bytes))
         self._h = h
 
+    @classmethod
+    def _wrap(cls, handle, rank, world, group, device):
+        self = cls.__new__(cls)
+        self.group, self.rank, self.world, self.device = tuple(group), rank, world, device
+        self._h = handle
+        return self
+
+    def set_wait_timeout(self, seconds):
+        """hz_set_wait_timeout: longest cross-GPU wait before the context aborts."""
+        _check(_lib.hz_set_wait_timeout(self._h, float(seconds)))
+
+    def abort(self):
+        """hz_abort: abort the context (waiting kernels return; later calls fail)."""
+        _check(_lib.hz_abort(self._h))
+
+    def check(self):
+        """hz_check: raises HZError(ERR_ABORTED / ERR_NCCL) if the context is dead."""
+        _check(_lib.hz_check(self._h))
+
     @property
     def levels(self):
         return len(self.group)
@@ -416,10 +491,12 @@ class Context:
         _check(_lib.hz_sym_alloc(self._h, numel * itemsize, ctypes.byref(ptr)))
         return _wrap_device_ptr(ptr.value, numel, dtype, self.device)
 
-    def partition(self, numel, block=256, w=1, s=1, gl=None):
+    def partition(self, numel, block=256, w=1, s=1, gl=None, hops=None):
         p = Partition()
         _check(_lib.hz_partition(self._h, numel, block, w, s, self.levels if gl is None else gl,
                                  ctypes.byref(p)))
+        if hops:
+            p.set_hops(hops)
         return p
 
     def allgather_params(self, p, primary, sec_codes, sec_scales, full_out, bits=8,
@@ -427,6 +504,15 @@ class Context:
         """Forward (backward=False): quantize ``primary`` (the rank's range_w), gather,
         fill the secondary buffers, dequantize into ``full_out`` (Np elements).
         Backward: gather from the secondary buffers and dequantize."""
+        import torch
+        B, Np = p.block, p.padded_numel
+        _, len_w = p.range(p.w)
+        _, len_s = p.range(p.s)
+        if not backward:
+            _need(primary, "primary", len_w, _float_dtypes())
+        _need(sec_codes, "sec_codes", len_s * bits // 8, (torch.uint8,))
+        _need(sec_scales, "sec_scales", len_s // B, (torch.float32,))
+        _need(full_out, "full_out", Np, _float_dtypes())
         dt = _dtype_code(primary) if primary is not None else BF16
         _check(_lib.hz_allgather_params(self._h, ctypes.byref(p), int(bool(backward)),
                                         _ptr(primary), dt, bits, _ptr(sec_codes),
@@ -437,7 +523,16 @@ class Context:
     def allgather_params_next(self, p, primary, sec_codes, sec_scales, full_out, bits=8, p_next=None,
                               next_primary=None, next_sec_codes=None, next_sec_scales=None, stream=None):
         """hz_allgather_params_next: forward gather of ``p`` with the quantize of the next
-        layer's primary (``p_next``) prefetched into the same launch."""
+        layer's primary (``p_next``) prefetched into the same launch (same bits / dtype)."""
+        import torch
+        _need(primary, "primary", p.range(p.w)[1], _float_dtypes())
+        _need(sec_codes, "sec_codes", p.range(p.s)[1] * bits // 8, (torch.uint8,))
+        _need(sec_scales, "sec_scales", p.range(p.s)[1] // p.block, (torch.float32,))
+        _need(full_out, "full_out", p.padded_numel, _float_dtypes())
+        if p_next is not None:
+            _need(next_primary, "next_primary", p_next.range(p_next.w)[1], _float_dtypes())
+            _need(next_sec_codes, "next_sec_codes", p_next.range(p_next.s)[1] * bits // 8, (torch.uint8,))
+            _need(next_sec_scales, "next_sec_scales", p_next.range(p_next.s)[1] // p_next.block, (torch.float32,))
         _check(_lib.hz_allgather_params_next(
             self._h, ctypes.byref(p), _ptr(primary), _dtype_code(primary), bits, _ptr(sec_codes), _ptr(sec_scales),
             _ptr(full_out), _dtype_code(full_out), ctypes.byref(p_next) if p_next is not None else None,
@@ -449,7 +544,15 @@ class Context:
                       accumulate=False, stream=None):
         """hz_backward_step: qgZ reduce-scatter of ``p``'s gradient and the backward gather
         of the previous layer ``p_prev`` (fused in one launch where possible)."""
+        import torch
         L = self.levels
+        to = L if to_level is None else to_level
+        _need(grad, "grad", p.range(from_level - 1)[1], _float_dtypes())
+        _need(shard, "shard", p.range(to)[1], (torch.float32,))
+        if p_prev is not None:
+            _need(prev_sec_codes, "prev_sec_codes", p_prev.range(p_prev.s)[1] * prev_bits // 8, (torch.uint8,))
+            _need(prev_sec_scales, "prev_sec_scales", p_prev.range(p_prev.s)[1] // p_prev.block, (torch.float32,))
+            _need(prev_full_out, "prev_full_out", p_prev.padded_numel, _float_dtypes())
         bpl = list(bits_per_level) if bits_per_level is not None else [4] * L
         bpl = bpl + [4] * (L - len(bpl))
         arr = (ctypes.c_int * L)(*bpl)
@@ -462,7 +565,10 @@ class Context:
 
     def reduce_scatter_grads(self, p, grad, shard, bits_per_level=None, from_level=1,
                              to_level=None, accumulate=False, stream=None):
+        import torch
         L = self.levels
+        _need(grad, "grad", p.range(from_level - 1)[1], _float_dtypes())
+        _need(shard, "shard", p.range(L if to_level is None else to_level)[1], (torch.float32,))
         bpl = list(bits_per_level) if bits_per_level is not None else [4] * L
         bpl = bpl + [4] * (L - len(bpl))
         arr = (ctypes.c_int * L)(*bpl)
@@ -474,6 +580,9 @@ class Context:
     def allreduce_select(self, p, shard_in, out, from_level, to_level=None, stream=None):
         """hz_allreduce_select: the paper-literal A10 step (fp32 allreduce over levels
         from..to, ascending digit, then this rank's range_to slice into ``out``)."""
+        import torch
+        _need(shard_in, "shard_in", p.range(from_level - 1)[1], (torch.float32,))
+        _need(out, "out", p.range(self.levels if to_level is None else to_level)[1], (torch.float32,))
         _check(_lib.hz_allreduce_select(self._h, ctypes.byref(p), _ptr(shard_in), int(from_level),
                                         self.levels if to_level is None else int(to_level), _ptr(out),
                                         _stream(stream)))
@@ -481,6 +590,11 @@ class Context:
 
     def adamw_step(self, p, grad_shard, master, m, v, hp, primary, stream=None):
         """hz_adamw_step: AdamW on range_L, then the post-update all-gather into primary."""
+        import torch
+        nL = p.range(p.levels)[1]
+        for t, name in ((grad_shard, "grad_shard"), (master, "master"), (m, "m"), (v, "v")):
+            _need(t, name, nL, (torch.float32,))
+        _need(primary, "primary", p.range(p.w)[1], _float_dtypes())
         _check(_lib.hz_adamw_step(self._h, ctypes.byref(p), _ptr(grad_shard), _ptr(master), _ptr(m), _ptr(v),
                                   ctypes.byref(hp), _ptr(primary), _dtype_code(primary), _stream(stream)))
         return primary
@@ -518,3 +632,23 @@ class Context:
         _check(_lib.hz_flat_reduce_scatter(self._h, _ptr(inp), _ptr(out_chunk), inp.numel(),
                                            _dtype_code(inp), _stream(stream)))
         return out_chunk
+
+
+def virtual_world(group, device=0, pool_bytes=64 << 20, cumulative=False):
+    """hz_init_virtual: one Context per rank of hierarchy ``group``, all in this process
+    on GPU ``device``, P2P-enabled with each other's pools as peers.  Drive each from
+    its own thread (tests/vworld.py)."""
+    g = list(group)
+    if cumulative:
+        rel, prev = [], 1
+        for c in g:
+            rel.append(c // prev)
+            prev = c
+        g = rel
+    world = 1
+    for x in g:
+        world *= x
+    arr, L = _groups(g)
+    hs = (_vp * world)()
+    _check(_lib.hz_init_virtual(hs, world, L, arr, device, int(pool_bytes)))
+    return [Context._wrap(_vp(hs[r]), r, world, g, device) for r in range(world)]

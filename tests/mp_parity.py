@@ -37,12 +37,19 @@ def role_cases(L):
     return sorted(c for c in cases if 0 <= c[0] <= L and 0 <= c[1] <= L)
 
 
-def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=False):
+def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=False, vctx=None):
+    """vctx: a virtual-world context (tests/vworld.py; P2P, one GPU, one thread per
+    rank) instead of a context made here — then the CUDA-graph and flat-NCCL parts,
+    which a virtual world does not support, are skipped."""
     errors = []
-    ctx = hz.Context(rank, world, uid, g, device)
+    virtual = vctx is not None
+    if virtual:
+        ctx, p2p = vctx, True
+    else:
+        ctx = hz.Context(rank, world, uid, g, device)
     L = len(g)
-    tag = "p2p" if p2p else "nccl"
-    if p2p:
+    tag = "vworld" if virtual else ("p2p" if p2p else "nccl")
+    if p2p and not virtual:
         ctx.enable_p2p(64 << 20)
 
     def sec_buffers(n_codes, n_scales):
@@ -196,6 +203,12 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
             except AssertionError as e:
                 errors.append(str(e))
 
+        if virtual:
+            errors += check_step_host(ctx, hz, rank, world, g, sec_buffers, tag, B)
+            errors += check_pipelined(ctx, hz, rank, world, g, sec_buffers, tag, B, p2p)
+            errors += check_hops(ctx, hz, rank, world, g, sec_buffers, tag, B)
+            return errors
+
         # CUDA graph: one captured step (forward gather, backward gather, qgZ) replayed
         # three times with fresh inputs copied into the captured buffers
         p = ctx.partition(numel, B, 1, 1, L)
@@ -258,6 +271,7 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
 
         errors += check_step_host(ctx, hz, rank, world, g, sec_buffers, tag, B)
         errors += check_pipelined(ctx, hz, rank, world, g, sec_buffers, tag, B, p2p)
+        errors += check_hops(ctx, hz, rank, world, g, sec_buffers, tag, B)
 
         # flat ZeRO-3 baseline collectives (plain NCCL)
         n = world * 4096
@@ -276,8 +290,72 @@ def check_hierarchy(hz, rank, world, g, uid, device, numel=150_001, B=256, p2p=F
         except AssertionError as e:
             errors.append(str(e))
     finally:
-        ctx.close()
+        if not virtual:
+            ctx.close()
     return errors
+
+
+def hop_groupings(L):
+    """Every qgZ hop grouping of L levels other than one hop per level (R15)."""
+    out = []
+    for mask in range(1 << (L - 1)):
+        hl = [l for l in range(1, L) if (mask >> (l - 1)) & 1] + [L]
+        if len(hl) < L:
+            out.append(tuple(hl))
+    return out
+
+
+def check_hops(ctx, hz, rank, world, g, sec_buffers, tag, B, numel=150_001):
+    """Merged-level qgZ (hz_partition_set_hops): every hop grouping of the hierarchy,
+    one call over all levels, bitwise against the oracle's reduce_scatter_hops; then the
+    paper-literal ZeRO-topo step: a 1-hop all-to-all over levels
+    1..L-1 per micro-batch (GA = 2, accumulated), then the fp32 allreduce + select over
+    level L (hz_allreduce_select)."""
+    errors = []
+    L = len(g)
+    if L < 2:
+        return errors
+    Np = pm.padded_numel(numel, g, B)
+    grads = {r: synth.gradient_like(Np, 4200 + r, block=B).astype(ml_dtypes.bfloat16) for r in range(world)}
+    for hl in hop_groupings(L):
+        for bits in (4, 8):
+            p = ctx.partition(numel, B, 1, 1, L, hops=hl)
+            want = col.reduce_scatter_hops(grads, g, Np, B, hops_from_last(hl), bits)
+            sh = torch.full((p.range(L)[1],), float("nan"), dtype=torch.float32, device="cuda")
+            ctx.reduce_scatter_grads(p, to_dev(grads[rank]), sh, [bits] * L)
+            torch.cuda.synchronize()
+            try:
+                assert_bitwise(to_host(sh), want[rank], f"[{tag}] g={g} hops={hl} bits={bits} qgZ")
+            except AssertionError as e:
+                errors.append(str(e))
+    # ZeRO-topo: hops (1..L-1), (L); GA = 2 on levels 1..L-1 then allreduce + select at L
+    hl = (L - 1, L)
+    p = ctx.partition(numel, B, 1, 1, L - 1, hops=hl)
+    grads2 = {r: synth.gradient_like(Np, 4300 + r, block=B).astype(ml_dtypes.bfloat16) for r in range(world)}
+    hops = hops_from_last(hl)
+    A = col.reduce_scatter_hops(grads, g, Np, B, hops[:1], 4)
+    A = col.reduce_scatter_hops(grads2, g, Np, B, hops[:1], 4, accum=A)
+    want = col.allreduce_select(A, g, Np, L, L)
+    acc = torch.empty(p.range(L - 1)[1], dtype=torch.float32, device="cuda")
+    ctx.reduce_scatter_grads(p, to_dev(grads[rank]), acc, [4] * L, 1, L - 1)
+    ctx.reduce_scatter_grads(p, to_dev(grads2[rank]), acc, [4] * L, 1, L - 1, accumulate=True)
+    out = torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")
+    ctx.allreduce_select(p, acc, out, L, L)
+    torch.cuda.synchronize()
+    try:
+        assert_bitwise(to_host(acc), A[rank], f"[{tag}] g={g} ZeRO-topo 1-hop accumulated shard")
+        assert_bitwise(to_host(out), want[rank], f"[{tag}] g={g} ZeRO-topo allreduce+select")
+    except AssertionError as e:
+        errors.append(str(e))
+    return errors
+
+
+def hops_from_last(hop_last):
+    out, a = [], 1
+    for b in hop_last:
+        out.append((a, b))
+        a = b + 1
+    return out
 
 
 def check_pipelined(ctx, hz, rank, world, g, sec_buffers, tag, B, p2p, sizes=(150_001, 70_000, 4097, 9000)):
