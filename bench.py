@@ -51,8 +51,7 @@ HIERARCHY = {
 }
 KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "gather_quantize", "dequantize_roundtrip",
                 "quantize_dequantize", "reduce",
-                "reduce_requant",
-                "quantize_push", "reduce_push", "ag_fused", "rs_fused")
+                "reduce_requant")
 NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 NVLINK_BIDIR_PROBE_GBS = 620.0   # both GPUs of a pair pulling at once, per direction (profiles/bulk_probe_r01.txt)
 

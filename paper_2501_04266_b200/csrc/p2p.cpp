@@ -142,12 +142,15 @@ SyncArgs make_sync(hz_ctx* ctx, const Phases& ph) {
 
 // One synchronised launch: in a virtual world the host first orders the stream after
 // the signals this kernel waits for, and records its own signals afterwards.
+// (HZ_TUNE vworder=0 disables the host ordering: a test of the device-side waits)
 template <class F>
 hz_status synced(hz_ctx* ctx, const SyncArgs& s, cudaStream_t st, F&& launch) {
+  static const bool order = tune_param("vworder", 1) != 0;
+  const bool vw = ctx->p2p.vw && order;
   hz_status rc;
-  if (ctx->p2p.vw && (rc = vw_wait(ctx, s, st)) != HZ_OK) return rc;
+  if (vw && (rc = vw_wait(ctx, s, st)) != HZ_OK) return rc;
   if ((rc = launch()) != HZ_OK) return rc;
-  if (ctx->p2p.vw) return vw_signal(ctx, s, st);
+  if (vw) return vw_signal(ctx, s, st);
   return HZ_OK;
 }
 

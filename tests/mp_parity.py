@@ -506,28 +506,41 @@ def check_step_host(ctx, hz, rank, world, g, sec_buffers, tag, B, sizes=(150_001
     return errors
 
 
-def check_full_size(hz, rank, world, g, uid, device, numel, p2p, B=256):
+def check_full_size(hz, rank, world, g, uid, device, numel, p2p, B=256, vctx=None):
     """The bench configuration (GPT layer size, setting T w=s=1, gl=L, int8 qwZ, int4
     qgZ) checked on sampled blocks: every output block depends only on the same global
     block of the inputs, and the qgZ reduction tree does not depend on the block's
-    position, so the oracle runs on a small layer made of the sampled blocks only."""
+    position, so the oracle runs on a small layer made of the sampled blocks only.
+    vctx: a virtual-world context (P2P; its pool must hold 2*Np + 64 MiB)."""
     errors = []
-    tag = "p2p" if p2p else "nccl"
-    ctx = hz.Context(rank, world, uid, g, device)
+    virtual = vctx is not None
+    tag = "vworld" if virtual else ("p2p" if p2p else "nccl")
+    ctx = vctx if virtual else hz.Context(rank, world, uid, g, device)
+    p2p = p2p or virtual
     L = len(g)
     try:
         p = ctx.partition(numel, B, 1, 1, L)
         Np = p.padded_numel
-        if p2p:
+        if p2p and not virtual:
             ctx.enable_p2p(2 * Np + (64 << 20))
         off, ln = p.range(1)
+        nb = Np // B
+        bounds = sorted({pm.range_at(r, g, Np, l)[0] // B for r in range(world) for l in range(L + 1)})
+        idx = synth.sample_blocks(nb, bounds, every=499)
+        it = torch.from_numpy(idx).cuda()
+        pick = lambda t: to_host(t.view(nb, B)[it].contiguous().view(-1))   # noqa: E731
         full = synth.torch_normal(Np, 7000, 0.02, torch.bfloat16, "cuda", outlier_every=0)
         full[numel:] = 0
-        grads = []
+        picked = {}
+        grad = None
         for q in range(world):                       # every rank can regenerate every gradient
             gq = synth.torch_normal(Np, 900 + q, 1e-3, torch.bfloat16, "cuda")
             gq[numel:] = 0
-            grads.append(gq)
+            picked[q] = pick(gq)
+            if q == rank:
+                grad = gq
+            else:
+                del gq
         if p2p:
             sec_c, sec_s = ctx.sym_alloc(ln, torch.uint8), ctx.sym_alloc(ln // B, torch.float32)
         else:
@@ -538,14 +551,9 @@ def check_full_size(hz, rank, world, g, uid, device, numel, p2p, B=256):
         shard = torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")
         ctx.allgather_params(p, full[off:off + ln].contiguous(), sec_c, sec_s, fwd, bits=8)
         ctx.allgather_params(p, None, sec_c, sec_s, bwd, bits=8, backward=True)
-        ctx.reduce_scatter_grads(p, grads[rank], shard, [4] * L)
+        ctx.reduce_scatter_grads(p, grad, shard, [4] * L)
         torch.cuda.synchronize()
 
-        nb = Np // B
-        bounds = sorted({pm.range_at(r, g, Np, l)[0] // B for r in range(world) for l in range(L + 1)})
-        idx = synth.sample_blocks(nb, bounds, every=499)
-        it = torch.from_numpy(idx).cuda()
-        pick = lambda t: to_host(t.view(nb, B)[it].contiguous().view(-1))   # noqa: E731
         xs = pick(full)
         want = quant.dequantize(*quant.quantize(xs, 8, B), B, out="bf16")
         for name, t in (("forward", fwd), ("backward", bwd)):
@@ -553,13 +561,14 @@ def check_full_size(hz, rank, world, g, uid, device, numel, p2p, B=256):
                 assert_bitwise(pick(t), want, f"[{tag}] g={g} full-size {name} layer ({len(idx)} sampled blocks)")
             except AssertionError as e:
                 errors.append(str(e))
+        del fwd, bwd, full, grad
         # qgZ: a small layer made of the sampled blocks, same hierarchy and bits
         ns = len(idx)
         tnp = pm.padded_numel(ns * B, g, B)
         tiny = {}
         for q in range(world):
             a = np.zeros(tnp, np.float32).astype(ml_dtypes.bfloat16)
-            a[:ns * B] = pick(grads[q])
+            a[:ns * B] = picked[q]
             tiny[q] = a
         tout = col.reduce_scatter(tiny, g, tnp, B, 1, L, {l: 4 for l in range(1, L + 1)})
         tflat = np.zeros(tnp, np.float32)
@@ -580,7 +589,8 @@ def check_full_size(hz, rank, world, g, uid, device, numel, p2p, B=256):
                 checked += 1
         assert checked > 0 or world > 8
     finally:
-        ctx.close()
+        if not virtual:
+            ctx.close()
     return errors
 
 

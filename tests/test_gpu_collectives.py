@@ -36,16 +36,11 @@ def test_multi_gpu(n):
 
 @pytest.mark.multigpu
 @pytest.mark.parametrize("n", [2, 4])
-@pytest.mark.parametrize("tune", ["fused=1", "fused=1,pf=20,pk=4", "pushf=40", "pushf=100,rspush=1", "gqc=4",
-                                  "gq=2,gqf=60"])
+@pytest.mark.parametrize("tune", ["gqc=4", "gq=2,gqf=60", "nofuse=1"])
 def test_multi_gpu_transport_variants(n, tune):
-    """The alternative P2P kernel schedules selected with HZ_TUNE: the one-launch
-    pipelined kernels (k_fused.cu, fused=1), the hybrid push/pull forward gather
-    (pushf=40: the quantize kernel also stores the head of its piece into every
-    member's receive buffer; the default is pull only), the full push gather
-    (pushf=100) and the push qgZ (rspush=1: producers store each chunk into its
-    consumer's receive buffer); the dual kernel's chunked interleave (gqc=4, the default for
-    large layers only) and its role split (gq=2)."""
+    """The alternative P2P kernel schedules selected with HZ_TUNE: the dual kernel's
+    chunked interleave (gqc=4, the default for large layers only), its role split
+    (gq=2), and the unpaired two-call path (nofuse=1)."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
