@@ -511,7 +511,8 @@ def check_full_size(hz, rank, world, g, uid, device, numel, p2p, B=256, vctx=Non
     qgZ) checked on sampled blocks: every output block depends only on the same global
     block of the inputs, and the qgZ reduction tree does not depend on the block's
     position, so the oracle runs on a small layer made of the sampled blocks only.
-    vctx: a virtual-world context (P2P; its pool must hold 2*Np + 64 MiB)."""
+    vctx: a virtual-world context (P2P; its pool must hold 2.5*Np + 64 MiB: the
+    secondary and one qgZ send buffer per level)."""
     errors = []
     virtual = vctx is not None
     tag = "vworld" if virtual else ("p2p" if p2p else "nccl")
