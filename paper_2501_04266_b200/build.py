@@ -19,8 +19,11 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(CSRC, "_obj")
-LIB = os.path.join(PKG, "libhz.so")
+# HZ_BUILD_VARIANT=name HZ_NVCC_DEFS="-DX=Y ...": an experimental build into
+# libhz_<name>.so (objects in csrc/_obj_<name>), loaded with HZ_LIB=libhz_<name>.so
+_VAR = os.environ.get("HZ_BUILD_VARIANT", "")
+OBJ = os.path.join(CSRC, "_obj" + ("_" + _VAR if _VAR else ""))
+LIB = os.path.join(PKG, "libhz" + ("_" + _VAR if _VAR else "") + ".so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -43,7 +46,7 @@ def _flags():
     return [
         *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-ftz=false", "-prec-div=true",
         "-prec-sqrt=true", "-Xcompiler", "-fPIC,-O2,-Wall,-fvisibility=hidden", "-I", os.path.join(ROOT, "include"),
-        "-I", os.path.join(nd, "include"),
+        "-I", os.path.join(nd, "include"), *os.environ.get("HZ_NVCC_DEFS", "").split(),
     ], nd
 
 

@@ -33,6 +33,11 @@
 
 #include "hz_internal.h"
 
+// load of codes / scales that may be peer memory (see the header comment)
+#ifndef HZ_PEER_LD
+#define HZ_PEER_LD __ldcg
+#endif
+
 namespace hz {
 namespace dev {
 
@@ -121,7 +126,7 @@ struct Codes8;
 template <>
 struct Codes8<8> {
   uint2 r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = HZ_PEER_LD(reinterpret_cast<const uint2*>(p)); }
   __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<uint2*>(p) = r; }
   __device__ __forceinline__ void zero() { r = make_uint2(0u, 0u); }
   // exact float value of each code
@@ -144,7 +149,7 @@ struct Codes8<8> {
 template <>
 struct Codes8<4> {
   unsigned r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const unsigned*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = HZ_PEER_LD(reinterpret_cast<const unsigned*>(p)); }
   __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<unsigned*>(p) = r; }
   __device__ __forceinline__ void zero() { r = 0u; }
   __device__ __forceinline__ void decode(float (&c)[8]) const {
@@ -174,7 +179,7 @@ struct Codes4;
 template <>
 struct Codes4<8> {
   unsigned r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const unsigned*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = HZ_PEER_LD(reinterpret_cast<const unsigned*>(p)); }
   __device__ __forceinline__ void decode(float (&c)[4]) const {
     const unsigned x = r ^ 0x80808080u;
 #pragma unroll
@@ -186,7 +191,7 @@ template <>
 struct Codes4<4> {
   unsigned short r;
   __device__ __forceinline__ void load(const uint8_t* p) {
-    r = __ldcg(reinterpret_cast<const unsigned short*>(p));
+    r = HZ_PEER_LD(reinterpret_cast<const unsigned short*>(p));
   }
   __device__ __forceinline__ void decode(float (&c)[4]) const {
     const unsigned x = static_cast<unsigned>(r) ^ 0x8888u;   // nibble ^ 8 = code + 8
@@ -466,17 +471,25 @@ __device__ __forceinline__ bool sync_wait(const SyncArgs& s) {
     const unsigned long long t0 = globaltimer();
     const unsigned long long e = s.epoch ? *s.epoch : 0ull;
     const unsigned long long wr = s.wait_ready + e, wd = s.wait_done + e;
-    int good = s.abort ? ld_volatile_u32(s.abort) == 0u : 1;
+    // the abort word lives in host memory: it is polled only once a wait has lasted
+    // 1 ms, then every 100 us (hundreds of CTAs reading it on every entry would
+    // serialise on PCIe)
+    int good = 1;
     unsigned it = 0;
+    unsigned long long next_poll = t0 + 1000000ull;
     for (int q = 0; q < kMaxWorld && good; ++q) {
       const bool r = (s.wr_mask >> q) & 1u, d = (s.wd_mask >> q) & 1u;
       while ((r && ld_acquire_sys(s.ready_local + q) < wr) || (d && ld_acquire_sys(s.done_local + q) < wd)) {
-        if ((++it & 127u) == 0u) {
-          if (s.abort && ld_volatile_u32(s.abort) != 0u) {
-            good = 0;
-            break;
+        if ((++it & 63u) == 0u) {
+          const unsigned long long now = globaltimer();
+          if (now >= next_poll) {
+            next_poll = now + 100000ull;
+            if (s.abort && ld_volatile_u32(s.abort) != 0u) {
+              good = 0;
+              break;
+            }
           }
-          if (globaltimer() - t0 > s.timeout_ns) {
+          if (now - t0 > s.timeout_ns) {
             if (s.abort) atomicExch(s.abort, 1u);
             good = 0;
             break;

@@ -41,7 +41,7 @@ __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits
         if (!inter) jt = 0;
         const int64_t r0 = ub * 8 - jt * pc.len;
         const uint8_t* cb = pc.c[jt] + (r0 + lane * 8) * BITS / 8;
-        const float4 s4 = __ldcg(reinterpret_cast<const float4*>(pc.s[jt] + (r0 >> 8)));
+        const float4 s4 = HZ_PEER_LD(reinterpret_cast<const float4*>(pc.s[jt] + (r0 >> 8)));
 #pragma unroll
         for (int u = 0; u < U; ++u) raw[u].load(cb + u * 256 * BITS / 8);
         sc[0] = s4.x;
@@ -58,7 +58,7 @@ __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits
         const int64_t r0 = ub * 8 - jt * pc.len;
         const uint8_t* cb = pc.c[jt] + (r0 + lane * 8) * BITS / 8;
         const int ns = log2b >= 10 ? 1 : (1024 >> log2b);
-        const float mine = __ldcg(pc.s[jt] + (r0 >> log2b) + (lane < ns ? lane : ns - 1));
+        const float mine = HZ_PEER_LD(pc.s[jt] + (r0 >> log2b) + (lane < ns ? lane : ns - 1));
 #pragma unroll
         for (int u = 0; u < U; ++u) raw[u].load(cb + u * 256 * BITS / 8);
 #pragma unroll
@@ -78,7 +78,7 @@ __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits
         }
         const int64_t r = e - j * pc.len;
         raw[u].load(pc.c[j] + r * BITS / 8);
-        sc[u] = __ldcg(pc.s[j] + (r >> log2b));
+        sc[u] = HZ_PEER_LD(pc.s[j] + (r >> log2b));
       }
     }
 #pragma unroll

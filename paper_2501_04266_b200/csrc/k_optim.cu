@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_copy(const __grid_constant_
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t q = vb + u * 32 + lane;
-      if (q < per) r[u] = __ldcg(reinterpret_cast<const uint4*>(pc.c[j]) + q);
+      if (q < per) r[u] = HZ_PEER_LD(reinterpret_cast<const uint4*>(pc.c[j]) + q);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -132,14 +132,14 @@ __global__ void __launch_bounds__(kThreads) k_sum_f32(const __grid_constant__ Pi
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + u * nth;
-      if (i < n4) acc[u] = __ldcg(reinterpret_cast<const float4*>(pc.c[0]) + i);
+      if (i < n4) acc[u] = HZ_PEER_LD(reinterpret_cast<const float4*>(pc.c[0]) + i);
     }
     for (int j = 1; j < g; ++j) {
       float4 x[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t i = base + u * nth;
-        if (i < n4) x[u] = __ldcg(reinterpret_cast<const float4*>(pc.c[j]) + i);
+        if (i < n4) x[u] = HZ_PEER_LD(reinterpret_cast<const float4*>(pc.c[j]) + i);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {

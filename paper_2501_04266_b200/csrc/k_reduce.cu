@@ -51,7 +51,7 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
       // 4 scales of an input are one 16-byte broadcast load
 #pragma unroll
       for (int p = 0; p < GT; ++p) {
-        const float4 s4 = __ldcg(reinterpret_cast<const float4*>(a.s[p] + blk0));
+        const float4 s4 = HZ_PEER_LD(reinterpret_cast<const float4*>(a.s[p] + blk0));
         sc[0][p] = s4.x;
         sc[1][p] = s4.y;
         sc[2][p] = s4.z;
@@ -70,7 +70,7 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
 #pragma unroll
           for (int k = 0; k < G::NSUB; ++k)
             raw[u][p][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
-          sc[u][p] = __ldcg(a.s[p] + blk);
+          sc[u][p] = HZ_PEER_LD(a.s[p] + blk);
         } else {
 #pragma unroll
           for (int k = 0; k < G::NSUB; ++k) raw[u][p][k].zero();
@@ -106,7 +106,7 @@ __device__ __forceinline__ void sum_steps(const RedArgs& a, int64_t blk0, int la
 #pragma unroll
           for (int k = 0; k < G::NSUB; ++k)
             raw[u][k].load(a.c[p] + (blk * B + k * G::SUBSTRIDE + ll * 8) * BIN / 8);
-          sc[u] = __ldcg(a.s[p] + blk);
+          sc[u] = HZ_PEER_LD(a.s[p] + blk);
         } else {
 #pragma unroll
           for (int k = 0; k < G::NSUB; ++k) raw[u][k].zero();
@@ -210,7 +210,7 @@ template <>
 struct Wide<8> {
   static constexpr int E = 8;
   uint2 r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = HZ_PEER_LD(reinterpret_cast<const uint2*>(p)); }
   __device__ __forceinline__ void decode(float (&c)[E]) const {
     Codes8<8> x;
     x.r = r;
@@ -221,7 +221,7 @@ template <>
 struct Wide<4> {
   static constexpr int E = 16;
   uint2 r;
-  __device__ __forceinline__ void load(const uint8_t* p) { r = __ldcg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void load(const uint8_t* p) { r = HZ_PEER_LD(reinterpret_cast<const uint2*>(p)); }
   __device__ __forceinline__ void decode(float (&c)[E]) const {
     Codes8<4> lo, hi;
     lo.r = r.x;
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
           raw[u][p].r = make_uint2(0u, 0u);
           if (unit < nunits) {
             raw[u][p].load(a.c[p] + unit * 8);
-            sc[u][p] = __ldcg(a.s[p] + ((unit * E) >> log2b));
+            sc[u][p] = HZ_PEER_LD(a.s[p] + ((unit * E) >> log2b));
           }
         }
       }
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
           raw[u].r = make_uint2(0u, 0u);
           if (unit < nunits) {
             raw[u].load(a.c[p] + unit * 8);
-            sc[u] = __ldcg(a.s[p] + ((unit * E) >> log2b));
+            sc[u] = HZ_PEER_LD(a.s[p] + ((unit * E) >> log2b));
           }
         }
 #pragma unroll

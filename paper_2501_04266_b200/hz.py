@@ -11,7 +11,7 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libhz.so")
+LIB_PATH = os.path.join(PKG, os.environ.get("HZ_LIB", "libhz.so"))   # HZ_LIB: experimental builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
