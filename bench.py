@@ -52,8 +52,9 @@ HIERARCHY = {
 KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "gather_quantize", "dequantize_roundtrip",
                 "quantize_dequantize", "reduce",
                 "reduce_requant")
-NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md); 900 nominal
-NVLINK_BIDIR_PROBE_GBS = 620.0   # both GPUs of a pair pulling at once, per direction (profiles/bulk_probe_r01.txt)
+NVLINK_NOMINAL_GBS = 900.0  # NVLink 5, per direction (north_star denominator)
+NVLINK_PEER_GBS = 770.0     # fallback: measured peer copy per direction (B200_PROFILING.md)
+NVLINK_BIDIR_PROBE_GBS = 620.0   # fallback: both GPUs of a pair pulling at once (profiles/bulk_probe_r01.txt)
 
 
 def parse():
@@ -79,6 +80,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flat", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="at 8 GPUs: skip the second hierarchy")
     ap.add_argument("--no-tail", action="store_true", help="skip the step-tail (AdamW + post-update gather) timing")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 collective transport: fused NVLink peer-memory kernels (p2p) or NCCL")
@@ -334,17 +336,44 @@ def step_model(recs, steps, hbm_peak, nvl_peak=NVLINK_PEER_GBS, nvl_bidir=NVLINK
     """the modeled minimum of one step = the sum over the step's
     launches of each launch's roofline time, max(local HBM bytes / HBM peak, peer bytes /
     NVLink peak) (NCCL calls: bytes sent / NVLink peak) — every kernel at its roofline,
-    back to back, no synchronisation.  Returned per step, with the NVLink term also taken
-    at the bidirectional peer-read probe (both GPUs of a group pull at once)."""
+    back to back, no synchronisation.  Local HBM bytes include the bytes the group's peers
+    read from this GPU (served bytes; equal to the bytes it reads from them, the
+    exchanges being symmetric).  Returned per step, with the NVLink term at the one-way
+    and at the bidirectional peer-read peak (both GPUs of a group pull at once), both
+    measured in this run when N > 1 (hz_nvlink_probe)."""
     t, tb = 0.0, 0.0
     for r in recs:
         b, rem = float(r["bytes"]), float(r.get("remote_bytes", 0) or 0)
         if r["kind"].startswith("nccl"):
             b, rem = 0.0, b
-        t += max(b / (hbm_peak * 1e9), rem / (nvl_peak * 1e9))
-        tb += max(b / (hbm_peak * 1e9), rem / (nvl_bidir * 1e9))
+        # the exchanges are symmetric: the members read from this GPU's HBM as many bytes
+        # as it reads from theirs (served bytes), so its HBM moves bytes + rem
+        t += max((b + rem) / (hbm_peak * 1e9), rem / (nvl_peak * 1e9))
+        tb += max((b + rem) / (hbm_peak * 1e9), rem / (nvl_bidir * 1e9))
     return {"model_ms": t / steps * 1e3, "model_ms_bidir_probe": tb / steps * 1e3,
             "hbm_peak_GBps": hbm_peak, "nvlink_peak_GBps": nvl_peak, "nvlink_bidir_probe_GBps": nvl_bidir}
+
+
+def nvlink_probe(ctx, rank, world, stream, nbytes=256 << 20):
+    """The NVLink denominators of this run (hz_nvlink_probe: the fused kernels' own load
+    path): one way (rank 0 pulls from rank 1 while the others idle) and bidirectional
+    (every rank pulls from its partner r^1 at once; min over ranks), GB/s per direction."""
+    if world < 2:
+        return None
+    try:
+        out = {}
+        barrier(world)
+        ms = ctx.nvlink_probe(1, nbytes, 5, stream=stream) if rank == 0 else 0.0
+        one = nbytes / (ms * 1e-3) / 1e9 if rank == 0 else 0.0
+        out["one_way_GBps"] = max_over_ranks(one, world)
+        barrier(world)
+        ms = ctx.nvlink_probe(rank ^ 1, nbytes, 5, stream=stream)
+        out["bidirectional_GBps"] = -max_over_ranks(-(nbytes / (ms * 1e-3) / 1e9), world)
+        out["bytes"] = nbytes
+        out["what"] = "hz_nvlink_probe: full-grid 16-byte coherent loads of a peer's pool (the gather/reduce load path)"
+        return out
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)[:200], "one_way_GBps": NVLINK_PEER_GBS, "bidirectional_GBps": NVLINK_BIDIR_PROBE_GBS}
 
 
 def summarize_trace(recs, steps):
@@ -355,7 +384,10 @@ def summarize_trace(recs, steps):
             r["ms"] = r.get("stamp_ms", -1.0)
         if r["ms"] < 0:
             continue
-        k = kinds.setdefault(r["kind"], {"launches": 0, "ms": 0.0, "bytes": 0, "elems": 0, "remote": 0,
+        key = r["kind"]
+        if key.startswith("reduce") or key.startswith("nccl"):
+            key = f"{key}@L{r['level']}"          # per-level rows of the qgZ levels / hops
+        k = kinds.setdefault(key, {"launches": 0, "ms": 0.0, "bytes": 0, "elems": 0, "remote": 0,
                                          "wait_ms": 0.0, "work_ms": 0.0, "publish_ms": 0.0, "stamped": 0})
         k["launches"] += 1
         k["ms"] += r["ms"]
@@ -484,7 +516,10 @@ def run_hz(args):
     # with a graph the trace holds one step's launches (events re-recorded by every replay)
     stages = summarize_trace(recs, 1 if graph is not None else args.steps)
     peak0, _ = measured_peaks()
-    smodel = step_model(recs, 1 if graph is not None else args.steps, peak0) if recs else None
+    nvl = nvlink_probe(ctx, rank, world, stream) if transport == "p2p" else None
+    nvl_uni = nvl["one_way_GBps"] if nvl else NVLINK_PEER_GBS
+    nvl_bi = nvl["bidirectional_GBps"] if nvl else NVLINK_BIDIR_PROBE_GBS
+    smodel = step_model(recs, 1 if graph is not None else args.steps, peak0, nvl_uni, nvl_bi) if recs else None
     if smodel:
         smodel["frac_of_model"] = smodel["model_ms"] / ms_per_step
         smodel["frac_of_model_bidir_probe"] = smodel["model_ms_bidir_probe"] / ms_per_step
@@ -493,37 +528,46 @@ def run_hz(args):
 
     # roofline: the kernel kind with the largest share of device time
     peak, peak_src = measured_peaks()
-    kern = {k: v for k, v in stages.items() if k in KERNEL_KINDS}
+    kern = {k: v for k, v in stages.items() if k.split("@")[0] in KERNEL_KINDS}
     roofline = None
     if kern:
         dom = max(kern, key=lambda k: kern[k]["share"])
         d = kern[dom]
+        base = dom.split("@")[0]
         traffic = None
-        tr = ncu_traffic().get(dom)
+        tr = ncu_traffic().get(dom) or ncu_traffic().get(base)
         if tr and tr.get("elems"):
             traffic = tr["dram_bytes"] / tr["elems"] * d["avg_elems"]
         roofline = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
                     "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes_per_launch": d["avg_bytes"],
                     "avg_launch_ms": d["avg_ms"], "peak_source": peak_src}
-        roofline.update(same_mix_probe(dom, d["avg_elems"], d["avg_ms"]))
+        roofline.update(same_mix_probe(base, d["avg_elems"], d["avg_ms"]))
         rb = d.get("avg_remote_bytes", 0)
         if rb:
-            # fused NVLink kernel: the floor is the slower of local HBM bytes / HBM peak and
-            # peer bytes / NVLink peer bandwidth (770 GB/s per direction, measured; 900 nominal)
-            t_hbm = d["avg_bytes"] / (peak * 1e9)
-            t_nvl = rb / (NVLINK_PEER_GBS * 1e9)
-            roofline.update({"hbm_frac": d["GBps"] / peak, "nvlink_achieved": d["nvlink_GBps"],
-                             "nvlink_peak": NVLINK_PEER_GBS, "nvlink_frac": d["nvlink_GBps"] / NVLINK_PEER_GBS,
-                             "remote_bytes_per_launch": rb,
-                             "nvlink_frac_of_bidirectional_probe": d["nvlink_GBps"] / NVLINK_BIDIR_PROBE_GBS,
+            # fused NVLink kernel: local HBM moves its own bytes plus the bytes the peers
+            # read from it (served = remote, symmetric exchange); NVLink moves rb each way
+            # at once, so the floor is the slower of (bytes + served) / HBM peak and rb /
+            # the bidirectional peer-read peak measured in this run
+            hbm_b = d["avg_bytes"] + rb
+            t_hbm = hbm_b / (peak * 1e9)
+            t_nvl = rb / (nvl_bi * 1e9)
+            hbm_ach = hbm_b / (d["avg_ms"] * 1e-3) / 1e9
+            roofline.update({"achieved": hbm_ach, "frac": hbm_ach / peak, "hbm_frac": hbm_ach / peak,
+                             "served_bytes_per_launch": rb, "remote_bytes_per_launch": rb,
+                             "nvlink_achieved": d["nvlink_GBps"],
+                             "nvlink_peak_measured_bidirectional": nvl_bi, "nvlink_peak_measured_one_way": nvl_uni,
+                             "nvlink_frac": d["nvlink_GBps"] / nvl_bi,
+                             "nvlink_frac_of_one_way": d["nvlink_GBps"] / nvl_uni,
+                             "nvlink_frac_of_900": d["nvlink_GBps"] / NVLINK_NOMINAL_GBS,
                              "floor_ms": max(t_hbm, t_nvl) * 1e3, "frac_of_floor": max(t_hbm, t_nvl) * 1e3 / d["avg_ms"]})
             if t_nvl > t_hbm:
-                roofline.update({"bound": "nvlink", "achieved": d["nvlink_GBps"], "peak": NVLINK_PEER_GBS,
-                                 "frac": d["nvlink_GBps"] / NVLINK_PEER_GBS,
-                                 "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"})
+                roofline.update({"bound": "nvlink", "achieved": d["nvlink_GBps"], "peak": nvl_bi,
+                                 "frac": d["nvlink_GBps"] / nvl_bi,
+                                 "peak_source": ("hz_nvlink_probe in this run: both GPUs of each pair pulling "
+                                                 "at once, per direction" if nvl else "fallback bidirectional probe")})
     nccl = {k: v for k, v in stages.items() if k.startswith("nccl")}
     for v in nccl.values():
-        v["frac_of_nvlink_770"] = (v["GBps"] or 0) / NVLINK_PEER_GBS
+        v["frac_of_nvlink_one_way"] = (v["GBps"] or 0) / nvl_uni
 
     # cross-check of the per-kernel durations with CUDA events on the launching stream
     # (a separate eager pass: the events add stream operations between launches)
@@ -558,6 +602,13 @@ def run_hz(args):
     if world > 1 and not args.no_flat:
         flat = extra(flat_baseline, hz, ctx, torch, model, stream, world, args)
 
+    # eight GPUs: the other 8-rank hierarchy of BASELINE configs 2-4 in the same command
+    # ((2,4) and (2,2,2)), its own context and tensors, same timing discipline
+    alt = None
+    if world == 8 and not args.hierarchy and not args.no_alt:
+        other = (2, 2, 2) if tuple(group) == (2, 4) else (2, 4)
+        alt = extra(alt_hierarchy, hz, torch, args, other, rank, world, local, device)
+
     e2e = None
     if not args.no_e2e:
         e2e = extra(run_e2e, hz, ctx, torch, model, stream, world, args)
@@ -589,9 +640,12 @@ def run_hz(args):
         "clocks": clocks,
         "stages": stages,
         "step_model": smodel,
+        "nvlink_probe": nvl,
         "flat_zero3_baseline": flat,
         "step_tail": tail,
         "a10_cross_node_step": a10,
+        "alt_hierarchy": alt,
+        "topology": topology(world) if rank == 0 else None,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -611,6 +665,70 @@ def extra(fn, *a):
         return fn(*a)
     except Exception as e:  # noqa: BLE001
         return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
+def topology(world):
+    """nvidia-smi topo -m row of GPU0 (link class to every peer) — a box whose GPUs talk
+    over PCIe instead of NVLink would make the N > 1 numbers meaningless."""
+    if world < 2:
+        return None
+    try:
+        out = subprocess.run(["nvidia-smi", "topo", "-m"], capture_output=True, text=True, timeout=20).stdout
+        for line in out.splitlines():
+            f = line.split()
+            if f and f[0].endswith("GPU0"):
+                return {"gpu0_row": f[1:1 + world]}
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return None
+
+
+def alt_hierarchy(hz, torch, args, group, rank, world, local, device):
+    """One more 8-rank hierarchy in the same process: its own hz context (P2P), tensors
+    and captured step; K replays timed with CUDA events, max over ranks; per-level stages
+    from the in-kernel stamps."""
+    uid = hz.get_uid() if rank == 0 else None
+    import torch.distributed as dist
+    box = [uid]
+    dist.broadcast_object_list(box, src=0)
+    ctx = hz.Context(rank, world, box[0], group, local)
+    try:
+        ctx.enable_p2p(p2p_pool_bytes(args, group))
+        model = Model(hz, ctx, torch, args.config, rank, world, args, device)
+        stream = torch.cuda.current_stream()
+        for _ in range(max(args.warmup, 3)):
+            model.step(stream)
+        torch.cuda.synchronize()
+        hz.trace_begin(capacity=5 * len(model.tensors) * 4 + 64, events=False, stamps=True)
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cs):
+            ctx.p2p_capture_begin()
+            model.step(cs)
+            ctx.p2p_capture_end(cs)
+        torch.cuda.synchronize()
+        graph.replay()
+        ctx.p2p_replayed(1)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ctx.p2p_replayed(args.steps)
+        hz.trace_end()
+        ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
+        stages = summarize_trace(hz.trace_read(), 1)
+        del graph
+        torch.cuda.synchronize()
+        return {"hierarchy": list(group), "ms_per_step": ms, "unit": UNIT,
+                "value": world * model.logical_bytes / (ms * 1e-3) / 1e9, "stages": stages}
+    finally:
+        ctx.close()
 
 
 def flat_baseline(hz, ctx, torch, model, stream, world, args):

@@ -355,6 +355,15 @@ HZ_API hz_status hz_init_virtual(hz_ctx** out, int world, int levels, const int*
  * returns HZ_ERR_ABORTED / HZ_ERR_NCCL (asynchronous errors of any of the context's
  * NCCL communicators, which are then aborted) or HZ_OK without enqueuing anything. */
 HZ_API hz_status hz_set_wait_timeout(hz_ctx* ctx, double seconds);
+
+/* Measurement helper (bench.py's NVLink roofline denominator):
+ * reads `bytes` (a multiple of 16, within the pool) of rank `peer`'s symmetric pool
+ * `reps` times with the load path of the fused gather / reduce kernels (16-byte
+ * coherent loads, a full grid) on `stream`, after one warm-up read, and writes the
+ * average milliseconds per read to *ms_out (synchronises the stream).  Not a
+ * collective: run it on several ranks at once (after a barrier) to measure both
+ * directions of a link loaded together.  Errors: HZ_ERR_INVALID, HZ_ERR_CUDA. */
+HZ_API hz_status hz_nvlink_probe(hz_ctx* ctx, int peer, size_t bytes, int reps, float* ms_out, void* stream);
 HZ_API hz_status hz_abort(hz_ctx* ctx);
 HZ_API hz_status hz_check(const hz_ctx* ctx);
 

@@ -98,6 +98,8 @@ struct AdamW {
 cudaError_t launch_adamw(const float* g, float* th, float* m, float* v, void* out, hz_dtype out_dt, int64_t n,
                          const AdamW& hp, cudaStream_t st, const SyncArgs* sync);
 cudaError_t launch_gather_copy(const Pieces& pc, void* out, cudaStream_t st, const SyncArgs* sync);
+// NVLink probe (hz_nvlink_probe): read `bytes` of (peer) memory at src, XOR into sink[grid]
+cudaError_t launch_peer_read(const void* src, int64_t bytes, unsigned* sink, cudaStream_t st);
 // out[i] = ((c[0][i] + c[1][i]) + ...) + c[n-1][i] over fp32 pieces (Pieces::c as
 // float arrays of n elements, n % 4 == 0; the pieces may be peer-mapped)
 cudaError_t launch_sum_f32(const Pieces& pc, int64_t n, float* out, cudaStream_t st, const SyncArgs* sync);

@@ -215,3 +215,40 @@ cudaError_t launch_gather_copy(const Pieces& pc, void* out, cudaStream_t st, con
 }
 
 }  // namespace hz
+
+// ---------------------------------------------------------------- NVLink probe
+// hz_nvlink_probe: how fast this GPU's SMs pull a peer's memory with the same load
+// path the fused gather / reduce kernels use (16-byte HZ_PEER_LD loads, U in flight
+// per thread, grid = SMs x resident CTAs).  The XOR of what a CTA read goes to
+// sink[blockIdx.x] so the loads cannot be elided.
+namespace hz {
+namespace {
+template <int U>
+__global__ void __launch_bounds__(dev::kThreads) k_peer_read(const uint4* __restrict__ src, int64_t n16,
+                                                            unsigned* __restrict__ sink) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * dev::kThreads + threadIdx.x;
+  const int64_t nth = static_cast<int64_t>(gridDim.x) * dev::kThreads;
+  unsigned acc = 0;
+  for (int64_t base = tid; base < n16; base += nth * U) {
+    uint4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * nth;
+      r[u] = i < n16 ? HZ_PEER_LD(src + i) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc ^= r[u].x ^ r[u].y ^ r[u].z ^ r[u].w;
+  }
+  acc = __reduce_xor_sync(0xffffffffu, acc);
+  if ((threadIdx.x & 31) == 0) atomicXor(sink + blockIdx.x, acc);
+}
+}  // namespace
+
+cudaError_t launch_peer_read(const void* src, int64_t bytes, unsigned* sink, cudaStream_t st) {
+  constexpr int U = 8;
+  auto kern = k_peer_read<U>;
+  const int64_t n16 = bytes / 16;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (n16 + 32 * U - 1) / (32 * U));
+  return launch_k(kern, grid, st, static_cast<const uint4*>(src), n16, sink);
+}
+}  // namespace hz

@@ -770,6 +770,38 @@ hz_status hz_check(const hz_ctx* ctx) {
   return HZ_OK;
 }
 
+hz_status hz_nvlink_probe(hz_ctx* ctx, int peer, size_t bytes, int reps, float* ms_out, void* stream) {
+  using namespace hz;
+  if (!ctx || !ms_out) return fail(HZ_ERR_INVALID, "ctx/ms_out: NULL");
+  if (!ctx->p2p.on) return fail(HZ_ERR_INVALID, "ctx: P2P not enabled");
+  if (peer < 0 || peer >= ctx->world) return fail(HZ_ERR_INVALID, "peer: must be in [0, world)");
+  if (reps < 1) return fail(HZ_ERR_INVALID, "reps: must be >= 1");
+  auto& P = ctx->p2p;
+  if (bytes < 16 || bytes % 16 || kPoolHeader + bytes > P.bytes)
+    return fail(HZ_ERR_INVALID, "bytes: must be a positive multiple of 16 within the pool");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned* sink = nullptr;
+  cudaEvent_t a = nullptr, b = nullptr;
+  P2P_CUDA(cudaMalloc(&sink, 4 * 4096), "probe sink cudaMalloc");
+  P2P_CUDA(cudaMemsetAsync(sink, 0, 4 * 4096, st), "probe sink memset");
+  P2P_CUDA(cudaEventCreate(&a), "probe event");
+  P2P_CUDA(cudaEventCreate(&b), "probe event");
+  const char* src = P.peer[peer] + kPoolHeader;
+  P2P_CUDA(launch_peer_read(src, static_cast<int64_t>(bytes), sink, st), "probe warm-up launch");
+  P2P_CUDA(cudaEventRecord(a, st), "probe event record");
+  for (int i = 0; i < reps; ++i) P2P_CUDA(launch_peer_read(src, static_cast<int64_t>(bytes), sink, st), "probe launch");
+  P2P_CUDA(cudaEventRecord(b, st), "probe event record");
+  P2P_CUDA(cudaEventSynchronize(b), "probe sync");
+  float ms = 0.f;
+  P2P_CUDA(cudaEventElapsedTime(&ms, a, b), "probe elapsed");
+  *ms_out = ms / reps;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  clear_error();
+  return HZ_OK;
+}
+
 hz_status hz_p2p_capture_begin(hz_ctx* ctx) {
   using namespace hz;
   if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");

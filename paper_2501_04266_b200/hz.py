@@ -182,6 +182,7 @@ _sig("hz_enable_p2p", [_vp, ctypes.c_size_t])
 _sig("hz_init_virtual", [ctypes.POINTER(_vp), _int, _int, ctypes.POINTER(ctypes.c_int), _int, ctypes.c_size_t])
 _sig("hz_set_wait_timeout", [_vp, ctypes.c_double])
 _sig("hz_abort", [_vp])
+_sig("hz_nvlink_probe", [_vp, _int, ctypes.c_size_t, _int, ctypes.POINTER(ctypes.c_float), _vp])
 _sig("hz_check", [_vp])
 _sig("hz_partition_set_hops", [ctypes.POINTER(Partition), _int, ctypes.POINTER(ctypes.c_int)])
 _sig("hz_p2p_enabled", [_vp, ctypes.POINTER(ctypes.c_int)])
@@ -440,6 +441,12 @@ class Context:
     def abort(self):
         """hz_abort: abort the context (waiting kernels return; later calls fail)."""
         _check(_lib.hz_abort(self._h))
+
+    def nvlink_probe(self, peer, nbytes, reps=5, stream=None):
+        """hz_nvlink_probe: ms per read of nbytes of rank peer's pool (SM loads)."""
+        ms = ctypes.c_float(0.0)
+        _check(_lib.hz_nvlink_probe(self._h, int(peer), int(nbytes), int(reps), ctypes.byref(ms), _stream(stream)))
+        return ms.value
 
     def check(self):
         """hz_check: raises HZError(ERR_ABORTED / ERR_NCCL) if the context is dead."""
