@@ -346,6 +346,18 @@ HZ_API hz_status hz_p2p_enabled(const hz_ctx* ctx, int* out);
 HZ_API hz_status hz_init_virtual(hz_ctx** out, int world, int levels, const int* group, int cuda_device,
                                  size_t pool_bytes);
 
+/* hz_init_virtual with rank r's pool and kernels on GPU devices[r] (devices: `world`
+ * ordinals; ranks on different GPUs read each other's pools over NVLink through peer
+ * access, enabled here; HZ_ERR_UNSUPPORTED if two of the devices cannot map each
+ * other).  Same protocol and host ordering as hz_init_virtual: every kernel starts
+ * after the kernels it waits for have completed, so a profiler that serialises
+ * launches (ncu) can replay the P2P exchange kernels of a real multi-GPU exchange
+ * from one process (tools/vw_profile.py).  Each rank's thread must make devices[r]
+ * current before calling into its context.  hz_init_virtual(..., d, ...) ==
+ * hz_init_virtual_ex with devices[r] = d for every r. */
+HZ_API hz_status hz_init_virtual_ex(hz_ctx** out, int world, int levels, const int* group, const int* devices,
+                                    size_t pool_bytes);
+
 /* Failure handling of the P2P transport.  A kernel waits for its peers'
  * phase flags at most `seconds` (default 600 s, so checkpoint saves or evaluation on
  * one rank do not break the others); a longer wait, or hz_abort (from any host thread,

@@ -52,7 +52,7 @@ const char* const kSymbols[] = {
     "hz_enable_p2p",       "hz_p2p_enabled",         "hz_sym_alloc",
     "hz_p2p_capture_begin", "hz_p2p_capture_end",    "hz_p2p_replayed",
     "hz_adamw_step",       "hz_set_sm_budget",     "hz_allreduce_select", "hz_step_host", "hz_allgather_params_next", "hz_backward_step",
-    "hz_partition_set_hops", "hz_init_virtual",    "hz_set_wait_timeout",
+    "hz_partition_set_hops", "hz_init_virtual",    "hz_init_virtual_ex",    "hz_set_wait_timeout",
     "hz_abort",            "hz_check",             "hz_adamw_params",
     "hz_nvlink_probe",
 };

@@ -1,4 +1,5 @@
-// Virtual world (hz_init_virtual): W hz contexts in ONE process on ONE GPU, whose
+// Virtual world (hz_init_virtual): W hz contexts in ONE process on ONE GPU (or, with
+// hz_init_virtual_ex, on several GPUs of this process with peer access), whose
 // "peer" pools are each other's allocations — the product's P2P exchange kernels,
 // flags and phase protocol, without IPC or NCCL.  It exists so that the multi-rank
 // path (multi-piece gathers, hop groups, the level-local protocol) can be checked
@@ -46,6 +47,7 @@ struct VWorld {
   std::deque<Ent> ready[kMaxWorld][kMaxWorld];   // [source][target]
   std::deque<Ent> done[kMaxWorld][kMaxWorld];
   char* pools[kMaxWorld] = {nullptr};
+  int devices[kMaxWorld] = {0};
 };
 
 namespace {
@@ -129,16 +131,25 @@ void vw_release(hz_ctx* ctx) {
     last = --vw->refs == 0;
   }
   if (!last) return;
-  cudaDeviceSynchronize();
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int q = 0; q < vw->world; ++q) {
+    cudaSetDevice(vw->devices[q]);
+    cudaDeviceSynchronize();
+  }
   for (int q = 0; q < vw->world; ++q)
-    if (vw->pools[q]) cudaFree(vw->pools[q]);
+    if (vw->pools[q]) {
+      cudaSetDevice(vw->devices[q]);
+      cudaFree(vw->pools[q]);
+    }
+  cudaSetDevice(cur);
   delete vw;
 }
 
 }  // namespace hz
 
-extern "C" hz_status hz_init_virtual(hz_ctx** out, int world, int levels, const int* group, int cuda_device,
-                                     size_t pool_bytes) {
+extern "C" hz_status hz_init_virtual_ex(hz_ctx** out, int world, int levels, const int* group, const int* devices,
+                                        size_t pool_bytes) {
   using namespace hz;
   if (!out) return fail(HZ_ERR_INVALID, "out: NULL");
   if (!group) return fail(HZ_ERR_INVALID, "group: NULL");
@@ -150,17 +161,40 @@ extern "C" hz_status hz_init_virtual(hz_ctx** out, int world, int levels, const 
   }
   if (world < 1 || prod != world) return fail(HZ_ERR_INVALID, "group: product must equal world");
   if (world > kMaxWorld) return fail(HZ_ERR_UNSUPPORTED, "virtual world: at most 8 ranks");
-  if (cuda_device < 0) return fail(HZ_ERR_INVALID, "cuda_device: negative");
+  if (!devices) return fail(HZ_ERR_INVALID, "devices: NULL");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  for (int r = 0; r < world; ++r)
+    if (devices[r] < 0 || devices[r] >= ndev)
+      return fail(HZ_ERR_INVALID, "devices[" + std::to_string(r) + "]: no such CUDA device");
+  // ranks on different GPUs read each other's pools directly (same process: peer
+  // access instead of IPC)
+  for (int a = 0; a < world; ++a)
+    for (int b = 0; b < world; ++b) {
+      if (devices[a] == devices[b]) continue;
+      int can = 0;
+      if ((e = cudaDeviceCanAccessPeer(&can, devices[a], devices[b])) != cudaSuccess)
+        return cuda_fail(e, "cudaDeviceCanAccessPeer");
+      if (!can) return fail(HZ_ERR_UNSUPPORTED, "virtual world: no peer access between the devices of ranks " +
+                                                    std::to_string(a) + " and " + std::to_string(b));
+      if ((e = cudaSetDevice(devices[a])) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+      e = cudaDeviceEnablePeerAccess(devices[b], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        (void)cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
   for (int r = 0; r < world; ++r) out[r] = nullptr;
-  cudaError_t e = cudaSetDevice(cuda_device);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   const size_t gran = size_t(2) << 20;
   const size_t total = (kPoolHeader + pool_bytes + gran - 1) / gran * gran;
   VWorld* vw = new VWorld();
   vw->world = world;
   hz_status rc = HZ_OK;
   for (int r = 0; r < world && rc == HZ_OK; ++r) {
-    if ((e = cudaMalloc(&vw->pools[r], total)) != cudaSuccess ||
+    vw->devices[r] = devices[r];
+    if ((e = cudaSetDevice(devices[r])) != cudaSuccess || (e = cudaMalloc(&vw->pools[r], total)) != cudaSuccess ||
         (e = cudaMemset(vw->pools[r], 0, kPoolHeader)) != cudaSuccess)
       rc = cuda_fail(e, "virtual world: pool cudaMalloc");
   }
@@ -169,7 +203,12 @@ extern "C" hz_status hz_init_virtual(hz_ctx** out, int world, int levels, const 
     ctx->rank = r;
     ctx->world = world;
     ctx->levels = levels;
-    ctx->device = cuda_device;
+    ctx->device = devices[r];
+    if ((e = cudaSetDevice(devices[r])) != cudaSuccess) {
+      rc = cuda_fail(e, "cudaSetDevice");
+      delete ctx;
+      break;
+    }
     int stride = 1;
     for (int l = 0; l < levels; ++l) {
       ctx->group[l] = group[l];
@@ -202,4 +241,14 @@ extern "C" hz_status hz_init_virtual(hz_ctx** out, int world, int levels, const 
   }
   clear_error();
   return HZ_OK;
+}
+
+extern "C" hz_status hz_init_virtual(hz_ctx** out, int world, int levels, const int* group, int cuda_device,
+                                     size_t pool_bytes) {
+  using namespace hz;
+  if (cuda_device < 0) return fail(HZ_ERR_INVALID, "cuda_device: negative");
+  if (world < 1 || world > kMaxWorld) return hz_init_virtual_ex(out, world, levels, group, nullptr, pool_bytes);
+  int dev[kMaxWorld];
+  for (int r = 0; r < world; ++r) dev[r] = cuda_device;
+  return hz_init_virtual_ex(out, world, levels, group, dev, pool_bytes);
 }

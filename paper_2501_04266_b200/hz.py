@@ -180,6 +180,8 @@ _sig("hz_trace_end", [])
 _sig("hz_trace_read", [ctypes.POINTER(TraceRec), _int, ctypes.POINTER(ctypes.c_int)])
 _sig("hz_enable_p2p", [_vp, ctypes.c_size_t])
 _sig("hz_init_virtual", [ctypes.POINTER(_vp), _int, _int, ctypes.POINTER(ctypes.c_int), _int, ctypes.c_size_t])
+_sig("hz_init_virtual_ex", [ctypes.POINTER(_vp), _int, _int, ctypes.POINTER(ctypes.c_int),
+                            ctypes.POINTER(ctypes.c_int), ctypes.c_size_t])
 _sig("hz_set_wait_timeout", [_vp, ctypes.c_double])
 _sig("hz_abort", [_vp])
 _sig("hz_nvlink_probe", [_vp, _int, ctypes.c_size_t, _int, ctypes.POINTER(ctypes.c_float), _vp])
@@ -641,10 +643,11 @@ class Context:
         return out_chunk
 
 
-def virtual_world(group, device=0, pool_bytes=64 << 20, cumulative=False):
+def virtual_world(group, device=0, pool_bytes=64 << 20, cumulative=False, devices=None):
     """hz_init_virtual: one Context per rank of hierarchy ``group``, all in this process
     on GPU ``device``, P2P-enabled with each other's pools as peers.  Drive each from
-    its own thread (tests/vworld.py)."""
+    its own thread (tests/vworld.py).  ``devices`` (one ordinal per rank):
+    hz_init_virtual_ex, rank r on GPU devices[r] (peer access over NVLink)."""
     g = list(group)
     if cumulative:
         rel, prev = [], 1
@@ -657,5 +660,11 @@ def virtual_world(group, device=0, pool_bytes=64 << 20, cumulative=False):
         world *= x
     arr, L = _groups(g)
     hs = (_vp * world)()
-    _check(_lib.hz_init_virtual(hs, world, L, arr, device, int(pool_bytes)))
-    return [Context._wrap(_vp(hs[r]), r, world, g, device) for r in range(world)]
+    if devices is None:
+        _check(_lib.hz_init_virtual(hs, world, L, arr, device, int(pool_bytes)))
+        return [Context._wrap(_vp(hs[r]), r, world, g, device) for r in range(world)]
+    devs = [int(d) for d in devices]
+    if len(devs) != world:
+        raise ValueError(f"devices: {len(devs)} ordinals for a world of {world}")
+    _check(_lib.hz_init_virtual_ex(hs, world, L, arr, (ctypes.c_int * world)(*devs), int(pool_bytes)))
+    return [Context._wrap(_vp(hs[r]), r, world, g, devs[r]) for r in range(world)]

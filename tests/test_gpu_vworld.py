@@ -34,6 +34,24 @@ def test_vworld_hierarchy(g):
     assert not errors, "\n".join(errors[:20])
 
 
+@pytest.mark.multigpu
+@pytest.mark.parametrize("g", [(2,), (2, 2), (2, 2, 2)], ids=lambda g: "x".join(map(str, g)))
+def test_vworld_multi_device(g):
+    """hz_init_virtual_ex: rank r on GPU r % ngpu, so pair partners sit on different
+    GPUs and every gather / qgZ piece of a partner crosses NVLink (peer access, one
+    process); the same bitwise checks as on one GPU."""
+    _need_gpu()
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    from paper_2501_04266_b200 import hz
+    from tests import mp_parity, vworld
+    devices = [r % n for r in range(int(np.prod(g)))]
+    errors = vworld.run_ranks(hz, g, lambda r, w, ctx: mp_parity.check_hierarchy(hz, r, w, g, None, 0, vctx=ctx),
+                              devices=devices)
+    assert not errors, "\n".join(errors[:20])
+
+
 @pytest.mark.parametrize("B", [64, 1024])
 def test_vworld_block_sizes(B):
     _need_gpu()

@@ -12,20 +12,21 @@ import traceback
 import torch
 
 
-def run_ranks(hz, group, fn, pool_bytes=96 << 20, device=0, timeout_s=300.0, ranks=None, ctxs=None):
+def run_ranks(hz, group, fn, pool_bytes=96 << 20, device=0, timeout_s=300.0, ranks=None, ctxs=None, devices=None):
     """Run fn(rank, world, ctx) -> list of error strings in one thread per rank (each on
-    its own stream).  Returns all errors (exceptions included, with their rank).
-    ``ranks``: only these ranks run (the others stay idle); ``ctxs``: reuse contexts."""
+    its own stream, on its context's GPU).  Returns all errors (exceptions included,
+    with their rank).  ``ranks``: only these ranks run (the others stay idle);
+    ``ctxs``: reuse contexts; ``devices``: rank r on GPU devices[r] (hz_init_virtual_ex)."""
     own = ctxs is None
     if own:
-        ctxs = hz.virtual_world(group, device=device, pool_bytes=pool_bytes)
+        ctxs = hz.virtual_world(group, device=device, pool_bytes=pool_bytes, devices=devices)
         for c in ctxs:
             c.set_wait_timeout(timeout_s)
     world = len(ctxs)
     errors = {r: [] for r in range(world)}
 
     def body(r):
-        torch.cuda.set_device(device)
+        torch.cuda.set_device(ctxs[r].device)
         st = torch.cuda.Stream()
         try:
             with torch.cuda.stream(st):
@@ -39,7 +40,8 @@ def run_ranks(hz, group, fn, pool_bytes=96 << 20, device=0, timeout_s=300.0, ran
         t.start()
     for t in threads:
         t.join()
-    torch.cuda.synchronize()
+    for d in sorted({c.device for c in ctxs}):
+        torch.cuda.synchronize(d)
     if own:
         for c in ctxs:
             c.close()
