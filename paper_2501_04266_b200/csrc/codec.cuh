@@ -382,20 +382,21 @@ __device__ __forceinline__ int64_t num_warps() {
 
 // host-side grid sizing (codec_util.cu): grid-stride kernels get
 // min(ceil(warp_tasks / warps per CTA), SMs x resident CTAs of that kernel).
-int64_t grid_for(const void* kernel, int64_t warp_tasks);
+int64_t grid_for(const void* kernel, int64_t warp_tasks, int dyn_smem = 0);
 int sm_count();   // SMs of the current device (cached)
 
-// Every libhz kernel launch: kThreads per CTA, no dynamic shared memory, and the
+// Every libhz kernel launch: kThreads per CTA, dynamic shared memory only for the link
+// kernels (launch_k_smem; grid_for with the same dyn_smem sets the opt-in limit), and the
 // programmatic-stream-serialization attribute when HZ_TUNE pdl=1 (PDL; off by
 // default, see pdl_enabled) — the kernel's prologue (sync_wait) then orders it after
 // the previous kernel on the stream.
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>
-cudaError_t launch_k(void (*kern)(KArgs...), int64_t grid, cudaStream_t st, Args&&... args) {
+cudaError_t launch_k_smem(void (*kern)(KArgs...), int64_t grid, int dyn_smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(dev::kThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = static_cast<size_t>(dyn_smem);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -403,6 +404,10 @@ cudaError_t launch_k(void (*kern)(KArgs...), int64_t grid, cudaStream_t st, Args
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), int64_t grid, cudaStream_t st, Args&&... args) {
+  return launch_k_smem(kern, grid, 0, st, std::forward<Args>(args)...);
 }
 
 }  // namespace hz

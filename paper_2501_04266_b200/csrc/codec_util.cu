@@ -23,18 +23,37 @@ int sm_count() {
 
 namespace {
 
-int resident_ctas(const void* kernel) {
+// per (device, kernel, dynamic shared memory); a kernel with dynamic shared memory above
+// the default 48 KB gets the opt-in attribute first (per device)
+int resident_ctas(const void* kernel, int dyn_smem) {
   static std::mutex mu;
-  static std::unordered_map<const void*, int> cache;
+  struct Key {
+    int dev;
+    const void* k;
+    int smem;
+    bool operator==(const Key& o) const { return dev == o.dev && k == o.k && smem == o.smem; }
+  };
+  struct H {
+    size_t operator()(const Key& x) const {
+      return std::hash<const void*>()(x.k) ^ (static_cast<size_t>(x.smem) << 8) ^ static_cast<size_t>(x.dev);
+    }
+  };
+  static std::unordered_map<Key, int, H> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(kernel);
+  const Key key{dev, kernel, dyn_smem};
+  auto it = cache.find(key);
   if (it != cache.end()) return it->second;
+  if (dyn_smem > 48 * 1024 &&
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem) != cudaSuccess)
+    cudaGetLastError();
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, dev::kThreads, 0) != cudaSuccess || n < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, dev::kThreads, dyn_smem) != cudaSuccess || n < 1) {
     cudaGetLastError();
     n = 1;
   }
-  cache[kernel] = n;
+  cache[key] = n;
   return n;
 }
 
@@ -42,12 +61,12 @@ int resident_ctas(const void* kernel) {
 
 std::atomic<int> g_sm_budget{0};
 
-int64_t grid_for(const void* kernel, int64_t warp_tasks) {
+int64_t grid_for(const void* kernel, int64_t warp_tasks, int dyn_smem) {
   const int64_t per_cta = dev::kThreads / 32;
   const int64_t need = (warp_tasks + per_cta - 1) / per_cta;
   const int budget = g_sm_budget.load(std::memory_order_relaxed);
   const int sms = budget > 0 && budget < sm_count() ? budget : sm_count();
-  int64_t cap = static_cast<int64_t>(sms) * resident_ctas(kernel);
+  int64_t cap = static_cast<int64_t>(sms) * resident_ctas(kernel, dyn_smem);
   // HZ_TUNE grid_np=k: non-persistent grids of up to k x the resident capacity
   // (short CTAs the block scheduler can interleave with other streams' kernels)
   static const int np = tune_param("grid_np", 0);

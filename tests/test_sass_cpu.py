@@ -80,3 +80,21 @@ def test_dual_kernel_default_variant_fits_64_registers(resources):
     one_pass = [r for f, r in resources.items() if "k_gather_quantize" in f and "Li0ELb0ELi4E" in f]
     assert one_pass
     assert all(r["REG"] <= 64 and r.get("STACK", 0) == 0 for r in one_pass), one_pass
+
+
+def test_link_kernels_use_tma_bulk_copies(sass, resources):
+    """The link-CTA dual kernel (k_gather_quantize_link) and the TMA-staged level reduce
+    (k_reduce_tma) move peer tiles with cp.async.bulk (SASS UBLKCP) completed on
+    mbarriers (SYNCS.ARRIVE.TRANS64 / SYNCS.PHASECHK), keep 4 CTAs per SM (<= 64
+    registers) and no FMA in the fp32 sums of the reduce."""
+    for kind in ("k_gather_quantize_link", "k_reduce_tma"):
+        names = [f for f in sass if kind in f]
+        assert names, f"{kind} not in the SASS"
+        for f in names:
+            text = "\n".join(sass[f])
+            assert "UBLKCP" in text, f"no bulk copy in {f}"
+            assert "SYNCS.ARRIVE.TRANS64" in text and "SYNCS.PHASECHK" in text, f"no mbarrier in {f}"
+            assert resources[f]["REG"] <= 64, (f, resources[f])
+    f32 = [f for f in sass if "k_reduce_tma" in f and re.search(r"k_reduce_tmaILi[48]ELi\d+ELi[01]E", f)]
+    assert f32
+    assert not [f for f in f32 if any("FFMA" in l for l in sass[f])]
