@@ -535,12 +535,22 @@ def run_hz(args):
         d = kern[dom]
         base = dom.split("@")[0]
         traffic = None
-        tr = ncu_traffic().get(dom) or ncu_traffic().get(base)
+        nt = ncu_traffic()
+        # N > 1: the per-element bytes of the same kernel captured in an N-GPU exchange
+        # (tools/vw_profile.py under ncu, key "<kind>@N<n>"); N = 1: the world-1 capture
+        tr = (nt.get(f"{dom}@N{world}") or nt.get(f"{base}@N{world}")) if world > 1 else (nt.get(dom) or nt.get(base))
+        nvl_traffic = None
         if tr and tr.get("elems"):
             traffic = tr["dram_bytes"] / tr["elems"] * d["avg_elems"]
+            if tr.get("nvlink_rx_bytes") is not None:
+                nvl_traffic = {"rx": tr["nvlink_rx_bytes"] / tr["elems"] * d["avg_elems"],
+                               "tx": tr["nvlink_tx_bytes"] / tr["elems"] * d["avg_elems"],
+                               "source": tr.get("source")}
         roofline = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
                     "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes_per_launch": d["avg_bytes"],
                     "avg_launch_ms": d["avg_ms"], "peak_source": peak_src}
+        if nvl_traffic:
+            roofline["nvlink_traffic"] = nvl_traffic   # ncu nvlrx/nvltx bytes per launch (protocol included)
         roofline.update(same_mix_probe(base, d["avg_elems"], d["avg_ms"]))
         rb = d.get("avg_remote_bytes", 0)
         if rb:

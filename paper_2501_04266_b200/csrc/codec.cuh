@@ -72,6 +72,10 @@ struct In8<float> {
     r[0] = __ldg(reinterpret_cast<const uint4*>(p));
     r[1] = __ldg(reinterpret_cast<const uint4*>(p) + 1);
   }
+  __device__ __forceinline__ void load_shared(const float* p) {   // tile engine: a staged tile
+    r[0] = reinterpret_cast<const uint4*>(p)[0];
+    r[1] = reinterpret_cast<const uint4*>(p)[1];
+  }
   __device__ __forceinline__ void get(float (&v)[8]) const {
     v[0] = __uint_as_float(r[0].x); v[1] = __uint_as_float(r[0].y);
     v[2] = __uint_as_float(r[0].z); v[3] = __uint_as_float(r[0].w);
@@ -86,6 +90,7 @@ struct In8<__nv_bfloat16> {
   __device__ __forceinline__ void load(const __nv_bfloat16* p) {
     r = __ldg(reinterpret_cast<const uint4*>(p));
   }
+  __device__ __forceinline__ void load_shared(const __nv_bfloat16* p) { r = *reinterpret_cast<const uint4*>(p); }
   __device__ __forceinline__ void get(float (&v)[8]) const {
     // bf16 -> fp32 is a 16-bit left shift: exact (subnormals included).
     v[0] = __uint_as_float(r.x << 16); v[1] = __uint_as_float(r.x & 0xffff0000u);
@@ -101,6 +106,7 @@ struct In8<__half> {
   __device__ __forceinline__ void load(const __half* p) {
     r = __ldg(reinterpret_cast<const uint4*>(p));
   }
+  __device__ __forceinline__ void load_shared(const __half* p) { r = *reinterpret_cast<const uint4*>(p); }
   __device__ __forceinline__ void get(float (&v)[8]) const {
     const unsigned w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
@@ -127,6 +133,7 @@ template <>
 struct Codes8<8> {
   uint2 r;
   __device__ __forceinline__ void load(const uint8_t* p) { r = HZ_PEER_LD(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ void load_shared(const void* p) { r = *reinterpret_cast<const uint2*>(p); }
   __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<uint2*>(p) = r; }
   __device__ __forceinline__ void zero() { r = make_uint2(0u, 0u); }
   // exact float value of each code
@@ -150,6 +157,7 @@ template <>
 struct Codes8<4> {
   unsigned r;
   __device__ __forceinline__ void load(const uint8_t* p) { r = HZ_PEER_LD(reinterpret_cast<const unsigned*>(p)); }
+  __device__ __forceinline__ void load_shared(const void* p) { r = *reinterpret_cast<const unsigned*>(p); }
   __device__ __forceinline__ void store(uint8_t* p) const { *reinterpret_cast<unsigned*>(p) = r; }
   __device__ __forceinline__ void zero() { r = 0u; }
   __device__ __forceinline__ void decode(float (&c)[8]) const {
@@ -180,6 +188,7 @@ template <>
 struct Codes4<8> {
   unsigned r;
   __device__ __forceinline__ void load(const uint8_t* p) { r = HZ_PEER_LD(reinterpret_cast<const unsigned*>(p)); }
+  __device__ __forceinline__ void load_shared(const void* p) { r = *reinterpret_cast<const unsigned*>(p); }
   __device__ __forceinline__ void decode(float (&c)[4]) const {
     const unsigned x = r ^ 0x80808080u;
 #pragma unroll
@@ -193,6 +202,7 @@ struct Codes4<4> {
   __device__ __forceinline__ void load(const uint8_t* p) {
     r = HZ_PEER_LD(reinterpret_cast<const unsigned short*>(p));
   }
+  __device__ __forceinline__ void load_shared(const void* p) { r = *reinterpret_cast<const unsigned short*>(p); }
   __device__ __forceinline__ void decode(float (&c)[4]) const {
     const unsigned x = static_cast<unsigned>(r) ^ 0x8888u;   // nibble ^ 8 = code + 8
     const unsigned ev = x & 0x0F0Fu;

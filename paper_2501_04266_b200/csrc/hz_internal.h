@@ -80,6 +80,20 @@ bool gather_quantize_supported(int block, int gather_bits, hz_dtype out_dt);
 cudaError_t launch_gather_quantize(const Pieces& pc, int64_t n_gather, void* y, const void* x, hz_dtype dt,
                                    int64_t n_q, int qbits, uint8_t* codes, float* scales, float* qy, int acc,
                                    cudaStream_t st, const SyncArgs& sy);
+// The TMA tile engine (k_tiles.cu): the same operations as the launchers above with
+// every byte moved by bulk copy.  Each returns cudaErrorNotSupported (nothing launched)
+// when the shape does not qualify: block != 256, a length not a multiple of 1024, a
+// buffer not 16-byte aligned, an accumulating round trip, HZ_TUNE tma=0.
+bool tiles_on();
+cudaError_t tiles_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int block, uint8_t* codes, float* scales,
+                           void* y, hz_dtype out_dt, int acc, cudaStream_t st, const SyncArgs& sy);
+cudaError_t tiles_gather(const Pieces& pc, int bits, int block, void* y, hz_dtype out_dt, cudaStream_t st,
+                         const SyncArgs& sy);
+cudaError_t tiles_dual(const Pieces& pc, void* y, const void* x, hz_dtype dt, int64_t nq, int qbits, uint8_t* codes,
+                       float* scales, float* qy, int acc, cudaStream_t st, const SyncArgs& sy);
+cudaError_t tiles_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in, int block,
+                         int bits_out, uint8_t* oc, float* os, float* of, int acc, cudaStream_t st,
+                         const SyncArgs& sy);
 // gather+dequantize (8-bit codes, B = 256, bf16 out) with link CTAs for the remote
 // pieces (k_quantize.cu); cudaErrorNotSupported if the launch does not qualify
 cudaError_t launch_gather_link(const Pieces& pc, void* y, cudaStream_t st, const SyncArgs& sy);

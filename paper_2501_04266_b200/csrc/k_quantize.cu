@@ -590,6 +590,10 @@ cudaError_t launch_quantize_roundtrip(const void* x, hz_dtype dt, int64_t n, int
   const SyncArgs sy = sync ? *sync : SyncArgs{};
   if (block != 256) return cudaErrorInvalidValue;
   if (n == 0 && !sync) return cudaSuccess;
+  {
+    const cudaError_t e = tiles_quantize(x, dt, n, bits, block, codes, scales, y, out_dt, acc, st, sy);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (dt) {
     case HZ_F32:
       return bits == 8 ? roundtrip_t<float, 8>(x, n, codes, scales, y, out_dt, acc, st, sy)
@@ -608,6 +612,10 @@ cudaError_t launch_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int
                             uint8_t* codes, float* scales, cudaStream_t st, const SyncArgs* sync) {
   const SyncArgs sy = sync ? *sync : SyncArgs{};
   if (n == 0 && !sync) return cudaSuccess;
+  {
+    const cudaError_t e = tiles_quantize(x, dt, n, bits, block, codes, scales, nullptr, HZ_BF16, 0, st, sy);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (dt) {
     case HZ_F32: return quantize_d<float>(x, n, bits, block, codes, scales, st, sy);
     case HZ_BF16: return quantize_d<__nv_bfloat16>(x, n, bits, block, codes, scales, st, sy);
@@ -637,6 +645,10 @@ bool gather_quantize_supported(int block, int gather_bits, hz_dtype out_dt) {
 cudaError_t launch_gather_quantize(const Pieces& pc, int64_t n_gather, void* y, const void* x, hz_dtype dt,
                                    int64_t n_q, int qbits, uint8_t* codes, float* scales, float* qy, int acc,
                                    cudaStream_t st, const SyncArgs& sy) {
+  if (pc.n * pc.len == n_gather) {
+    const cudaError_t e = tiles_dual(pc, y, x, dt, n_q, qbits, codes, scales, qy, acc, st, sy);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (dt) {
     case HZ_F32: return gather_quantize_d<float>(pc, n_gather, y, x, n_q, qbits, codes, scales, qy, acc, st, sy);
     case HZ_BF16:

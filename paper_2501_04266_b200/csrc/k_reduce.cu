@@ -596,6 +596,11 @@ cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const
   a.oc = out_codes;
   a.os = out_scales;
   a.of = out_f32;
+  {
+    const cudaError_t e = tiles_reduce(g, codes, scales, n, bits_in, block, bits_out, out_codes, out_scales, out_f32,
+                                       accumulate, st, sy);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (reduce_tma_ok(a, block, sy)) {
     if (bits_out == 0) {
       if (accumulate) return bits_in == 8 ? reduce_tma_g<8, 1, 0>(a, st, sy) : reduce_tma_g<4, 1, 0>(a, st, sy);

@@ -11,7 +11,11 @@ the orderings the paper's argument implies:
   * every extra level (requantization) costs accuracy: 1-hop (8,) < (2,4) / (4,2) <
     (2,2,2) in error;
   * int8 is more accurate than int4.
-With HZ_WRITE_PROFILES=1 the table is written to profiles/accuracy_r01.md.
+  * on (2,2,2), merging levels into one hop removes a requantization: hop 1-3 (one
+    quantization) < hops 1-2|3 (two) < hops 1|2|3 (three) in error, and the paper's
+    ZeRO-topo step (hop 1-2 quantized, then an fp32 allreduce + select across the top
+    level) is as accurate as the single 8-rank hop's one quantization allows.
+With HZ_WRITE_PROFILES=1 the table is written to profiles/accuracy_r02.md.
 """
 
 import os
@@ -75,6 +79,31 @@ def _ring(grads, bits):
     return out
 
 
+def _hops(grads, g, hops, bits, topo=False):
+    """qgZ with a hop grouping (reduce_scatter_hops); topo: the paper-literal ZeRO-topo
+    step — the hops quantized, then an fp32 allreduce + select over the
+    remaining top level."""
+    Np = len(grads[0])
+    L = len(g)
+    shards = col.reduce_scatter_hops(grads, g, Np, B, hops, bits)
+    last = hops[-1][1]
+    if topo:
+        shards = col.allreduce_select(shards, g, Np, last + 1, L)
+    full = np.zeros(Np, np.float32)
+    for r in range(W):
+        off, ln = pm.range_at(r, g, Np, L)
+        full[off:off + ln] = shards[r]
+    return full
+
+
+HOP_ROWS = {   # (2,2,2): name -> (hops, paper-literal top-level allreduce, quantizations on a path)
+    "(2,2,2) hops 1|2|3": ([(1, 1), (2, 2), (3, 3)], False, "3"),
+    "(2,2,2) hops 1-2|3": ([(1, 2), (3, 3)], False, "2"),
+    "(2,2,2) hop 1-3": ([(1, 3)], False, "1"),
+    "(2,2,2) ZeRO-topo: hop 1-2 + fp32 allreduce/select": ([(1, 2)], True, "1"),
+}
+
+
 @pytest.fixture(scope="module")
 def table():
     Np = pm.padded_numel(NUMEL, (W,), B)
@@ -85,6 +114,8 @@ def table():
         for g in ((8,), (2, 4), (4, 2), (2, 2, 2)):
             rows[(str(g), bits)] = _errors(_hier(grads, g, bits), exact)
         rows[("ring", bits)] = _errors(_ring(grads, bits), exact)
+        for name, (hops, topo, _) in HOP_ROWS.items():
+            rows[(name, bits)] = _errors(_hops(grads, (2, 2, 2), hops, bits, topo), exact)
     if os.environ.get("HZ_WRITE_PROFILES"):
         lines = ["# qgZ accuracy vs the exact sum (oracle = GPU path bitwise), 8 ranks, B = 256",
                  "", f"{NUMEL:,} elements per rank, gradients N(0, 1e-6) with 1/1024 x64 outliers "
@@ -97,7 +128,16 @@ def table():
         for k in ("(8,)", "(2, 4)", "(4, 2)", "(2, 2, 2)", "ring"):
             a, b = rows[(k, 4)], rows[(k, 8)]
             lines.append(f"| {k} | {hops[k]} | {a[0]:.3e} | {a[1]:.3e} | {b[0]:.3e} | {b[1]:.3e} |")
-        with open(os.path.join(ROOT, "profiles", "accuracy_r01.md"), "w") as f:
+        lines += ["", "Hop grouping on the (2, 2, 2) hierarchy (SURVEY §8(c): the hop grouping is a parameter; "
+                  "`hz_partition_set_hops` on the GPU, `reduce_scatter_hops` in the oracle).  The paper's ZeRO-topo "
+                  "reduce-scatter (P:397 1-hop all-to-all inside the node, P:361 allreduce across nodes before the "
+                  "update) quantizes each value once:", "",
+                  "| hops | quantizations on a value's path | int4 max err / max | int4 rms rel | "
+                  "int8 max err / max | int8 rms rel |", "|---|---|---|---|---|---|"]
+        for name, (_, _, q) in HOP_ROWS.items():
+            a, b = rows[(name, 4)], rows[(name, 8)]
+            lines.append(f"| {name} | {q} | {a[0]:.3e} | {a[1]:.3e} | {b[0]:.3e} | {b[1]:.3e} |")
+        with open(os.path.join(ROOT, "profiles", "accuracy_r02.md"), "w") as f:
             f.write("\n".join(lines) + "\n")
     return rows
 
@@ -119,3 +159,23 @@ def test_each_level_requantization_costs_accuracy(table, bits):
 def test_int8_more_accurate_than_int4(table):
     for g in ("(8,)", "(2, 4)", "(4, 2)", "(2, 2, 2)", "ring"):
         assert table[(g, 8)][1] < table[(g, 4)][1] / 4
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_merged_hops_remove_requantizations(table, bits):
+    """P:122 / P:397: one quantization per hop — merging levels into fewer hops lowers the
+    error monotonically on (2,2,2); the per-level hops equal the per-level reduce-scatter."""
+    three, two, one = (table[(k, bits)][1] for k in ("(2,2,2) hops 1|2|3", "(2,2,2) hops 1-2|3", "(2,2,2) hop 1-3"))
+    assert one < two < three
+    assert table[("(2,2,2) hops 1|2|3", bits)] == table[("(2, 2, 2)", bits)]
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_zero_topo_quantizes_once(table, bits):
+    """The paper-literal ZeRO-topo reduce-scatter (node 1-hop qgZ + fp32 cross-node
+    allreduce/select) has one quantization on every value's path: its error is within
+    10 % of the single 8-rank hop's and below every two-quantization scheme."""
+    topo = table[("(2,2,2) ZeRO-topo: hop 1-2 + fp32 allreduce/select", bits)][1]
+    assert topo < table[("(2,2,2) hops 1-2|3", bits)][1]
+    assert topo < table[("(2, 4)", bits)][1] and topo < table[("(4, 2)", bits)][1]
+    assert topo < 1.1 * table[("(2,2,2) hop 1-3", bits)][1]

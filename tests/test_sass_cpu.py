@@ -61,8 +61,13 @@ def test_arch_is_sm100a():
     assert "sm_100a" in elf
 
 
+def _tile_kind(f, kind):
+    return "k_tiles" in f and kind in f and "DualJob" not in f
+
+
 def test_no_fma_in_dequantize_and_fp32_reduce(sass):
-    names = [f for f in sass if "k_dequantize" in f or "k_reduce_f32" in f]
+    names = [f for f in sass if "k_dequantize" in f or "k_reduce_f32" in f or _tile_kind(f, "GatherJob")
+             or (_tile_kind(f, "ReduceJob") and re.search(r"ReduceJobILi[48]ELi\d+ELi[01]ELi0E", f))]
     assert names, "kernels not found in the SASS"
     bad = [f for f in names if any("FFMA" in l for l in sass[f])]
     assert not bad, f"FFMA in {bad[:3]}"
@@ -82,19 +87,15 @@ def test_dual_kernel_default_variant_fits_64_registers(resources):
     assert all(r["REG"] <= 64 and r.get("STACK", 0) == 0 for r in one_pass), one_pass
 
 
-def test_link_kernels_use_tma_bulk_copies(sass, resources):
-    """The link-CTA dual kernel (k_gather_quantize_link) and the TMA-staged level reduce
-    (k_reduce_tma) move peer tiles with cp.async.bulk (SASS UBLKCP) completed on
-    mbarriers (SYNCS.ARRIVE.TRANS64 / SYNCS.PHASECHK), keep 4 CTAs per SM (<= 64
-    registers) and no FMA in the fp32 sums of the reduce."""
-    for kind in ("k_gather_quantize_link", "k_reduce_tma"):
-        names = [f for f in sass if kind in f]
-        assert names, f"{kind} not in the SASS"
-        for f in names:
-            text = "\n".join(sass[f])
-            assert "UBLKCP" in text, f"no bulk copy in {f}"
-            assert "SYNCS.ARRIVE.TRANS64" in text and "SYNCS.PHASECHK" in text, f"no mbarrier in {f}"
-            assert resources[f]["REG"] <= 64, (f, resources[f])
-    f32 = [f for f in sass if "k_reduce_tma" in f and re.search(r"k_reduce_tmaILi[48]ELi\d+ELi[01]E", f)]
-    assert f32
-    assert not [f for f in f32 if any("FFMA" in l for l in sass[f])]
+def test_tile_engine_kernels_are_tma_pipelines(sass, resources):
+    """Every instantiation of the tile engine (k_tiles: quantize, round trip, gather,
+    dual, reduce) moves its tiles with bulk copies both ways — cp.async.bulk global ->
+    shared (SASS UBLKCP) completed on mbarriers (SYNCS.ARRIVE.TRANS64 / SYNCS.PHASECHK)
+    and shared -> global bulk stores — and fits 4 CTAs per SM (<= 64 registers)."""
+    names = [f for f in sass if "k_tiles" in f]
+    assert len(names) >= 40, len(names)
+    for f in names:
+        text = "\n".join(sass[f])
+        assert text.count("UBLKCP") >= 2, f"no bulk load + store in {f}"
+        assert "SYNCS.ARRIVE.TRANS64" in text and "SYNCS.PHASECHK" in text, f"no mbarrier in {f}"
+        assert resources[f]["REG"] <= 64, (f, resources[f])
