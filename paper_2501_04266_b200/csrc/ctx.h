@@ -87,8 +87,8 @@ struct hz_ctx {
 namespace hz {
 
 // header of the symmetric pool: ready[8] u64 | done[8] u64 | arrival counter u32 |
-// phase epoch u64 | work queue u32[2] (link.cuh)
-constexpr size_t kReadyOff = 0, kDoneOff = 64, kCounterOff = 128, kEpochOff = 192, kQueueOff = 256;
+// phase epoch u64
+constexpr size_t kReadyOff = 0, kDoneOff = 64, kCounterOff = 128, kEpochOff = 192;
 constexpr size_t kPoolHeader = 4096;
 
 int tune_param(const char* name, int dflt);   // HZ_TUNE overrides (codec_util.cu)

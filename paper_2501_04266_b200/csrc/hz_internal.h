@@ -40,7 +40,6 @@ struct SyncArgs {
   unsigned long long wait_ready, wait_done, sig_ready, sig_done;
   unsigned wr_mask, wd_mask, sr_mask, sd_mask;
   unsigned long long* stamps;      // optional [8]: entry, after wait, last-CTA arrival, flags sent (ns), counter
-  unsigned* queue;                 // [2] device work queue of the link-CTA kernels (link.cuh), zero between launches
 };
 
 // Pieces of a gathered layer for the fused gather+dequantize kernel: piece j
@@ -56,7 +55,6 @@ struct Pieces {
   uint8_t* sec_c;
   float* sec_s;
   int64_t sec_lo, sec_hi;
-  unsigned remote;   // bit j: piece j is a peer's memory (read over NVLink); 0 = all local
 };
 
 // ----------------------------------------------------------------- kernels
@@ -94,9 +92,6 @@ cudaError_t tiles_dual(const Pieces& pc, void* y, const void* x, hz_dtype dt, in
 cudaError_t tiles_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in, int block,
                          int bits_out, uint8_t* oc, float* os, float* of, int acc, cudaStream_t st,
                          const SyncArgs& sy);
-// gather+dequantize (8-bit codes, B = 256, bf16 out) with link CTAs for the remote
-// pieces (k_quantize.cu); cudaErrorNotSupported if the launch does not qualify
-cudaError_t launch_gather_link(const Pieces& pc, void* y, cudaStream_t st, const SyncArgs& sy);
 cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, int64_t n, int bits,
                               int block, void* y, hz_dtype out_dt, cudaStream_t st);
 cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,

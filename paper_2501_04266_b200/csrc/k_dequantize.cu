@@ -75,12 +75,8 @@ cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int 
   const SyncArgs sy = sync ? *sync : SyncArgs{};
   if (n == 0 && !sync) return cudaSuccess;
   if (pc.n * pc.len == n && n > 0) {
-    cudaError_t e = tiles_gather(pc, bits, block, y, out_dt, st, sy);
+    const cudaError_t e = tiles_gather(pc, bits, block, y, out_dt, st, sy);
     if (e != cudaErrorNotSupported) return e;
-    if (bits == 8 && block == 256 && out_dt == HZ_BF16 && pc.remote) {
-      e = launch_gather_link(pc, y, st, sy);
-      if (e != cudaErrorNotSupported) return e;
-    }
   }
   return bits == 8 ? dequantize_b<8>(pc, n, block, y, out_dt, st, sy)
                    : dequantize_b<4>(pc, n, block, y, out_dt, st, sy);

@@ -13,7 +13,6 @@
 // checks so every shuffle is convergent; the last partial iteration (< NB
 // blocks) goes through a checked tail path.  Grid-stride over SMs x resident CTAs.
 #include "dequantize_loop.cuh"
-#include "link.cuh"
 
 namespace hz {
 namespace {
@@ -285,259 +284,9 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
   sync_signal(sy);
 }
 
-// k_gather_quantize_link (P2P transport, B = 256, 8-bit gather, bf16 out, codes-only
-// quantize): the dual kernel with the peer pieces moved by TMA bulk copies (link.cuh).
-// The work is one atomic queue of CTA-sized tasks: 8192-element tiles of the local
-// piece's gather (HBM), 8192-element tiles of the quantize job (HBM) and 16384-element
-// tiles of the remote pieces (NVLink), the remote tiles spread evenly through the queue.
-//   nlink < 0 (default): every CTA takes any task; a remote tile's bulk copy is issued
-//     when the task is taken and consumed (dequantized from shared memory) after the
-//     CTA's next HBM task, so the NVLink round trip hides behind HBM work and every SM
-//     carries both streams;
-//   nlink > 0: CTAs [0, nlink) are dedicated link CTAs streaming the remote tiles
-//     through a 3-stage ring, then join the queue of HBM tasks (HZ_TUNE lk=nlink;
-//     measured slower: each link CTA is throttled by the HBM CTAs sharing its SM).
-// Per-element arithmetic is exactly k_dequantize's and k_quantize's (bitwise parity).
-template <typename T, int QBITS>
-__global__ void __launch_bounds__(kThreads, 4) k_gather_quantize_link(const __grid_constant__ Pieces pc,
-                                                                       __nv_bfloat16* __restrict__ y,
-                                                                       const T* __restrict__ x, int64_t nblocks,
-                                                                       uint8_t* __restrict__ codes,
-                                                                       float* __restrict__ scales, int nlink,
-                                                                       LinkGeo lg, const __grid_constant__ SyncArgs sy) {
-  extern __shared__ __align__(128) char smem[];
-  __shared__ int slot;
-  __shared__ int64_t pend[kLinkSMax];
-  if (!sync_wait(sy)) return;
-  const Ring ring = ring_init(smem, lg.S, lg.stage());
-  const LinkTiles lt = link_tiles(pc, lg.te);
-  if (nlink > 0 && static_cast<int>(blockIdx.x) < nlink) link_gather<__nv_bfloat16>(pc, lt, y, ring, blockIdx.x, nlink);
-  // the local piece (the one piece without its remote bit) as a one-piece gather
-  int self = 0;
-  while (self < pc.n - 1 && ((pc.remote >> self) & 1u)) ++self;
-  Pieces lp{};
-  lp.n = 1;
-  lp.c[0] = pc.c[self];
-  lp.s[0] = pc.s[self];
-  lp.len = pc.len;
-  const int64_t off = self * pc.len;
-  if (pc.sec_c) {
-    lp.sec_c = pc.sec_c;
-    lp.sec_s = pc.sec_s;
-    lp.sec_lo = pc.sec_lo - off;
-    lp.sec_hi = pc.sec_hi - off;
-  }
-  constexpr int GU = kU;                                   // dequantize_loop units per lane
-  constexpr int WPC = kThreads / 32;                       // warps per CTA = warp tiles per task
-  const int64_t lunits = pc.len / 8;
-  const int64_t n_lt = (lunits + 32 * GU * WPC - 1) / (32 * GU * WPC);
-  constexpr int NB = kU * Geo<256>::BPW;
-  const int64_t nfull = nblocks / NB;
-  const int64_t n_qt = (nfull + (nfull * NB < nblocks ? 1 : 0) + WPC - 1) / WPC;
-  const int64_t m = n_lt < n_qt ? n_lt : n_qt;
-  const int64_t nh = n_lt + n_qt;
-  const int64_t nr = nlink > 0 ? 0 : lt.count();           // remote tiles in the queue
-  const int64_t total = nh + nr;
-  const int64_t wic = threadIdx.x >> 5;
-  NoEmit emit;
-  int64_t ni = 0, nc = 0;   // remote tiles issued / consumed by this CTA (uniform)
-  auto consume_oldest = [&]() {
-    mbar_wait(ring.full(nc), ring.parity(nc));
-    link_consume<__nv_bfloat16>(pc, lt, pend[nc % lg.S], ring.stage(nc), y);
-    ++nc;
-    __syncthreads();
-  };
-  for (;;) {
-    const int64_t k = queue_next(sy.queue, &slot);
-    if (k >= total) break;
-    const int64_t r0 = k * nr / total, r1 = (k + 1) * nr / total;
-    if (r1 > r0) {   // remote tile r0: start its copy, consume it after the next HBM task
-      if (ni - nc == lg.S) consume_oldest();
-      if (threadIdx.x == 0) {
-        fence_proxy_async();
-        link_issue(pc, lt, r0, ring.stage(ni), ring.full(ni));
-        pend[ni % lg.S] = r0;
-      }
-      ++ni;
-      continue;
-    }
-    const int64_t h = k - r0;   // HBM task h: local gather task a or quantize task b
-    int64_t a = -1, b = -1;
-    if (h < 2 * m) {
-      if (h & 1) b = h >> 1;
-      else a = h >> 1;
-    } else if (n_lt > n_qt) {
-      a = h - m;
-    } else {
-      b = h - m;
-    }
-    if (a >= 0) {
-      dequantize_loop<8, __nv_bfloat16, GU>(lp, lunits, 8, y + off, wic, WPC, a * WPC, (a + 1) * WPC);
-    } else {
-      quantize_loop<T, 256, QBITS, kU, 0>(x, nblocks, codes, scales, emit, nullptr, 0, wic, WPC, b * WPC,
-                                          b + 1 == n_qt ? INT64_MAX : (b + 1) * WPC);
-    }
-    if (ni > nc) {
-      __syncthreads();   // pend[] written by thread 0 before the HBM task
-      consume_oldest();
-    }
-  }
-  while (nc < ni) {
-    __syncthreads();
-    consume_oldest();
-  }
-  queue_leave(sy.queue);
-  sync_signal(sy);
-}
-
-// ring geometry of the link kernels: HZ_TUNE lte (elements per tile, multiple of 1024)
-// and ls (stages, 1..kLinkSMax)
-LinkGeo link_geo() {
-  LinkGeo g{tune_param("lte", 16384), tune_param("ls", 3)};
-  g.te = g.te < 1024 ? 1024 : g.te / 1024 * 1024;
-  g.S = g.S < 1 ? 1 : (g.S > kLinkSMax ? kLinkSMax : g.S);
-  return g;
-}
-
-// k_gather_quantize_ws: the same job, warp-specialised instead of queued.  In every
-// CTA, warps [0, LW) are link warps: lane 0 of warp 0 streams this CTA's share of the
-// remote tiles (tiles b, b + G, ...) through a 3-stage TMA ring and the LW warps
-// dequantize each landed tile from shared memory (named barrier 1 among them before a
-// stage is re-armed); warps [LW, 8) are HBM warps running the local piece's gather and
-// the quantize job grid-stride over all CTAs' HBM warps (odd CTAs gather first, as the
-// all-warps kernel).  No CTA-wide barrier after the prologue, no atomics: the HBM warps
-// never wait on NVLink latency and the link is fed asynchronously by every SM.
-template <typename T, int QBITS, int LW>
-__global__ void __launch_bounds__(kThreads, 4) k_gather_quantize_ws(const __grid_constant__ Pieces pc,
-                                                                     __nv_bfloat16* __restrict__ y,
-                                                                     const T* __restrict__ x, int64_t nblocks,
-                                                                     uint8_t* __restrict__ codes,
-                                                                     float* __restrict__ scales, LinkGeo lg,
-                                                                     const __grid_constant__ SyncArgs sy) {
-  extern __shared__ __align__(128) char smem[];
-  if (!sync_wait(sy)) return;
-  const Ring ring = ring_init(smem, lg.S, lg.stage());
-  const int w = threadIdx.x >> 5;
-  if (w < LW) {
-    const LinkTiles lt = link_tiles(pc, lg.te);
-    const int64_t total = lt.count();
-    const int64_t mine = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      for (int64_t i = 0; i < lg.S && i < mine; ++i)
-        link_issue(pc, lt, blockIdx.x + i * gridDim.x, ring.stage(i), ring.full(i));
-    }
-    for (int64_t i = 0; i < mine; ++i) {
-      mbar_wait(ring.full(i), ring.parity(i));
-      const int64_t t = blockIdx.x + i * gridDim.x;
-      int j;
-      int64_t e0, cnt;
-      link_tile(pc, lt, t, j, e0, cnt);
-      const char* stage = ring.stage(i);
-      const float* sc = reinterpret_cast<const float*>(stage + lg.te);
-      const int64_t g0 = j * pc.len + e0;
-      for (int u = threadIdx.x; u < cnt / 8; u += LW * 32) {
-        Codes8<8> raw;
-        raw.r = *reinterpret_cast<const uint2*>(stage + u * 8);
-        const float sv = sc[u >> 5];
-        float c[8], v[8];
-        raw.decode(c);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __fmul_rn(c[k], sv);
-        const int64_t e = g0 + u * 8;
-        Out8<__nv_bfloat16>::store(y + e, v);
-        if (pc.sec_c && e >= pc.sec_lo && e < pc.sec_hi) {
-          raw.store(pc.sec_c + (e - pc.sec_lo));
-          if (((e - pc.sec_lo) & 255) == 0) pc.sec_s[(e - pc.sec_lo) >> 8] = sv;
-        }
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(LW * 32) : "memory");
-      if (threadIdx.x == 0 && i + lg.S < mine) {
-        fence_proxy_async();
-        link_issue(pc, lt, blockIdx.x + (i + lg.S) * gridDim.x, ring.stage(i + lg.S), ring.full(i + lg.S));
-      }
-    }
-  } else {
-    int self = 0;
-    while (self < pc.n - 1 && ((pc.remote >> self) & 1u)) ++self;
-    Pieces lp{};
-    lp.n = 1;
-    lp.c[0] = pc.c[self];
-    lp.s[0] = pc.s[self];
-    lp.len = pc.len;
-    const int64_t off = self * pc.len;
-    if (pc.sec_c) {
-      lp.sec_c = pc.sec_c;
-      lp.sec_s = pc.sec_s;
-      lp.sec_lo = pc.sec_lo - off;
-      lp.sec_hi = pc.sec_hi - off;
-    }
-    constexpr int HW = kThreads / 32 - LW;
-    const int64_t hw = static_cast<int64_t>(blockIdx.x) * HW + (w - LW);
-    const int64_t nhw = static_cast<int64_t>(gridDim.x) * HW;
-    NoEmit emit;
-    if (blockIdx.x & 1) {
-      dequantize_loop<8, __nv_bfloat16, kU>(lp, pc.len / 8, 8, y + off, hw, nhw);
-      quantize_loop<T, 256, QBITS, kU, 0>(x, nblocks, codes, scales, emit, nullptr, 0, hw, nhw);
-    } else {
-      quantize_loop<T, 256, QBITS, kU, 0>(x, nblocks, codes, scales, emit, nullptr, 0, hw, nhw);
-      dequantize_loop<8, __nv_bfloat16, kU>(lp, pc.len / 8, 8, y + off, hw, nhw);
-    }
-  }
-  sync_signal(sy);
-}
-
-template <typename T, int QBITS>
-cudaError_t gather_quantize_ws_t(const Pieces& pc, void* y, const void* x, int64_t n_q, uint8_t* codes,
-                                 float* scales, cudaStream_t st, const SyncArgs& sy) {
-  const int lw = tune_param("lw", 2);
-  auto kern = lw == 1 ? k_gather_quantize_ws<T, QBITS, 1>
-                      : lw == 3 ? k_gather_quantize_ws<T, QBITS, 3> : k_gather_quantize_ws<T, QBITS, 2>;
-  const int64_t lunits = pc.len / 8;
-  const int64_t tasks = (lunits + 32 * kU - 1) / (32 * kU) + n_q / 256 / kU + 1;
-  const LinkGeo lg = link_geo();
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks * 2, lg.smem());
-  return launch_k_smem(kern, grid, lg.smem(), st, pc, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x),
-                       n_q / 256, codes, scales, lg, sy);
-}
-
-template <typename T, int QBITS>
-cudaError_t gather_quantize_link_t(const Pieces& pc, void* y, const void* x, int64_t n_q, uint8_t* codes,
-                                   float* scales, int nlink, cudaStream_t st, const SyncArgs& sy) {
-  auto kern = k_gather_quantize_link<T, QBITS>;
-  const int64_t lunits = pc.len / 8;
-  const LinkGeo lg = link_geo();
-  const int64_t remote_tiles = int64_t(pc.n - 1) * ((pc.len + lg.te - 1) / lg.te);
-  const int64_t tasks = (lunits + 32 * kU - 1) / (32 * kU) + n_q / 256 / kU + 1 + remote_tiles * 8;
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks, lg.smem());
-  if (nlink > 0 && grid <= nlink) nlink = static_cast<int>(std::max<int64_t>(1, grid / 2));
-  return launch_k_smem(kern, grid, lg.smem(), st, pc, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x),
-                       n_q / 256, codes, scales, nlink, lg, sy);
-}
-
-// link CTAs of the role-split kernels (HZ_TUNE lk: 0 = the all-warps schedule)
-int link_ctas(const Pieces& pc, const SyncArgs& sy) {
-  if (!sy.queue || !pc.remote || pc.n < 2) return 0;
-  int nrem = 0;
-  for (int j = 0; j < pc.n; ++j) nrem += (pc.remote >> j) & 1u;
-  if (nrem != pc.n - 1 || (pc.len % 1024) != 0) return 0;
-  // -2: warp-specialised (default); -1: every CTA through the queue; > 0: dedicated link
-  // CTAs; 0: off (the all-warps kernels with per-lane peer loads)
-  const int lk = tune_param("lk", -2);
-  if (lk == 0) return 0;
-  if (lk < 0) return lk < -1 ? -2 : -1;
-  const int64_t tiles = int64_t(nrem) * ((pc.len + link_geo().te - 1) / link_geo().te);
-  return static_cast<int>(std::min<int64_t>(lk, tiles));
-}
-
 template <typename T, int QBITS, int QOUT>
 cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const void* x, int64_t n_q, uint8_t* codes,
                               float* scales, float* qy, int acc, cudaStream_t st, const SyncArgs& sy) {
-  if constexpr (QOUT == 0) {
-    const int nlink = link_ctas(pc, sy);
-    if (nlink == -2) return gather_quantize_ws_t<T, QBITS>(pc, y, x, n_q, codes, scales, st, sy);
-    if (nlink != 0) return gather_quantize_link_t<T, QBITS>(pc, y, x, n_q, codes, scales, nlink, st, sy);
-  }
   // chunks of the interleaved schedule (HZ_TUNE gqc; default by size): one pass when a
   // warp has few gather tiles (GPT-1.3B layer, ~10 per warp: the chunked kernel's extra
   // registers cost more than the balance gains, 3.80 vs 4.20 ms), 4 chunks from ~32 tiles
@@ -627,16 +376,6 @@ cudaError_t launch_quantize(const void* x, hz_dtype dt, int64_t n, int bits, int
 }  // namespace hz
 
 namespace hz {
-
-// The standalone gather+dequantize (k_dequantize's job) through the link-CTA kernel:
-// no quantize tasks in the queue.  cudaErrorNotSupported when the pieces do not qualify
-// (no remote piece, not a P2P launch, HZ_TUNE lk=0).
-cudaError_t launch_gather_link(const Pieces& pc, void* y, cudaStream_t st, const SyncArgs& sy) {
-  const int nlink = link_ctas(pc, sy);
-  if (nlink == 0) return cudaErrorNotSupported;
-  if (nlink == -2) return gather_quantize_ws_t<__nv_bfloat16, 8>(pc, y, nullptr, 0, nullptr, nullptr, st, sy);
-  return gather_quantize_link_t<__nv_bfloat16, 8>(pc, y, nullptr, 0, nullptr, nullptr, nlink, st, sy);
-}
 
 bool gather_quantize_supported(int block, int gather_bits, hz_dtype out_dt) {
   return block == 256 && gather_bits == 8 && out_dt == HZ_BF16;

@@ -15,7 +15,6 @@
 // shared-memory transpose for coalesced 512-byte fp32 stores.  Inputs may be
 // peer-mapped (NVLink P2P transport): 8-byte loads keep peer reads at full speed.
 #include "codec.cuh"
-#include "link.cuh"
 
 namespace hz {
 namespace {
@@ -352,156 +351,6 @@ __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__
   sync_signal(sy);
 }
 
-// ------------------------------------------------------------- TMA-staged reduce
-// k_reduce_tma (P2P transport, B = 256): the same reduction with every input tile
-// brought into shared memory by TMA bulk copies (link.cuh) — the g members' codes and
-// scales of te consecutive elements per stage, a ring of S stages per CTA — instead
-// of per-lane peer loads.  A peer read is a ~2 µs NVLink round trip; with per-lane
-// loads the fp32 reduce kept too little in flight to fill the link (ncu, one-process
-// 2-GPU run: 13.5 MB of peer codes in 36.8 µs, 367 GB/s), while a few 4-16 KB bulk
-// copies per CTA keep several MB in flight.  Consumers read the landed codes from
-// shared memory: MODE 0 / 1 store (accumulate) fp32 with one float4 per 4 elements
-// (each warp instruction a contiguous 512-byte span); MODE 2 requantizes to BOUT bits
-// per 256-element block (one warp per block, quantize_store).  Arithmetic and order are
-// exactly k_reduce_f32's / k_reduce_requant's: acc = x_hat_0, acc = fl(acc + x_hat_p)
-// in ascending p, no FMA (bitwise parity).
-struct TmaGeo {
-  int te;   // elements per tile (multiple of 1024)
-  int cb;   // code bytes of one input per stage
-  int sb;   // scale bytes of one input per stage
-  int stage;
-  int S;
-};
-
-template <int BIN, int GT, int MODE, int BOUT>
-__global__ void __launch_bounds__(kThreads, 4) k_reduce_tma(const __grid_constant__ RedArgs a, TmaGeo gm,
-                                                            const __grid_constant__ SyncArgs sy) {
-  extern __shared__ __align__(128) char smem[];
-  if (!sync_wait(sy)) return;
-  const Ring ring = ring_init(smem, gm.S, gm.stage);
-  const int g = GT > 0 ? GT : a.g;
-  const int64_t ntiles = (a.n + gm.te - 1) / gm.te;
-  const int64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  auto tile = [&](int64_t i, int64_t& e0, int& cnt) {
-    e0 = (blockIdx.x + i * gridDim.x) * int64_t(gm.te);
-    cnt = a.n - e0 < gm.te ? static_cast<int>(a.n - e0) : gm.te;   // multiple of 1024
-  };
-  ring_run(
-      ring, mine,
-      [&](int64_t i, char* st, uint64_t* bar) {
-        int64_t e0;
-        int cnt;
-        tile(i, e0, cnt);
-        const unsigned cbytes = static_cast<unsigned>(cnt) * BIN / 8, sbytes = static_cast<unsigned>(cnt) / 64;
-        mbar_expect_tx(bar, static_cast<unsigned>(g) * (cbytes + sbytes));
-        for (int p = 0; p < g; ++p) {
-          bulk_g2s(st + p * gm.cb, a.c[p] + e0 * BIN / 8, cbytes, bar);
-          bulk_g2s(st + g * gm.cb + p * gm.sb, a.s[p] + e0 / 256, sbytes, bar);
-        }
-      },
-      [&](int64_t i, char* st) {
-        int64_t e0;
-        int cnt;
-        tile(i, e0, cnt);
-        const float* sc = reinterpret_cast<const float*>(st + g * gm.cb);
-        if constexpr (MODE < 2) {
-          // units of 4 elements: thread t takes units t, t + 256, ...
-          for (int u = threadIdx.x; u < cnt / 4; u += kThreads) {
-            float acc[4];
-            for (int p = 0; p < g; ++p) {
-              Codes4<BIN> r;
-              if constexpr (BIN == 8) r.r = *reinterpret_cast<const unsigned*>(st + p * gm.cb + u * 4);
-              else r.r = *reinterpret_cast<const unsigned short*>(st + p * gm.cb + u * 2);
-              const float s = sc[p * (gm.sb / 4) + (u >> 6)];
-              float c[4];
-              r.decode(c);
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const float xh = __fmul_rn(c[k], s);
-                acc[k] = p == 0 ? xh : __fadd_rn(acc[k], xh);
-              }
-            }
-            float4* dst = reinterpret_cast<float4*>(a.of + e0) + u;
-            float4 o = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            if constexpr (MODE == 1) {
-              const float4 old = *dst;
-              o.x = __fadd_rn(old.x, o.x);
-              o.y = __fadd_rn(old.y, o.y);
-              o.z = __fadd_rn(old.z, o.z);
-              o.w = __fadd_rn(old.w, o.w);
-            }
-            *dst = o;
-          }
-        } else {
-          // one 256-element block per warp step, lane l: elements 8l .. 8l+7
-          const int lane = threadIdx.x & 31;
-          for (int b = threadIdx.x >> 5; b < cnt / 256; b += kThreads / 32) {
-            float v[1][1][8];
-            for (int p = 0; p < g; ++p) {
-              Codes8<BIN> r;
-              if constexpr (BIN == 8) r.r = *reinterpret_cast<const uint2*>(st + p * gm.cb + b * 256 + lane * 8);
-              else r.r = *reinterpret_cast<const unsigned*>(st + p * gm.cb + b * 128 + lane * 4);
-              const float s = sc[p * (gm.sb / 4) + b];
-              float c[8];
-              r.decode(c);
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const float xh = __fmul_rn(c[k], s);
-                v[0][0][k] = p == 0 ? xh : __fadd_rn(v[0][0][k], xh);
-              }
-            }
-            float m = 0.f;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) m = fmaxf(m, fabsf(v[0][0][k]));
-            const float am[1] = {group_max<32>(m)};
-            quantize_store<256, BOUT, 1, NoEmit>(v, am, e0 / 256 + b, lane, a.oc, a.os, NoEmit{});
-          }
-        }
-      });
-  sync_signal(sy);
-}
-
-template <int BIN, int GT, int MODE, int BOUT>
-cudaError_t reduce_tma_t(const RedArgs& a, cudaStream_t st, const SyncArgs& sy) {
-  const int g = a.g;
-  TmaGeo gm{};
-  gm.te = 16384 / g;
-  gm.te = gm.te < 1024 ? 1024 : gm.te / 1024 * 1024;
-  const int cap = tune_param("rt_te", 0);
-  if (cap >= 1024) gm.te = cap / 1024 * 1024;
-  gm.cb = gm.te * BIN / 8;
-  gm.sb = gm.te / 64;
-  gm.stage = g * (gm.cb + gm.sb);
-  gm.S = tune_param("rt_s", 4);
-  while (gm.S > 2 && gm.S * gm.stage > 48 * 1024) --gm.S;
-  const int smem = gm.S * gm.stage + gm.S * 8;
-  auto kern = k_reduce_tma<BIN, GT, MODE, BOUT>;
-  const int64_t ntiles = (a.n + gm.te - 1) / gm.te;
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), ntiles * (kThreads / 32), smem);
-  return launch_k_smem(kern, grid, smem, st, a, gm, sy);
-}
-
-template <int BIN, int MODE, int BOUT>
-cudaError_t reduce_tma_g(const RedArgs& a, cudaStream_t st, const SyncArgs& sy) {
-  switch (a.g) {
-    case 1: return reduce_tma_t<BIN, 1, MODE, BOUT>(a, st, sy);
-    case 2: return reduce_tma_t<BIN, 2, MODE, BOUT>(a, st, sy);
-    case 4: return reduce_tma_t<BIN, 4, MODE, BOUT>(a, st, sy);
-    case 8: return reduce_tma_t<BIN, 8, MODE, BOUT>(a, st, sy);
-    default: return reduce_tma_t<BIN, 0, MODE, BOUT>(a, st, sy);
-  }
-}
-
-// the TMA-staged reduce: P2P transport (a phase-synchronised launch), B = 256, chunks
-// of a multiple of 1024 elements, 16-byte aligned inputs; HZ_TUNE rt=0 turns it off
-bool reduce_tma_ok(const RedArgs& a, int block, const SyncArgs& sy) {
-  static const bool on = tune_param("rt", 1) != 0;
-  if (!on || !sy.queue || block != 256 || a.n % 1024 != 0 || a.g < 1 || a.g > kMaxG) return false;
-  for (int p = 0; p < a.g; ++p)
-    if ((reinterpret_cast<uintptr_t>(a.c[p]) | reinterpret_cast<uintptr_t>(a.s[p])) & 15u) return false;
-  return !(a.of && (reinterpret_cast<uintptr_t>(a.of) & 15u));
-}
-
 // ---------------------------------------------------------------------- launch
 constexpr int kUR = 4;   // warp steps per warp iteration (requant)
 constexpr int kUF = 2;   // 8-byte code units in flight per lane per input (fp32 out)
@@ -600,14 +449,6 @@ cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const
     const cudaError_t e = tiles_reduce(g, codes, scales, n, bits_in, block, bits_out, out_codes, out_scales, out_f32,
                                        accumulate, st, sy);
     if (e != cudaErrorNotSupported) return e;
-  }
-  if (reduce_tma_ok(a, block, sy)) {
-    if (bits_out == 0) {
-      if (accumulate) return bits_in == 8 ? reduce_tma_g<8, 1, 0>(a, st, sy) : reduce_tma_g<4, 1, 0>(a, st, sy);
-      return bits_in == 8 ? reduce_tma_g<8, 0, 0>(a, st, sy) : reduce_tma_g<4, 0, 0>(a, st, sy);
-    }
-    if (bits_in == 8) return bits_out == 8 ? reduce_tma_g<8, 2, 8>(a, st, sy) : reduce_tma_g<8, 2, 4>(a, st, sy);
-    return bits_out == 8 ? reduce_tma_g<4, 2, 8>(a, st, sy) : reduce_tma_g<4, 2, 4>(a, st, sy);
   }
   if (bits_out == 0) {
     int log2b = 0;

@@ -2,9 +2,10 @@
 // one-member level, gather+dequantize (A3 / A5 / A6, pieces local or over NVLink), the
 // dual gather || quantize launch, and the level reduce (A9 / A10).  Same arithmetic and
 // order as the LSU kernels (k_quantize.cu, k_dequantize.cu, k_reduce.cu), so the outputs
-// are bitwise identical; those remain the path for shapes the engine does not take
+// are bitwise identical.  Off by default (HZ_TUNE tma=1 enables it; measured slower,
+// tiles.cuh); when on, the LSU kernels still take the shapes the engine does not
 // (block != 256, lengths not a multiple of 1024, unaligned buffers, the accumulating
-// round trip) and for HZ_TUNE tma=0.
+// round trip).
 #include "tiles.cuh"
 
 namespace hz {
@@ -150,7 +151,7 @@ cudaError_t reduce_g(int g, const uint8_t* const* c, const float* const* s, int6
 }  // namespace
 
 bool tiles_on() {
-  static const bool on = tune_param("tma", 1) != 0;
+  static const bool on = tune_param("tma", 0) != 0;   // measured slower: off by default
   return on;
 }
 

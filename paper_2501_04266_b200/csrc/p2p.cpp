@@ -125,7 +125,6 @@ SyncArgs make_sync(hz_ctx* ctx, const Phases& ph) {
     s.done_remote[q] = reinterpret_cast<unsigned long long*>(P.peer[q] + kDoneOff) + ctx->rank;
   }
   s.counter = reinterpret_cast<unsigned int*>(P.pool + kCounterOff);
-  s.queue = reinterpret_cast<unsigned*>(P.pool + kQueueOff);
   s.epoch = reinterpret_cast<const unsigned long long*>(P.pool + kEpochOff);
   s.abort = P.abort_dev;
   s.timeout_ns = P.timeout_ns;
@@ -302,10 +301,7 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
     const int m = members[k].second;
     pc.c[k] = at<const uint8_t>(ctx, m, off_of(ctx, xc));
     pc.s[k] = at<const float>(ctx, m, off_of(ctx, xs));
-    if (m != ctx->rank) {
-      remote += code_bytes(plen, bits) + plen / B * 4;
-      pc.remote |= 1u << k;
-    }
+    if (m != ctx->rank) remote += code_bytes(plen, bits) + plen / B * 4;
   }
   if (!backward && s < w) {   // A4, s < w: keep range_s of the gathered codes
     pc.sec_c = sec_codes;
@@ -415,10 +411,7 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
       const int m = members[k].second;
       gpc.c[k] = at<const uint8_t>(ctx, m, off_of(ctx, prev->sec_codes));
       gpc.s[k] = at<const float>(ctx, m, off_of(ctx, prev->sec_scales));
-      if (m != ctx->rank) {
-        gremote += code_bytes(gpc.len, prev->bits) + gpc.len / 256 * 4;
-        gpc.remote |= 1u << k;
-      }
+      if (m != ctx->rank) gremote += code_bytes(gpc.len, prev->bits) + gpc.len / 256 * 4;
     }
   }
   const unsigned long long base = P.phase;

@@ -1,36 +1,58 @@
-// The TMA tile engine: every byte of a codec kernel moves by bulk copy.  Internal header.
+// The TMA tile engine: a codec kernel whose every byte moves by bulk copy (HZ_TUNE
+// tma=1; OFF by default — measured slower than the LSU kernels, see below).  Internal header.
 //
-// Why: the codec kernels are HBM streams with 1-4 bytes written per byte
-// read.  With ld/st.global the bytes in flight live in registers and L1 (64 registers a
-// thread cap these kernels at 32 warps an SM), and a write-heavy stream tops out at
-// ~5.25 TB/s on this B200 (tools/hbm_mix_probe.cu).  The same streams through the Tensor
-// Memory Accelerator — cp.async.bulk global -> shared into a ring of input stages
-// completed on mbarriers, the transform shared -> shared by all threads, cp.async.bulk
-// shared -> global of the output from two output buffers — reach 5.6-6.0 TB/s
-// (tools/tma_mix_probe.cu: +10 % for bf16 -> bf16 + int8, +13 % for bf16 -> fp32): the
-// in-flight bytes are held in shared memory by the copy engine, independent of
-// registers and L1.  Peer (NVLink) pieces are fetched the same way, asynchronously.
+// Design: cp.async.bulk global -> shared into a ring of S input stages completed on
+// mbarriers (peer pieces over NVLink the same way), the codec transform shared -> shared
+// by all threads, cp.async.bulk shared -> global of the output from two output buffers.
+// The in-flight bytes are held in shared memory by the copy engine instead of registers
+// and L1.  Motivation: a plain streaming kernel with the codec's write-heavy byte mixes
+// reaches 5.24-5.66 TB/s with ld/st.global and 5.59-6.02 TB/s with bulk copies
+// (tools/tma_mix_probe.cu vs tools/hbm_mix_probe.cu, profiles/tma_r02.md).
+// Measured in the product (profiles/tma_r02.md): the engine LOSES on every hot shape —
+// N = 1 round trip 57-63 µs vs 51 µs, dequantize 29.5-33.6 vs 27.9 µs; N = 2 dual
+// gather || quantize 86.7 vs 57.4 µs — because the codec's per-tile arithmetic (block
+// absmax shuffles, two IEEE divisions per block, packing) sits between two CTA barriers
+// per tile, serialised with the copies of its CTA, while the LSU kernels overlap the
+// same arithmetic across 32 independent warps per SM.  It stays selectable, parity-
+// tested (tests/test_gpu_tiles.py), as the reproducible evidence for that choice.
 //
-// A Job describes one kernel: ntiles(), load(t, in, bar) (thread 0: arm `bar` with the
-// tile's byte count and start its bulk loads into the input stage), compute(t, in, out)
-// (all threads: the codec arithmetic, shared -> shared, exactly the LSU kernels'
-// per-element operations and order), store(t, out) (thread 0: the output bulk stores,
-// one bulk group).  run_tiles() pipelines a CTA's tiles (t = first + i * stride):
-//   prologue: loads of tiles 0..S-1;
-//   tile i:   wait input i; out buffer i % 2 free (bulk stores of tile i-2 have read it);
-//             compute; proxy fence + barrier; stores of tile i; loads of tile i + S into
-//             the input stage just consumed.
-// Ordering: the phase wait (sync_wait) precedes the first load, and the issuing thread
-// fences the generic -> async proxy; compute's shared-memory writes are fenced to the
-// async proxy before the stores; at the end thread 0 waits for its bulk stores to
-// complete (cp.async.bulk.wait_group 0) and fences, so the kernel's phase publication
-// (sync_signal) and stream completion cover them.
 #pragma once
 
-#include "link.cuh"
+#include "codec.cuh"
 
 namespace hz {
 namespace dev {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+}
+// bulk load global -> shared (bytes % 16 == 0, src / dst 16-byte aligned), completion
+// counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 // bulk store shared -> global (bytes % 16 == 0, both 16-byte aligned), in the current
 // bulk group
