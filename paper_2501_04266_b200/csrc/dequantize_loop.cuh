@@ -25,9 +25,17 @@ __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits
     int64_t ub = base;            // first unit of this warp tile in the layer
     int jt = -1;                  // its piece, when interleaved
     if (inter) {
+      // tile -> (piece, tile of that piece): for each q = tile / n the n tiles go to the n
+      // pieces, rotated by one piece per grid-stride pass (q / (nwarps / n)), so a warp's
+      // successive tiles alternate between the local piece and the peers' pieces.  (With
+      // piece = tile % n and nwarps a multiple of n, every warp would read the same piece
+      // on every pass: half the warps all-NVLink, half all-HBM, the launch ending with
+      // the slower half.)
       const int64_t tile = base / (32 * U);
-      jt = static_cast<int>(tile % pc.n);
-      ub = jt * (pc.len / 8) + (tile / pc.n) * (32 * U);
+      const int64_t q = tile / pc.n;
+      const int64_t rot = nwarps >= pc.n ? q / (nwarps / pc.n) : 0;
+      jt = static_cast<int>((tile % pc.n + rot) % pc.n);
+      ub = jt * (pc.len / 8) + q * (32 * U);
       (void)tiles_per_piece;
     }
     Codes8<BITS> raw[U];

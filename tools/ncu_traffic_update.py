@@ -9,11 +9,11 @@ the summed element counts into profiles/ncu_traffic.json under the key "<kind>@N
 (bench.py looks this key up first for an N-GPU line; "traffic" = bytes per element x
 the launch's elements).  Element counts come from the launch arguments the library
 traces (one vw_profile pass with HZ trace stamps), so they are given here per kernel
-name: --elems 'regex=count,...' (the number of elements one launch of that kernel
+name: --elems 'regex=count,...' (';'-separated; the number of elements one launch of that kernel
 processes: gathered + quantized).
 
     python tools/ncu_traffic_update.py gpurun_out/e8_vwp_ncu.csv --n 2 \\
-        --kind 'k_gather_quantize=gather_quantize' --elems 'Li8E=75546624,Li4E=100728832'
+        --kind 'k_gather_quantize=gather_quantize' --elems 'quantize<__nv_bfloat16, 8=75537408;quantize<__nv_bfloat16, 4=100716544'
 """
 
 import argparse
@@ -48,12 +48,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("csv")
     ap.add_argument("--n", type=int, required=True, help="GPUs of the profiled exchange")
-    ap.add_argument("--kind", required=True, help="kernel-name regex=kind,...")
-    ap.add_argument("--elems", required=True, help="kernel-name regex=elements per launch,...")
+    ap.add_argument("--kind", required=True, help="kernel-name regex=kind;...")
+    ap.add_argument("--elems", required=True, help="kernel-name regex=elements per launch;...")
     ap.add_argument("--source", default="")
     args = ap.parse_args()
-    kinds = [kv.split("=", 1) for kv in args.kind.split(",")]
-    elems = [(k, int(v)) for k, v in (kv.split("=", 1) for kv in args.elems.split(","))]
+    kinds = [kv.split("=", 1) for kv in args.kind.split(";")]
+    elems = [(k, int(v)) for k, v in (kv.split("=", 1) for kv in args.elems.split(";"))]
     acc = defaultdict(lambda: defaultdict(float))
     for (_, name), m in read(args.csv).items():
         kind = next((k for rx, k in kinds if re.search(rx, name)), None)

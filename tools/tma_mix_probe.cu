@@ -90,6 +90,81 @@ __global__ void __launch_bounds__(256) tma_k(const char* __restrict__ in, char* 
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Hybrid: ld.global loads (registers, 32 warps per SM) and per-warp bulk STORES — each
+// warp writes its output span to its own shared-memory buffer (double-buffered) and lane 0
+// issues one cp.async.bulk shared -> global per span; no CTA barrier anywhere.  16
+// elements per lane per iteration (U units of 16 B input per lane).
+template <int RB, int WB, int U>
+__global__ void __launch_bounds__(256) hyb_k(const uint4* __restrict__ in, char* __restrict__ out, long units) {
+  extern __shared__ __align__(128) char smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int SPAN = 32 * U * 16 * WB / RB;            // output bytes per warp iteration
+  char* buf = smem + w * 2 * SPAN;
+  const long gw = (blockIdx.x * 256L + threadIdx.x) >> 5, nw = (gridDim.x * 256L) >> 5;
+  int it = 0;
+  for (long base = gw * 32 * U; base < units; base += nw * 32 * U, ++it) {
+    uint4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = in[base + u * 32 + lane];
+    char* b = buf + (it & 1) * SPAN;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    uint4* o = reinterpret_cast<uint4*>(b);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < WB / RB; ++k) o[(u * (WB / RB) + k) * 32 + lane] = make_uint4(r[u].x ^ k, r[u].y, r[u].z + 1, r[u].w);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + base * 16 * WB / RB),
+                   "r"(sa(b)), "r"(SPAN)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int RB, int WB, int U>
+void run_hyb(const char* what, long n, int sms, int cpb) {
+  const long units = n * RB / 16;
+  const int sets = 4;
+  char *in[sets], *out[sets];
+  for (int s = 0; s < sets; ++s) {
+    CK(cudaMalloc(&in[s], n * RB));
+    CK(cudaMalloc(&out[s], n * WB));
+    CK(cudaMemset(in[s], 1, n * RB));
+  }
+  const int smem = 8 * 2 * (32 * U * 16 * WB / RB);
+  CK(cudaFuncSetAttribute(hyb_k<RB, WB, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hyb_k<RB, WB, U>, 256, smem));
+  const int c = cpb < occ ? cpb : occ;
+  const int grid = sms * (c > 0 ? c : 1);
+  for (int s = 0; s < sets; ++s) hyb_k<RB, WB, U><<<grid, 256, smem>>>((const uint4*)in[s], out[s], units);
+  CK(cudaGetLastError());
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  const int iters = 20;
+  CK(cudaEventRecord(a));
+  for (int i = 0; i < iters; ++i) hyb_k<RB, WB, U><<<grid, 256, smem>>>((const uint4*)in[i % sets], out[i % sets], units);
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  CK(cudaGetLastError());
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  ms /= iters;
+  const double bytes = double(n) * (RB + WB);
+  printf("HYB %-36s U=%d ctas/SM=%d (smem %6d): %7.1f us  %7.1f GB/s\n", what, U, c, smem, ms * 1e3,
+         bytes / (ms * 1e-3) / 1e9);
+  for (int s = 0; s < sets; ++s) {
+    CK(cudaFree(in[s]));
+    CK(cudaFree(out[s]));
+  }
+}
+
 template <int RB, int WB>
 void run(const char* what, long n, int sms, int te, int s_in, int cpb) {
   const long ntiles = n / te;
@@ -133,6 +208,18 @@ int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const long n = 50364416;   // GPT-1.3B layer, padded (multiple of 8192)
+  if (getenv("HYB")) {
+    for (int cpb : {2, 3, 4, 6, 8}) {
+      run_hyb<2, 4, 2>("qgZ round trip mix (bf16 -> fp32)", n, sms, cpb);
+      run_hyb<2, 4, 4>("qgZ round trip mix (bf16 -> fp32)", n, sms, cpb);
+      run_hyb<1, 2, 2>("dequantize mix (int8 -> bf16)", n, sms, cpb);
+      run_hyb<1, 2, 4>("dequantize mix (int8 -> bf16)", n, sms, cpb);
+      run_hyb<2, 2, 2>("1:1 copy (bf16 -> bf16)", n, sms, cpb);
+      run_hyb<2, 2, 4>("1:1 copy (bf16 -> bf16)", n, sms, cpb);
+    }
+    printf("done\n");
+    return 0;
+  }
   for (int te : {2048, 4096, 8192}) {
     for (int s_in : {2, 3, 4}) {
       for (int cpb : {2, 4}) {

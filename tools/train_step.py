@@ -51,6 +51,9 @@ def main():
     ap.add_argument("--green", type=int, default=0,
                     help="run the communication stream in a CUDA green context of this many SMs "
                          "(libhz grids sized to it: hz_set_sm_budget)")
+    ap.add_argument("--budget", type=int, default=0,
+                    help="hz_set_sm_budget for the libhz grids (SMs x resident CTAs; e.g. 37 = 148 CTAs, one "
+                         "per SM, leaving each SM room for a GEMM CTA)")
     ap.add_argument("--prio", action="store_true",
                     help="compute stream at high priority, communication stream at the lowest")
     args = ap.parse_args()
@@ -84,6 +87,8 @@ def main():
         from tools.green_probe import green_stream
         comm_green, green_sms = green_stream(args.green)
         hz.set_sm_budget(green_sms)
+    if args.budget:
+        hz.set_sm_budget(args.budget)
     L = len(group)
     numel = synth.layer_numel(h)
     p = ctx.partition(numel, B, 1, 1, L)
@@ -251,7 +256,7 @@ def main():
     line = {"what": "synthetic ZeRO-topo training step (layer GEMMs + sharded collectives, overlapped)",
             "config": args.config, "layers": nl, "tokens_per_gpu": T, "n_gpus": world, "hierarchy": list(group),
             "transport": "p2p" if use_p2p else ("nccl" if world > 1 else "local"),
-            "green_sms": green_sms if args.green else 0, "prio": args.prio, "pair": args.pair, "hz_tune": os.environ.get("HZ_TUNE", ""),
+            "green_sms": green_sms if args.green else 0, "sm_budget": args.budget, "prio": args.prio, "pair": args.pair, "hz_tune": os.environ.get("HZ_TUNE", ""),
             "results": results}
     ctx.close()
     if rank == 0:
