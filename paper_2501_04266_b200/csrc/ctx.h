@@ -81,6 +81,7 @@ struct hz_ctx {
     std::vector<cudaEvent_t> ev;        // 3 per tensor: primary in, grad in, shard ready
     cudaEvent_t kernels_done = nullptr; // the previous call's last kernel
     cudaEvent_t d2h_done = nullptr;
+    cudaEvent_t entry = nullptr;         // the stream position at the start of a call
   } exec;
 };
 
@@ -120,6 +121,9 @@ hz_status p2p_allreduce_select(hz_ctx* ctx, const hz_partition_t* p, const float
 
 // P2P transport (p2p.cpp)
 bool in_pool(const hz_ctx* ctx, const void* p, size_t bytes);
+// partition made for this context (rank, world, levels, group sizes), valid block,
+// padding and hop grouping (engine.cpp)
+hz_status check_partition(const hz_ctx* ctx, const hz_partition_t* p);
 // the next layer's quantize fused into this layer's forward gather (k_gather_quantize)
 struct NextQ {
   const hz_partition_t* p;

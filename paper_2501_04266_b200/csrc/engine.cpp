@@ -131,8 +131,6 @@ hz_status hop_comm(hz_ctx* ctx, int a, int b, ncclComm_t* out) {
   return HZ_OK;
 }
 
-namespace {
-
 hz_status check_partition(const hz_ctx* ctx, const hz_partition_t* p) {
   if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
   if (!p) return fail(HZ_ERR_INVALID, "p: NULL");
@@ -149,8 +147,6 @@ hz_status check_partition(const hz_ctx* ctx, const hz_partition_t* p) {
       return fail(HZ_ERR_INVALID, "p.hop_last: must be strictly ascending and end at level L");
   return HZ_OK;
 }
-
-}  // namespace
 
 int64_t elem_bytes(hz_dtype dt) { return dt == HZ_F32 ? 4 : 2; }
 

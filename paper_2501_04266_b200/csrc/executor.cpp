@@ -12,9 +12,11 @@
 // n-1..0), so the kernels of tensor i start as soon as its bytes are on the GPU
 // and the download of shard i overlaps the upload of gradient i-1.  A call's
 // uploads wait only for the previous call's kernels (its staging buffers were
-// read by them), not for its downloads: back-to-back steps keep both PCIe
-// directions busy.  The kernel stream waits for the last download at the end, so
-// the call is stream-ordered on `stream` like every other entry point.  The kernels
+// read by them) and whatever else the caller enqueued on the stream before the call
+// (an entry event).  The kernel stream waits for the last download at the end, so
+// the call is stream-ordered on `stream` like every other entry point.  Every argument
+// (partitions, alignment, P2P-pool secondaries) is validated before anything is
+// enqueued.  The kernels
 // are issued as the paired calls (hz_allgather_params_next / hz_backward_step).
 #include <string>
 
@@ -34,6 +36,7 @@ hz_status ensure_exec(hz_ctx* ctx, int n) {
     if ((e = cudaStreamCreateWithFlags(&ex.h2d, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ex.d2h, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ex.kernels_done, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ex.entry, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ex.d2h_done, cudaEventDisableTiming)) != cudaSuccess)
       return cuda_fail(e, "hz_step_host: stream / event creation");
   }
@@ -53,6 +56,7 @@ void exec_release(hz_ctx* ctx) {
   for (cudaEvent_t e : ex.ev) cudaEventDestroy(e);
   ex.ev.clear();
   if (ex.kernels_done) cudaEventDestroy(ex.kernels_done);
+  if (ex.entry) cudaEventDestroy(ex.entry);
   if (ex.d2h_done) cudaEventDestroy(ex.d2h_done);
   if (ex.h2d) cudaStreamDestroy(ex.h2d);
   if (ex.d2h) cudaStreamDestroy(ex.d2h);
@@ -81,8 +85,7 @@ extern "C" hz_status hz_step_host(hz_ctx* ctx, int n, const hz_tensor_io* t, hz_
     const hz_tensor_io& x = t[i];
     const hz_partition_t* p = x.p;
     if (!p) return bad(i, "p", "NULL");
-    if (p->rank != ctx->rank || p->world != ctx->world || p->levels != ctx->levels)
-      return bad(i, "p", "partition was not made for this context (rank/world/levels)");
+    if (check_partition(ctx, p) != HZ_OK) return bad(i, "p", hz_last_error());
     if (!x.h_primary) return bad(i, "h_primary", "NULL");
     if (!x.h_grad) return bad(i, "h_grad", "NULL");
     if (!x.h_shard) return bad(i, "h_shard", "NULL");
@@ -91,6 +94,13 @@ extern "C" hz_status hz_step_host(hz_ctx* ctx, int n, const hz_tensor_io* t, hz_
     if (!x.d_shard || !aligned16(x.d_shard)) return bad(i, "d_shard", "NULL or not 16-byte aligned");
     if (!x.sec_codes || !aligned16(x.sec_codes)) return bad(i, "sec_codes", "NULL or not 16-byte aligned");
     if (!x.sec_scales || !aligned16(x.sec_scales)) return bad(i, "sec_scales", "NULL or not 16-byte aligned");
+    if (ctx->p2p.on) {   // peers read the secondaries in place: symmetric-pool memory (hz_sym_alloc)
+      const int64_t ls = p->len[p->s];
+      if (!in_pool(ctx, x.sec_codes, size_t(ls) * qwz_bits / 8))
+        return bad(i, "sec_codes", "not hz_sym_alloc memory of the P2P pool (or too small)");
+      if (!in_pool(ctx, x.sec_scales, size_t(ls / p->block) * 4))
+        return bad(i, "sec_scales", "not hz_sym_alloc memory of the P2P pool (or too small)");
+    }
   }
   hz_status rc = ensure_exec(ctx, n);
   if (rc != HZ_OK) return rc;
@@ -105,8 +115,11 @@ extern "C" hz_status hz_step_host(hz_ctx* ctx, int n, const hz_tensor_io* t, hz_
     if ((e = (call)) != cudaSuccess) return cuda_fail(e, what); \
   } while (0)
 
-  // uploads: after the previous call's kernels, in consumption order
-  HZ_X(cudaStreamWaitEvent(ex.h2d, ex.kernels_done, 0), "hz_step_host: wait previous kernels");
+  // uploads: after everything enqueued on `stream` before this call (the previous call's
+  // kernels and downloads, and whatever the caller ran on the stream in between, e.g.
+  // hz_adamw_step writing the device primaries), in consumption order
+  HZ_X(cudaEventRecord(ex.entry, st), "hz_step_host: cudaEventRecord");
+  HZ_X(cudaStreamWaitEvent(ex.h2d, ex.entry, 0), "hz_step_host: wait stream entry");
   for (int i = 0; i < n; ++i) {
     const hz_partition_t* p = t[i].p;
     HZ_X(cudaMemcpyAsync(t[i].d_primary, t[i].h_primary, size_t(p->len[p->w] * eb), cudaMemcpyHostToDevice,

@@ -239,3 +239,31 @@ print("DONE")
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert p.returncode == 0 and "DONE" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+def test_step_host_rejects_non_pool_secondaries():
+    """P2P transport: hz_step_host validates, before enqueuing anything, that every
+    tensor's hpZ secondary is symmetric-pool memory (peers read it in place) — a plain
+    device allocation is HZ_ERR_INVALID naming the tensor and field."""
+    _need_gpu()
+    from paper_2501_04266_b200 import hz
+    ctxs = hz.virtual_world((2,), pool_bytes=8 << 20)
+    try:
+        c = ctxs[0]
+        p = c.partition(8192, 256, 1, 1, 1)
+        n = p.range(1)[1]
+        d = lambda k, dt: torch.empty(k, dtype=dt, device="cuda")
+        t = {"p": p, "h_primary": torch.empty(n, dtype=torch.bfloat16).pin_memory(), "d_primary": d(n, torch.bfloat16),
+             "h_grad": torch.empty(p.padded_numel, dtype=torch.bfloat16).pin_memory(),
+             "d_grad": d(p.padded_numel, torch.bfloat16), "sec_codes": d(n, torch.uint8),
+             "sec_scales": d(n // 256, torch.float32), "d_shard": d(n, torch.float32),
+             "h_shard": torch.empty(n, dtype=torch.float32).pin_memory()}
+        full = [d(p.padded_numel, torch.bfloat16) for _ in range(2)]
+        with pytest.raises(hz.HZError) as ei:
+            c.step_host([t], full)
+        assert ei.value.status == hz.ERR_INVALID and "t[0].sec_codes" in str(ei.value), str(ei.value)
+        c.check()                                   # nothing enqueued, context healthy
+    finally:
+        torch.cuda.synchronize()
+        for x in ctxs:
+            x.close()
