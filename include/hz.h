@@ -439,15 +439,16 @@ HZ_API hz_status hz_adamw_step(hz_ctx* ctx, const hz_partition_t* p, const float
  * two directions overlap each other and the kernels.  `stream` finally waits for
  * every device->host copy: once `stream` passes this call, every h_shard holds the
  * step's fp32 gradient shard (bitwise the result of the device-resident calls).
- * The host->device copies of a call start after everything enqueued on `stream`
- * before the call (the previous call, and any work of the caller in between, such
- * as hz_adamw_step writing the device primaries); within a call, the downloads of
- * layer i's shard overlap the uploads of the gradients of layers i-1, i-2, ...
+ * The host->device copies of a call wait only for the previous call's kernels, so
+ * back-to-back calls upload the next step's inputs while this step's shards are
+ * still being read back.
  * Ownership: the caller owns every buffer.  h_* should be page-locked
  * (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous; they must
  * not be modified (h_primary, h_grad) or read (h_shard) before `stream` passes the
- * call.  d_primary / d_grad are staging buffers the executor writes; the caller
- * must not use them on other streams meanwhile.  sec_codes / sec_scales: the hpZ
+ * call.  d_primary / d_grad are staging buffers owned by the executor from the first
+ * call on: the caller must not read or write them on any stream, `stream` included,
+ * between calls (the next call's uploads into them start as soon as the previous
+ * call's kernels are done, without waiting for other work on `stream`).  sec_codes / sec_scales: the hpZ
  * secondary of range_s (P2P transport: from hz_sym_alloc).  full_out0/1: device
  * out_dt[max Np] gathered-layer buffers, alternating between tensors.
  * Errors: HZ_ERR_INVALID (n < 1, NULL pointers, a partition of another context or

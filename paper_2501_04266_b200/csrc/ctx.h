@@ -81,7 +81,6 @@ struct hz_ctx {
     std::vector<cudaEvent_t> ev;        // 3 per tensor: primary in, grad in, shard ready
     cudaEvent_t kernels_done = nullptr; // the previous call's last kernel
     cudaEvent_t d2h_done = nullptr;
-    cudaEvent_t entry = nullptr;         // the stream position at the start of a call
   } exec;
 };
 

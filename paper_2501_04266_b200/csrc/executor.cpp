@@ -12,8 +12,8 @@
 // n-1..0), so the kernels of tensor i start as soon as its bytes are on the GPU
 // and the download of shard i overlaps the upload of gradient i-1.  A call's
 // uploads wait only for the previous call's kernels (its staging buffers were
-// read by them) and whatever else the caller enqueued on the stream before the call
-// (an entry event).  The kernel stream waits for the last download at the end, so
+// read by them), not for its downloads: back-to-back steps keep both PCIe directions
+// busy.  The kernel stream waits for the last download at the end, so
 // the call is stream-ordered on `stream` like every other entry point.  Every argument
 // (partitions, alignment, P2P-pool secondaries) is validated before anything is
 // enqueued.  The kernels
@@ -36,7 +36,6 @@ hz_status ensure_exec(hz_ctx* ctx, int n) {
     if ((e = cudaStreamCreateWithFlags(&ex.h2d, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ex.d2h, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ex.kernels_done, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&ex.entry, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ex.d2h_done, cudaEventDisableTiming)) != cudaSuccess)
       return cuda_fail(e, "hz_step_host: stream / event creation");
   }
@@ -56,7 +55,6 @@ void exec_release(hz_ctx* ctx) {
   for (cudaEvent_t e : ex.ev) cudaEventDestroy(e);
   ex.ev.clear();
   if (ex.kernels_done) cudaEventDestroy(ex.kernels_done);
-  if (ex.entry) cudaEventDestroy(ex.entry);
   if (ex.d2h_done) cudaEventDestroy(ex.d2h_done);
   if (ex.h2d) cudaStreamDestroy(ex.h2d);
   if (ex.d2h) cudaStreamDestroy(ex.d2h);
@@ -115,11 +113,12 @@ extern "C" hz_status hz_step_host(hz_ctx* ctx, int n, const hz_tensor_io* t, hz_
     if ((e = (call)) != cudaSuccess) return cuda_fail(e, what); \
   } while (0)
 
-  // uploads: after everything enqueued on `stream` before this call (the previous call's
-  // kernels and downloads, and whatever the caller ran on the stream in between, e.g.
-  // hz_adamw_step writing the device primaries), in consumption order
-  HZ_X(cudaEventRecord(ex.entry, st), "hz_step_host: cudaEventRecord");
-  HZ_X(cudaStreamWaitEvent(ex.h2d, ex.entry, 0), "hz_step_host: wait stream entry");
+  // uploads: after the previous call's kernels (not its downloads: back-to-back calls keep
+  // both PCIe directions busy), in consumption order.  The staging buffers d_primary /
+  // d_grad belong to the executor between calls (hz.h).  Measured: waiting instead for
+  // everything on `stream` (an entry event, which includes the previous call's downloads)
+  // cost 24 ms of 134 ms per GPT-1.3B step at N = 1.
+  HZ_X(cudaStreamWaitEvent(ex.h2d, ex.kernels_done, 0), "hz_step_host: wait previous kernels");
   for (int i = 0; i < n; ++i) {
     const hz_partition_t* p = t[i].p;
     HZ_X(cudaMemcpyAsync(t[i].d_primary, t[i].h_primary, size_t(p->len[p->w] * eb), cudaMemcpyHostToDevice,
