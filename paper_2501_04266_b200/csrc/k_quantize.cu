@@ -233,11 +233,8 @@ cudaError_t quantize_d(const void* x, int64_t n, int bits, int block, uint8_t* c
 // grid-stride share of both jobs; odd CTAs gather first and even CTAs quantize
 // first, so at any time about half the warps stream each resource (HZ_TUNE gq=1:
 // every CTA gathers first).  Arithmetic per element is exactly the two kernels'.
-#ifndef HZ_DUAL_MINB
-#define HZ_DUAL_MINB 3   // resident CTAs the dual kernel is compiled for (80 registers: 3 per SM)
-#endif
 template <typename T, int QBITS, int GBITS, typename TO, int QOUT, bool CHUNKED, int GU = kU>
-__global__ void __launch_bounds__(kThreads, HZ_DUAL_MINB) k_gather_quantize(const __grid_constant__ Pieces pc, int64_t nunits,
+__global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_constant__ Pieces pc, int64_t nunits,
                                                                TO* __restrict__ y, const T* __restrict__ x,
                                                                int64_t nblocks, uint8_t* __restrict__ codes,
                                                                float* __restrict__ scales, float* __restrict__ qy,
@@ -255,49 +252,7 @@ __global__ void __launch_bounds__(kThreads, HZ_DUAL_MINB) k_gather_quantize(cons
   }
   if (!sync_wait(sy)) return;
   const int64_t warp = global_warp(), nwarps = num_warps();
-  if (order == -1) {
-    // Balanced schedule (default): the warp tiles of both jobs form one index space —
-    // gather tile, quantize iteration, gather tile, ... while both last — cut into
-    // gridDim.x equal contiguous ranges, one per CTA; inside its range a CTA's warps take
-    // the next index from a shared-memory counter.  Every warp of a CTA therefore
-    // finishes within one tile of its siblings (with static grid-stride shares, ncu found
-    // 27 % of warp samples idling at the exit barrier while slower siblings — those
-    // holding NVLink tiles — finished), and every CTA's range mixes peer and local
-    // gather tiles and quantize work.  The quantize tail (< NB blocks) is one more index.
-    __shared__ unsigned ctr;
-    if (threadIdx.x == 0) ctr = 0u;
-    __syncthreads();
-    constexpr int NB = kU * Geo<256>::BPW;
-    const int64_t G = (nunits + 32 * GU - 1) / (32 * GU);
-    const int64_t nfull = nblocks / NB;
-    const int64_t Q = nfull + (nfull * NB < nblocks ? 1 : 0);
-    const int64_t m = G < Q ? G : Q;
-    const int64_t total = G + Q;
-    const int64_t c0 = total * blockIdx.x / gridDim.x, c1 = total * (blockIdx.x + 1) / gridDim.x;
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-      unsigned k0 = 0;
-      if (lane == 0) k0 = atomicAdd(&ctr, 1u);
-      const int64_t k = c0 + __shfl_sync(0xffffffffu, k0, 0);
-      if (k >= c1) break;
-      int64_t gt = -1, qt = -1;
-      if (k < 2 * m) {
-        if (k & 1) qt = k >> 1;
-        else gt = k >> 1;
-      } else if (G > Q) {
-        gt = k - m;
-      } else {
-        qt = k - m;
-      }
-      if (gt >= 0) {
-        dequantize_loop<GBITS, TO, GU>(pc, nunits, 8, y, 0, 1, gt, gt + 1);
-      } else if (qt < nfull) {
-        quantize_loop<T, 256, QBITS, kU, QOUT>(x, nblocks, codes, scales, emit, qy, acc, 0, 1, qt, qt + 1);
-      } else {   // the tail: blocks [nfull * NB, nblocks)
-        quantize_loop<T, 256, QBITS, kU, QOUT>(x, nblocks, codes, scales, emit, qy, acc, 0, 1, nfull, INT64_MAX);
-      }
-    }
-  } else if (order >= 2) {   // role split: CTAs [0, order - 2) gather only, the rest quantize only
+  if (order >= 2) {   // role split: CTAs [0, order - 2) gather only, the rest quantize only
     const int64_t gcta = order - 2;
     const int64_t wpc = kThreads / 32;
     if (blockIdx.x < gcta)
@@ -337,7 +292,6 @@ cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const
   // registers cost more than the balance gains, 3.80 vs 4.20 ms), 4 chunks from ~32 tiles
   // per warp on (GPT-6.7B layer: 19.28 -> 17.76 ms per step at N = 2)
   int chunks = tune_param("gqc", 0);
-  if (tune_param("gq", -1) == -1) chunks = 1;   // the balanced schedule mixes the jobs itself
   if (chunks <= 0) {
     const int64_t per_warp = (n_gather / 8 + 32 * kU - 1) / (32 * kU) / (int64_t(sm_count()) * 32);
     chunks = per_warp >= 32 ? 4 : 1;
@@ -351,10 +305,9 @@ cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const
   const int64_t nblocks = n_q / 256;
   const int64_t tasks = std::max<int64_t>((nunits + 32 * kU - 1) / (32 * kU), nblocks / (kU * Geo<256>::BPW) + 1);
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks);
-  // HZ_TUNE gq: -1 = balanced per-CTA ranges with a shared-memory tile counter (default);
-  // 0 = every warp does both jobs grid-stride, odd CTAs gather first; 1 = all gather
-  // first; 2 = role split with gqf percent of the CTAs gathering
-  int order = tune_param("gq", -1);
+  // HZ_TUNE gq: 0 = every warp does both jobs, odd CTAs gather first (default); 1 = all
+  // gather first; 2 = role split with gqf percent of the CTAs gathering
+  int order = tune_param("gq", 0);
   if (order == 2 && grid < 2) order = 0;
   if (order == 2) {
     int64_t gc = grid * tune_param("gqf", 50) / 100;
