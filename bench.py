@@ -1017,12 +1017,18 @@ def cpu_baseline(args, group, model):
     info = _host_info()
     # BASELINE config 1 as well: the flat 1M-element tensor over 8 simulated ranks (2,2,2)
     s1, b1 = _oracle_layer((2, 2, 2), 1 << 20, 11, args)
+    # and SURVEY §8(d)'s CPU sample of config 2: one GPT-1.3B layer over the 8 simulated
+    # ranks of the (2,4) hierarchy the config names (8 x 50.4 M elements)
+    s2, b2 = _oracle_layer((2, 4), numel, 41, args)
     return {"value": byts / secs / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{n} tensors of {numel:,} params ({args.config} layer size), all {math.prod(group)} simulated "
                       f"rank(s) of hierarchy {list(group)}: fwd+bwd qwZ all-gather + qgZ reduce-scatter, NumPy "
                       f"single thread; {secs:.1f} s",
             "config1": {"value": b1 / s1 / 1e9, "unit": UNIT, "seconds": s1,
                         "sample": "BASELINE config 1: 1,048,576 elements, 8 simulated ranks as (2,2,2), same step"},
+            "config2_layer_2x4": {"value": b2 / s2 / 1e9, "unit": UNIT, "seconds": s2,
+                                  "sample": f"one {args.config} layer ({numel:,} params) over the 8 simulated ranks of "
+                                            "hierarchy (2,4) (SURVEY 8(d)), same step, NumPy single thread"},
             **info}
 
 
