@@ -14,23 +14,13 @@
 // elementwise mapping with one 8-byte code load per lane per input and a
 // shared-memory transpose for coalesced 512-byte fp32 stores.  Inputs may be
 // peer-mapped (NVLink P2P transport): 8-byte loads keep peer reads at full speed.
-#include "codec.cuh"
+#include "reduce_loop.cuh"
 
 namespace hz {
 namespace {
 
 using namespace dev;
 
-struct RedArgs {
-  const uint8_t* c[kMaxG];
-  const float* s[kMaxG];
-  int g;
-  int accumulate;
-  int64_t n;          // elements
-  uint8_t* oc;
-  float* os;
-  float* of;
-};
 
 // ------------------------------------------------------------ requantizing reduce
 // Sum of the inputs for U warp steps starting at block blk0 (this lane's 8-element
@@ -240,114 +230,9 @@ struct Wide<4> {
 template <int BIN, int GT, int U, bool ACC>
 __global__ void __launch_bounds__(kThreads) k_reduce_f32(const __grid_constant__ RedArgs a, int log2b,
                                                          const __grid_constant__ SyncArgs sy) {
-  constexpr int E = Wide<BIN>::E;
-  constexpr int G = E / 4;                         // float4 granules per lane per unit
-  __shared__ float4 stage[kThreads / 32][32 * G];
+  __shared__ float4 stage[kThreads / 32][32 * red_granules<BIN>()];
   if (!sync_wait(sy)) return;
-  const int lane = threadIdx.x & 31;
-  float4* st = stage[threadIdx.x >> 5];
-  const int64_t warp = global_warp();
-  const int64_t nwarps = num_warps();
-  const int64_t nunits = a.n / E;
-  constexpr int GP = GT > 0 ? GT : 1;
-  for (int64_t base = warp * 32 * U; base < nunits; base += nwarps * 32 * U) {
-    float acc[U][E];
-    float4 old[ACC ? U : 1][G];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t chunk = base + u * 32;            // first unit of this warp chunk
-      if (ACC && chunk < nunits) {
-#pragma unroll
-        for (int k = 0; k < G; ++k) {
-          const int64_t g4 = chunk * G + k * 32 + lane;   // float4 index, contiguous per k
-          if (g4 < nunits * G) old[u][k] = reinterpret_cast<const float4*>(a.of)[g4];
-        }
-      }
-    }
-    if constexpr (GT > 0) {
-      Wide<BIN> raw[U][GP];
-      float sc[U][GP];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t unit = base + u * 32 + lane;
-#pragma unroll
-        for (int p = 0; p < GP; ++p) {
-          sc[u][p] = 0.f;
-          raw[u][p].r = make_uint2(0u, 0u);
-          if (unit < nunits) {
-            raw[u][p].load(a.c[p] + unit * 8);
-            sc[u][p] = HZ_PEER_LD(a.s[p] + ((unit * E) >> log2b));
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        float c[E];
-        raw[u][0].decode(c);
-#pragma unroll
-        for (int i = 0; i < E; ++i) acc[u][i] = __fmul_rn(c[i], sc[u][0]);
-#pragma unroll
-        for (int p = 1; p < GP; ++p) {
-          raw[u][p].decode(c);
-#pragma unroll
-          for (int i = 0; i < E; ++i) acc[u][i] = __fadd_rn(acc[u][i], __fmul_rn(c[i], sc[u][p]));
-        }
-      }
-    } else {
-      for (int p = 0; p < a.g; ++p) {
-        Wide<BIN> raw[U];
-        float sc[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t unit = base + u * 32 + lane;
-          sc[u] = 0.f;
-          raw[u].r = make_uint2(0u, 0u);
-          if (unit < nunits) {
-            raw[u].load(a.c[p] + unit * 8);
-            sc[u] = HZ_PEER_LD(a.s[p] + ((unit * E) >> log2b));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          float c[E];
-          raw[u].decode(c);
-#pragma unroll
-          for (int i = 0; i < E; ++i) {
-            const float xh = __fmul_rn(c[i], sc[u]);
-            acc[u][i] = p == 0 ? xh : __fadd_rn(acc[u][i], xh);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t chunk = base + u * 32;
-      if (chunk >= nunits) break;                      // warp-uniform
-      // lane's E sums -> granules lane*G + j (swizzled), then read back granule k*32 + lane
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const int gi = lane * G + j;
-        st[gi ^ ((gi >> 3) & (G - 1))] = make_float4(acc[u][4 * j], acc[u][4 * j + 1], acc[u][4 * j + 2], acc[u][4 * j + 3]);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < G; ++k) {
-        const int gi = k * 32 + lane;
-        float4 o = st[gi ^ ((gi >> 3) & (G - 1))];
-        const int64_t g4 = chunk * G + gi;
-        if (g4 < nunits * G) {
-          if constexpr (ACC) {
-            o.x = __fadd_rn(old[u][k].x, o.x);
-            o.y = __fadd_rn(old[u][k].y, o.y);
-            o.z = __fadd_rn(old[u][k].z, o.z);
-            o.w = __fadd_rn(old[u][k].w, o.w);
-          }
-          reinterpret_cast<float4*>(a.of)[g4] = o;
-        }
-      }
-      __syncwarp();
-    }
-  }
+  reduce_f32_loop<BIN, GT, U, ACC>(a, log2b, stage[threadIdx.x >> 5], global_warp(), num_warps());
   sync_signal(sy);
 }
 
