@@ -49,7 +49,8 @@ HIERARCHY = {
     "gpt6.7b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
     "neox20b": {1: (1,), 2: (2,), 4: (2, 2), 8: (2, 2, 2)},
 }
-KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "gather_quantize", "dequantize_roundtrip",
+KERNEL_KINDS = ("quantize", "dequantize", "gather_dequantize", "gather_quantize", "gather_quantize_reduce",
+                "dequantize_roundtrip",
                 "quantize_dequantize", "reduce",
                 "reduce_requant")
 NVLINK_NOMINAL_GBS = 900.0  # NVLink 5, per direction (north_star denominator)
@@ -309,7 +310,7 @@ def p2p_pool_bytes(args, group):
         if args.s != args.w:                                      # quantized-primary slot
             total += len_w * args.qwz_bits // 8 + len_w // B * 4 + 512
         max_np = max(max_np, Np)
-    total += 2 * len(group) * (max_np + max_np // B * 4 + 512)   # slots (may grow once)
+    total += 2 * (len(group) + 1) * (max_np + max_np // B * 4 + 512)   # slots + the last hop's 2nd (may grow once)
     total += 2 * (max_np // W) * 4 + 1024                       # step-tail update slot
     top = max_np // (W // group[-1])                             # len_{L-1}
     total += 2 * top * 4 + 1024                                 # allreduce + select ping-pong

@@ -276,7 +276,15 @@ HZ_API hz_status hz_allgather_params_next(hz_ctx* ctx, const hz_partition_t* p, 
  * order a training step issues them in (layer i's gradients are reduced while layer
  * i-1's weights are gathered for its backward).  P2P transport, B = 256, bf16
  * output: the gather and the level-`from` quantize run in ONE kernel; otherwise the
- * gather then the reduce-scatter.  p_prev == NULL: exactly hz_reduce_scatter_grads. */
+ * gather then the reduce-scatter.  p_prev == NULL: exactly hz_reduce_scatter_grads.
+ * Deferred last hop (P2P transport, B = 256, p_prev given): the last qgZ hop of layer
+ * p (its fp32 shard) is not launched by this call but carried by the next call on the
+ * context — the next hz_backward_step runs it in the same kernel as its own gather and
+ * quantize (the backward triple kernel: one launch and one cross-GPU synchronisation
+ * fewer per layer), any other call (or hz_flush) first launches it on its own.  So
+ * `shard` holds layer p's result once the stream passes the NEXT call on this context
+ * (a training step's last hz_backward_step, with p_prev == NULL, completes everything);
+ * results are bitwise those of hz_reduce_scatter_grads.  HZ_TUNE defer=0 disables it. */
 HZ_API hz_status hz_backward_step(hz_ctx* ctx, const hz_partition_t* p, const void* grad, hz_dtype dt,
                                   int from_level, int to_level, const int* bits_per_level, float* shard,
                                   int accumulate, const hz_partition_t* p_prev, uint8_t* prev_sec_codes,
@@ -377,6 +385,12 @@ HZ_API hz_status hz_set_wait_timeout(hz_ctx* ctx, double seconds);
  * directions of a link loaded together.  Errors: HZ_ERR_INVALID, HZ_ERR_CUDA. */
 HZ_API hz_status hz_nvlink_probe(hz_ctx* ctx, int peer, size_t bytes, int reps, float* ms_out, void* stream);
 HZ_API hz_status hz_abort(hz_ctx* ctx);
+/* Complete deferred work of the P2P transport on `stream`: a deferred last qgZ hop of
+ * hz_backward_step and the phase of a prefetched quantize of hz_allgather_params_next
+ * (a later call does this implicitly).  Collective: every rank issues it at the same
+ * point of the call sequence.  No-op without the P2P transport or pending work.
+ * Errors: HZ_ERR_INVALID (ctx NULL), HZ_ERR_ABORTED, HZ_ERR_CUDA. */
+HZ_API hz_status hz_flush(hz_ctx* ctx, void* stream);
 HZ_API hz_status hz_check(const hz_ctx* ctx);
 
 /* CUDA-graph support for the P2P transport.  The cross-GPU phase numbers are

@@ -54,7 +54,7 @@ const char* const kSymbols[] = {
     "hz_adamw_step",       "hz_set_sm_budget",     "hz_allreduce_select", "hz_step_host", "hz_allgather_params_next", "hz_backward_step",
     "hz_partition_set_hops", "hz_init_virtual",    "hz_init_virtual_ex",    "hz_set_wait_timeout",
     "hz_abort",            "hz_check",             "hz_adamw_params",
-    "hz_nvlink_probe",
+    "hz_nvlink_probe",     "hz_flush",
 };
 }  // namespace
 }  // namespace hz

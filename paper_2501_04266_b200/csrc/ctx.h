@@ -59,7 +59,28 @@ struct hz_ctx {
       size_t off = 0, cap = 0;
     };
     Slot ag_prim_c, ag_prim_s;                  // quantized primary when s != w
-    Slot rs_c[HZ_MAX_LEVELS + 1], rs_s[HZ_MAX_LEVELS + 1];   // level-l send buffers
+    // level-l qgZ send buffers; the last hop's input has two (alternating per reduce-scatter
+    // call, rs_par): a call's deferred last hop still reads one while the next call writes
+    // the other
+    Slot rs_c[HZ_MAX_LEVELS + 1][2], rs_s[HZ_MAX_LEVELS + 1][2];
+    int rs_par = 0;
+    // deferred last qgZ hop of a hz_backward_step (p2p.cpp): run by the next call's
+    // launch (the backward triple kernel) or flushed before any other phase
+    struct PendRed {
+      bool on = false;
+      int g = 0;
+      const uint8_t* c[hz::kMaxG] = {nullptr};
+      const float* s[hz::kMaxG] = {nullptr};
+      int64_t n = 0;
+      int bits = 4;
+      int block = 256;
+      float* shard = nullptr;
+      int acc = 0;
+      int level = 0;
+      unsigned long long ph = 0;   // its phase (wait ready >= ph from wr_mask)
+      unsigned wr_mask = 0;
+      int64_t remote = 0;
+    } pend;
     Slot upd;                                   // updated weights of range_L (step tail)
     Slot ar_a, ar_b;                            // allreduce + select: ping-pong fp32 buffers
     // level-local synchronisation (host bookkeeping, p2p.cpp): the ranks this rank
@@ -109,6 +130,10 @@ hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int6
                      int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
                      cudaStream_t st, int level, const SyncArgs* sync = nullptr,
                      int64_t remote_bytes = 0);
+hz_status run_gather_quantize_reduce(const Pieces& pc, int64_t n, void* y, const void* x, hz_dtype dt, int64_t nq,
+                                     int qbits, uint8_t* c, float* s, int rg, const uint8_t* const* rc,
+                                     const float* const* rs, int64_t rn, int rbits, float* shard, int acc, int level,
+                                     cudaStream_t st, const SyncArgs& sync, int64_t remote_bytes);
 hz_status run_gather_quantize(const Pieces& pc, int64_t n, int bits, void* y, hz_dtype odt, const void* x,
                               hz_dtype dt, int64_t nq, int qbits, uint8_t* c, float* s, cudaStream_t st,
                               const SyncArgs& sync, int64_t remote_bytes, float* qy = nullptr, int acc = 0);

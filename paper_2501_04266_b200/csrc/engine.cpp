@@ -214,6 +214,24 @@ hz_status run_gather_quantize(const Pieces& pc, int64_t n, int bits, void* y, hz
   return HZ_OK;
 }
 
+hz_status run_gather_quantize_reduce(const Pieces& pc, int64_t n, void* y, const void* x, hz_dtype dt, int64_t nq,
+                                     int qbits, uint8_t* c, float* s, int rg, const uint8_t* const* rc,
+                                     const float* const* rs, int64_t rn, int rbits, float* shard, int acc, int level,
+                                     cudaStream_t st, const SyncArgs& sync, int64_t remote_bytes) {
+  const int64_t g_bytes = code_bytes(n, 8) + n / 256 * 4 + n * 2;
+  const int64_t q_bytes = nq * elem_bytes(dt) + code_bytes(nq, qbits) + nq / 256 * 4;
+  const int64_t r_bytes = rg * (code_bytes(rn, rbits) + rn / 256 * 4) + rn * 4 * (acc ? 2 : 1);
+  TraceScope t(st, "gather_quantize_reduce", level, rbits, n + nq + rn, g_bytes + q_bytes + r_bytes - remote_bytes,
+               remote_bytes);
+  SyncArgs sy = sync;
+  sy.stamps = t.stamps;
+  cudaError_t e = launch_gather_quantize_reduce(pc, n, y, x, dt, nq, qbits, c, s, rg, rc, rs, rn, rbits, shard, acc,
+                                                st, sy);
+  t.end();
+  if (e != cudaSuccess) return cuda_fail(e, "gather+quantize+reduce kernel launch");
+  return HZ_OK;
+}
+
 hz_status run_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in,
                      int block, int bits_out, uint8_t* oc, float* os, float* of, int acc,
                      cudaStream_t st, int level, const SyncArgs* sync, int64_t remote_bytes) {

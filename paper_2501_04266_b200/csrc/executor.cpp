@@ -157,10 +157,20 @@ extern "C" hz_status hz_step_host(hz_ctx* ctx, int n, const hz_tensor_io* t, hz_
                           pv ? t[i - 1].sec_codes : nullptr, pv ? t[i - 1].sec_scales : nullptr, qwz_bits,
                           pv ? full[(i - 1) & 1] : nullptr, out_dt, stream);
     if (rc != HZ_OK) return rc;
-    HZ_X(cudaEventRecord(ex.ev[3 * i + 2], st), "hz_step_host: cudaEventRecord");
-    HZ_X(cudaStreamWaitEvent(ex.d2h, ex.ev[3 * i + 2], 0), "hz_step_host: wait shard");
-    HZ_X(cudaMemcpyAsync(t[i].h_shard, t[i].d_shard, size_t(p->len[L] * 4), cudaMemcpyDeviceToHost, ex.d2h),
-         "hz_step_host: shard download");
+    // P2P transport: hz_backward_step with a previous layer defers its last qgZ hop into
+    // the next call's launch, so layer i+1's shard is complete once this call is enqueued
+    // (and, after the last call, layer 0's as well)
+    int ready[2], nready = 0;
+    if (i + 1 <= n - 1) ready[nready++] = i + 1;
+    if (i == 0) ready[nready++] = 0;
+    for (int k = 0; k < nready; ++k) {
+      const int j = ready[k];
+      HZ_X(cudaEventRecord(ex.ev[3 * j + 2], st), "hz_step_host: cudaEventRecord");
+      HZ_X(cudaStreamWaitEvent(ex.d2h, ex.ev[3 * j + 2], 0), "hz_step_host: wait shard");
+      HZ_X(cudaMemcpyAsync(t[j].h_shard, t[j].d_shard, size_t(t[j].p->len[L] * 4), cudaMemcpyDeviceToHost,
+                           ex.d2h),
+           "hz_step_host: shard download");
+    }
   }
   HZ_X(cudaEventRecord(ex.kernels_done, st), "hz_step_host: cudaEventRecord");
   HZ_X(cudaEventRecord(ex.d2h_done, ex.d2h), "hz_step_host: cudaEventRecord");

@@ -92,6 +92,14 @@ cudaError_t tiles_dual(const Pieces& pc, void* y, const void* x, hz_dtype dt, in
 cudaError_t tiles_reduce(int g, const uint8_t* const* c, const float* const* s, int64_t n, int bits_in, int block,
                          int bits_out, uint8_t* oc, float* os, float* of, int acc, cudaStream_t st,
                          const SyncArgs& sy);
+// Backward triple kernel (k_reduce.cu): the dual kernel's gather (8-bit, bf16 out) and
+// quantize plus the fp32 level reduce of g (2 or 4) coded inputs into `shard` (+= when
+// acc), one launch.  B = 256.
+bool gather_quantize_reduce_supported(int gather_bits, hz_dtype out_dt, int g, int red_bits);
+cudaError_t launch_gather_quantize_reduce(const Pieces& pc, int64_t n_gather, void* y, const void* x, hz_dtype dt,
+                                          int64_t n_q, int qbits, uint8_t* codes, float* scales, int g,
+                                          const uint8_t* const* rc, const float* const* rs, int64_t rn, int rbits,
+                                          float* shard, int acc, cudaStream_t st, const SyncArgs& sy);
 cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, int64_t n, int bits,
                               int block, void* y, hz_dtype out_dt, cudaStream_t st);
 cudaError_t launch_gather_dequantize(const Pieces& pc, int64_t n, int bits, int block, void* y,

@@ -14,6 +14,8 @@
 // elementwise mapping with one 8-byte code load per lane per input and a
 // shared-memory transpose for coalesced 512-byte fp32 stores.  Inputs may be
 // peer-mapped (NVLink P2P transport): 8-byte loads keep peer reads at full speed.
+#include "dequantize_loop.cuh"
+#include "quantize_loop.cuh"
 #include "reduce_loop.cuh"
 
 namespace hz {
@@ -311,6 +313,89 @@ cudaError_t f32_g(const RedArgs& a, int log2b, cudaStream_t st, const SyncArgs& 
   }
 }
 
+constexpr int kUF_ = 2;   // = kUF: 8-byte code units in flight per lane per input (fp32 out)
+
+// ------------------------------------------------------------ backward triple kernel
+// k_gather_quantize_reduce (P2P transport, the backward step of layer i-1 with the
+// deferred last qgZ hop of layer i): three independent jobs of three phases in ONE
+// launch — the hpZ gather+dequantize of layer i-2 (NVLink + HBM writes), the int4 / int8
+// quantize of layer i-1's gradient into its send buffer (HBM reads) and the fp32 level
+// reduce of layer i (NVLink + HBM writes) — so the HBM-read and the link/write-heavy
+// streams overlap and one launch, one cross-GPU wait and one publication disappear per
+// layer.  Every warp does its grid-stride share of all three; CTAs rotate the order
+// (blockIdx % 3) so that each job is being streamed by a third of the GPU at any time.
+// Per-element arithmetic is exactly k_dequantize's, k_quantize's and k_reduce_f32's.
+// each job a separate (non-inlined) function: one register allocation each, so the
+// kernel keeps 4 CTAs per SM (64 registers) instead of the union of the three loops'
+template <typename T, int QBITS>
+__device__ __noinline__ void gqr_quantize(const T* __restrict__ x, int64_t nblocks, uint8_t* __restrict__ codes,
+                                          float* __restrict__ scales, int64_t warp, int64_t nwarps) {
+  NoEmit emit;
+  quantize_loop<T, 256, QBITS, 4, 0>(x, nblocks, codes, scales, emit, nullptr, 0, warp, nwarps);
+}
+__device__ __noinline__ void gqr_gather(const Pieces& pc, int64_t nunits, __nv_bfloat16* __restrict__ y,
+                                        int64_t warp, int64_t nwarps) {
+  dequantize_loop<8, __nv_bfloat16, 4>(pc, nunits, 8, y, warp, nwarps);
+}
+template <int RBIN, int RGT, bool RACC>
+__device__ __noinline__ void gqr_reduce(const RedArgs& ra, int log2b, float4* st, int64_t warp, int64_t nwarps) {
+  reduce_f32_loop<RBIN, RGT, 2, RACC>(ra, log2b, st, warp, nwarps);
+}
+
+template <typename T, int QBITS, int RBIN, int RGT, bool RACC>
+__global__ void __launch_bounds__(kThreads, 4) k_gather_quantize_reduce(
+    const __grid_constant__ Pieces pc, int64_t nunits, __nv_bfloat16* __restrict__ y, const T* __restrict__ x,
+    int64_t nblocks, uint8_t* __restrict__ codes, float* __restrict__ scales, const __grid_constant__ RedArgs ra,
+    int log2b, const __grid_constant__ SyncArgs sy) {
+  __shared__ float4 stage[kThreads / 32][32 * red_granules<RBIN>()];
+  if (!sync_wait(sy)) return;
+  const int64_t warp = global_warp(), nwarps = num_warps();
+  float4* st = stage[threadIdx.x >> 5];
+  const int order = static_cast<int>(blockIdx.x % 3);
+#pragma unroll 1
+  for (int k = 0; k < 3; ++k) {
+    const int job = (order + k) % 3;
+    if (job == 0) gqr_gather(pc, nunits, y, warp, nwarps);
+    else if (job == 1) gqr_quantize<T, QBITS>(x, nblocks, codes, scales, warp, nwarps);
+    else gqr_reduce<RBIN, RGT, RACC>(ra, log2b, st, warp, nwarps);
+  }
+  sync_signal(sy);
+}
+
+template <typename T, int QBITS, int RBIN, int RGT, bool RACC>
+cudaError_t gqr_t(const Pieces& pc, int64_t n_gather, void* y, const void* x, int64_t n_q, uint8_t* codes,
+                  float* scales, const RedArgs& ra, cudaStream_t st, const SyncArgs& sy) {
+  auto kern = k_gather_quantize_reduce<T, QBITS, RBIN, RGT, RACC>;
+  constexpr int E = Wide<RBIN>::E;
+  const int64_t tasks = std::max<int64_t>(std::max<int64_t>(n_gather / 8 / (32 * 4), n_q / 256 / 4),
+                                          ra.n / E / (32 * kUF_)) + 1;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks);
+  return launch_k(kern, grid, st, pc, n_gather / 8, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x),
+                  n_q / 256, codes, scales, ra, 8, sy);
+}
+
+template <typename T, int QBITS, int RBIN>
+cudaError_t gqr_g(const Pieces& pc, int64_t n_gather, void* y, const void* x, int64_t n_q, uint8_t* codes,
+                  float* scales, const RedArgs& ra, cudaStream_t st, const SyncArgs& sy) {
+  switch (ra.g) {
+    case 2: return ra.accumulate ? gqr_t<T, QBITS, RBIN, 2, true>(pc, n_gather, y, x, n_q, codes, scales, ra, st, sy)
+                                 : gqr_t<T, QBITS, RBIN, 2, false>(pc, n_gather, y, x, n_q, codes, scales, ra, st, sy);
+    case 4: return ra.accumulate ? gqr_t<T, QBITS, RBIN, 4, true>(pc, n_gather, y, x, n_q, codes, scales, ra, st, sy)
+                                 : gqr_t<T, QBITS, RBIN, 4, false>(pc, n_gather, y, x, n_q, codes, scales, ra, st, sy);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <typename T>
+cudaError_t gqr_d(const Pieces& pc, int64_t n_gather, void* y, const void* x, int64_t n_q, int qbits, uint8_t* codes,
+                  float* scales, const RedArgs& ra, int rbits, cudaStream_t st, const SyncArgs& sy) {
+  if (qbits == 4)
+    return rbits == 4 ? gqr_g<T, 4, 4>(pc, n_gather, y, x, n_q, codes, scales, ra, st, sy)
+                      : gqr_g<T, 4, 8>(pc, n_gather, y, x, n_q, codes, scales, ra, st, sy);
+  return rbits == 4 ? gqr_g<T, 8, 4>(pc, n_gather, y, x, n_q, codes, scales, ra, st, sy)
+                    : gqr_g<T, 8, 8>(pc, n_gather, y, x, n_q, codes, scales, ra, st, sy);
+}
+
 }  // namespace
 
 cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const* scales,
@@ -348,6 +433,35 @@ cudaError_t launch_reduce(int g, const uint8_t* const* codes, const float* const
     case 512: return requant_b<512>(a, bits_in, bits_out, st, sy);
     case 1024: return requant_b<1024>(a, bits_in, bits_out, st, sy);
     case 2048: return requant_b<2048>(a, bits_in, bits_out, st, sy);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hz
+
+namespace hz {
+
+bool gather_quantize_reduce_supported(int gather_bits, hz_dtype out_dt, int g, int red_bits) {
+  return gather_bits == 8 && out_dt == HZ_BF16 && (g == 2 || g == 4) && (red_bits == 4 || red_bits == 8);
+}
+
+cudaError_t launch_gather_quantize_reduce(const Pieces& pc, int64_t n_gather, void* y, const void* x, hz_dtype dt,
+                                          int64_t n_q, int qbits, uint8_t* codes, float* scales, int g,
+                                          const uint8_t* const* rc, const float* const* rs, int64_t rn, int rbits,
+                                          float* shard, int acc, cudaStream_t st, const SyncArgs& sy) {
+  RedArgs ra{};
+  for (int p = 0; p < g; ++p) {
+    ra.c[p] = rc[p];
+    ra.s[p] = rs[p];
+  }
+  ra.g = g;
+  ra.accumulate = acc;
+  ra.n = rn;
+  ra.of = shard;
+  switch (dt) {
+    case HZ_F32: return gqr_d<float>(pc, n_gather, y, x, n_q, qbits, codes, scales, ra, rbits, st, sy);
+    case HZ_BF16: return gqr_d<__nv_bfloat16>(pc, n_gather, y, x, n_q, qbits, codes, scales, ra, rbits, st, sy);
+    case HZ_F16: return gqr_d<__half>(pc, n_gather, y, x, n_q, qbits, codes, scales, ra, rbits, st, sy);
   }
   return cudaErrorInvalidValue;
 }

@@ -192,8 +192,34 @@ hz_status p2p_check(const hz_ctx* ctx) {
 // leaves its phase without a `done`; complete it before any other phase starts: a
 // one-CTA kernel signalling done(pre_phase) — nobody reads those codes in that phase,
 // and every earlier read of this rank is complete in stream order.
-hz_status flush_prefetch(hz_ctx* ctx, cudaStream_t st) {
+// The deferred last qgZ hop of the previous hz_backward_step, as its own launch (when
+// the next call cannot carry it): waits for the hop's inputs (ready >= its phase from
+// the hop group) and signals done(its phase) — no phase was issued since.
+hz_status flush_reduce(hz_ctx* ctx, cudaStream_t st) {
   auto& P = ctx->p2p;
+  if (!P.pend.on) return HZ_OK;
+  const auto r = P.pend;
+  P.pend.on = false;
+  Phases f;
+  f.wr = r.ph;
+  f.wr_mask = r.wr_mask;
+  f.sd = r.ph;
+  f.sd_mask = P.nbr;
+  SyncArgs sr = make_sync(ctx, f);
+  return synced(ctx, sr, st, [&] {
+    return run_reduce(r.g, r.c, r.s, r.n, r.bits, r.block, 0, nullptr, nullptr, r.shard, r.acc, st, r.level, &sr,
+                      r.remote);
+  });
+}
+
+hz_status flush_prefetch(hz_ctx* ctx, cudaStream_t st, bool keep_reduce = false) {
+  auto& P = ctx->p2p;
+  // (a deferred reduce and a prefetched quantize are never pending together: each
+  // call flushes the other kind on entry; flags stay monotone)
+  if (!keep_reduce) {
+    hz_status rc = flush_reduce(ctx, st);
+    if (rc != HZ_OK) return rc;
+  }
   if (!P.pre_phase) return HZ_OK;
   const unsigned long long ph = P.pre_phase;
   P.pre_phase = 0;
@@ -245,6 +271,7 @@ hz_status p2p_allgather(hz_ctx* ctx, const hz_partition_t* p, int backward, cons
   if (pre) {
     P.pre_phase = 0;
     P.pre_codes = P.pre_primary = nullptr;
+    if ((rc = flush_reduce(ctx, st)) != HZ_OK) return rc;
   } else if ((rc = flush_prefetch(ctx, st)) != HZ_OK) {
     return rc;
   }
@@ -389,10 +416,23 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
     if (static_cast<int>(hr[h].size()) > kMaxG) return fail(HZ_ERR_UNSUPPORTED, "more than 16 ranks in one qgZ hop");
     hmask[h] = mask_of(hr[h], ctx->rank);
   }
-  if ((rc = flush_prefetch(ctx, st)) != HZ_OK) return rc;
-  for (const Hop& h : hops) {   // hop send buffers (8-bit capacity), indexed by the first level
-    if ((rc = slot(ctx, P.rs_c[h.a], code_bytes(p->len[h.a - 1], 8))) != HZ_OK) return rc;
-    if ((rc = slot(ctx, P.rs_s[h.a], p->len[h.a - 1] / B * 4)) != HZ_OK) return rc;
+  // a deferred hop of the previous call rides in this call's first launch when that is a
+  // backward triple kernel (prev given, the pending reduce of the supported shape);
+  // otherwise it is flushed as its own launch first
+  const bool carry = prev && P.pend.on &&
+                     gather_quantize_reduce_supported(prev->bits, prev->out_dt, P.pend.g, P.pend.bits) &&
+                     P.pend.block == 256 && tune_param("defer", 1) != 0;
+  if ((rc = flush_prefetch(ctx, st, carry)) != HZ_OK) return rc;
+  // hop send buffers (8-bit capacity), indexed by the first level.  The last hop's input
+  // alternates between two buffers per call (a deferred last hop of the previous call
+  // still reads the other one); the other hops' buffers are single
+  const int par = P.rs_par;
+  P.rs_par ^= 1;
+  auto bi = [&](int h) { return h == H - 1 ? par : 0; };
+  for (int h = 0; h < H; ++h) {
+    const Hop& hp = hops[h];
+    if ((rc = slot(ctx, P.rs_c[hp.a][bi(h)], code_bytes(p->len[hp.a - 1], 8))) != HZ_OK) return rc;
+    if ((rc = slot(ctx, P.rs_s[hp.a][bi(h)], p->len[hp.a - 1] / B * 4)) != HZ_OK) return rc;
   }
   // the previous layer's backward gather (phase gph) fused into this call's first
   // quantize (hz_backward_step; the caller checked p2p_prev_fusable)
@@ -420,8 +460,8 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
   for (int h = 0; h < H; ++h) P.nbr |= hmask[h];
   P.nbr |= pmask;
 
-  uint8_t* c0 = at<uint8_t>(ctx, ctx->rank, P.rs_c[hops[0].a].off);
-  float* s0 = at<float>(ctx, ctx->rank, P.rs_s[hops[0].a].off);
+  uint8_t* c0 = at<uint8_t>(ctx, ctx->rank, P.rs_c[hops[0].a][bi(0)].off);
+  float* s0 = at<float>(ctx, ctx->rank, P.rs_s[hops[0].a][bi(0)].off);
   const unsigned rb0 = readers_of(ctx, c0);
   add_readers(ctx, c0, hmask[0]);
   if (prev) {
@@ -436,12 +476,36 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
     f.sd_mask = P.nbr;
     f.sr = phase_of(0);
     f.sr_mask = hmask[0];
-    SyncArgs sq = make_sync(ctx, f);
-    if ((rc = synced(ctx, sq, st, [&] {
-           return run_gather_quantize(gpc, prev->p->padded_numel, prev->bits, prev->full_out, prev->out_dt, grad, dt,
-                                      p->len[from_level - 1], bits_per_level[from_level - 1], c0, s0, st, sq, gremote);
-         })) != HZ_OK)
-      return rc;
+    if (carry) {
+      // + the previous call's deferred last hop (phase pend.ph = gph - 1): also wait for
+      // its inputs (ready >= pend.ph from its hop group); done(gph) covers its phase.  The
+      // done-wait drops to pend.ph - 1: the members' deferred phase completes only in
+      // their own triple kernel (this same launch, on their side), and everything the
+      // wait protects — the previous layer's secondaries, the last reads of the send
+      // buffer c0 (the previous call's hops, or the launch before for the alternating
+      // buffer) — completed in phases <= pend.ph - 1
+      const auto r = P.pend;
+      P.pend.on = false;
+      f.wd = r.ph - 1;
+      f.wr = r.ph;
+      f.wr_mask = r.wr_mask;
+      SyncArgs sq = make_sync(ctx, f);
+      if ((rc = synced(ctx, sq, st, [&] {
+             return run_gather_quantize_reduce(gpc, prev->p->padded_numel, prev->full_out, grad, dt,
+                                               p->len[from_level - 1], bits_per_level[from_level - 1], c0, s0,
+                                               r.g, r.c, r.s, r.n, r.bits, r.shard, r.acc, r.level, st, sq,
+                                               gremote + r.remote);
+           })) != HZ_OK)
+        return rc;
+    } else {
+      SyncArgs sq = make_sync(ctx, f);
+      if ((rc = synced(ctx, sq, st, [&] {
+             return run_gather_quantize(gpc, prev->p->padded_numel, prev->bits, prev->full_out, prev->out_dt, grad,
+                                        dt, p->len[from_level - 1], bits_per_level[from_level - 1], c0, s0, st, sq,
+                                        gremote);
+           })) != HZ_OK)
+        return rc;
+    }
   } else {
     // A7: quantize the input range_{from-1} into this rank's first send buffer
     Phases f;
@@ -465,8 +529,8 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
     const uint8_t* ptr_c[kMaxG];
     const float* ptr_s[kMaxG];
     for (int j = 0; j < g; ++j) {   // A8+A9: this rank's chunk of member j's send buffer, over NVLink
-      ptr_c[j] = at<const uint8_t>(ctx, hr[h][j], P.rs_c[hp.a].off) + code_bytes(my_rel, bits);
-      ptr_s[j] = at<const float>(ctx, hr[h][j], P.rs_s[hp.a].off) + my_rel / B;
+      ptr_c[j] = at<const uint8_t>(ctx, hr[h][j], P.rs_c[hp.a][bi(h)].off) + code_bytes(my_rel, bits);
+      ptr_s[j] = at<const float>(ctx, hr[h][j], P.rs_s[hp.a][bi(h)].off) + my_rel / B;
     }
     const unsigned long long ph = phase_of(h);
     const int64_t remote = (g - 1) * (code_bytes(cl, bits) + cl / B * 4);
@@ -476,8 +540,8 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
     f.sd = ph;
     f.sd_mask = P.nbr;
     if (h + 1 < H) {
-      uint8_t* oc = at<uint8_t>(ctx, ctx->rank, P.rs_c[hops[h + 1].a].off);
-      float* os = at<float>(ctx, ctx->rank, P.rs_s[hops[h + 1].a].off);
+      uint8_t* oc = at<uint8_t>(ctx, ctx->rank, P.rs_c[hops[h + 1].a][bi(h + 1)].off);
+      float* os = at<float>(ctx, ctx->rank, P.rs_s[hops[h + 1].a][bi(h + 1)].off);
       f.wd = ph - 1;
       f.wd_mask = readers_of(ctx, oc);
       add_readers(ctx, oc, hmask[h + 1]);
@@ -489,6 +553,25 @@ hz_status p2p_reduce_scatter(hz_ctx* ctx, const hz_partition_t* p, const void* g
                                hp.b, &sr, remote);
            })) != HZ_OK)
         return rc;
+    } else if (prev && B == 256 && tune_param("defer", 1) != 0) {
+      // hz_backward_step: defer the last hop (fp32 shard) into the next call's launch —
+      // the next layer's backward triple kernel (or a standalone flush)
+      auto& r = P.pend;
+      r.on = true;
+      r.g = g;
+      for (int j = 0; j < g; ++j) {
+        r.c[j] = ptr_c[j];
+        r.s[j] = ptr_s[j];
+      }
+      r.n = cl;
+      r.bits = bits;
+      r.block = B;
+      r.shard = shard;
+      r.acc = accumulate;
+      r.level = hp.b;
+      r.ph = ph;
+      r.wr_mask = hmask[h];
+      r.remote = remote;
     } else {
       SyncArgs sr = make_sync(ctx, f);
       if ((rc = synced(ctx, sr, st, [&] {
@@ -798,6 +881,20 @@ hz_status hz_nvlink_probe(hz_ctx* ctx, int peer, size_t bytes, int reps, float* 
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(sink);
+  clear_error();
+  return HZ_OK;
+}
+
+hz_status hz_flush(hz_ctx* ctx, void* stream) {
+  using namespace hz;
+  if (!ctx) return fail(HZ_ERR_INVALID, "ctx: NULL");
+  if (!ctx->p2p.on) {
+    clear_error();
+    return HZ_OK;
+  }
+  hz_status rc = p2p_check(ctx);
+  if (rc != HZ_OK) return rc;
+  if ((rc = flush_prefetch(ctx, static_cast<cudaStream_t>(stream))) != HZ_OK) return rc;
   clear_error();
   return HZ_OK;
 }

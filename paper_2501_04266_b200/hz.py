@@ -186,6 +186,7 @@ _sig("hz_set_wait_timeout", [_vp, ctypes.c_double])
 _sig("hz_abort", [_vp])
 _sig("hz_nvlink_probe", [_vp, _int, ctypes.c_size_t, _int, ctypes.POINTER(ctypes.c_float), _vp])
 _sig("hz_check", [_vp])
+_sig("hz_flush", [_vp, _vp])
 _sig("hz_partition_set_hops", [ctypes.POINTER(Partition), _int, ctypes.POINTER(ctypes.c_int)])
 _sig("hz_p2p_enabled", [_vp, ctypes.POINTER(ctypes.c_int)])
 _sig("hz_sym_alloc", [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)])
@@ -453,6 +454,11 @@ class Context:
     def check(self):
         """hz_check: raises HZError(ERR_ABORTED / ERR_NCCL) if the context is dead."""
         _check(_lib.hz_check(self._h))
+
+    def flush(self, stream=None):
+        """hz_flush: complete deferred P2P work (a deferred last qgZ hop of backward_step,
+        a prefetched quantize's phase) on the stream."""
+        _check(_lib.hz_flush(self._h, _stream(stream)))
 
     @property
     def levels(self):

@@ -75,7 +75,7 @@ def test_vworld_full_size(model, g):
     Np = numel + 8192
     errors = vworld.run_ranks(hz, g, lambda r, w, ctx: mp_parity.check_full_size(hz, r, w, g, None, 0, numel, True,
                                                                                   vctx=ctx),
-                              pool_bytes=5 * Np // 2 + (64 << 20))
+                              pool_bytes=7 * Np // 2 + (64 << 20))
     torch.cuda.empty_cache()
     assert not errors, "\n".join(errors[:20])
 

@@ -75,7 +75,7 @@ def main():
     _, len_lm = pmax.range(L)
     p2p = args.transport == "p2p"
     if p2p:
-        ctx.enable_p2p(len_wm + len_wm // B * 4 + 2 * L * (Npm + Npm // B * 4 + 512) + (64 << 20))
+        ctx.enable_p2p(len_wm + len_wm // B * 4 + 2 * (L + 1) * (Npm + Npm // B * 4 + 512) + (64 << 20))
     sec_c = ctx.sym_alloc(len_wm, torch.uint8) if p2p else torch.empty(len_wm, dtype=torch.uint8, device=dev)
     sec_s = (ctx.sym_alloc(len_wm // B, torch.float32) if p2p
              else torch.empty(len_wm // B, dtype=torch.float32, device=dev))
