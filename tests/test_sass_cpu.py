@@ -99,3 +99,13 @@ def test_tile_engine_kernels_are_tma_pipelines(sass, resources):
         assert text.count("UBLKCP") >= 2, f"no bulk load + store in {f}"
         assert "SYNCS.ARRIVE.TRANS64" in text and "SYNCS.PHASECHK" in text, f"no mbarrier in {f}"
         assert resources[f]["REG"] <= 64, (f, resources[f])
+
+
+def test_backward_triple_kernel_keeps_four_ctas_per_sm(sass, resources):
+    """The backward triple kernel (gather || quantize || deferred fp32 reduce) keeps the
+    dual kernel's 4 CTAs of 256 threads per SM (<= 64 registers; its three jobs are
+    separate non-inlined functions) and touches no local memory."""
+    names = [f for f in resources if "k_gather_quantize_reduce" in f]
+    assert names, "k_gather_quantize_reduce not in the library"
+    assert all(resources[f]["REG"] <= 64 and resources[f].get("LOCAL", 0) == 0 for f in names), \
+        {f: resources[f] for f in names}
