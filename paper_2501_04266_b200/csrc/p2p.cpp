@@ -908,6 +908,9 @@ hz_status hz_p2p_capture_begin(hz_ctx* ctx) {
   if (ctx->p2p.pre_phase)
     return fail(HZ_ERR_INVALID, "ctx: a prefetched quantize (hz_allgather_params_next) is pending; gather that "
                                 "layer before beginning a capture");
+  if (ctx->p2p.pend.on)
+    return fail(HZ_ERR_INVALID, "ctx: a deferred qgZ hop (hz_backward_step) is pending; call hz_flush (or finish "
+                                "the backward pass) before beginning a capture");
   ctx->p2p.capturing = true;
   ctx->p2p.capture_start = ctx->p2p.phase;
   clear_error();

@@ -267,3 +267,57 @@ def test_step_host_rejects_non_pool_secondaries():
         torch.cuda.synchronize()
         for x in ctxs:
             x.close()
+
+
+def test_deferred_last_hop_completes_on_flush():
+    """hz_backward_step with a previous layer defers the last qgZ hop (P2P, B = 256): the
+    shard is not written by that call; hz_flush (or any later call) launches it, and the
+    result is bitwise hz_reduce_scatter_grads'.  Checked on (2,) with the trace: no reduce
+    launch before the flush, one after."""
+    _need_gpu()
+    import ml_dtypes
+    from oracle import collectives as col
+    from oracle import partition as pm
+    from paper_2501_04266_b200 import hz, synth
+    from tests import vworld
+    from tests.gpu_util import assert_bitwise, to_dev, to_host
+    g = (2,)
+    numel, B = 60_001, 256
+    Np = pm.padded_numel(numel, g, B)
+    grads = {r: synth.gradient_like(Np, 900 + r, block=B).astype(ml_dtypes.bfloat16) for r in range(2)}
+    want = col.reduce_scatter(grads, g, Np, B, 1, 1, {1: 4})
+    full = np.zeros(Np, np.float32)
+    full[:numel] = synth.params_like(numel, 77, block=B)
+    full = full.astype(ml_dtypes.bfloat16)
+    got = {}
+
+    def fn(r, w, ctx):
+        p = ctx.partition(numel, B, 1, 1, 1)
+        n1 = p.range(1)[1]
+        sc, ss = ctx.sym_alloc(n1, torch.uint8), ctx.sym_alloc(n1 // B, torch.float32)
+        prim = to_dev(full[pm.range_at(r, g, Np, 1)[0]:sum(pm.range_at(r, g, Np, 1))])
+        out = torch.empty(Np, dtype=torch.bfloat16, device="cuda")
+        ctx.allgather_params(p, prim, sc, ss, out, bits=8)             # the previous layer's secondary
+        shard = torch.full((n1,), float("nan"), dtype=torch.float32, device="cuda")
+        hz.trace_begin(capacity=64, events=False, stamps=True)
+        ctx.backward_step(p, to_dev(grads[r]), shard, [4], p_prev=p, prev_sec_codes=sc, prev_sec_scales=ss,
+                          prev_full_out=out, prev_bits=8)
+        torch.cuda.current_stream().synchronize()
+        hz.trace_end()
+        before = [x["kind"] for x in hz.trace_read()]
+        pending = bool(torch.isnan(shard).all())
+        hz.trace_begin(capacity=64, events=False, stamps=True)
+        ctx.flush()
+        torch.cuda.current_stream().synchronize()
+        hz.trace_end()
+        after = [x["kind"] for x in hz.trace_read()]
+        got[r] = (before, pending, after, to_host(shard))
+        return []
+
+    errors = vworld.run_ranks(hz, g, fn)
+    assert not errors, "\n".join(errors)
+    for r in range(2):
+        before, pending, after, shard = got[r]
+        assert "reduce" not in before and pending, (before, pending)
+        assert after.count("reduce") == 1, after
+        assert_bitwise(shard, want[r], f"rank {r} deferred qgZ shard")
