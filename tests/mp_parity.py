@@ -601,6 +601,88 @@ def check_full_size(hz, rank, world, g, uid, device, numel, p2p, B=256, vctx=Non
     return errors
 
 
+def check_full_size_paired(hz, rank, world, g, numel, vctx, B=256, layers=3):
+    """The bench's PAIRED call sequence at full layer size (P2P): three layers of `numel`
+    through hz_allgather_params_next (dual kernels), the first backward gather, and
+    hz_backward_step with the previous layer (dual kernel, then the backward triple
+    kernel carrying the deferred last hop, then the final flush) — every layer's forward
+    and backward gathered layer and qgZ shard checked on sampled blocks against the
+    oracle (block locality, as check_full_size)."""
+    errors = []
+    ctx = vctx
+    L = len(g)
+    p = ctx.partition(numel, B, 1, 1, L)
+    Np = p.padded_numel
+    off, ln = p.range(1)
+    nb = Np // B
+    bounds = sorted({pm.range_at(r, g, Np, l)[0] // B for r in range(world) for l in range(L + 1)})
+    idx = synth.sample_blocks(nb, bounds, every=997)
+    it = torch.from_numpy(idx).cuda()
+    pick = lambda t: to_host(t.view(nb, B)[it].contiguous().view(-1))   # noqa: E731
+    T = []
+    for k in range(layers):
+        full = synth.torch_normal(Np, 7100 + k, 0.02, torch.bfloat16, "cuda", outlier_every=0)
+        full[numel:] = 0
+        picked = {}
+        grad = None
+        for q in range(world):
+            gq = synth.torch_normal(Np, 1900 + 10 * k + q, 1e-3, torch.bfloat16, "cuda")
+            gq[numel:] = 0
+            picked[q] = pick(gq)
+            if q == rank:
+                grad = gq
+            else:
+                del gq
+        T.append({"prim": full[off:off + ln].contiguous(), "want_w": pick(full), "picked": picked, "grad": grad,
+                  "sec_c": ctx.sym_alloc(ln, torch.uint8), "sec_s": ctx.sym_alloc(ln // B, torch.float32),
+                  "fwd": torch.empty(Np, dtype=torch.bfloat16, device="cuda"),
+                  "bwd": torch.empty(Np, dtype=torch.bfloat16, device="cuda"),
+                  "shard": torch.empty(p.range(L)[1], dtype=torch.float32, device="cuda")})
+        del full
+    for k, t in enumerate(T):
+        nx = T[k + 1] if k + 1 < layers else None
+        ctx.allgather_params_next(p, t["prim"], t["sec_c"], t["sec_s"], t["fwd"], bits=8,
+                                  p_next=p if nx else None, next_primary=nx["prim"] if nx else None,
+                                  next_sec_codes=nx["sec_c"] if nx else None,
+                                  next_sec_scales=nx["sec_s"] if nx else None)
+    ctx.allgather_params(p, None, T[-1]["sec_c"], T[-1]["sec_s"], T[-1]["bwd"], bits=8, backward=True)
+    for k in range(layers - 1, -1, -1):
+        t, pv = T[k], (T[k - 1] if k > 0 else None)
+        ctx.backward_step(p, t["grad"], t["shard"], [4] * L, p_prev=p if pv else None,
+                          prev_sec_codes=pv["sec_c"] if pv else None, prev_sec_scales=pv["sec_s"] if pv else None,
+                          prev_full_out=pv["bwd"] if pv else None, prev_bits=8)
+    torch.cuda.current_stream().synchronize()
+    ns = len(idx)
+    tnp = pm.padded_numel(ns * B, g, B)
+    my_off, my_len = p.range(L)
+    for k, t in enumerate(T):
+        want = quant.dequantize(*quant.quantize(t["want_w"], 8, B), B, out="bf16")
+        for name in ("fwd", "bwd"):
+            try:
+                assert_bitwise(pick(t[name]), want, f"[vworld] g={g} paired full-size layer {k} {name}")
+            except AssertionError as e:
+                errors.append(str(e))
+        tiny = {}
+        for q in range(world):
+            a = np.zeros(tnp, np.float32).astype(ml_dtypes.bfloat16)
+            a[:ns * B] = t["picked"][q]
+            tiny[q] = a
+        tout = col.reduce_scatter(tiny, g, tnp, B, 1, L, {l: 4 for l in range(1, L + 1)})
+        tflat = np.zeros(tnp, np.float32)
+        for q in range(world):
+            o, n_ = pm.range_at(q, g, tnp, L)
+            tflat[o:o + n_] = tout[q]
+        sh = to_host(t["shard"])
+        for i, b in enumerate(idx):
+            e0 = int(b) * B
+            if my_off <= e0 < my_off + my_len:
+                if not np.array_equal(sh[e0 - my_off:e0 - my_off + B].view(np.uint32),
+                                      tflat[i * B:(i + 1) * B].view(np.uint32)):
+                    errors.append(f"[vworld] g={g} paired full-size layer {k} qgZ block {b}: mismatch")
+                    break
+    return errors
+
+
 def run(rank, world, local, bcast=None):
     from paper_2501_04266_b200 import hz
     torch.cuda.set_device(local)

@@ -80,6 +80,22 @@ def test_vworld_full_size(model, g):
     assert not errors, "\n".join(errors[:20])
 
 
+@pytest.mark.parametrize("model,g", [("gpt1.3b", (2, 4)), ("gpt6.7b", (2, 2, 2))])
+def test_vworld_full_size_paired(model, g):
+    """The bench's paired sequence (dual kernels forward, dual + backward triple kernels
+    backward, the deferred last hop) at BASELINE layer size on 8 ranks, sampled-block
+    parity for every layer."""
+    _need_gpu()
+    from paper_2501_04266_b200 import hz, synth
+    from tests import mp_parity, vworld
+    numel = synth.layer_numel(synth.GPT_CONFIGS[model]["hidden"])
+    Np = numel + 8192
+    errors = vworld.run_ranks(hz, g, lambda r, w, ctx: mp_parity.check_full_size_paired(hz, r, w, g, numel, ctx),
+                              pool_bytes=4 * Np + (64 << 20))
+    torch.cuda.empty_cache()
+    assert not errors, "\n".join(errors[:20])
+
+
 def test_vworld_trace_shows_multi_rank_kernels():
     """At W = 8 the pipelined step launches the dual gather+quantize kernels and the
     gathers read remote pieces (remote_bytes > 0) on every rank."""
