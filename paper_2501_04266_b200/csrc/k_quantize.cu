@@ -173,15 +173,13 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
 template <typename T, int QBITS, int QOUT>
 cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const void* x, int64_t n_q, uint8_t* codes,
                               float* scales, float* qy, int acc, cudaStream_t st, const SyncArgs& sy) {
-  // chunks of the interleaved schedule (HZ_TUNE gqc; default by size): one pass when a
-  // warp has few gather tiles (GPT-1.3B layer, ~10 per warp: the chunked kernel's extra
-  // registers cost more than the balance gains, 3.80 vs 4.20 ms), 4 chunks from ~32 tiles
-  // per warp on (GPT-6.7B layer: 19.28 -> 17.76 ms per step at N = 2)
-  int chunks = tune_param("gqc", 0);
-  if (chunks <= 0) {
-    const int64_t per_warp = (n_gather / 8 + 32 * kU - 1) / (32 * kU) / (int64_t(sm_count()) * 32);
-    chunks = per_warp >= 32 ? 4 : 1;
-  }
+  // chunks of the interleaved schedule (HZ_TUNE gqc, default 1 = one pass).  Round 1
+  // chose 4 chunks from ~32 gather tiles per warp on (GPT-6.7B / NeoX-20B layers); with
+  // the round-2 protocol the one-pass kernel is faster at every size (GPT-6.7B N = 2:
+  // 17.96 vs 18.41 ms per step, N = 4: 19.17 vs 19.61; NeoX-20B N = 2: 55.13 vs 55.79,
+  // N = 4: 58.12 vs 58.62)
+  int chunks = tune_param("gqc", 1);
+  if (chunks < 1) chunks = 1;
   // HZ_TUNE gqu=8: 8 gather units in flight per lane (one-pass codes-only variant)
   auto kern = chunks > 1 ? k_gather_quantize<T, QBITS, 8, __nv_bfloat16, QOUT, true>
                          : k_gather_quantize<T, QBITS, 8, __nv_bfloat16, QOUT, false>;
