@@ -381,6 +381,69 @@ struct EmitF32 {
   }
 };
 
+// fp32 round trip without accumulate, stores by TMA: each warp step's 256 x_hat land in
+// natural order in one of this warp's two 1 KB shared-memory buffers and lane 0 issues a
+// cp.async.bulk shared -> global of the 1 KB span (the next-but-one step reuses a buffer
+// after its bulk store has read it).  finish() waits for the warp's stores.  Values and
+// rounding are EmitF32's.
+struct EmitF32Bulk {
+  static constexpr bool on = true;
+  float* y;
+  float4* stage;   // this warp's 2 x 64 granules
+  mutable int buf;
+  __device__ __forceinline__ void operator()(int64_t e0, int lane, const float (&xh)[8]) const {
+    const int64_t base = e0 - 8 * lane;   // first element of the warp step's 256
+    float4* st = stage + buf * 64;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    st[lane * 2] = make_float4(xh[0], xh[1], xh[2], xh[3]);
+    st[lane * 2 + 1] = make_float4(xh[4], xh[5], xh[6], xh[7]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 1024;" ::"l"(y + base),
+                   "r"(static_cast<uint32_t>(__cvta_generic_to_shared(st)))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    buf ^= 1;
+  }
+  __device__ __forceinline__ void finish(int lane) const {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+};
+
+// bf16 / fp16 round-trip output stored by TMA: as EmitF32Bulk with 512-byte spans (the
+// 256 16-bit x_hat of a warp step), two buffers per warp.
+template <typename TO>
+struct EmitOutBulk {
+  static constexpr bool on = true;
+  TO* y;
+  uint4* stage;   // this warp's 2 x 32 granules
+  mutable int buf;
+  __device__ __forceinline__ void operator()(int64_t e0, int lane, const float (&xh)[8]) const {
+    const int64_t base = e0 - 8 * lane;
+    uint4* st = stage + buf * 32;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    Out8<TO>::store(reinterpret_cast<TO*>(st) + lane * 8, xh);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;" ::"l"(y + base),
+                   "r"(static_cast<uint32_t>(__cvta_generic_to_shared(st)))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    buf ^= 1;
+  }
+  __device__ __forceinline__ void finish(int lane) const {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+};
+
 __device__ __forceinline__ int64_t global_warp() {
   return (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
 }

@@ -8,11 +8,40 @@
 namespace hz {
 namespace dev {
 
+// Optional TMA stores of the output (k_dequantize): a full warp step's 256 outputs land in
+// one of this warp's two shared-memory buffers (256 * sizeof(TO) bytes each) and lane 0
+// bulk-stores the contiguous span; the buffer is reused after its store has read it.
+struct BulkOut {
+  uint4* stage;   // 2 buffers of 256 * sizeof(TO) bytes
+  int buf;
+};
+template <typename TO>
+__device__ __forceinline__ void bulk_out_step(BulkOut& bo, TO* dst, int lane, const float (&v)[8]) {
+  constexpr int SPAN = 256 * static_cast<int>(sizeof(TO));
+  TO* st = reinterpret_cast<TO*>(reinterpret_cast<char*>(bo.stage) + bo.buf * SPAN);
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  __syncwarp();
+  Out8<TO>::store(st + lane * 8, v);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(static_cast<uint32_t>(__cvta_generic_to_shared(st))), "n"(SPAN)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  bo.buf ^= 1;
+}
+__device__ __forceinline__ void bulk_out_finish(int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncwarp();
+}
+
 // Warp tiles [tile0, tile1) of the layer only (32*U units each; default: all of them).
 template <int BITS, typename TO, int U>
 __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits, int log2b, TO* __restrict__ y,
                                                 int64_t warp, int64_t nwarps, int64_t tile0 = 0,
-                                                int64_t tile1 = INT64_MAX) {
+                                                int64_t tile1 = INT64_MAX, BulkOut* bo = nullptr) {
   const int lane = threadIdx.x & 31;
   const bool copy_sec = pc.sec_c != nullptr;
   // Pieces interleaved by warp tile (32*U units): consecutive tiles alternate between
@@ -88,6 +117,17 @@ __device__ __forceinline__ void dequantize_loop(const Pieces& pc, int64_t nunits
         raw[u].load(pc.c[j] + r * BITS / 8);
         sc[u] = HZ_PEER_LD(pc.s[j] + (r >> log2b));
       }
+    }
+    if (bo && fast && !copy_sec) {   // a full tile: 32*U contiguous units, TMA stores
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float c[8], v[8];
+        raw[u].decode(c);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __fmul_rn(c[i], sc[u]);
+        bulk_out_step<TO>(*bo, y + (ub + u * 32) * 8, lane, v);
+      }
+      continue;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {

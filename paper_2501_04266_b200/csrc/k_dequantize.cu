@@ -26,10 +26,15 @@ using namespace dev;
 template <int BITS, typename TO, int U>
 __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__ Pieces pc,
                                                          int64_t nunits, int log2b,
-                                                         TO* __restrict__ y,
+                                                         TO* __restrict__ y, int bulk_on,
                                                          const __grid_constant__ SyncArgs sy) {
+  __shared__ __align__(128) uint4 stage[kThreads / 32][2 * 256 * sizeof(TO) / 16];
   if (!sync_wait(sy)) return;
-  dequantize_loop<BITS, TO, U>(pc, nunits, log2b, y, global_warp(), num_warps());
+  // the output by TMA bulk stores (HZ_TUNE fbd=0: LSU stores)
+  BulkOut bo{stage[threadIdx.x >> 5], 0};
+  const bool bulk = bulk_on && (reinterpret_cast<uintptr_t>(y) & 15u) == 0;
+  dequantize_loop<BITS, TO, U>(pc, nunits, log2b, y, global_warp(), num_warps(), 0, INT64_MAX, bulk ? &bo : nullptr);
+  if (bulk) bulk_out_finish(threadIdx.x & 31);
   sync_signal(sy);
 }
 
@@ -40,7 +45,7 @@ cudaError_t dequantize_u(const Pieces& pc, int64_t nunits, int log2b, void* y, c
                          const SyncArgs& sy) {
   auto kern = k_dequantize<BITS, TO, U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
-  return launch_k(kern, grid, st, pc, nunits, log2b, static_cast<TO*>(y), sy);
+  return launch_k(kern, grid, st, pc, nunits, log2b, static_cast<TO*>(y), tune_param("fbd", 1), sy);
 }
 
 template <int BITS, typename TO>

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
                                                        void* __restrict__ y, int acc) {
   using G = Geo<B>;
   using Emit = typename OutOf<OUT>::E;
-  __shared__ float4 stage[OUT == 3 ? kThreads / 32 : 1][OUT == 3 ? 64 : 1];
+  __shared__ __align__(128) float4 stage[OUT >= 3 ? kThreads / 32 : 1][OUT == 4 ? 128 : (OUT >= 3 ? 64 : 1)];
   Emit emit;
   if constexpr (OUT == 1 || OUT == 2) {
     emit.y = static_cast<decltype(emit.y)>(y);
@@ -36,9 +36,18 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const T* __restrict__ x, 
     emit.y = static_cast<float*>(y);
     emit.stage = stage[threadIdx.x >> 5];
     emit.acc = acc;
+  } else if constexpr (OUT == 4) {
+    emit.y = static_cast<float*>(y);
+    emit.stage = stage[threadIdx.x >> 5];
+    emit.buf = 0;
+  } else if constexpr (OUT == 5 || OUT == 6) {
+    emit.y = static_cast<decltype(emit.y)>(y);
+    emit.stage = reinterpret_cast<uint4*>(stage[threadIdx.x >> 5]);
+    emit.buf = 0;
   }
   if (!sync_wait(sy)) return;   // P2P mode: the readers of what this call overwrites are done
   quantize_loop<T, B, BITS, U, OUT>(x, nblocks, codes, scales, emit, y, acc, global_warp(), num_warps());
+  if constexpr (OUT >= 4) emit.finish(threadIdx.x & 31);
   sync_signal(sy);   // P2P mode: codes of this phase are ready for the peers
 }
 
@@ -67,10 +76,22 @@ cudaError_t roundtrip_t(const void* x, int64_t n, uint8_t* codes, float* scales,
     }
     return cudaErrorInvalidValue;
   }
+  // the x_hat stores by TMA: fp32 (HZ_TUNE fb, default on: N = 1 step 3.280 vs 3.301 ms),
+  // bf16 / fp16 (HZ_TUNE fbb, default off: no measured gain)
+  const bool al = (reinterpret_cast<uintptr_t>(y) & 15u) == 0;
+  const bool bulk = tune_param("fb", 1) != 0 && al;
+  const bool bulk16 = tune_param("fbb", 0) != 0 && al;
   switch (out_dt) {
-    case HZ_BF16: return quantize_u<T, 256, BITS, kU, 1>(x, n, codes, scales, st, sy, y, 0);
-    case HZ_F16: return quantize_u<T, 256, BITS, kU, 2>(x, n, codes, scales, st, sy, y, 0);
-    case HZ_F32: return quantize_u<T, 256, BITS, kU, 3>(x, n, codes, scales, st, sy, y, acc);
+    case HZ_BF16:
+      return bulk16 ? quantize_u<T, 256, BITS, kU, 5>(x, n, codes, scales, st, sy, y, 0)
+                    : quantize_u<T, 256, BITS, kU, 1>(x, n, codes, scales, st, sy, y, 0);
+    case HZ_F16:
+      return bulk16 ? quantize_u<T, 256, BITS, kU, 6>(x, n, codes, scales, st, sy, y, 0)
+                    : quantize_u<T, 256, BITS, kU, 2>(x, n, codes, scales, st, sy, y, 0);
+    case HZ_F32:
+      // no accumulate: the fp32 stores by TMA (HZ_TUNE fb=0: the LSU stores)
+      if (!acc && bulk) return quantize_u<T, 256, BITS, kU, 4>(x, n, codes, scales, st, sy, y, 0);
+      return quantize_u<T, 256, BITS, kU, 3>(x, n, codes, scales, st, sy, y, acc);
   }
   return cudaErrorInvalidValue;
 }

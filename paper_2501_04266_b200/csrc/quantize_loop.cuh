@@ -22,6 +22,12 @@ template <>
 struct OutOf<2> { using E = EmitOut<__half>; };
 template <>
 struct OutOf<3> { using E = EmitF32; };
+template <>
+struct OutOf<4> { using E = EmitF32Bulk; };   // fp32 round trip, no accumulate, TMA stores
+template <>
+struct OutOf<5> { using E = EmitOutBulk<__nv_bfloat16>; };   // bf16 round trip, TMA stores
+template <>
+struct OutOf<6> { using E = EmitOutBulk<__half>; };          // fp16 round trip, TMA stores
 
 // The quantize loop: warp `warp` of `nwarps` processes its grid-stride share of the
 // blocks (main loop without bounds checks, then the checked tail on the last warp).
@@ -100,14 +106,14 @@ __device__ __forceinline__ void quantize_loop(const T* __restrict__ x, int64_t n
           out.set(b);
           out.store(codes + (blk * B + k * G::SUBSTRIDE + ll * 8) * BITS / 8);
         }
-        if constexpr (OUT == 1 || OUT == 2) {
-          if (valid) {
+        if constexpr (OUT == 1 || OUT == 2 || OUT == 5 || OUT == 6) {
+          if (valid) {   // warp-uniform for B = 256 (the round trip's block)
             float xh[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) xh[i] = __fmul_rn(__fsub_rn(__uint_as_float(b[i]), kMagic), scale);
             emit(blk * B + k * G::SUBSTRIDE + ll * 8, lane, xh);
           }
-        } else if constexpr (OUT == 3) {
+        } else if constexpr (OUT == 3 || OUT == 4) {
           // tail (< U blocks): plain per-lane stores, no staging
           float xh[8];
 #pragma unroll
