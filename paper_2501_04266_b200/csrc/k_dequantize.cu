@@ -32,7 +32,9 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
   if (!sync_wait(sy)) return;
   // the output by TMA bulk stores (HZ_TUNE fbd=0: LSU stores)
   BulkOut bo{stage[threadIdx.x >> 5], 0};
-  const bool bulk = bulk_on && (reinterpret_cast<uintptr_t>(y) & 15u) == 0;
+  // (one local piece: the N = 1 dequantize; gathers with peer pieces keep the LSU stores,
+  // bulk stores measured neutral-to-slower there)
+  const bool bulk = bulk_on && pc.n == 1 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0;
   dequantize_loop<BITS, TO, U>(pc, nunits, log2b, y, global_warp(), num_warps(), 0, INT64_MAX, bulk ? &bo : nullptr);
   if (bulk) bulk_out_finish(threadIdx.x & 31);
   sync_signal(sy);

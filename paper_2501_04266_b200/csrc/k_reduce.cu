@@ -334,8 +334,8 @@ __device__ __noinline__ void gqr_quantize(const T* __restrict__ x, int64_t nbloc
   quantize_loop<T, 256, QBITS, 4, 0>(x, nblocks, codes, scales, emit, nullptr, 0, warp, nwarps);
 }
 __device__ __noinline__ void gqr_gather(const Pieces& pc, int64_t nunits, __nv_bfloat16* __restrict__ y,
-                                        int64_t warp, int64_t nwarps) {
-  dequantize_loop<8, __nv_bfloat16, 4>(pc, nunits, 8, y, warp, nwarps);
+                                        int64_t warp, int64_t nwarps, BulkOut* bo) {
+  dequantize_loop<8, __nv_bfloat16, 4>(pc, nunits, 8, y, warp, nwarps, 0, INT64_MAX, bo);
 }
 template <int RBIN, int RGT, bool RACC>
 __device__ __noinline__ void gqr_reduce(const RedArgs& ra, int log2b, float4* st, int64_t warp, int64_t nwarps) {
@@ -346,19 +346,23 @@ template <typename T, int QBITS, int RBIN, int RGT, bool RACC>
 __global__ void __launch_bounds__(kThreads, 4) k_gather_quantize_reduce(
     const __grid_constant__ Pieces pc, int64_t nunits, __nv_bfloat16* __restrict__ y, const T* __restrict__ x,
     int64_t nblocks, uint8_t* __restrict__ codes, float* __restrict__ scales, const __grid_constant__ RedArgs ra,
-    int log2b, const __grid_constant__ SyncArgs sy) {
+    int log2b, int gbulk, const __grid_constant__ SyncArgs sy) {
   __shared__ float4 stage[kThreads / 32][32 * red_granules<RBIN>()];
+  __shared__ __align__(128) uint4 gstage[kThreads / 32][2 * 256 * 2 / 16];
   if (!sync_wait(sy)) return;
   const int64_t warp = global_warp(), nwarps = num_warps();
   float4* st = stage[threadIdx.x >> 5];
+  BulkOut bo{gstage[threadIdx.x >> 5], 0};
+  BulkOut* bop = gbulk ? &bo : nullptr;
   const int order = static_cast<int>(blockIdx.x % 3);
 #pragma unroll 1
   for (int k = 0; k < 3; ++k) {
     const int job = (order + k) % 3;
-    if (job == 0) gqr_gather(pc, nunits, y, warp, nwarps);
+    if (job == 0) gqr_gather(pc, nunits, y, warp, nwarps, bop);
     else if (job == 1) gqr_quantize<T, QBITS>(x, nblocks, codes, scales, warp, nwarps);
     else gqr_reduce<RBIN, RGT, RACC>(ra, log2b, st, warp, nwarps);
   }
+  if (bop) bulk_out_finish(threadIdx.x & 31);
   sync_signal(sy);
 }
 
@@ -370,8 +374,9 @@ cudaError_t gqr_t(const Pieces& pc, int64_t n_gather, void* y, const void* x, in
   const int64_t tasks = std::max<int64_t>(std::max<int64_t>(n_gather / 8 / (32 * 4), n_q / 256 / 4),
                                           ra.n / E / (32 * kUF_)) + 1;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks);
+  const int gbulk = tune_param("dgb", 0) != 0 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0 ? 1 : 0;
   return launch_k(kern, grid, st, pc, n_gather / 8, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x),
-                  n_q / 256, codes, scales, ra, 8, sy);
+                  n_q / 256, codes, scales, ra, 8, gbulk, sy);
 }
 
 template <typename T, int QBITS, int RBIN>
