@@ -19,15 +19,14 @@ import re
 import subprocess
 
 KIND = [  # (regex on the demangled kernel name, kind used by the library trace)
-    (r"k_quantize<[^,<>]+, \d+, \d+, \d+, \d+, [\w:]*(?<!No)Push>", "quantize_push"),
-    (r"k_quantize<[^,<>]+, \d+, \d+, \d+, [1-3]\b", "quantize_dequantize"),
+    (r"k_gather_quantize_reduce", "gather_quantize_reduce"),
+    (r"k_gather_quantize", "gather_quantize"),
+    (r"k_tiles", "tiles"),
+    (r"k_quantize<[^,<>]+, \d+, \d+, \d+, [1-6]\b", "quantize_dequantize"),
     (r"k_quantize", "quantize"),
     (r"k_dequantize", "dequantize"),
-    (r"k_reduce_requant<[^<>]*(?<!No)Push>", "reduce_push"),
     (r"k_reduce_requant", "reduce_requant"),
     (r"k_reduce_f32", "reduce"),
-    (r"k_ag_pipe", "ag_fused"),
-    (r"k_rs_pipe", "rs_fused"),
     (r"k_adamw", "adamw"),
     (r"k_gather_copy", "gather_copy"),
 ]
