@@ -35,7 +35,7 @@ def test_vworld_hierarchy(g):
 
 
 @pytest.mark.multigpu
-@pytest.mark.parametrize("g", [(2,), (2, 2), (2, 2, 2)], ids=lambda g: "x".join(map(str, g)))
+@pytest.mark.parametrize("g", [(2,), (2, 2), (2, 2, 2), (2, 4)], ids=lambda g: "x".join(map(str, g)))
 def test_vworld_multi_device(g):
     """hz_init_virtual_ex: rank r on GPU r % ngpu, so pair partners sit on different
     GPUs and every gather / qgZ piece of a partner crosses NVLink (peer access, one
