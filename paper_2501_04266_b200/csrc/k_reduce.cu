@@ -346,7 +346,7 @@ template <typename T, int QBITS, int RBIN, int RGT, bool RACC>
 __global__ void __launch_bounds__(kThreads, 4) k_gather_quantize_reduce(
     const __grid_constant__ Pieces pc, int64_t nunits, __nv_bfloat16* __restrict__ y, const T* __restrict__ x,
     int64_t nblocks, uint8_t* __restrict__ codes, float* __restrict__ scales, const __grid_constant__ RedArgs ra,
-    int log2b, int gbulk, const __grid_constant__ SyncArgs sy) {
+    int log2b, int gbulk, int jorder, const __grid_constant__ SyncArgs sy) {
   __shared__ float4 stage[kThreads / 32][32 * red_granules<RBIN>()];
   __shared__ __align__(128) uint4 gstage[kThreads / 32][2 * 256 * 2 / 16];
   if (!sync_wait(sy)) return;
@@ -354,10 +354,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather_quantize_reduce(
   float4* st = stage[threadIdx.x >> 5];
   BulkOut bo{gstage[threadIdx.x >> 5], 0};
   BulkOut* bop = gbulk ? &bo : nullptr;
-  const int order = static_cast<int>(blockIdx.x % 3);
+  // job order per CTA (HZ_TUNE gqro): 0 = rotate by blockIdx % 3 (default); 1 = quantize,
+  // gather, reduce; 2 = gather, reduce, quantize; 3 = even CTAs quantize first, odd CTAs
+  // gather first, reduce last
+  int seq[3];
+  if (jorder == 1) {
+    seq[0] = 1; seq[1] = 0; seq[2] = 2;
+  } else if (jorder == 2) {
+    seq[0] = 0; seq[1] = 2; seq[2] = 1;
+  } else if (jorder == 3) {
+    seq[0] = (blockIdx.x & 1) ? 0 : 1; seq[1] = (blockIdx.x & 1) ? 1 : 0; seq[2] = 2;
+  } else {
+    const int o = static_cast<int>(blockIdx.x % 3);
+    seq[0] = o; seq[1] = (o + 1) % 3; seq[2] = (o + 2) % 3;
+  }
 #pragma unroll 1
   for (int k = 0; k < 3; ++k) {
-    const int job = (order + k) % 3;
+    const int job = seq[k];
     if (job == 0) gqr_gather(pc, nunits, y, warp, nwarps, bop);
     else if (job == 1) gqr_quantize<T, QBITS>(x, nblocks, codes, scales, warp, nwarps);
     else gqr_reduce<RBIN, RGT, RACC>(ra, log2b, st, warp, nwarps);
@@ -376,7 +389,7 @@ cudaError_t gqr_t(const Pieces& pc, int64_t n_gather, void* y, const void* x, in
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks);
   const int gbulk = tune_param("dgb", 0) != 0 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0 ? 1 : 0;
   return launch_k(kern, grid, st, pc, n_gather / 8, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x),
-                  n_q / 256, codes, scales, ra, 8, gbulk, sy);
+                  n_q / 256, codes, scales, ra, 8, gbulk, tune_param("gqro", 0), sy);
 }
 
 template <typename T, int QBITS, int RBIN>
