@@ -48,6 +48,7 @@
 // what it waits for (CUDA events), so the W streams cannot deadlock on shared
 // hardware queues or SMs.
 #include <algorithm>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -143,12 +144,26 @@ SyncArgs make_sync(hz_ctx* ctx, const Phases& ph) {
 // One synchronised launch: in a virtual world the host first orders the stream after
 // the signals this kernel waits for, and records its own signals afterwards.
 // (HZ_TUNE vworder=0 disables the host ordering: a test of the device-side waits)
+// HZ_TUNE vwserial=1 (profiling tool mode, tools/vw_profile.py under ncu): in a virtual
+// world, one synchronised launch at a time in the whole process, each completed before
+// the next starts — so a profiler replaying one GPU's kernel (and restoring that GPU's
+// memory between passes) never races a peer kernel writing flags into that memory.
+std::mutex g_vw_serial;
+
 template <class F>
 hz_status synced(hz_ctx* ctx, const SyncArgs& s, cudaStream_t st, F&& launch) {
   static const bool order = tune_param("vworder", 1) != 0;
+  static const bool serial = tune_param("vwserial", 0) != 0;
   const bool vw = ctx->p2p.vw && order;
   hz_status rc;
   if (vw && (rc = vw_wait(ctx, s, st)) != HZ_OK) return rc;
+  if (vw && serial) {
+    std::lock_guard<std::mutex> lock(g_vw_serial);
+    if ((rc = launch()) != HZ_OK) return rc;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "virtual world: serial launch");
+    return vw_signal(ctx, s, st);
+  }
   if ((rc = launch()) != HZ_OK) return rc;
   if (vw) return vw_signal(ctx, s, st);
   return HZ_OK;

@@ -13,8 +13,12 @@ link carries one direction at a time (ncu's per-kernel view; the concurrent bidi
 case is the bench's).
 
     python tools/vw_profile.py --gpus 2 [--config gpt1.3b] [--layers 3] [--steps 2] [--time]
-    ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,\\
+    HZ_TUNE=vwserial=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,\\
         nvlrx__bytes.sum,nvltx__bytes.sum -k regex:k_ python tools/vw_profile.py --gpus 2
+
+Under ncu set HZ_TUNE=vwserial=1: every synchronised launch then runs alone (ncu restores a
+GPU's memory between replay passes of one of its kernels; a peer kernel running meanwhile
+would have its flag writes into that memory reverted).
 """
 
 import argparse
