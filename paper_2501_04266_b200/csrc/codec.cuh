@@ -462,8 +462,10 @@ int sm_count();   // SMs of the current device (cached)
 // kernels (launch_k_smem; grid_for with the same dyn_smem sets the opt-in limit), and the
 // programmatic-stream-serialization attribute when HZ_TUNE pdl=1 (PDL; off by
 // default, see pdl_enabled) — the kernel's prologue (sync_wait) then orders it after
-// the previous kernel on the stream.
+// the previous kernel on the stream; and the shared-memory carveout of the API call's
+// CarveScope (hz_internal.h), when set.
 bool pdl_enabled();
+int launch_carve();
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k_smem(void (*kern)(KArgs...), int64_t grid, int dyn_smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg{};
@@ -471,11 +473,17 @@ cudaError_t launch_k_smem(void (*kern)(KArgs...), int64_t grid, int dyn_smem, cu
   cfg.blockDim = dim3(dev::kThreads);
   cfg.dynamicSmemBytes = static_cast<size_t>(dyn_smem);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const int carve = launch_carve();   // CarveScope of the API call (hz_internal.h)
+  if (carve >= 0) {
+    attr[1].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+    attr[1].val.sharedMemCarveout = static_cast<unsigned>(carve);
+    cfg.numAttrs = 2;
+  }
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 template <typename... KArgs, typename... Args>

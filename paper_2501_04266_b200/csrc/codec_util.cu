@@ -116,6 +116,17 @@ cudaError_t launch_epoch_advance(unsigned long long* epoch, unsigned long long s
 }  // namespace hz
 
 namespace hz {
+namespace {
+thread_local int t_carve = -1;
+}
+int launch_carve() { return t_carve; }
+CarveScope::CarveScope(int world) : prev(t_carve) {
+  static const int c1 = tune_param("carve1", 100);
+  static const int cn = tune_param("carve", -1);
+  t_carve = world == 1 ? c1 : cn;
+}
+CarveScope::~CarveScope() { t_carve = prev; }
+
 // Off by default: measured on B200 (profiles/bench_r01.md) PDL left the multi-GPU
 // step unchanged and made the N = 1 step 7 % slower (the fused round trip 51 -> 56 µs).
 bool pdl_enabled() {

@@ -425,6 +425,7 @@ hz_status hz_allgather_params_next(hz_ctx* ctx, const hz_partition_t* p, const v
                                    hz_dtype out_dt, const hz_partition_t* p_next, const void* next_primary,
                                    uint8_t* next_sec_codes, float* next_sec_scales, void* stream) {
   using namespace hz;
+  const CarveScope carve_scope(ctx ? ctx->world : 0);
   if (!p_next) return allgather_impl(ctx, p, 0, primary, dt, bits, sec_codes, sec_scales, full_out, out_dt, stream,
                                      nullptr);
   hz_status rc = check_partition(ctx, p_next);
@@ -444,6 +445,7 @@ static hz_status allgather_impl(hz_ctx* ctx, const hz_partition_t* p, int backwa
                                 hz_dtype dt, int bits, uint8_t* sec_codes, float* sec_scales, void* full_out,
                                 hz_dtype out_dt, void* stream, const hz::NextQ* nextq) {
   using namespace hz;
+  const CarveScope carve_scope(ctx ? ctx->world : 0);
   hz_status st0 = check_allgather(ctx, p, backward, primary, dt, bits, sec_codes, sec_scales, full_out, out_dt);
   if (st0 != HZ_OK) return st0;
   st0 = check_async(ctx);
@@ -558,6 +560,7 @@ hz_status hz_backward_step(hz_ctx* ctx, const hz_partition_t* p, const void* gra
                            const hz_partition_t* p_prev, uint8_t* prev_sec_codes, float* prev_sec_scales,
                            int prev_bits, void* prev_full_out, hz_dtype prev_out_dt, void* stream) {
   using namespace hz;
+  const CarveScope carve_scope(ctx ? ctx->world : 0);
   hz_status rc = check_reduce_scatter(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard);
   if (rc != HZ_OK) return rc;
   if (!p_prev)
@@ -605,6 +608,7 @@ hz_status hz_reduce_scatter_grads(hz_ctx* ctx, const hz_partition_t* p, const vo
                                   const int* bits_per_level, float* shard, int accumulate,
                                   void* stream) {
   using namespace hz;
+  const CarveScope carve_scope(ctx ? ctx->world : 0);
   hz_status rc = check_reduce_scatter(ctx, p, grad, dt, from_level, to_level, bits_per_level, shard);
   if (rc != HZ_OK) return rc;
   if ((rc = check_async(ctx)) != HZ_OK) return rc;

@@ -15,6 +15,22 @@ namespace hz {
 hz_status fail(hz_status st, const std::string& msg);
 void clear_error();
 
+// ------------------------------------------------- shared-memory carveout
+// Preferred shared-memory carveout (percent, -1 = driver default) that launch_k_smem
+// (codec.cuh) attaches to every libhz launch of this host thread, set per API call by
+// CarveScope.  A world-1 context uses 100 (HZ_TUNE carve1): with every kernel of its
+// sequence at one carveout, the SMs need no shared-memory reconfiguration between the
+// dequantize and round-trip launches (N = 1 step 3.233 vs 3.278 ms, round trip 49.1 vs
+// 49.9 us; profiles/tma_r02.md, carveout addendum).  World > 1 keeps the driver default
+// (HZ_TUNE carve): the P2P kernels read through L1 and measured slower at 100 (N = 2 step
+// 4.32 vs 3.93 ms).
+int launch_carve();
+struct CarveScope {
+  int prev;
+  explicit CarveScope(int world);
+  ~CarveScope();
+};
+
 // --------------------------------------------------------------- validation
 bool block_ok(int block);          // power of two in [32, 2048]
 bool bits_ok(int bits);            // 4 or 8
