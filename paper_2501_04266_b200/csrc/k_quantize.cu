@@ -150,9 +150,10 @@ __global__ void __launch_bounds__(kThreads) k_gather_quantize(const __grid_const
   // QOUT 3: the quantize job is the round trip of a one-member level (fp32 x_hat into
   // qy, += when acc; codes not stored) — the world-1 backward pair
   __shared__ float4 stage[QOUT == 3 ? kThreads / 32 : 1][QOUT == 3 ? 64 : 1];
-  // gbulk: the gathered layer by TMA bulk stores (BulkOut, dequantize_loop.cuh)
-  __shared__ __align__(128) uint4 gstage[kThreads / 32][2 * 256 * sizeof(TO) / 16];
-  BulkOut bo{gstage[threadIdx.x >> 5], 0};
+  // gbulk: the gathered layer by TMA bulk stores (BulkOut, dequantize_loop.cuh), staged in
+  // dynamic shared memory sized by the launcher (0 bytes when off: more L1 for the loads)
+  extern __shared__ __align__(128) uint4 gq_gstage[];
+  BulkOut bo{gq_gstage + (threadIdx.x >> 5) * (2 * 256 * sizeof(TO) / 16), 0};
   BulkOut* bop = gbulk ? &bo : nullptr;
   using Emit = typename OutOf<QOUT>::E;
   Emit emit;
@@ -214,23 +215,23 @@ cudaError_t gather_quantize_t(const Pieces& pc, int64_t n_gather, void* y, const
   const int64_t nunits = n_gather / 8;
   const int64_t nblocks = n_q / 256;
   const int64_t tasks = std::max<int64_t>((nunits + 32 * kU - 1) / (32 * kU), nblocks / (kU * Geo<256>::BPW) + 1);
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks);
   // HZ_TUNE gq: 0 = every warp does both jobs, odd CTAs gather first (default); 1 = all
   // gather first; 2 = role split with gqf percent of the CTAs gathering
   int order = tune_param("gq", 0);
+  // HZ_TUNE dgb=1: the gathered layer by TMA bulk stores (one-pass schedules only; off by
+  // default: N = 2 step 4.06 vs 3.92-3.94 ms, N = 4 4.59 vs 4.43 ms)
+  const int gbulk = (order <= 1 && chunks == 1 && tune_param("dgb", 0) != 0 &&
+                     (reinterpret_cast<uintptr_t>(y) & 15u) == 0) ? 1 : 0;
+  const int dyn = gbulk ? (kThreads / 32) * 2 * 256 * static_cast<int>(sizeof(__nv_bfloat16)) : 0;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks, dyn);
   if (order == 2 && grid < 2) order = 0;
   if (order == 2) {
     int64_t gc = grid * tune_param("gqf", 50) / 100;
     gc = std::min<int64_t>(std::max<int64_t>(gc, 1), grid - 1);
     order = static_cast<int>(2 + gc);
   }
-  // HZ_TUNE gqc: chunks of the interleaved schedule (order 0)
-  // HZ_TUNE dgb=1: the gathered layer by TMA bulk stores (one-pass schedules only; off by
-  // default: N = 2 step 4.06 vs 3.92-3.94 ms, N = 4 4.59 vs 4.43 ms)
-  const int gbulk = (order <= 1 && chunks == 1 && tune_param("dgb", 0) != 0 &&
-                     (reinterpret_cast<uintptr_t>(y) & 15u) == 0) ? 1 : 0;
-  return launch_k(kern, grid, st, pc, nunits, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x), nblocks,
-                  codes, scales, qy, acc, order, chunks, gbulk, sy);
+  return launch_k_smem(kern, grid, dyn, st, pc, nunits, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x),
+                       nblocks, codes, scales, qy, acc, order, chunks, gbulk, sy);
 }
 
 template <typename T>

@@ -348,11 +348,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather_quantize_reduce(
     int64_t nblocks, uint8_t* __restrict__ codes, float* __restrict__ scales, const __grid_constant__ RedArgs ra,
     int log2b, int gbulk, int jorder, const __grid_constant__ SyncArgs sy) {
   __shared__ float4 stage[kThreads / 32][32 * red_granules<RBIN>()];
-  __shared__ __align__(128) uint4 gstage[kThreads / 32][2 * 256 * 2 / 16];
+  // gbulk: the bulk-store staging of the gathered layer, in dynamic shared memory sized by
+  // the launcher (0 bytes when off: a smaller shared-memory configuration leaves more L1
+  // for the loads in flight)
+  extern __shared__ __align__(128) uint4 gqr_gstage[];
   if (!sync_wait(sy)) return;
   const int64_t warp = global_warp(), nwarps = num_warps();
   float4* st = stage[threadIdx.x >> 5];
-  BulkOut bo{gstage[threadIdx.x >> 5], 0};
+  BulkOut bo{gqr_gstage + (threadIdx.x >> 5) * (2 * 256 * 2 / 16), 0};
   BulkOut* bop = gbulk ? &bo : nullptr;
   // job order per CTA (HZ_TUNE gqro): 0 = rotate by blockIdx % 3 (default); 1 = quantize,
   // gather, reduce; 2 = gather, reduce, quantize; 3 = even CTAs quantize first, odd CTAs
@@ -386,10 +389,11 @@ cudaError_t gqr_t(const Pieces& pc, int64_t n_gather, void* y, const void* x, in
   constexpr int E = Wide<RBIN>::E;
   const int64_t tasks = std::max<int64_t>(std::max<int64_t>(n_gather / 8 / (32 * 4), n_q / 256 / 4),
                                           ra.n / E / (32 * kUF_)) + 1;
-  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks);
   const int gbulk = tune_param("dgb", 0) != 0 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0 ? 1 : 0;
-  return launch_k(kern, grid, st, pc, n_gather / 8, static_cast<__nv_bfloat16*>(y), static_cast<const T*>(x),
-                  n_q / 256, codes, scales, ra, 8, gbulk, tune_param("gqro", 0), sy);
+  const int dyn = gbulk ? (kThreads / 32) * 2 * 256 * 2 : 0;
+  const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), tasks, dyn);
+  return launch_k_smem(kern, grid, dyn, st, pc, n_gather / 8, static_cast<__nv_bfloat16*>(y),
+                       static_cast<const T*>(x), n_q / 256, codes, scales, ra, 8, gbulk, tune_param("gqro", 0), sy);
 }
 
 template <typename T, int QBITS, int RBIN>
