@@ -25,3 +25,19 @@ def test_tile_engine_parity():
            os.path.join(ROOT, "tests", "test_gpu_collectives.py") + "::test_world1_context"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-2000:]
+
+
+def test_bulk_store_gather_parity():
+    """HZ_TUNE dgb=1 (off by default, measured slower at N >= 2 — profiles/tma_r02.md): the
+    dual and triple kernels store the gathered layer by TMA bulk stores from dynamic shared
+    memory.  The paired virtual-world schedule (dual + triple kernels) and the hierarchy
+    checks rerun with it, bitwise against the oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, HZ_TUNE="dgb=1")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+           os.path.join(ROOT, "tests", "test_gpu_vworld.py") + "::test_vworld_hierarchy",
+           os.path.join(ROOT, "tests", "test_gpu_vworld.py") + "::test_vworld_trace_shows_multi_rank_kernels",
+           os.path.join(ROOT, "tests", "test_gpu_vworld.py") + "::test_deferred_last_hop_completes_on_flush"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-2000:]
