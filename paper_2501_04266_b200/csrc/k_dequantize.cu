@@ -30,7 +30,9 @@ __global__ void __launch_bounds__(kThreads) k_dequantize(const __grid_constant__
                                                          const __grid_constant__ SyncArgs sy) {
   __shared__ __align__(128) uint4 stage[kThreads / 32][2 * 256 * sizeof(TO) / 16];
   if (!sync_wait(sy)) return;
-  // the output by TMA bulk stores (HZ_TUNE fbd=0: LSU stores)
+  // HZ_TUNE fbd=1: the output by TMA bulk stores.  Off by default since the world-1 carveout
+  // (hz_internal.h CarveScope): with it the LSU stores are faster, 27.0 vs 29.0 us per launch
+  // (profiles/tma_r02.md, carveout addendum)
   BulkOut bo{stage[threadIdx.x >> 5], 0};
   // (one local piece: the N = 1 dequantize; gathers with peer pieces keep the LSU stores,
   // bulk stores measured neutral-to-slower there)
@@ -47,7 +49,7 @@ cudaError_t dequantize_u(const Pieces& pc, int64_t nunits, int log2b, void* y, c
                          const SyncArgs& sy) {
   auto kern = k_dequantize<BITS, TO, U>;
   const int64_t grid = grid_for(reinterpret_cast<const void*>(kern), (nunits + 32 * U - 1) / (32 * U));
-  return launch_k(kern, grid, st, pc, nunits, log2b, static_cast<TO*>(y), tune_param("fbd", 1), sy);
+  return launch_k(kern, grid, st, pc, nunits, log2b, static_cast<TO*>(y), tune_param("fbd", 0), sy);
 }
 
 template <int BITS, typename TO>

@@ -28,14 +28,16 @@ def test_tile_engine_parity():
 
 
 def test_bulk_store_gather_parity():
-    """HZ_TUNE dgb=1 (off by default, measured slower at N >= 2 — profiles/tma_r02.md): the
+    """The non-default store modes stay parity-tested (profiles/tma_r02.md): HZ_TUNE dgb=1 (the
     dual and triple kernels store the gathered layer by TMA bulk stores from dynamic shared
-    memory.  The paired virtual-world schedule (dual + triple kernels) and the hierarchy
-    checks rerun with it, bitwise against the oracle."""
+    memory), fbd=1 (the world-1 dequantize by bulk stores) and fbb=0 (the bf16 round trip by
+    st.global).  The codec tests, the paired virtual-world schedule (dual + triple kernels)
+    and the hierarchy checks rerun with them, bitwise against the oracle."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    env = dict(os.environ, HZ_TUNE="dgb=1")
+    env = dict(os.environ, HZ_TUNE="dgb=1,fbd=1,fbb=0")
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+           os.path.join(ROOT, "tests", "test_gpu_codec.py"),
            os.path.join(ROOT, "tests", "test_gpu_vworld.py") + "::test_vworld_hierarchy",
            os.path.join(ROOT, "tests", "test_gpu_vworld.py") + "::test_vworld_trace_shows_multi_rank_kernels",
            os.path.join(ROOT, "tests", "test_gpu_vworld.py") + "::test_deferred_last_hop_completes_on_flush"]
