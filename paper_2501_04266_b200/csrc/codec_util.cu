@@ -123,7 +123,8 @@ int launch_carve() { return t_carve; }
 CarveScope::CarveScope(int world) : prev(t_carve) {
   static const int c1 = tune_param("carve1", 100);
   static const int cn = tune_param("carve", -1);
-  t_carve = world == 1 ? c1 : cn;
+  const int c = world == 1 ? c1 : cn;
+  t_carve = c > 100 ? 100 : c;   // percent; negative = the driver default
 }
 CarveScope::~CarveScope() { t_carve = prev; }
 
